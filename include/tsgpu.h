@@ -1,0 +1,181 @@
+/*
+ * tsgpu.h — C ABI of the B200-native tetsolve solve path (libtsgpu.so).
+ *
+ * This is the drop-in boundary for the reference's solve path
+ * (/root/reference/proj/include/tetsolve, "tetsolve" C++20 headers). Every
+ * entry point below replaces one reference interface; the replaced symbol is
+ * cited as file:line (relative to /root/reference/proj/include/tetsolve/).
+ * The C++ mirror headers in include/tetsolve_b200/ re-expose the reference's
+ * own class/function names on top of this ABI, and INTEGRATION.md shows the
+ * ctypes / C++ bindings a maintainer would add.
+ *
+ * Conventions
+ *  - Vectors use the reference layout [node][axis][batch]: entry (dof, b) at
+ *    data[dof * batch + b], dof = 3 * node + axis (vector_batch.hpp:12-28).
+ *  - Construction data (meshes, materials, masks) are HOST pointers.
+ *  - *_apply / *_device entry points take DEVICE pointers and a cudaStream_t
+ *    passed as void* (NULL = legacy default stream). *_host entry points take
+ *    HOST pointers and copy in/out themselves.
+ *  - prec is 32 (float) or 64 (double): the reference's T in EbeOperator<T>.
+ *  - Every call returns ts_status; on failure ts_last_error() (thread-local)
+ *    carries the message. Status codes map 1:1 to the reference's exception
+ *    classes (errors.hpp:9-31, solver_config.hpp:111-116).
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point returns TS_ERR_CUDA.
+ */
+#ifndef TSGPU_H
+#define TSGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TS_OK = 0,
+  TS_ERR_VALIDATION = 1,     /* tetsolve::ValidationError            errors.hpp:18-21 */
+  TS_ERR_BREAKDOWN = 2,      /* SolverError: (p,Ap) <= 0             pcg.hpp:105-107, adaptive_cg.hpp:211-212 */
+  TS_ERR_NONFINITE = 3,      /* SolverError: NaN residual            pcg.hpp:70,118-120, adaptive_cg.hpp:171 */
+  TS_ERR_NO_CONVERGENCE = 4, /* ConvergenceError (carries report)    adaptive_cg.hpp:179-188 */
+  TS_ERR_CUDA = 5,
+  TS_ERR_NCCL = 6
+} ts_status;
+
+const char* ts_last_error(void);
+const char* ts_version(void);
+
+/* ---------------------------------------------------------------- config */
+
+/* SolverConfig (solver_config.hpp:21-48); defaults via ts_config_default. */
+typedef struct {
+  double outer_tol;          /* relative residual norm ||r||/||f||   :22 */
+  int32_t outer_max_iter;    /* :23 */
+  double level_tol[3];       /* level0/1/2 tolerance                 :24-26 */
+  int32_t level_max_iter[3]; /* level0/1/2 max update steps          :24-26 */
+  int32_t batch_size;        /* CLI/Greens batch width only          :27 */
+  int32_t aggregate_target;  /* :28 */
+  int32_t residual_history_stride; /* 0 disables history             :29 */
+} ts_solver_config;
+
+void ts_config_default(ts_solver_config* cfg);
+ts_status ts_config_validate(const ts_solver_config* cfg); /* SolverConfig::validate :31-47 */
+
+/* SolveReport (solver_config.hpp:50-63). Arrays are caller-owned; any may be
+ * NULL. history is row-major [history_capacity][batch]. */
+typedef struct {
+  int32_t converged;
+  int32_t outer_iterations;
+  int64_t inner_iterations[3];
+  double time_setup_s;
+  double time_outer_s;
+  double time_inner_s[3];
+  double time_total_s;
+  int32_t batch_size;
+  int32_t method;            /* 0 = "amg", 1 = "pcge" */
+  int32_t inner_precision;   /* 32 = "float32", 64 = "float64" */
+  int32_t history_count;     /* rows written */
+  int32_t history_capacity;  /* rows available (in) */
+  double* final_rel_residual;/* [batch] */
+  int32_t* history_iter;     /* [history_capacity] */
+  double* history;           /* [history_capacity][batch] */
+} ts_solve_report;
+
+/* ------------------------------------------------------------------ mesh */
+
+/* Host-side mesh container mirroring tetsolve::Mesh (mesh.hpp:26-42):
+ * vertices first, tets10 = 4 vertices + 6 edge nodes on edges
+ * (0,1),(1,2),(2,0),(0,3),(1,3),(2,3). */
+typedef struct ts_mesh ts_mesh;
+
+/* generate_box_mesh (box_mesh.hpp:55-157); fixed_boundary: 0 none,
+ * 1 bottom_and_sides, 2 all_clamped (box_mesh.hpp:13-17). Node numbering is
+ * identical to the reference (vertices lexicographic z,y,x; edge midpoints in
+ * element discovery order). */
+ts_status ts_box_mesh(const double extents[3], const int32_t divisions[3],
+                      int32_t n_interfaces, const double* layer_interfaces,
+                      int32_t fixed_boundary, ts_mesh** out);
+ts_status ts_mesh_from_arrays(int32_t n_nodes, int32_t vertex_count, const double* coords,
+                              int32_t n_elems, const int32_t* tets10,
+                              const int32_t* material_id, int32_t n_dirichlet,
+                              const int32_t* bc_node, const int8_t* bc_axis, ts_mesh** out);
+ts_status ts_mesh_sizes(const ts_mesh* m, int32_t* n_nodes, int32_t* vertex_count,
+                        int32_t* n_elems, int32_t* n_dirichlet);
+/* any output pointer may be NULL */
+ts_status ts_mesh_export(const ts_mesh* m, double* coords, int32_t* tets10,
+                         int32_t* material_id, int32_t* bc_node, int8_t* bc_axis);
+/* dirichlet_mask (mesh.hpp:150-154): 3*n_nodes bytes */
+ts_status ts_mesh_dirichlet_mask(const ts_mesh* m, uint8_t* mask);
+void ts_mesh_destroy(ts_mesh* m);
+
+/* material_from_wavespeeds (material.hpp:22-34) */
+ts_status ts_material_from_wavespeeds(double vp, double vs, double rho, double* lambda,
+                                      double* mu);
+
+/* ------------------------------------------------------- EBE operator */
+
+/* EbeOperator<T> (ebe_operator.hpp:29-226), matrix-free
+ * f = mask_id(u) + sum_e Q_e K_e Q_e^T (masked u). Immutable after creation;
+ * apply may run concurrently on different streams. */
+typedef struct ts_ebe ts_ebe;
+
+/* EbeOperator(mesh, order, materials, dof_mask) (ebe_operator.hpp:35-65).
+ * materials are given as Lame pairs; dof_mask may be NULL (no constraints)
+ * and otherwise has 3 * n_nodes(order) entries. */
+ts_status ts_ebe_create(const ts_mesh* mesh, int32_t order, int32_t n_materials,
+                        const double* lambda, const double* mu, const uint8_t* dof_mask,
+                        int32_t prec, ts_ebe** out);
+void ts_ebe_destroy(ts_ebe* op);
+ts_status ts_ebe_info(const ts_ebe* op, int32_t* n_nodes, int32_t* n_elements, int32_t* order,
+                      int32_t* prec);
+/* EbeOperator::apply (ebe_operator.hpp:90-134) on device pointers. */
+ts_status ts_ebe_apply(const ts_ebe* op, const void* u, void* f, int32_t batch, void* stream);
+/* same, host pointers (H2D + apply + D2H inside) */
+ts_status ts_ebe_apply_host(const ts_ebe* op, const void* u, void* f, int32_t batch);
+/* extract_block_jacobi(EbeOperator) (ebe_operator.hpp:288-313): inverse 3x3
+ * node blocks in the operator precision, written to a HOST array
+ * [n_nodes][9] of prec-sized scalars. */
+ts_status ts_ebe_block_jacobi_host(const ts_ebe* op, void* inv_blocks);
+/* tuning / introspection: number of kernel launches of one apply, and the
+ * device time of the last apply's EBE kernel when timing is enabled. */
+ts_status ts_ebe_set_timing(ts_ebe* op, int32_t enable);
+ts_status ts_ebe_last_kernel_ms(const ts_ebe* op, float* ms);
+ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t* n);
+
+/* ------------------------------------------------------------ level set */
+
+/* SolverLevels / build_solver_levels (adaptive_cg.hpp:27-67), plus
+ * build_crust_model (model.hpp:21-29) when dof_mask is NULL (mask derived
+ * from the mesh Dirichlet list). */
+typedef struct ts_levels ts_levels;
+ts_status ts_levels_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda,
+                           const double* mu, const uint8_t* dof_mask,
+                           const ts_solver_config* cfg, ts_levels** out);
+void ts_levels_destroy(ts_levels* lv);
+ts_status ts_levels_sizes(const ts_levels* lv, int32_t* n0, int32_t* n1, int32_t* n2,
+                          int64_t* nnzb2);
+/* setup introspection for parity tests (any pointer may be NULL):
+ * agg_of_node [n1], level-2 BCSR row_ptr [n2+1], col_idx [nnzb2],
+ * blocks [nnzb2][9] float, mask2 [3*n2], m2 inverse blocks [n2][9] float */
+ts_status ts_levels_export(const ts_levels* lv, int32_t* agg_of_node, int32_t* row_ptr2,
+                           int32_t* col_idx2, float* blocks2, uint8_t* mask2, float* m2_inv);
+/* the operators inside the level set (borrowed, owned by lv) */
+ts_status ts_levels_operator(const ts_levels* lv, int32_t which /*0 outer,1 level0,2 level1*/,
+                             const ts_ebe** op);
+
+/* solve (adaptive_cg.hpp:242-263) with host buffers; u_out may alias u0. */
+ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_out,
+                   int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);
+/* solve with device buffers on a stream */
+ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, double* u_out,
+                          int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep,
+                          void* stream);
+/* solve_pcge (adaptive_cg.hpp:267-279), host buffers, 64-bit operator. */
+ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, double* u_out,
+                        int32_t batch, double tol, int32_t max_iter, ts_solve_report* rep);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSGPU_H */
