@@ -1,0 +1,22 @@
+"""B200-native drop-in for the tetsolve solve path (arXiv 1710.08679).
+
+The compute lives in ``libtsgpu.so`` (hand-written sm_100a CUDA + C++ host,
+C ABI in include/tsgpu.h). This package is a thin ctypes mirror of the
+reference interface for tests, benchmarks and Python users.
+"""
+from .tetsolve import (  # noqa: F401
+    ConvergenceError,
+    DeviceError,
+    EbeOperator,
+    Error,
+    InnerLoopConfig,
+    Material,
+    Mesh,
+    SolveReport,
+    SolverConfig,
+    SolverError,
+    ValidationError,
+    dirichlet_mask,
+    generate_box_mesh,
+    material_from_wavespeeds,
+)

@@ -1,0 +1,124 @@
+"""ctypes binding of libtsgpu.so (include/tsgpu.h).
+
+The library is the product: there is no Python/CPU fallback. Importing this
+module loads the in-tree ``libtsgpu.so`` and raises if it is missing; compute
+entry points return TS_ERR_CUDA (raised as ``TsError``) when no GPU exists.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtsgpu.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "tsgpu.h")
+
+TS_OK = 0
+TS_ERR_VALIDATION = 1
+TS_ERR_BREAKDOWN = 2
+TS_ERR_NONFINITE = 3
+TS_ERR_NO_CONVERGENCE = 4
+TS_ERR_CUDA = 5
+TS_ERR_NCCL = 6
+
+
+class SolverConfig(C.Structure):
+    """ts_solver_config == tetsolve::SolverConfig (solver_config.hpp:21-48)."""
+
+    _fields_ = [
+        ("outer_tol", C.c_double),
+        ("outer_max_iter", C.c_int32),
+        ("level_tol", C.c_double * 3),
+        ("level_max_iter", C.c_int32 * 3),
+        ("batch_size", C.c_int32),
+        ("aggregate_target", C.c_int32),
+        ("residual_history_stride", C.c_int32),
+    ]
+
+
+class SolveReportC(C.Structure):
+    """ts_solve_report == tetsolve::SolveReport (solver_config.hpp:50-63)."""
+
+    _fields_ = [
+        ("converged", C.c_int32),
+        ("outer_iterations", C.c_int32),
+        ("inner_iterations", C.c_int64 * 3),
+        ("time_setup_s", C.c_double),
+        ("time_outer_s", C.c_double),
+        ("time_inner_s", C.c_double * 3),
+        ("time_total_s", C.c_double),
+        ("batch_size", C.c_int32),
+        ("method", C.c_int32),
+        ("inner_precision", C.c_int32),
+        ("history_count", C.c_int32),
+        ("history_capacity", C.c_int32),
+        ("final_rel_residual", C.POINTER(C.c_double)),
+        ("history_iter", C.POINTER(C.c_int32)),
+        ("history", C.POINTER(C.c_double)),
+    ]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libtsgpu.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+lib = C.CDLL(LIB_PATH)
+
+vp = C.c_void_p
+i32 = C.c_int32
+_sig = {
+    "ts_last_error": (C.c_char_p, []),
+    "ts_version": (C.c_char_p, []),
+    "ts_config_default": (None, [vp]),
+    "ts_config_validate": (C.c_int, [vp]),
+    "ts_box_mesh": (C.c_int, [vp, vp, i32, vp, i32, vp]),
+    "ts_mesh_from_arrays": (C.c_int, [i32, i32, vp, i32, vp, vp, i32, vp, vp, vp]),
+    "ts_mesh_sizes": (C.c_int, [vp, vp, vp, vp, vp]),
+    "ts_mesh_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "ts_mesh_dirichlet_mask": (C.c_int, [vp, vp]),
+    "ts_mesh_destroy": (None, [vp]),
+    "ts_material_from_wavespeeds": (C.c_int, [C.c_double, C.c_double, C.c_double, vp, vp]),
+    "ts_ebe_create": (C.c_int, [vp, i32, i32, vp, vp, vp, i32, vp]),
+    "ts_ebe_destroy": (None, [vp]),
+    "ts_ebe_info": (C.c_int, [vp, vp, vp, vp, vp]),
+    "ts_ebe_apply": (C.c_int, [vp, vp, vp, i32, vp]),
+    "ts_ebe_apply_host": (C.c_int, [vp, vp, vp, i32]),
+    "ts_ebe_block_jacobi_host": (C.c_int, [vp, vp]),
+    "ts_ebe_set_timing": (C.c_int, [vp, i32]),
+    "ts_ebe_last_kernel_ms": (C.c_int, [vp, vp]),
+    "ts_ebe_launches_per_apply": (C.c_int, [vp, vp]),
+    "ts_levels_create": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
+    "ts_levels_destroy": (None, [vp]),
+    "ts_levels_sizes": (C.c_int, [vp, vp, vp, vp, vp]),
+    "ts_levels_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "ts_levels_operator": (C.c_int, [vp, i32, vp]),
+    "ts_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
+    "ts_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
+    "ts_solve_pcge": (C.c_int, [vp, vp, vp, vp, i32, C.c_double, i32, vp]),
+}
+for _name, (_res, _args) in _sig.items():
+    _fn = getattr(lib, _name, None)
+    if _fn is not None:
+        _fn.restype = _res
+        _fn.argtypes = _args
+
+
+class TsError(RuntimeError):
+    """Raised for a non-OK ts_status; ``code`` is the status."""
+
+    def __init__(self, code: int, msg: str, report=None):
+        super().__init__(msg)
+        self.code = code
+        self.report = report
+
+
+def check(rc: int):
+    if rc != TS_OK:
+        raise TsError(rc, lib.ts_last_error().decode())
+
+
+def declared_symbols() -> list[str]:
+    """Every function prototype declared in include/tsgpu.h."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ts_[a-z0-9_]+)\s*\(", src)))

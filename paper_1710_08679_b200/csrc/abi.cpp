@@ -1,0 +1,239 @@
+// abi.cpp — extern "C" boundary of libtsgpu.so (include/tsgpu.h): argument
+// validation, exception -> ts_status translation, host-buffer conveniences.
+#include <cstring>
+#include <memory>
+
+#include "ebe.h"
+
+namespace tsg {
+const std::string& last_error();
+}
+
+#define TS_API_BEGIN try {
+#define TS_API_END                                                  \
+  }                                                                 \
+  catch (const tsg::Error& e) {                                     \
+    tsg::set_last_error(e.what());                                  \
+    return e.code;                                                  \
+  }                                                                 \
+  catch (const std::bad_alloc&) {                                   \
+    tsg::set_last_error("out of host memory");                      \
+    return TS_ERR_VALIDATION;                                       \
+  }                                                                 \
+  catch (const std::exception& e) {                                 \
+    tsg::set_last_error(e.what());                                  \
+    return TS_ERR_VALIDATION;                                       \
+  }                                                                 \
+  return TS_OK;
+
+#define TS_REQUIRE(cond, msg) \
+  do {                        \
+    if (!(cond)) tsg::validation(msg); \
+  } while (0)
+
+extern "C" {
+
+const char* ts_last_error(void) { return tsg::last_error().c_str(); }
+const char* ts_version(void) { return "tsgpu 0.1 (sm_100a)"; }
+
+void ts_config_default(ts_solver_config* c) {
+  if (!c) return;
+  c->outer_tol = 1e-8;
+  c->outer_max_iter = 5000;
+  c->level_tol[0] = 0.1;
+  c->level_tol[1] = 0.05;
+  c->level_tol[2] = 0.025;
+  c->level_max_iter[0] = 30;
+  c->level_max_iter[1] = 300;
+  c->level_max_iter[2] = 3000;
+  c->batch_size = 16;
+  c->aggregate_target = 8;
+  c->residual_history_stride = 1;
+}
+
+ts_status ts_config_validate(const ts_solver_config* c) {
+  TS_API_BEGIN
+  TS_REQUIRE(c, "solver config: null");
+  auto check_tol = [](double t, const char* what) {
+    if (!(t > 0.0 && t < 1.0))
+      tsg::validation(std::string("solver config: ") + what + " tolerance must lie in (0, 1)");
+  };
+  check_tol(c->outer_tol, "outer");
+  check_tol(c->level_tol[0], "level 0");
+  check_tol(c->level_tol[1], "level 1");
+  check_tol(c->level_tol[2], "level 2");
+  if (c->outer_max_iter < 1 || c->level_max_iter[0] < 1 || c->level_max_iter[1] < 1 ||
+      c->level_max_iter[2] < 1)
+    tsg::validation("solver config: max iterations must be >= 1");
+  if (c->batch_size < 1) tsg::validation("solver config: batch size must be >= 1");
+  if (c->aggregate_target < 2) tsg::validation("solver config: aggregate target must be >= 2");
+  TS_API_END
+}
+
+// ------------------------------------------------------------------- mesh
+ts_status ts_box_mesh(const double extents[3], const int32_t divisions[3], int32_t n_interfaces,
+                      const double* layer_interfaces, int32_t fixed_boundary, ts_mesh** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(extents && divisions && out, "box mesh: null argument");
+  TS_REQUIRE(fixed_boundary >= 0 && fixed_boundary <= 2, "box mesh: fixed_boundary must be 0, 1 or 2");
+  std::vector<double> ifs;
+  if (n_interfaces > 0) ifs.assign(layer_interfaces, layer_interfaces + n_interfaces);
+  auto h = std::make_unique<ts_mesh>();
+  h->m = tsg::generate_box_mesh(extents, divisions, ifs, fixed_boundary);
+  *out = h.release();
+  TS_API_END
+}
+
+ts_status ts_mesh_from_arrays(int32_t n_nodes, int32_t vertex_count, const double* coords,
+                              int32_t n_elems, const int32_t* tets10, const int32_t* material_id,
+                              int32_t n_dirichlet, const int32_t* bc_node, const int8_t* bc_axis,
+                              ts_mesh** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(out && n_nodes >= 0 && n_elems >= 0 && vertex_count >= 0 && vertex_count <= n_nodes,
+             "mesh: bad sizes");
+  TS_REQUIRE((n_nodes == 0 || coords) && (n_elems == 0 || (tets10 && material_id)),
+             "mesh: null array");
+  auto h = std::make_unique<ts_mesh>();
+  auto& m = h->m;
+  m.coords.assign(coords, coords + 3 * static_cast<size_t>(n_nodes));
+  m.tets10.assign(tets10, tets10 + 10 * static_cast<size_t>(n_elems));
+  m.material_id.assign(material_id, material_id + n_elems);
+  m.vertex_count = vertex_count;
+  for (int32_t i = 0; i < n_dirichlet; ++i) {
+    TS_REQUIRE(bc_node[i] >= 0 && bc_node[i] < n_nodes && bc_axis[i] >= 0 && bc_axis[i] <= 2,
+               "mesh: dirichlet entry out of range");
+    m.bc_node.push_back(bc_node[i]);
+    m.bc_axis.push_back(bc_axis[i]);
+  }
+  for (size_t q = 0; q < m.tets10.size(); ++q)
+    TS_REQUIRE(m.tets10[q] >= 0 && m.tets10[q] < n_nodes,
+               "mesh: element " + std::to_string(q / 10) + " references node " +
+                   std::to_string(m.tets10[q]) + " out of range");
+  *out = h.release();
+  TS_API_END
+}
+
+ts_status ts_mesh_sizes(const ts_mesh* h, int32_t* nn, int32_t* nv, int32_t* ne, int32_t* nbc) {
+  TS_API_BEGIN
+  TS_REQUIRE(h, "mesh: null handle");
+  if (nn) *nn = h->m.n_nodes();
+  if (nv) *nv = h->m.vertex_count;
+  if (ne) *ne = h->m.n_elems();
+  if (nbc) *nbc = static_cast<int32_t>(h->m.bc_node.size());
+  TS_API_END
+}
+
+ts_status ts_mesh_export(const ts_mesh* h, double* coords, int32_t* tets10, int32_t* material_id,
+                         int32_t* bc_node, int8_t* bc_axis) {
+  TS_API_BEGIN
+  TS_REQUIRE(h, "mesh: null handle");
+  const auto& m = h->m;
+  if (coords) std::memcpy(coords, m.coords.data(), m.coords.size() * sizeof(double));
+  if (tets10) std::memcpy(tets10, m.tets10.data(), m.tets10.size() * sizeof(int32_t));
+  if (material_id) std::memcpy(material_id, m.material_id.data(), m.material_id.size() * sizeof(int32_t));
+  if (bc_node) std::memcpy(bc_node, m.bc_node.data(), m.bc_node.size() * sizeof(int32_t));
+  if (bc_axis) std::memcpy(bc_axis, m.bc_axis.data(), m.bc_axis.size());
+  TS_API_END
+}
+
+ts_status ts_mesh_dirichlet_mask(const ts_mesh* h, uint8_t* mask) {
+  TS_API_BEGIN
+  TS_REQUIRE(h && mask, "mesh: null argument");
+  const auto v = h->m.dirichlet_mask();
+  std::memcpy(mask, v.data(), v.size());
+  TS_API_END
+}
+
+void ts_mesh_destroy(ts_mesh* m) { delete m; }
+
+ts_status ts_material_from_wavespeeds(double vp, double vs, double rho, double* lambda, double* mu) {
+  TS_API_BEGIN
+  TS_REQUIRE(lambda && mu, "material: null output");
+  if (vp <= 0.0 || vs <= 0.0 || rho <= 0.0) tsg::validation("material: vp, vs, rho must be positive");
+  if (vp * vp <= 2.0 * vs * vs)
+    tsg::validation("material: requires vp^2 > 2*vs^2 (lambda must be positive)");
+  *mu = rho * vs * vs;
+  *lambda = rho * (vp * vp - 2.0 * vs * vs);
+  TS_API_END
+}
+
+// ------------------------------------------------------------------- EBE
+ts_status ts_ebe_create(const ts_mesh* mesh, int32_t order, int32_t n_materials,
+                        const double* lambda, const double* mu, const uint8_t* dof_mask,
+                        int32_t prec, ts_ebe** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && out && lambda && mu && n_materials >= 0, "ebe: null argument");
+  *out = tsg::ebe_create(mesh->m, order, n_materials, lambda, mu, dof_mask, prec);
+  TS_API_END
+}
+
+void ts_ebe_destroy(ts_ebe* op) { delete op; }
+
+ts_status ts_ebe_info(const ts_ebe* op, int32_t* n_nodes, int32_t* n_elements, int32_t* order,
+                      int32_t* prec) {
+  TS_API_BEGIN
+  TS_REQUIRE(op, "ebe: null handle");
+  if (n_nodes) *n_nodes = op->n_nodes;
+  if (n_elements) *n_elements = op->n_elems;
+  if (order) *order = op->order;
+  if (prec) *prec = op->prec;
+  TS_API_END
+}
+
+ts_status ts_ebe_apply(const ts_ebe* op, const void* u, void* f, int32_t batch, void* stream) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && u && f, "ebe apply: null argument");
+  tsg::ebe_apply(*op, u, f, batch, static_cast<cudaStream_t>(stream));
+  TS_API_END
+}
+
+ts_status ts_ebe_apply_host(const ts_ebe* op, const void* u, void* f, int32_t batch) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && u && f, "ebe apply: null argument");
+  TS_REQUIRE(batch >= 1, "ebe apply: batch must be >= 1");
+  const size_t bytes = 3 * static_cast<size_t>(op->n_nodes) * batch * (op->prec / 8);
+  tsg::DevBuf<unsigned char> du(bytes), df(bytes);
+  TS_CUDA(cudaMemcpy(du.get(), u, bytes, cudaMemcpyHostToDevice));
+  tsg::ebe_apply(*op, du.get(), df.get(), batch, nullptr);
+  TS_CUDA(cudaMemcpy(f, df.get(), bytes, cudaMemcpyDeviceToHost));
+  TS_API_END
+}
+
+ts_status ts_ebe_block_jacobi_host(const ts_ebe* op, void* inv_blocks) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && inv_blocks, "ebe block jacobi: null argument");
+  const size_t bytes = 9 * static_cast<size_t>(op->n_nodes) * (op->prec / 8);
+  tsg::DevBuf<unsigned char> d(bytes);
+  tsg::ebe_block_jacobi(*op, d.get(), nullptr);
+  TS_CUDA(cudaMemcpy(inv_blocks, d.get(), bytes, cudaMemcpyDeviceToHost));
+  TS_API_END
+}
+
+ts_status ts_ebe_set_timing(ts_ebe* op, int32_t enable) {
+  TS_API_BEGIN
+  TS_REQUIRE(op, "ebe: null handle");
+  if (enable && !op->ev0) {
+    TS_CUDA(cudaEventCreate(&op->ev0));
+    TS_CUDA(cudaEventCreate(&op->ev1));
+  }
+  op->timing = enable != 0;
+  TS_API_END
+}
+
+ts_status ts_ebe_last_kernel_ms(const ts_ebe* op, float* ms) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && ms, "ebe: null argument");
+  TS_REQUIRE(op->timing, "ebe: timing not enabled");
+  TS_CUDA(cudaEventSynchronize(op->ev1));
+  TS_CUDA(cudaEventElapsedTime(ms, op->ev0, op->ev1));
+  TS_API_END
+}
+
+ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t* n) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && n, "ebe: null argument");
+  *n = 2;  // masked-identity init (or memset) + one element sweep per 32 cases
+  TS_API_END
+}
+
+}  // extern "C"

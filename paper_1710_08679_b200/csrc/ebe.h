@@ -1,0 +1,34 @@
+// ebe.h — device-resident matrix-free EBE operator (EbeOperator<T>,
+// ebe_operator.hpp:29-226), shared by the solver translation units.
+#pragma once
+#include "ts_common.h"
+
+struct ts_ebe {
+  int order = 2;   // 1 = tet4 on the vertex grid, 2 = tet10
+  int npe = 10;
+  int prec = 32;   // 32 | 64 : the reference's T
+  int32_t n_nodes = 0;
+  int32_t n_elems = 0;
+  bool has_mask = false;
+  int conn_stride = 12;                 // int32 per element (npe padded to 4)
+  tsg::DevBuf<int32_t> conn;            // [E][conn_stride]: node | (dof-mask bits << 28)
+  tsg::DevBuf<unsigned char> coef;      // [E][12] of T: b_1,b_2,b_3, lp, mp, 0
+  tsg::DevBuf<unsigned char> mask;      // [3N] uint8 (empty if unconstrained)
+  std::vector<double> coef64;           // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
+  std::vector<int32_t> host_conn;       // host [E][npe] (setup only)
+  std::vector<uint8_t> host_mask;       // host [3N]
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  ~ts_ebe();
+};
+
+namespace tsg {
+// f = A u on device pointers (EbeOperator::apply, ebe_operator.hpp:90-134)
+void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s);
+// inverse nodal diagonal blocks, fp64 math, rounded to prec (ebe_operator.hpp:288-313);
+// writes a DEVICE array [n_nodes][9] of the operator precision
+void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s);
+ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda,
+                   const double* mu, const uint8_t* dof_mask, int prec);
+}  // namespace tsg

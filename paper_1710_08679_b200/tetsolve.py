@@ -1,0 +1,369 @@
+"""Python mirror of the reference ``tetsolve`` solve-path interface over libtsgpu.
+
+Names, argument meaning and error behaviour follow the reference C++ headers
+(/root/reference/proj/include/tetsolve); each class cites the symbol it
+mirrors. Vectors are ``[node][axis][case]`` (vector_batch.hpp:12-28): a
+``VectorBatch`` here is a 2-D array of shape ``(3 * n_nodes, batch)`` — a
+torch CUDA tensor for the device path, or a numpy array for the host path
+(copies in/out inside the call, like the reference's host ``VectorBatch``).
+
+Errors map to the reference's exception classes (errors.hpp:9-31):
+``ValidationError``, ``SolverError`` and ``ConvergenceError`` (carrying the
+report, solver_config.hpp:111-116).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import SolverConfig as _CConfig
+from ._lib import SolveReportC as _CReport
+from ._lib import lib
+
+try:  # torch is plumbing for device memory and streams only
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+# ----------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """tetsolve::Error (errors.hpp:9-12)."""
+
+
+class ValidationError(Error):
+    """tetsolve::ValidationError (errors.hpp:15-18)."""
+
+
+class SolverError(Error):
+    """tetsolve::SolverError (errors.hpp:27-30)."""
+
+
+class ConvergenceError(SolverError):
+    """tetsolve::ConvergenceError (solver_config.hpp:111-116); carries .report."""
+
+    def __init__(self, msg, report):
+        super().__init__(msg)
+        self.report = report
+
+
+class DeviceError(Error):
+    """CUDA failure or no device: the product has no CPU fallback."""
+
+
+def _raise(rc: int, report=None):
+    msg = lib.ts_last_error().decode()
+    if rc == _lib.TS_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if rc == _lib.TS_ERR_NO_CONVERGENCE:
+        raise ConvergenceError(msg, report)
+    if rc in (_lib.TS_ERR_BREAKDOWN, _lib.TS_ERR_NONFINITE):
+        raise SolverError(msg)
+    raise DeviceError(msg)
+
+
+def _ck(rc: int, report=None):
+    if rc != 0:
+        _raise(rc, report)
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+# ------------------------------------------------------------------ config
+@dataclass
+class InnerLoopConfig:
+    """tetsolve::InnerLoopConfig (solver_config.hpp:16-19)."""
+
+    tol: float = 0.1
+    max_iter: int = 30
+
+
+@dataclass
+class SolverConfig:
+    """tetsolve::SolverConfig (solver_config.hpp:21-48); defaults from Table 2."""
+
+    outer_tol: float = 1e-8
+    outer_max_iter: int = 5000
+    level0: InnerLoopConfig = field(default_factory=lambda: InnerLoopConfig(0.1, 30))
+    level1: InnerLoopConfig = field(default_factory=lambda: InnerLoopConfig(0.05, 300))
+    level2: InnerLoopConfig = field(default_factory=lambda: InnerLoopConfig(0.025, 3000))
+    batch_size: int = 16
+    aggregate_target: int = 8
+    residual_history_stride: int = 1
+
+    def to_c(self) -> _CConfig:
+        c = _CConfig()
+        c.outer_tol = self.outer_tol
+        c.outer_max_iter = self.outer_max_iter
+        c.level_tol[:] = [self.level0.tol, self.level1.tol, self.level2.tol]
+        c.level_max_iter[:] = [self.level0.max_iter, self.level1.max_iter, self.level2.max_iter]
+        c.batch_size = self.batch_size
+        c.aggregate_target = self.aggregate_target
+        c.residual_history_stride = self.residual_history_stride
+        return c
+
+    def validate(self):
+        """SolverConfig::validate (solver_config.hpp:31-47)."""
+        c = self.to_c()
+        _ck(lib.ts_config_validate(C.byref(c)))
+
+
+@dataclass
+class SolveReport:
+    """tetsolve::SolveReport (solver_config.hpp:50-108)."""
+
+    converged: bool = False
+    residual_history_stride: int = 0
+    outer_iterations: int = 0
+    inner_iterations: list = field(default_factory=lambda: [0, 0, 0])
+    final_rel_residual: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    residual_history: list = field(default_factory=list)  # [(iter, per-column ndarray)]
+    time_setup_s: float = 0.0
+    time_outer_s: float = 0.0
+    time_inner_s: list = field(default_factory=lambda: [0.0, 0.0, 0.0])
+    time_total_s: float = 0.0
+    batch_size: int = 0
+    method: str = "amg"
+    inner_precision: str = "float32"
+
+    def max_final_residual(self) -> float:
+        return float(self.final_rel_residual.max()) if len(self.final_rel_residual) else 0.0
+
+
+class _ReportBuf:
+    def __init__(self, batch: int, capacity: int):
+        self.c = _CReport()
+        self.final = np.zeros(batch, np.float64)
+        self.hit = np.zeros(max(capacity, 1), np.int32)
+        self.hist = np.zeros((max(capacity, 1), batch), np.float64)
+        self.c.final_rel_residual = self.final.ctypes.data_as(C.POINTER(C.c_double))
+        self.c.history_iter = self.hit.ctypes.data_as(C.POINTER(C.c_int32))
+        self.c.history = self.hist.ctypes.data_as(C.POINTER(C.c_double))
+        self.c.history_capacity = capacity
+
+    def report(self, stride: int) -> SolveReport:
+        c = self.c
+        n = c.history_count
+        return SolveReport(
+            converged=bool(c.converged),
+            residual_history_stride=stride,
+            outer_iterations=int(c.outer_iterations),
+            inner_iterations=[int(x) for x in c.inner_iterations],
+            final_rel_residual=self.final.copy(),
+            residual_history=[(int(self.hit[i]), self.hist[i].copy()) for i in range(n)],
+            time_setup_s=float(c.time_setup_s),
+            time_outer_s=float(c.time_outer_s),
+            time_inner_s=[float(x) for x in c.time_inner_s],
+            time_total_s=float(c.time_total_s),
+            batch_size=int(c.batch_size),
+            method="pcge" if c.method == 1 else "amg",
+            inner_precision="float64" if c.inner_precision == 64 else "float32",
+        )
+
+
+# -------------------------------------------------------------- materials
+@dataclass
+class Material:
+    """tetsolve::Material (material.hpp:14-20)."""
+
+    vp: float = 0.0
+    vs: float = 0.0
+    rho: float = 0.0
+    lam: float = 0.0
+    mu: float = 0.0
+
+
+def material_from_wavespeeds(vp: float, vs: float, rho: float) -> Material:
+    """material_from_wavespeeds (material.hpp:22-34)."""
+    lam, mu = C.c_double(), C.c_double()
+    _ck(lib.ts_material_from_wavespeeds(vp, vs, rho, C.byref(lam), C.byref(mu)))
+    return Material(vp, vs, rho, lam.value, mu.value)
+
+
+def _lame(materials):
+    lam = np.ascontiguousarray([m.lam for m in materials], np.float64)
+    mu = np.ascontiguousarray([m.mu for m in materials], np.float64)
+    return lam, mu
+
+
+# ------------------------------------------------------------------- mesh
+FIXED = {"none": 0, "bottom_and_sides": 1, "all_clamped": 2}
+
+
+class Mesh:
+    """tetsolve::Mesh (mesh.hpp:26-42), held by libtsgpu as a host container."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        nn, nv, ne, nbc = (C.c_int32() for _ in range(4))
+        _ck(lib.ts_mesh_sizes(self._h, C.byref(nn), C.byref(nv), C.byref(ne), C.byref(nbc)))
+        self._sizes = (nn.value, nv.value, ne.value, nbc.value)
+        self._arrays = None
+
+    @classmethod
+    def from_arrays(cls, coords, tets10, material_id, vertex_count, bc_node=(), bc_axis=()):
+        c = np.ascontiguousarray(coords, np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(tets10, np.int32).reshape(-1, 10)
+        m = np.ascontiguousarray(material_id, np.int32)
+        bn = np.ascontiguousarray(bc_node, np.int32)
+        ba = np.ascontiguousarray(bc_axis, np.int8)
+        h = C.c_void_p()
+        _ck(lib.ts_mesh_from_arrays(c.shape[0], vertex_count, _p(c), t.shape[0], _p(t), _p(m),
+                                    len(bn), _p(bn) if len(bn) else None, _p(ba) if len(ba) else None,
+                                    C.byref(h)))
+        return cls(h)
+
+    def node_count(self) -> int:
+        return self._sizes[0]
+
+    @property
+    def vertex_count(self) -> int:
+        return self._sizes[1]
+
+    def element_count(self) -> int:
+        return self._sizes[2]
+
+    def arrays(self):
+        if self._arrays is None:
+            nn, nv, ne, nbc = self._sizes
+            coords = np.zeros((nn, 3), np.float64)
+            tets = np.zeros((ne, 10), np.int32)
+            mat = np.zeros(ne, np.int32)
+            bn = np.zeros(max(nbc, 1), np.int32)
+            ba = np.zeros(max(nbc, 1), np.int8)
+            _ck(lib.ts_mesh_export(self._h, _p(coords), _p(tets), _p(mat), _p(bn), _p(ba)))
+            self._arrays = dict(coords=coords, tets10=tets, material_id=mat, bc_node=bn[:nbc], bc_axis=ba[:nbc])
+        return self._arrays
+
+    @property
+    def coords(self):
+        return self.arrays()["coords"]
+
+    @property
+    def tets10(self):
+        return self.arrays()["tets10"]
+
+    @property
+    def material_id(self):
+        return self.arrays()["material_id"]
+
+    def dirichlet_mask(self) -> np.ndarray:
+        mask = np.zeros(3 * self.node_count(), np.uint8)
+        _ck(lib.ts_mesh_dirichlet_mask(self._h, _p(mask)))
+        return mask
+
+    def __del__(self):
+        try:
+            lib.ts_mesh_destroy(self._h)
+        except Exception:
+            pass
+
+
+def generate_box_mesh(extents, divisions, layer_interfaces=(), fixed_boundary="bottom_and_sides") -> Mesh:
+    """generate_box_mesh (box_mesh.hpp:55-157), identical numbering."""
+    ext = np.ascontiguousarray(extents, np.float64)
+    div = np.ascontiguousarray(divisions, np.int32)
+    ifs = np.ascontiguousarray(layer_interfaces, np.float64) if len(layer_interfaces) else None
+    fb = FIXED[fixed_boundary] if isinstance(fixed_boundary, str) else int(fixed_boundary)
+    h = C.c_void_p()
+    _ck(lib.ts_box_mesh(_p(ext), _p(div), len(layer_interfaces), _p(ifs), fb, C.byref(h)))
+    return Mesh(h)
+
+
+def dirichlet_mask(mesh: Mesh) -> np.ndarray:
+    """dirichlet_mask (mesh.hpp:150-154)."""
+    return mesh.dirichlet_mask()
+
+
+# -------------------------------------------------------------- operators
+def _is_torch(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class EbeOperator:
+    """EbeOperator<T> (ebe_operator.hpp:29-226) on the device.
+
+    ``prec`` is 32 (EbeOperator<float>) or 64 (EbeOperator<double>). ``workers``
+    is accepted for signature compatibility and ignored (the device kernel is
+    order-independent up to rounding).
+    """
+
+    def __init__(self, mesh: Mesh, order: int, materials, dof_mask=None, workers: int = 1, prec: int = 64,
+                 _borrowed=None):
+        self._own = _borrowed is None
+        if _borrowed is not None:
+            self._h = _borrowed
+        else:
+            lam, mu = _lame(materials)
+            mk = None if dof_mask is None or len(dof_mask) == 0 else np.ascontiguousarray(dof_mask, np.uint8)
+            if mk is not None:
+                nn = mesh.vertex_count if order == 1 else mesh.node_count()
+                if len(mk) != 3 * nn:
+                    raise ValidationError("ebe: dof mask length mismatch")
+            self._h = C.c_void_p()
+            _ck(lib.ts_ebe_create(mesh._h, order, len(lam), _p(lam), _p(mu), _p(mk), prec, C.byref(self._h)))
+        nn, ne, od, pr = (C.c_int32() for _ in range(4))
+        _ck(lib.ts_ebe_info(self._h, C.byref(nn), C.byref(ne), C.byref(od), C.byref(pr)))
+        self._n, self._e, self._order, self.prec = nn.value, ne.value, od.value, pr.value
+        self.dtype_np = np.float32 if self.prec == 32 else np.float64
+
+    def n_nodes(self) -> int:
+        return self._n
+
+    def n_elements(self) -> int:
+        return self._e
+
+    def order(self) -> int:
+        return self._order
+
+    def nodes_per_element(self) -> int:
+        return 4 if self._order == 1 else 10
+
+    def apply(self, u, f=None):
+        """f = A u for all batch columns (ebe_operator.hpp:90-134)."""
+        if u.ndim != 2 or u.shape[0] != 3 * self._n:
+            raise ValidationError("ebe apply: dimension mismatch")
+        batch = int(u.shape[1])
+        if _is_torch(u):
+            want = torch.float32 if self.prec == 32 else torch.float64
+            if u.dtype != want or not u.is_cuda:
+                raise ValidationError("ebe apply: input must be a CUDA tensor of the operator precision")
+            u = u.contiguous()
+            if f is None or f.shape != u.shape or f.dtype != u.dtype:
+                f = torch.empty_like(u)
+            _ck(lib.ts_ebe_apply(self._h, C.c_void_p(u.data_ptr()), C.c_void_p(f.data_ptr()), batch, _stream()))
+            return f
+        u = np.ascontiguousarray(u, self.dtype_np)
+        out = np.empty_like(u) if f is None or f.shape != u.shape else f
+        _ck(lib.ts_ebe_apply_host(self._h, _p(u), _p(out), batch))
+        return out
+
+    def block_jacobi(self) -> np.ndarray:
+        """extract_block_jacobi(EbeOperator) (ebe_operator.hpp:288-313): [n_nodes, 9]."""
+        inv = np.zeros((self._n, 9), self.dtype_np)
+        _ck(lib.ts_ebe_block_jacobi_host(self._h, _p(inv)))
+        return inv
+
+    def set_timing(self, enable: bool = True):
+        _ck(lib.ts_ebe_set_timing(self._h, int(enable)))
+
+    def last_kernel_ms(self) -> float:
+        ms = C.c_float()
+        _ck(lib.ts_ebe_last_kernel_ms(self._h, C.byref(ms)))
+        return ms.value
+
+    def __del__(self):
+        if getattr(self, "_own", False):
+            try:
+                lib.ts_ebe_destroy(self._h)
+            except Exception:
+                pass
