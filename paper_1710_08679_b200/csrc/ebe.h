@@ -1,7 +1,24 @@
 // ebe.h — device-resident matrix-free EBE operator (EbeOperator<T>,
 // ebe_operator.hpp:29-226), shared by the solver translation units.
 #pragma once
+#include <memory>
+#include <mutex>
+
 #include "ts_common.h"
+
+// Element clusters for the aggregated scatter (one cluster = the W elements a
+// thread block processes; W = block threads / threads per element). Built
+// lazily per W on the host from the Morton-ordered element list.
+struct EbeClusters {
+  int W = 0;
+  int32_t n_clusters = 0;
+  int32_t max_nodes = 0;
+  double nodes_per_elem = 0.0;
+  tsg::DevBuf<int32_t> node_ptr;   // [C+1]
+  tsg::DevBuf<int32_t> nodes;      // [sum PN]: global node | (dof-mask bits << 28)
+  tsg::DevBuf<int32_t> inc_ptr;    // [sum PN + 1] into inc
+  tsg::DevBuf<uint16_t> inc;       // slot * npe + local index, element order
+};
 
 struct ts_ebe {
   int order = 2;   // 1 = tet4 on the vertex grid, 2 = tet10
@@ -12,11 +29,20 @@ struct ts_ebe {
   bool has_mask = false;
   int conn_stride = 12;                 // int32 per element (npe padded to 4)
   tsg::DevBuf<int32_t> conn;            // [E][conn_stride]: node | (dof-mask bits << 28)
+  tsg::DevBuf<int32_t> conn3;           // [E][12|8]: 3*node per local node, then dof-mask word
+  std::vector<int32_t> slab_ptr;        // element range of each slab (fast kernel)
+  std::vector<int32_t> slab_init_ptr;   // offsets into slab_init per slab
+  tsg::DevBuf<int32_t> slab_init;       // nodes first touched by each slab (| mask bits << 28)
+  tsg::DevBuf<int32_t> slab_ptr_dev, slab_init_ptr_dev;
+  tsg::DevBuf<int> slab_ready;          // per-slab arrival counters (persistent kernel gates)
   tsg::DevBuf<unsigned char> coef;      // [E][12] of T: b_1,b_2,b_3, lp, mp, 0
   tsg::DevBuf<unsigned char> mask;      // [3N] uint8 (empty if unconstrained)
   std::vector<double> coef64;           // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
   std::vector<int32_t> host_conn;       // host [E][npe] (setup only)
   std::vector<uint8_t> host_mask;       // host [3N]
+  mutable std::vector<std::unique_ptr<EbeClusters>> clusters;  // cached per W
+  mutable std::mutex clusters_mu;
+  int kernel = 3;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised (default), 4 slab-gated
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
