@@ -12,7 +12,13 @@ from .tetsolve import (  # noqa: F401
     InnerLoopConfig,
     Material,
     Mesh,
+    CrustModel,
     SolveReport,
+    SolverLevels,
+    build_crust_model,
+    build_solver_levels,
+    solve,
+    solve_pcge,
     SolverConfig,
     SolverError,
     ValidationError,

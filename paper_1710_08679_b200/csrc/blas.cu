@@ -1,0 +1,594 @@
+// blas.cu — the solve path's vector kernels: fused PCG/CG steps with
+// deterministic per-column fp64 reductions, block Jacobi, level-2 BCSR,
+// inter-grid transfers. Reference semantics cited per kernel.
+//
+// Reductions: every dot product accumulates in fp64 (vector_batch.hpp:51-64).
+// A fixed grid (kRedBlocks) owns fixed entry ranges; each block writes one
+// partial per column and a one-block finalize sums the partials in block
+// order, so results are bit-reproducible run to run and column-independent
+// (identical columns stay identical, test_solver.cpp:183-201).
+#include <cfloat>
+#include <cmath>
+
+#include "blas.h"
+
+namespace tsg {
+
+namespace {
+
+template <int ND, typename F>
+__device__ __forceinline__ void reduce_pass(int64_t len, int32_t B, double* __restrict__ partial, F&& f) {
+  __shared__ double sm[kRedThreads * 4];
+  const int S = (kRedThreads / B) * B;
+  const int t = threadIdx.x;
+  double acc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) acc[k] = 0.0;
+  if (t < S) {
+    const int b = t % B;
+    const int64_t per = ((len + gridDim.x - 1) / gridDim.x + S - 1) / S * S;
+    const int64_t lo = per * blockIdx.x;
+    const int64_t hi = lo + per < len ? lo + per : len;
+    for (int64_t i = lo + t; i < hi; i += S) f(i, b, acc);
+  }
+#pragma unroll
+  for (int k = 0; k < ND; ++k) sm[k * kRedThreads + t] = acc[k];
+  __syncthreads();
+  if (t < B) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      double s = 0.0;
+      for (int j = t; j < S; j += B) s += sm[k * kRedThreads + j];
+      partial[(static_cast<int64_t>(blockIdx.x) * ND + k) * B + t] = s;
+    }
+  }
+}
+
+// column total of partial k
+__device__ __forceinline__ double col_total(const double* __restrict__ partial, int nd, int k, int32_t B,
+                                            int b) {
+  double s = 0.0;
+  for (int blk = 0; blk < kRedBlocks; ++blk) s += partial[(static_cast<int64_t>(blk) * nd + k) * B + b];
+  return s;
+}
+
+// max_rel_ratio (pcg.hpp:32-42): max_b num/den; 0/0 converged; x/0 -> inf
+__device__ void write_ratio(const double* num, const double* den, int32_t B, PcgStatus* st) {
+  if (threadIdx.x != 0) return;
+  double worst = 0.0;
+  bool inf = false;
+  for (int b = 0; b < B; ++b) {
+    if (den[b] == 0.0) {
+      if (num[b] != 0.0) inf = true;
+      continue;
+    }
+    const double q = num[b] / den[b];
+    if (q > worst || isnan(q)) worst = isnan(q) ? q : (isnan(worst) ? worst : q);
+  }
+  const double r = inf ? INFINITY : worst;
+  st->ratio = r;
+  st->nonfinite = isnan(r) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- kernels
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_dot2(const T* __restrict__ x0, const T* __restrict__ y0,
+                                                      const T* __restrict__ x1, const T* __restrict__ y1,
+                                                      int64_t len, int32_t B, double* partial) {
+  if (x1) {
+    reduce_pass<2>(len, B, partial, [&](int64_t i, int, double* acc) {
+      acc[0] += double(x0[i]) * double(y0[i]);
+      acc[1] += double(x1[i]) * double(y1[i]);
+    });
+  } else {
+    reduce_pass<1>(len, B, partial, [&](int64_t i, int, double* acc) { acc[0] += double(x0[i]) * double(y0[i]); });
+  }
+}
+
+__global__ void k_sum_partials(const double* partial, int nd, int32_t B, double* out) {
+  const int t = threadIdx.x;
+  if (t < nd * B) out[t] = col_total(partial, nd, t / B, B, t % B);
+}
+
+// z = M^-1 e (fp64 math, rounded to T), accumulate (z, e)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_rho(const T* __restrict__ inv, const T* __restrict__ e,
+                                                     int32_t n, int32_t B, double* partial) {
+  reduce_pass<1>(int64_t(n) * B, B, partial, [&](int64_t it, int b, double* acc) {
+    const int64_t node = it / B;
+    const T* m = inv + 9 * node;
+    const T* ev = e + 3 * node * B + b;
+    const double e0 = double(ev[0]), e1 = double(ev[B]), e2 = double(ev[2 * B]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const T z = static_cast<T>(double(m[3 * i]) * e0 + double(m[3 * i + 1]) * e1 + double(m[3 * i + 2]) * e2);
+      acc[0] += double(z) * double(ev[i * B]);
+    }
+  });
+}
+
+__global__ void k_rho_final(const double* partial, int32_t B, int first, double* rho_a, const double* rho_b,
+                            double* beta) {
+  const int b = threadIdx.x;
+  if (b >= B) return;
+  const double r = col_total(partial, 1, 0, B, b);
+  rho_a[b] = r;
+  beta[b] = first ? 0.0 : (rho_b[b] != 0.0 ? r / rho_b[b] : 0.0);  // pcg.hpp:74-80
+}
+
+// p = z + (T)beta p, z = M^-1 e (xpby_columns, vector_batch.hpp:86-97); first: p = z
+template <typename T>
+__global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, T* __restrict__ p, int32_t n,
+                            int32_t B, int first, const double* __restrict__ beta) {
+  const int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (it >= int64_t(n) * B) return;
+  const int64_t node = it / B;
+  const int b = static_cast<int>(it % B);
+  const T* m = inv + 9 * node;
+  const T* ev = e + 3 * node * B + b;
+  T* pv = p + 3 * node * B + b;
+  const double e0 = double(ev[0]), e1 = double(ev[B]), e2 = double(ev[2 * B]);
+  const T bt = static_cast<T>(beta[b]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const T z = static_cast<T>(double(m[3 * i]) * e0 + double(m[3 * i + 1]) * e1 + double(m[3 * i + 2]) * e2);
+    pv[i * B] = first ? z : z + bt * pv[i * B];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_gamma(const T* __restrict__ p, const T* __restrict__ q, int64_t len,
+                                                       int32_t B, double* partial) {
+  reduce_pass<3>(len, B, partial, [&](int64_t i, int, double* acc) {
+    const double a = double(p[i]), c = double(q[i]);
+    acc[0] += a * c;
+    acc[1] += a * a;
+    acc[2] += c * c;
+  });
+}
+
+// alpha with the reference's breakdown / stagnation rules (pcg.hpp:83-110)
+template <typename T>
+__global__ void k_gamma_final(const double* partial, int32_t B, const double* rho_a, double* rho_b,
+                              double* gamma, double* alpha, PcgStatus* st) {
+  __shared__ int stag, brk;
+  if (threadIdx.x == 0) {
+    stag = 0;
+    brk = INT32_MAX;
+  }
+  __syncthreads();
+  const int b = threadIdx.x;
+  if (b < B) {
+    const double g = col_total(partial, 3, 0, B, b);
+    gamma[b] = g;
+    double a = 0.0;
+    if (g > 0.0) {
+      a = rho_a[b] / g;
+    } else if (g == 0.0 && rho_a[b] == 0.0) {
+      a = 0.0;
+    } else {
+      const double pn = col_total(partial, 3, 1, B, b), qn = col_total(partial, 3, 2, B, b);
+      const double scale = sqrt(pn) * sqrt(qn);
+      const double eps16 = 16.0 * (sizeof(T) == 4 ? double(FLT_EPSILON) : DBL_EPSILON);
+      if (fabs(g) <= eps16 * scale) atomicExch(&stag, 1);
+      else atomicMin(&brk, b);
+      a = 0.0;
+    }
+    alpha[b] = a;
+  }
+  __syncthreads();
+  if (b < B && !stag && brk == INT32_MAX) rho_b[b] = rho_a[b];
+  if (threadIdx.x == 0) {
+    st->stagnated = stag;
+    st->breakdown_col = brk == INT32_MAX ? -1 : brk;
+  }
+}
+
+// e += (T)(-alpha) q ; u += (T)alpha p ; ||e||^2  (axpy_columns, vector_batch.hpp:72-83)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_update(T* __restrict__ e, T* __restrict__ u,
+                                                        const T* __restrict__ p, const T* __restrict__ q,
+                                                        int64_t len, int32_t B, const double* __restrict__ alpha,
+                                                        const PcgStatus* __restrict__ st, double* partial) {
+  const bool skip = st->stagnated || st->breakdown_col >= 0;
+  reduce_pass<1>(len, B, partial, [&](int64_t i, int b, double* acc) {
+    T ev = e[i];
+    if (!skip) {
+      const T a = static_cast<T>(alpha[b]);
+      const T na = static_cast<T>(-alpha[b]);
+      ev = ev + na * q[i];
+      e[i] = ev;
+      u[i] = u[i] + a * p[i];
+    }
+    acc[0] += double(ev) * double(ev);
+  });
+}
+
+__global__ void k_ratio_final(const double* partial, int32_t B, double* num, const double* den, PcgStatus* st) {
+  const int b = threadIdx.x;
+  if (b < B) num[b] = col_total(partial, 1, 0, B, b);
+  __syncthreads();
+  write_ratio(num, den, B, st);
+}
+
+// e = r - e (e holds A u); partials: ||r||^2, ||e||^2 (pcg.hpp:59-65)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_init(const T* __restrict__ r, T* __restrict__ e, int64_t len,
+                                                      int32_t B, double* partial) {
+  reduce_pass<2>(len, B, partial, [&](int64_t i, int, double* acc) {
+    const T rv = r[i];
+    const T ev = rv - e[i];
+    e[i] = ev;
+    acc[0] += double(rv) * double(rv);
+    acc[1] += double(ev) * double(ev);
+  });
+}
+
+__global__ void k_init_final(const double* partial, int32_t B, double* rn2, double* en2, PcgStatus* st) {
+  const int b = threadIdx.x;
+  if (b < B) {
+    rn2[b] = col_total(partial, 2, 0, B, b);
+    en2[b] = col_total(partial, 2, 1, B, b);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->stagnated = 0;
+    st->breakdown_col = -1;
+  }
+  write_ratio(en2, rn2, B, st);
+}
+
+// ---- outer CG (fp64) ----
+__global__ void __launch_bounds__(kRedThreads) k_true_res(const double* __restrict__ f, double* __restrict__ r,
+                                                          int64_t len, int32_t B, double* partial) {
+  reduce_pass<1>(len, B, partial, [&](int64_t i, int, double* acc) {
+    const double v = f[i] - r[i];
+    r[i] = v;
+    acc[0] += v * v;
+  });
+}
+
+__global__ void k_cg_beta(const double* partial, int32_t B, const double* gprev, double* beta) {
+  const int b = threadIdx.x;
+  if (b >= B) return;
+  const double zq = col_total(partial, 1, 0, B, b);
+  beta[b] = gprev[b] != 0.0 ? -zq / gprev[b] : 0.0;  // adaptive_cg.hpp:196-200
+}
+
+__global__ void k_xpby(const double* __restrict__ z, double* __restrict__ p, int64_t len, int32_t B, int first,
+                       const double* __restrict__ beta) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  p[i] = first ? z[i] : z[i] + beta[i % B] * p[i];
+}
+
+__global__ void k_cg_alpha(const double* partial, int32_t B, double* rho, double* gamma, double* gprev,
+                           double* alpha, PcgStatus* st) {
+  __shared__ int brk;
+  if (threadIdx.x == 0) brk = INT32_MAX;
+  __syncthreads();
+  const int b = threadIdx.x;
+  if (b < B) {
+    const double r = col_total(partial, 2, 0, B, b), g = col_total(partial, 2, 1, B, b);
+    rho[b] = r;
+    gamma[b] = g;
+    double a = 0.0;
+    if (g > 0.0) a = r / g;
+    else if (g == 0.0 && r == 0.0) a = 0.0;
+    else atomicMin(&brk, b);  // adaptive_cg.hpp:205-213
+    alpha[b] = a;
+    gprev[b] = g;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->stagnated = 0;
+    st->breakdown_col = brk == INT32_MAX ? -1 : brk;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ r, double* __restrict__ u,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ q, int64_t len, int32_t B,
+                                                           const double* __restrict__ alpha, double* partial) {
+  reduce_pass<1>(len, B, partial, [&](int64_t i, int b, double* acc) {
+    const double a = alpha[b];
+    const double rv = r[i] + (-a) * q[i];
+    r[i] = rv;
+    u[i] = u[i] + a * p[i];
+    acc[0] += rv * rv;
+  });
+}
+
+// ---- small operators ----
+template <typename T>
+__global__ void k_bj_apply(const T* __restrict__ inv, const T* __restrict__ r, T* __restrict__ z, int32_t n,
+                           int32_t B) {
+  const int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (it >= int64_t(n) * B) return;
+  const int64_t node = it / B;
+  const int b = static_cast<int>(it % B);
+  const T* m = inv + 9 * node;
+  const T* rv = r + 3 * node * B + b;
+  const double r0 = double(rv[0]), r1 = double(rv[B]), r2 = double(rv[2 * B]);
+  T* zv = z + 3 * node * B + b;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    zv[i * B] = static_cast<T>(double(m[3 * i]) * r0 + double(m[3 * i + 1]) * r1 + double(m[3 * i + 2]) * r2);
+}
+
+// one thread per (block row, case): 3 outputs, fp64 accumulation in the
+// reference's order a[b] += b0 u0 + b1 u1 + b2 u2 per stored block
+__global__ void k_bcsr(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                       const float* __restrict__ blocks, int32_t n, const float* __restrict__ u,
+                       float* __restrict__ f, int32_t B) {
+  const int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (it >= int64_t(n) * B) return;
+  const int32_t r = static_cast<int32_t>(it / B);
+  const int b = static_cast<int>(it % B);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int32_t e = __ldg(row_ptr + r); e < __ldg(row_ptr + r + 1); ++e) {
+    const float* blk = blocks + 9 * int64_t(e);
+    const float* uc = u + 3 * int64_t(__ldg(col_idx + e)) * B + b;
+    const double u0 = double(uc[0]), u1 = double(uc[B]), u2 = double(uc[2 * B]);
+    a0 += double(blk[0]) * u0 + double(blk[1]) * u1 + double(blk[2]) * u2;
+    a1 += double(blk[3]) * u0 + double(blk[4]) * u1 + double(blk[5]) * u2;
+    a2 += double(blk[6]) * u0 + double(blk[7]) * u1 + double(blk[8]) * u2;
+  }
+  float* fr = f + 3 * int64_t(r) * B + b;
+  fr[0] = static_cast<float>(a0);
+  fr[B] = static_cast<float>(a1);
+  fr[2 * B] = static_cast<float>(a2);
+}
+
+__global__ void k_cast_d2f(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = static_cast<float>(x[i]);
+}
+__global__ void k_cast_f2d(const float* __restrict__ x, double* __restrict__ y, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = static_cast<double>(x[i]);
+}
+__global__ void k_zero_masked(float* __restrict__ x, const uint8_t* __restrict__ mask, int64_t len, int32_t B) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < len && mask[i / B]) x[i] = 0.0f;
+}
+
+// out = 0 ; out += w * in per stored entry (float ops, no contraction)
+__global__ void k_p1_apply(const float* __restrict__ c, float* __restrict__ fine, const int32_t* __restrict__ ends,
+                           int32_t nv, int32_t nf, const uint8_t* __restrict__ mask, int32_t B) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t len = 3 * int64_t(nf) * B;
+  if (i >= len) return;
+  const int64_t dof = i / B;
+  const int64_t node = dof / 3;
+  const int64_t rem = i - node * 3 * B;  // axis * B + b
+  float v;
+  if (node < nv) {
+    v = c[i];
+  } else {
+    const int64_t k = node - nv;
+    const float a = c[3 * int64_t(ends[2 * k]) * B + rem];
+    const float bb = c[3 * int64_t(ends[2 * k + 1]) * B + rem];
+    v = __fadd_rn(__fmul_rn(0.5f, a), __fmul_rn(0.5f, bb));
+  }
+  fine[i] = (mask && mask[dof]) ? 0.0f : v;
+}
+
+__global__ void k_p1_restrict(const float* __restrict__ fine, float* __restrict__ coarse,
+                              const int32_t* __restrict__ t_ptr, const int32_t* __restrict__ t_idx, int32_t nv,
+                              const uint8_t* __restrict__ mask, int32_t B) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t len = 3 * int64_t(nv) * B;
+  if (i >= len) return;
+  const int64_t dof = i / B;
+  const int64_t node = dof / 3;
+  const int64_t rem = i - node * 3 * B;
+  float v = 0.0f + fine[i];  // fn = node itself first (weight 1)
+  for (int32_t k = t_ptr[node]; k < t_ptr[node + 1]; ++k)
+    v = __fadd_rn(v, __fmul_rn(0.5f, fine[3 * int64_t(t_idx[k]) * B + rem]));
+  coarse[i] = (mask && mask[dof]) ? 0.0f : v;
+}
+
+__global__ void k_p2_apply(const float* __restrict__ c, float* __restrict__ fine, const int32_t* __restrict__ agg,
+                           int32_t nf, const uint8_t* __restrict__ mask, int32_t B) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t len = 3 * int64_t(nf) * B;
+  if (i >= len) return;
+  const int64_t dof = i / B;
+  const int64_t node = dof / 3;
+  const int64_t rem = i - node * 3 * B;
+  const float v = 0.0f + c[3 * int64_t(agg[node]) * B + rem];
+  fine[i] = (mask && mask[dof]) ? 0.0f : v;
+}
+
+__global__ void k_p2_restrict(const float* __restrict__ fine, float* __restrict__ coarse,
+                              const int32_t* __restrict__ a_ptr, const int32_t* __restrict__ a_idx, int32_t nc,
+                              const uint8_t* __restrict__ mask, int32_t B) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t len = 3 * int64_t(nc) * B;
+  if (i >= len) return;
+  const int64_t dof = i / B;
+  const int64_t node = dof / 3;
+  const int64_t rem = i - node * 3 * B;
+  float v = 0.0f;
+  for (int32_t k = a_ptr[node]; k < a_ptr[node + 1]; ++k) v = __fadd_rn(v, fine[3 * int64_t(a_idx[k]) * B + rem]);
+  coarse[i] = (mask && mask[dof]) ? 0.0f : v;
+}
+
+void check_batch(int32_t B) {
+  if (B < 1 || B > kRedThreads) validation("batch must be in [1, 256]");
+}
+
+}  // namespace
+
+void Workspace::ensure(int32_t batch) {
+  partial.ensure(static_cast<size_t>(kRedBlocks) * 4 * batch);
+  if (!status.get()) {
+    status.alloc(1);
+    TS_CUDA(cudaMallocHost(&host_status, sizeof(PcgStatus)));
+  }
+}
+Workspace::~Workspace() {
+  if (host_status) cudaFreeHost(host_status);
+}
+
+template <typename T>
+void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int32_t batch, double* out,
+          Workspace& ws, cudaStream_t s) {
+  check_batch(batch);
+  ws.ensure(batch);
+  k_dot2<T><<<kRedBlocks, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch, ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_sum_partials<<<1, 512, 0, s>>>(ws.partial.get(), x1 ? 2 : 1, batch, out);
+  TS_CUDA_LAUNCH();
+}
+template void dot2<float>(const float*, const float*, const float*, const float*, int64_t, int32_t, double*,
+                          Workspace&, cudaStream_t);
+template void dot2<double>(const double*, const double*, const double*, const double*, int64_t, int32_t, double*,
+                           Workspace&, cudaStream_t);
+
+template <typename T>
+void pcg_rho(const T* inv, const T* e, int32_t n, int32_t B, bool first, const ColScalars& cs, Workspace& ws,
+             cudaStream_t s) {
+  k_rho<T><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, n, B, ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_rho_final<<<1, 256, 0, s>>>(ws.partial.get(), B, first ? 1 : 0, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+                                cs[ColScalars::BETA]);
+  TS_CUDA_LAUNCH();
+}
+
+template <typename T>
+void pcg_direction(const T* inv, const T* e, T* p, int32_t n, int32_t B, bool first, const ColScalars& cs,
+                   cudaStream_t s) {
+  k_direction<T><<<grid_for(int64_t(n) * B, 256), 256, 0, s>>>(inv, e, p, n, B, first ? 1 : 0,
+                                                               cs[ColScalars::BETA]);
+  TS_CUDA_LAUNCH();
+}
+
+template <typename T>
+void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
+               cudaStream_t s) {
+  k_gamma<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B, ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_gamma_final<T><<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+                                     cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+
+template <typename T>
+void pcg_update(T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
+                cudaStream_t s) {
+  k_update<T><<<kRedBlocks, kRedThreads, 0, s>>>(e, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
+                                                 ws.status.get(), ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_ratio_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::EN2], cs[ColScalars::RN2], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+
+template <typename T>
+void pcg_init(const T* r, T* e, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
+  k_init<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, e, 3 * int64_t(n) * B, B, ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_init_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RN2], cs[ColScalars::EN2], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+
+#define INST(T)                                                                                              \
+  template void pcg_rho<T>(const T*, const T*, int32_t, int32_t, bool, const ColScalars&, Workspace&,       \
+                           cudaStream_t);                                                                    \
+  template void pcg_direction<T>(const T*, const T*, T*, int32_t, int32_t, bool, const ColScalars&,         \
+                                 cudaStream_t);                                                              \
+  template void pcg_gamma<T>(const T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,           \
+                             cudaStream_t);                                                                  \
+  template void pcg_update<T>(T*, T*, const T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,  \
+                              cudaStream_t);                                                                 \
+  template void pcg_init<T>(const T*, T*, int32_t, int32_t, const ColScalars&, Workspace&, cudaStream_t);    \
+  template void bj_apply<T>(const T*, const T*, T*, int32_t, int32_t, cudaStream_t);
+template <typename T>
+void bj_apply(const T* inv, const T* r, T* z, int32_t n, int32_t B, cudaStream_t s) {
+  k_bj_apply<T><<<grid_for(int64_t(n) * B, 256), 256, 0, s>>>(inv, r, z, n, B);
+  TS_CUDA_LAUNCH();
+}
+INST(float)
+INST(double)
+#undef INST
+
+void cg_true_residual(const double* f, double* r, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
+                      cudaStream_t s) {
+  k_true_res<<<kRedBlocks, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B, ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_ratio_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+
+void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_t B, bool first,
+                  const ColScalars& cs, Workspace& ws, cudaStream_t s) {
+  const int64_t len = 3 * int64_t(n) * B;
+  if (!first) {
+    k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B, ws.partial.get());
+    TS_CUDA_LAUNCH();
+    k_cg_beta<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::GPREV], cs[ColScalars::BETA]);
+    TS_CUDA_LAUNCH();
+  }
+  k_xpby<<<grid_for(len, 256), 256, 0, s>>>(z, p, len, B, first ? 1 : 0, cs[ColScalars::BETA]);
+  TS_CUDA_LAUNCH();
+}
+
+void cg_alpha(const double* z, const double* r, const double* p, const double* q, int32_t n, int32_t B,
+              const ColScalars& cs, Workspace& ws, cudaStream_t s) {
+  k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B, ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_cg_alpha<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RHO_A], cs[ColScalars::GAMMA],
+                               cs[ColScalars::GPREV], cs[ColScalars::ALPHA], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+
+void cg_update(double* r, double* u, const double* p, const double* q, int32_t n, int32_t B, const ColScalars& cs,
+               Workspace& ws, cudaStream_t s) {
+  k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(r, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
+                                                 ws.partial.get());
+  TS_CUDA_LAUNCH();
+  k_ratio_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+
+void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
+                    float* f, int32_t B, cudaStream_t s) {
+  k_bcsr<<<grid_for(int64_t(n) * B, 128), 128, 0, s>>>(row_ptr, col_idx, blocks, n, u, f, B);
+  TS_CUDA_LAUNCH();
+}
+void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s) {
+  k_cast_d2f<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+  TS_CUDA_LAUNCH();
+}
+void cast_f2d(const float* x, double* y, int64_t n, cudaStream_t s) {
+  k_cast_f2d<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+  TS_CUDA_LAUNCH();
+}
+void zero_masked_f32(float* x, const uint8_t* mask, int64_t ndof, int32_t B, cudaStream_t s) {
+  if (!mask) return;
+  k_zero_masked<<<grid_for(ndof * B, 256), 256, 0, s>>>(x, mask, ndof * B, B);
+  TS_CUDA_LAUNCH();
+}
+void p1_apply(const float* coarse, float* fine, const int32_t* edge_ends, int32_t nv, int32_t nf,
+              const uint8_t* fine_mask, int32_t B, cudaStream_t s) {
+  k_p1_apply<<<grid_for(3 * int64_t(nf) * B, 256), 256, 0, s>>>(coarse, fine, edge_ends, nv, nf, fine_mask, B);
+  TS_CUDA_LAUNCH();
+}
+void p1_restrict(const float* fine, float* coarse, const int32_t* t_ptr, const int32_t* t_idx, int32_t nv,
+                 const uint8_t* coarse_mask, int32_t B, cudaStream_t s) {
+  k_p1_restrict<<<grid_for(3 * int64_t(nv) * B, 256), 256, 0, s>>>(fine, coarse, t_ptr, t_idx, nv, coarse_mask, B);
+  TS_CUDA_LAUNCH();
+}
+void p2_apply(const float* coarse, float* fine, const int32_t* agg, int32_t nf, const uint8_t* fine_mask, int32_t B,
+              cudaStream_t s) {
+  k_p2_apply<<<grid_for(3 * int64_t(nf) * B, 256), 256, 0, s>>>(coarse, fine, agg, nf, fine_mask, B);
+  TS_CUDA_LAUNCH();
+}
+void p2_restrict(const float* fine, float* coarse, const int32_t* a_ptr, const int32_t* a_idx, int32_t nc,
+                 const uint8_t* coarse_mask, int32_t B, cudaStream_t s) {
+  k_p2_restrict<<<grid_for(3 * int64_t(nc) * B, 256), 256, 0, s>>>(fine, coarse, a_ptr, a_idx, nc, coarse_mask, B);
+  TS_CUDA_LAUNCH();
+}
+
+}  // namespace tsg

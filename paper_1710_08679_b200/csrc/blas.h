@@ -1,0 +1,110 @@
+// blas.h — device vector / transfer / small-operator kernels of the solve path.
+// All vectors are [node][axis][case] with `batch` cases (vector_batch.hpp:12-28).
+#pragma once
+#include "ts_common.h"
+
+namespace tsg {
+
+// fixed reduction geometry: deterministic per-column fp64 sums
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+
+// Per-column solver scalars living on the device (one array of `batch` each).
+struct ColScalars {
+  DevBuf<double> buf;
+  int32_t batch = 0;
+  enum { RN2, EN2, RHO_A, RHO_B, BETA, GAMMA, ALPHA, PP, QQ, FN2, ZQ, GPREV, TMP, N_ };
+  void ensure(int32_t b) {
+    if (b != batch) {
+      buf.alloc(static_cast<size_t>(N_) * b);
+      batch = b;
+    }
+  }
+  double* operator[](int k) const { return buf.get() + static_cast<size_t>(k) * batch; }
+};
+
+// status read back by the host once per iteration
+struct PcgStatus {
+  double ratio;       // max_b num/den (pcg.hpp:32-42)
+  int stagnated;      // pcg.hpp:99-104
+  int breakdown_col;  // first column with (p,Ap) <= 0 and no stagnation, else -1
+  int nonfinite;
+  int pad;
+};
+
+struct Workspace {
+  DevBuf<double> partial;  // [kRedBlocks][4][batch]
+  DevBuf<PcgStatus> status;
+  PcgStatus* host_status = nullptr;  // pinned
+  void ensure(int32_t batch);
+  ~Workspace();
+};
+
+// ---- reductions ------------------------------------------------------------
+// out[b] = (x0,y0)_b and, when x1 != null, out[batch + b] = (x1,y1)_b; fp64 accumulation
+template <typename T>
+void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int32_t batch, double* out,
+          Workspace& ws, cudaStream_t s);
+
+// ---- inner PCG steps (pcg.hpp:52-124), T = float | double --------------------
+// rho_a = (M^-1 e, e); beta = first ? 0 : (rho_b != 0 ? rho_a / rho_b : 0)
+template <typename T>
+void pcg_rho(const T* inv, const T* e, int32_t n_nodes, int32_t batch, bool first, const ColScalars& cs,
+             Workspace& ws, cudaStream_t s);
+// p = M^-1 e + beta p  (first: p = M^-1 e)
+template <typename T>
+void pcg_direction(const T* inv, const T* e, T* p, int32_t n_nodes, int32_t batch, bool first,
+                   const ColScalars& cs, cudaStream_t s);
+// gamma = (p,q), plus ||p||^2, ||q||^2; alpha + stagnation/breakdown flags
+template <typename T>
+void pcg_gamma(const T* p, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,
+               cudaStream_t s);
+// unless stagnated/broken: e -= alpha q ; u += alpha p ; en2 = ||e||^2 ; ratio
+template <typename T>
+void pcg_update(T* e, T* u, const T* p, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs,
+                Workspace& ws, cudaStream_t s);
+// e = r - Au (Au in e on entry); rn2 = ||r||^2, en2 = ||e||^2, ratio
+template <typename T>
+void pcg_init(const T* r, T* e, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,
+              cudaStream_t s);
+
+// ---- outer CG steps (adaptive_cg.hpp:126-233), fp64 -------------------------
+// r = f - r (K u in r on entry); rn2 = ||r||^2 ; ratio vs fn2
+void cg_true_residual(const double* f, double* r, int32_t n_nodes, int32_t batch, const ColScalars& cs,
+                      Workspace& ws, cudaStream_t s);
+// beta = gprev != 0 ? -(z,q)/gprev : 0 ; p = z + beta p  (first: p = z)
+void cg_direction(const double* z, const double* q, double* p, int32_t n_nodes, int32_t batch, bool first,
+                  const ColScalars& cs, Workspace& ws, cudaStream_t s);
+// rho = (z,r), gamma = (p,q); alpha with breakdown check; gprev = gamma
+void cg_alpha(const double* z, const double* r, const double* p, const double* q, int32_t n_nodes,
+              int32_t batch, const ColScalars& cs, Workspace& ws, cudaStream_t s);
+// r -= alpha q ; u += alpha p ; rn2 ; ratio vs fn2
+void cg_update(double* r, double* u, const double* p, const double* q, int32_t n_nodes, int32_t batch,
+               const ColScalars& cs, Workspace& ws, cudaStream_t s);
+
+// ---- small operators ---------------------------------------------------------
+// z = M^-1 r per node, fp64 math rounded to T (block_jacobi.hpp:22-38)
+template <typename T>
+void bj_apply(const T* inv, const T* r, T* z, int32_t n_nodes, int32_t batch, cudaStream_t s);
+// f = A u, 3x3 float blocks, fp64 row accumulation (block_csr.hpp:33-69)
+void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
+                    const float* u, float* f, int32_t batch, cudaStream_t s);
+// casts (cast_batch, vector_batch.hpp:43-49)
+void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s);
+void cast_f2d(const float* x, double* y, int64_t n, cudaStream_t s);
+// zero constrained dofs (zero_masked, vector_batch.hpp:109-119)
+void zero_masked_f32(float* x, const uint8_t* mask, int64_t ndof, int32_t batch, cudaStream_t s);
+// geometric P1->P2: vertex rows copy, edge rows 0.5 a + 0.5 b (prolongation.hpp:25-40,67-98)
+void p1_apply(const float* coarse, float* fine, const int32_t* edge_ends, int32_t n_vert, int32_t n_fine,
+              const uint8_t* fine_mask, int32_t batch, cudaStream_t s);
+// restriction P1^T as a gather over the transpose in ascending fine order (bit-exact
+// with the reference's serial scatter, prolongation.hpp:44-61), then zero_masked
+void p1_restrict(const float* fine, float* coarse, const int32_t* t_ptr, const int32_t* t_idx,
+                 int32_t n_vert, const uint8_t* coarse_mask, int32_t batch, cudaStream_t s);
+// aggregation P2: fine = coarse[agg]; restrict = ascending-member sums
+void p2_apply(const float* coarse, float* fine, const int32_t* agg, int32_t n_fine, const uint8_t* fine_mask,
+              int32_t batch, cudaStream_t s);
+void p2_restrict(const float* fine, float* coarse, const int32_t* a_ptr, const int32_t* a_idx, int32_t n_coarse,
+                 const uint8_t* coarse_mask, int32_t batch, cudaStream_t s);
+
+}  // namespace tsg

@@ -1159,6 +1159,8 @@ void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStre
 }
 
 void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s) {
+  if (op.coef64.size() != 12 * static_cast<size_t>(op.n_elems))
+    validation("block jacobi: operator setup data released (level-set inner operators keep only device state)");
   DevBuf<double> diag(9 * static_cast<size_t>(op.n_nodes));
   DevBuf<double> c64;
   DevBuf<int32_t> bad(1);

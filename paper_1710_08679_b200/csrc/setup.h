@@ -1,0 +1,28 @@
+// setup.h — host-side hierarchy construction (see setup.cpp).
+#pragma once
+#include <vector>
+
+#include "ts_common.h"
+
+namespace tsg {
+
+// 3x3-block CSR with fp64 values (BlockCsrMatrix<double>, block_csr.hpp:16-70)
+struct BcsrD {
+  int32_t n = 0;
+  std::vector<int32_t> row_ptr, col_idx;
+  std::vector<double> blocks;  // [nnzb][9]
+};
+
+struct Aggregation {  // aggregation.hpp:13-17
+  std::vector<int32_t> agg_of_node;
+  int32_t n_aggregates = 0;
+};
+
+BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
+                    const std::vector<uint8_t>& mask1);
+Aggregation aggregate_p1(const BcsrD& a, int32_t target);
+BcsrD build_level2(const BcsrD& k1, const Aggregation& agg, const std::vector<uint8_t>& fine_mask);
+std::vector<uint8_t> coarse_mask(const Aggregation& agg, const std::vector<uint8_t>& fine_mask);
+std::vector<float> bcsr_block_jacobi_f32(const BcsrD& a);
+
+}  // namespace tsg

@@ -1,0 +1,508 @@
+// solver.cu — the device-resident solve path: inner PCG (pcg.hpp:52-124),
+// the 3-level mixed-precision multigrid preconditioner (adaptive_cg.hpp:80-120),
+// the fp64 flexible outer CG (adaptive_cg.hpp:126-233), solve / solve_pcge
+// (adaptive_cg.hpp:242-279) and the level-set construction
+// (build_solver_levels, adaptive_cg.hpp:39-67).
+//
+// All vectors live in HBM for the whole solve; the host only sequences
+// kernels and reads one 24-byte status record per iteration (the reference's
+// convergence test is a host-side max over columns, pcg.hpp:71,116-117).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "blas.h"
+#include "ebe.h"
+#include "setup.h"
+
+using tsg::ColScalars;
+using tsg::DevBuf;
+
+struct LevelVecs {
+  int32_t batch = 0;
+  DevBuf<double> r, q, z, p, scratch, f, u;  // outer (fp64); f/u used by the host-buffer entry
+  DevBuf<float> r0, u0, e0, p0, q0;          // level 0 (N nodes)
+  DevBuf<float> r1, u1, e1, p1, q1;          // level 1 (V nodes)
+  DevBuf<float> r2, u2, e2, p2, q2;          // level 2 (n2 nodes)
+};
+
+struct ts_levels {
+  int32_t n0 = 0, n1 = 0, n2 = 0;
+  std::unique_ptr<ts_ebe> outer, l0, l1;
+  DevBuf<int32_t> l2_row_ptr, l2_col_idx;
+  DevBuf<float> l2_blocks;
+  DevBuf<int32_t> p1_ends, p1t_ptr, p1t_idx, agg, p2t_ptr, p2t_idx;
+  DevBuf<float> m0, m1, m2;
+  DevBuf<uint8_t> mask0, mask1, mask2;
+  std::vector<int32_t> h_agg, h_rp2, h_ci2;
+  std::vector<float> h_bl2, h_m2;
+  std::vector<uint8_t> h_mask2;
+  double setup_s = 0.0;
+  LevelVecs v;
+  ColScalars cs;
+  tsg::Workspace ws;
+  std::mutex mu;
+};
+
+namespace tsg {
+namespace {
+
+using clk = std::chrono::steady_clock;
+double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
+
+const PcgStatus& read_status(Workspace& ws, cudaStream_t s) {
+  TS_CUDA(cudaMemcpyAsync(ws.host_status, ws.status.get(), sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
+  TS_CUDA(cudaStreamSynchronize(s));
+  return *ws.host_status;
+}
+
+struct InnerStats {
+  int iterations = 0;
+  bool converged = false;
+};
+
+// inner_pcg (pcg.hpp:52-124). A(x, y): y = A x on the stream.
+template <typename T, typename Op>
+InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t B, double tol, int max_iter, T* e,
+                     T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s) {
+  if (max_iter < 1) validation("inner_pcg: max_iter must be >= 1");
+  A(u, e);
+  pcg_init<T>(r, e, n, B, cs, ws, s);
+  InnerStats st;
+  const double tol2 = tol * tol;
+  double ratio = read_status(ws, s).ratio;
+  if (std::isnan(ratio)) fail(TS_ERR_NONFINITE, "inner_pcg: non-finite initial residual");
+  while (ratio > tol2 && st.iterations < max_iter) {
+    const bool first = st.iterations == 0;
+    pcg_rho<T>(inv, e, n, B, first, cs, ws, s);
+    pcg_direction<T>(inv, e, p, n, B, first, cs, s);
+    A(p, q);
+    pcg_gamma<T>(p, q, n, B, cs, ws, s);
+    pcg_update<T>(e, u, p, q, n, B, cs, ws, s);
+    const PcgStatus& ps = read_status(ws, s);
+    if (ps.breakdown_col >= 0)
+      fail(TS_ERR_BREAKDOWN, "inner_pcg: breakdown (p,Ap) <= 0 at iteration " + std::to_string(st.iterations + 1) +
+                                 ", column " + std::to_string(ps.breakdown_col));
+    if (ps.stagnated) break;
+    ++st.iterations;
+    ratio = ps.ratio;
+    if (std::isnan(ratio))
+      fail(TS_ERR_NONFINITE, "inner_pcg: non-finite residual at iteration " + std::to_string(st.iterations));
+  }
+  st.converged = ratio <= tol2;
+  return st;
+}
+
+void ensure_vecs(ts_levels& lv, int32_t B) {
+  LevelVecs& v = lv.v;
+  if (v.batch == B) return;
+  const size_t l0 = 3 * size_t(lv.n0) * B, l1 = 3 * size_t(lv.n1) * B, l2 = 3 * size_t(lv.n2) * B;
+  for (auto* b : {&v.r, &v.q, &v.z, &v.p, &v.scratch}) b->alloc(l0);
+  for (auto* b : {&v.r0, &v.u0, &v.e0, &v.p0, &v.q0}) b->alloc(l0);
+  for (auto* b : {&v.r1, &v.u1, &v.e1, &v.p1, &v.q1}) b->alloc(l1);
+  for (auto* b : {&v.r2, &v.u2, &v.e2, &v.p2, &v.q2}) b->alloc(l2);
+  v.f.release();
+  v.u.release();
+  v.batch = B;
+  lv.cs.ensure(B);
+  lv.ws.ensure(B);
+}
+
+// apply_multigrid_preconditioner (adaptive_cg.hpp:80-120)
+void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, double* z, int32_t B,
+                ts_solve_report& rep, cudaStream_t s) {
+  LevelVecs& v = lv.v;
+  const int64_t len0 = 3 * int64_t(lv.n0) * B;
+  cast_d2f(r, v.r0.get(), len0, s);
+  bj_apply<float>(lv.m0.get(), v.r0.get(), v.u0.get(), lv.n0, B, s);
+  p1_restrict(v.r0.get(), v.r1.get(), lv.p1t_ptr.get(), lv.p1t_idx.get(), lv.n1, lv.mask1.get(), B, s);
+  p1_restrict(v.u0.get(), v.u1.get(), lv.p1t_ptr.get(), lv.p1t_idx.get(), lv.n1, lv.mask1.get(), B, s);
+  p2_restrict(v.r1.get(), v.r2.get(), lv.p2t_ptr.get(), lv.p2t_idx.get(), lv.n2, lv.mask2.get(), B, s);
+  p2_restrict(v.u1.get(), v.u2.get(), lv.p2t_ptr.get(), lv.p2t_idx.get(), lv.n2, lv.mask2.get(), B, s);
+  const auto t0 = clk::now();
+  auto a2 = [&](const float* x, float* y) {
+    bcsr_apply_f32(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s);
+  };
+  const InnerStats s2 = inner_pcg<float>(a2, lv.m2.get(), v.r2.get(), v.u2.get(), lv.n2, B, cfg.level_tol[2],
+                                         cfg.level_max_iter[2], v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s);
+  const auto t1 = clk::now();
+  p2_apply(v.u2.get(), v.u1.get(), lv.agg.get(), lv.n1, lv.mask1.get(), B, s);
+  auto a1 = [&](const float* x, float* y) { ebe_apply(*lv.l1, x, y, B, s); };
+  const InnerStats s1 = inner_pcg<float>(a1, lv.m1.get(), v.r1.get(), v.u1.get(), lv.n1, B, cfg.level_tol[1],
+                                         cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s);
+  const auto t2 = clk::now();
+  p1_apply(v.u1.get(), v.u0.get(), lv.p1_ends.get(), lv.n1, lv.n0, lv.mask0.get(), B, s);
+  auto a0 = [&](const float* x, float* y) { ebe_apply(*lv.l0, x, y, B, s); };
+  const InnerStats s0 = inner_pcg<float>(a0, lv.m0.get(), v.r0.get(), v.u0.get(), lv.n0, B, cfg.level_tol[0],
+                                         cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s);
+  const auto t3 = clk::now();
+  rep.inner_iterations[2] += s2.iterations;
+  rep.inner_iterations[1] += s1.iterations;
+  rep.inner_iterations[0] += s0.iterations;
+  rep.time_inner_s[2] += secs(t0, t1);
+  rep.time_inner_s[1] += secs(t1, t2);
+  rep.time_inner_s[0] += secs(t2, t3);
+  cast_f2d(v.u0.get(), z, len0, s);
+}
+
+void report_reset(ts_solve_report& rep, int method, int prec) {
+  rep.converged = 0;
+  rep.outer_iterations = 0;
+  for (int i = 0; i < 3; ++i) {
+    rep.inner_iterations[i] = 0;
+    rep.time_inner_s[i] = 0.0;
+  }
+  rep.time_setup_s = rep.time_outer_s = rep.time_total_s = 0.0;
+  rep.history_count = 0;
+  rep.method = method;
+  rep.inner_precision = prec;
+}
+
+// run_outer_cg (adaptive_cg.hpp:126-233); vectors r,q,z,p,scratch of `lv.v`.
+template <typename Precond>
+void run_outer_cg(const ts_ebe& k, const double* f, double* u, int32_t B, double tol, int max_iter, int stride,
+                  Precond&& precond, LevelVecs& v, ColScalars& cs, Workspace& ws, ts_solve_report& rep,
+                  cudaStream_t s) {
+  const auto t_start = clk::now();
+  const int32_t n = k.n_nodes;
+  std::vector<double> fn2(B), rn2(B);
+  dot2<double>(f, f, nullptr, nullptr, 3 * int64_t(n), B, cs[ColScalars::FN2], ws, s);
+  TS_CUDA(cudaMemcpyAsync(fn2.data(), cs[ColScalars::FN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
+  auto true_residual = [&]() -> double {
+    ebe_apply(k, u, v.r.get(), B, s);
+    cg_true_residual(f, v.r.get(), n, B, cs, ws, s);
+    return read_status(ws, s).ratio;
+  };
+  auto finalize = [&]() {
+    TS_CUDA(cudaMemcpyAsync(rn2.data(), cs[ColScalars::RN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TS_CUDA(cudaStreamSynchronize(s));
+    rep.batch_size = B;
+    if (rep.final_rel_residual)
+      for (int b = 0; b < B; ++b)
+        rep.final_rel_residual[b] = fn2[b] > 0.0 ? std::sqrt(rn2[b] / fn2[b])
+                                                 : (rn2[b] > 0.0 ? std::numeric_limits<double>::infinity() : 0.0);
+    rep.time_total_s = secs(t_start, clk::now());
+    rep.time_outer_s = rep.time_total_s - rep.time_inner_s[0] - rep.time_inner_s[1] - rep.time_inner_s[2];
+  };
+  double ratio = true_residual();
+  const double tol2 = tol * tol;
+  rep.batch_size = B;
+  int it = 0;
+  bool r_is_true = true, first = true;
+  while (true) {
+    if (std::isnan(ratio)) fail(TS_ERR_NONFINITE, "solve: non-finite residual");
+    if (ratio <= tol2) {
+      if (r_is_true) break;
+      ratio = true_residual();
+      r_is_true = true;
+      if (ratio <= tol2) break;
+    }
+    if (it >= max_iter) {
+      if (!r_is_true) ratio = true_residual();
+      rep.outer_iterations = it;
+      rep.converged = 0;
+      finalize();
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%f", std::sqrt(ratio));
+      fail(TS_ERR_NO_CONVERGENCE, "solve: outer loop did not converge within " + std::to_string(max_iter) +
+                                      " iterations (max residual " + buf + ")");
+    }
+    precond(v.r.get(), v.z.get());
+    cg_direction(v.z.get(), v.q.get(), v.p.get(), n, B, first, cs, ws, s);
+    first = false;
+    ebe_apply(k, v.p.get(), v.q.get(), B, s);
+    cg_alpha(v.z.get(), v.r.get(), v.p.get(), v.q.get(), n, B, cs, ws, s);
+    cg_update(v.r.get(), u, v.p.get(), v.q.get(), n, B, cs, ws, s);
+    const PcgStatus& ps = read_status(ws, s);
+    if (ps.breakdown_col >= 0)
+      fail(TS_ERR_BREAKDOWN, "solve: breakdown (p,Kp) <= 0 at outer iteration " + std::to_string(it + 1) +
+                                 ", column " + std::to_string(ps.breakdown_col));
+    ratio = ps.ratio;
+    r_is_true = false;
+    ++it;
+    if (stride > 0 && it % stride == 0 && rep.history_count < rep.history_capacity) {
+      TS_CUDA(cudaMemcpyAsync(rn2.data(), cs[ColScalars::RN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
+      TS_CUDA(cudaStreamSynchronize(s));
+      const int32_t row = rep.history_count++;
+      if (rep.history_iter) rep.history_iter[row] = it;
+      if (rep.history)
+        for (int b = 0; b < B; ++b)
+          rep.history[size_t(row) * B + b] = fn2[b] > 0.0 ? std::sqrt(rn2[b] / fn2[b]) : 0.0;
+    }
+  }
+  rep.outer_iterations = it;
+  rep.converged = 1;
+  finalize();
+}
+
+void check_cfg(const ts_solver_config* c) {
+  const ts_status rc = ts_config_validate(c);
+  if (rc != TS_OK) fail(rc, ts_last_error());
+}
+
+// solve (adaptive_cg.hpp:242-263) on device buffers
+void solve_device(ts_levels& lv, const double* f, const double* u0, double* u, int32_t B, const ts_solver_config& cfg,
+                  ts_solve_report& rep, cudaStream_t s) {
+  check_cfg(&cfg);
+  if (B < 1 || B > kRedThreads) validation("solve: batch must be in [1, 256]");
+  ensure_vecs(lv, B);
+  dot2<double>(f, f, nullptr, nullptr, 3 * int64_t(lv.n0), B, lv.cs[ColScalars::FN2], lv.ws, s);
+  std::vector<double> fn2(B);
+  TS_CUDA(cudaMemcpyAsync(fn2.data(), lv.cs[ColScalars::FN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TS_CUDA(cudaStreamSynchronize(s));
+  bool any = false;
+  for (double x : fn2) any |= x != 0.0;
+  if (!any) validation("solve: right-hand side has no nonzero column");
+  report_reset(rep, 0, 32);
+  rep.time_setup_s = lv.setup_s;
+  if (u != u0)
+    TS_CUDA(cudaMemcpyAsync(u, u0, 3 * size_t(lv.n0) * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  auto precond = [&](const double* r, double* z) { mg_precond(lv, cfg, r, z, B, rep, s); };
+  run_outer_cg(*lv.outer, f, u, B, cfg.outer_tol, cfg.outer_max_iter, cfg.residual_history_stride, precond, lv.v,
+               lv.cs, lv.ws, rep, s);
+}
+
+std::vector<double> lame_per_element(const Mesh& m, int32_t n_mat, const double* x) {
+  std::vector<double> out(m.n_elems());
+  for (int32_t e = 0; e < m.n_elems(); ++e) {
+    const int32_t mid = m.material_id[e];
+    if (mid < 0 || mid >= n_mat)
+      validation("ebe: element " + std::to_string(e) + " references material " + std::to_string(mid) +
+                 " but only " + std::to_string(n_mat) + " defined");
+    out[e] = x[mid];
+  }
+  return out;
+}
+
+ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const double* mu, const uint8_t* dof_mask,
+                         const ts_solver_config& cfg) {
+  const auto t0 = clk::now();
+  check_cfg(&cfg);
+  require_device();
+  auto lv = std::make_unique<ts_levels>();
+  const int32_t N = m.n_nodes(), V = m.vertex_count;
+  std::vector<uint8_t> mask0 = dof_mask ? std::vector<uint8_t>(dof_mask, dof_mask + 3 * size_t(N)) : m.dirichlet_mask();
+  std::vector<uint8_t> mask1(mask0.begin(), mask0.begin() + 3 * size_t(V));
+  lv->n0 = N;
+  lv->n1 = V;
+  lv->outer.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 64));
+  lv->l0.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 32));
+  lv->l1.reset(ebe_create(m, 1, n_mat, lam, mu, mask1.data(), 32));
+  // geometric P1 (prolongation.hpp:67-98): edge endpoints (vmin, vmax) + transpose
+  {
+    static constexpr int ee[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
+    std::vector<int32_t> ends(2 * size_t(N - V), -1);
+    for (int32_t e = 0; e < m.n_elems(); ++e) {
+      const int32_t* t = m.tets10.data() + 10 * size_t(e);
+      for (int q = 0; q < 6; ++q) {
+        int32_t a = t[ee[q][0]], b = t[ee[q][1]];
+        if (a > b) std::swap(a, b);
+        const int32_t mid = t[4 + q];
+        if (mid < V) validation("geometric prolongation: edge node " + std::to_string(mid) + " is a vertex id");
+        if (a >= V || b >= V) validation("geometric prolongation: edge endpoints must be vertices");
+        ends[2 * size_t(mid - V)] = a;
+        ends[2 * size_t(mid - V) + 1] = b;
+      }
+    }
+    std::vector<int32_t> tptr(V + 1, 0);
+    for (int32_t k = 0; k < N - V; ++k) {
+      if (ends[2 * size_t(k)] < 0)
+        validation("geometric prolongation: edge node " + std::to_string(k + V) + " not present in edge map");
+      ++tptr[ends[2 * size_t(k)] + 1];
+      ++tptr[ends[2 * size_t(k) + 1] + 1];
+    }
+    for (int32_t i = 0; i < V; ++i) tptr[i + 1] += tptr[i];
+    std::vector<int32_t> tidx(tptr[V]), cur(tptr.begin(), tptr.end() - 1);
+    for (int32_t k = 0; k < N - V; ++k) {  // ascending fine node id
+      tidx[cur[ends[2 * size_t(k)]]++] = k + V;
+      tidx[cur[ends[2 * size_t(k) + 1]]++] = k + V;
+    }
+    lv->p1_ends.upload(ends);
+    lv->p1t_ptr.upload(tptr);
+    lv->p1t_idx.upload(tidx);
+  }
+  // K1 -> aggregation -> Galerkin level 2 (adaptive_cg.hpp:53-60)
+  const std::vector<double> lam_e = lame_per_element(m, n_mat, lam), mu_e = lame_per_element(m, n_mat, mu);
+  const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1);
+  Aggregation agg = aggregate_p1(k1, cfg.aggregate_target);
+  const BcsrD a2 = build_level2(k1, agg, mask1);
+  lv->n2 = agg.n_aggregates;
+  lv->h_mask2 = coarse_mask(agg, mask1);
+  lv->h_m2 = bcsr_block_jacobi_f32(a2);
+  lv->h_agg = agg.agg_of_node;
+  lv->h_rp2 = a2.row_ptr;
+  lv->h_ci2 = a2.col_idx;
+  lv->h_bl2.resize(a2.blocks.size());
+  for (size_t q = 0; q < a2.blocks.size(); ++q) lv->h_bl2[q] = static_cast<float>(a2.blocks[q]);
+  {
+    std::vector<int32_t> aptr(lv->n2 + 1, 0), amem(V);
+    for (int32_t r = 0; r < V; ++r) ++aptr[agg.agg_of_node[r] + 1];
+    for (int32_t i = 0; i < lv->n2; ++i) aptr[i + 1] += aptr[i];
+    std::vector<int32_t> cur(aptr.begin(), aptr.end() - 1);
+    for (int32_t r = 0; r < V; ++r) amem[cur[agg.agg_of_node[r]]++] = r;
+    lv->p2t_ptr.upload(aptr);
+    lv->p2t_idx.upload(amem);
+  }
+  lv->agg.upload(lv->h_agg);
+  lv->l2_row_ptr.upload(lv->h_rp2);
+  lv->l2_col_idx.upload(lv->h_ci2);
+  lv->l2_blocks.upload(lv->h_bl2);
+  lv->m2.upload(lv->h_m2);
+  lv->mask0.upload(mask0);
+  lv->mask1.upload(mask1);
+  lv->mask2.upload(lv->h_mask2);
+  lv->m0.alloc(9 * size_t(N));
+  lv->m1.alloc(9 * size_t(V));
+  ebe_block_jacobi(*lv->l0, lv->m0.get(), nullptr);
+  ebe_block_jacobi(*lv->l1, lv->m1.get(), nullptr);
+  // host setup copies no longer needed by the operators
+  for (ts_ebe* op : {lv->l0.get(), lv->l1.get()}) {  // outer keeps them for solve_pcge's block Jacobi
+    std::vector<double>().swap(op->coef64);
+  }
+  TS_CUDA(cudaDeviceSynchronize());
+  lv->setup_s = secs(t0, clk::now());
+  return lv.release();
+}
+
+}  // namespace
+}  // namespace tsg
+
+#define TS_API_BEGIN try {
+#define TS_API_END                                   \
+  }                                                  \
+  catch (const tsg::Error& e) {                      \
+    tsg::set_last_error(e.what());                   \
+    return e.code;                                   \
+  }                                                  \
+  catch (const std::exception& e) {                  \
+    tsg::set_last_error(e.what());                   \
+    return TS_ERR_VALIDATION;                        \
+  }                                                  \
+  return TS_OK;
+
+extern "C" {
+
+ts_status ts_levels_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda, const double* mu,
+                           const uint8_t* dof_mask, const ts_solver_config* cfg, ts_levels** out) {
+  TS_API_BEGIN
+  if (!mesh || !lambda || !mu || !cfg || !out) tsg::validation("levels: null argument");
+  *out = tsg::levels_create(mesh->m, n_materials, lambda, mu, dof_mask, *cfg);
+  TS_API_END
+}
+
+void ts_levels_destroy(ts_levels* lv) { delete lv; }
+
+ts_status ts_levels_sizes(const ts_levels* lv, int32_t* n0, int32_t* n1, int32_t* n2, int64_t* nnzb2) {
+  TS_API_BEGIN
+  if (!lv) tsg::validation("levels: null handle");
+  if (n0) *n0 = lv->n0;
+  if (n1) *n1 = lv->n1;
+  if (n2) *n2 = lv->n2;
+  if (nnzb2) *nnzb2 = static_cast<int64_t>(lv->h_ci2.size());
+  TS_API_END
+}
+
+ts_status ts_levels_export(const ts_levels* lv, int32_t* agg, int32_t* row_ptr2, int32_t* col_idx2, float* blocks2,
+                           uint8_t* mask2, float* m2_inv) {
+  TS_API_BEGIN
+  if (!lv) tsg::validation("levels: null handle");
+  if (agg) std::memcpy(agg, lv->h_agg.data(), lv->h_agg.size() * sizeof(int32_t));
+  if (row_ptr2) std::memcpy(row_ptr2, lv->h_rp2.data(), lv->h_rp2.size() * sizeof(int32_t));
+  if (col_idx2) std::memcpy(col_idx2, lv->h_ci2.data(), lv->h_ci2.size() * sizeof(int32_t));
+  if (blocks2) std::memcpy(blocks2, lv->h_bl2.data(), lv->h_bl2.size() * sizeof(float));
+  if (mask2) std::memcpy(mask2, lv->h_mask2.data(), lv->h_mask2.size());
+  if (m2_inv) std::memcpy(m2_inv, lv->h_m2.data(), lv->h_m2.size() * sizeof(float));
+  TS_API_END
+}
+
+ts_status ts_levels_operator(const ts_levels* lv, int32_t which, const ts_ebe** op) {
+  TS_API_BEGIN
+  if (!lv || !op) tsg::validation("levels: null argument");
+  if (which == 0) *op = lv->outer.get();
+  else if (which == 1) *op = lv->l0.get();
+  else if (which == 2) *op = lv->l1.get();
+  else tsg::validation("levels: operator index must be 0 (outer), 1 (level0) or 2 (level1)");
+  TS_API_END
+}
+
+ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
+                          const ts_solver_config* cfg, ts_solve_report* rep, void* stream) {
+  TS_API_BEGIN
+  if (!lv || !f || !u0 || !u_out || !cfg) tsg::validation("solve: null argument");
+  ts_solve_report local{};
+  ts_solve_report& r = rep ? *rep : local;
+  std::lock_guard<std::mutex> lock(lv->mu);
+  tsg::solve_device(*lv, f, u0, u_out, batch, *cfg, r, static_cast<cudaStream_t>(stream));
+  TS_API_END
+}
+
+ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
+                   const ts_solver_config* cfg, ts_solve_report* rep) {
+  TS_API_BEGIN
+  if (!lv || !f || !u0 || !u_out || !cfg) tsg::validation("solve: null argument");
+  if (batch < 1) tsg::validation("solve: batch must be >= 1");
+  ts_solve_report local{};
+  ts_solve_report& r = rep ? *rep : local;
+  std::lock_guard<std::mutex> lock(lv->mu);
+  const size_t bytes = 3 * size_t(lv->n0) * batch * sizeof(double);
+  DevBuf<double> df(bytes / 8), du(bytes / 8);
+  cudaStream_t s = nullptr;
+  TS_CUDA(cudaMemcpyAsync(df.get(), f, bytes, cudaMemcpyHostToDevice, s));
+  TS_CUDA(cudaMemcpyAsync(du.get(), u0, bytes, cudaMemcpyHostToDevice, s));
+  ts_status rc = TS_OK;
+  std::string msg;
+  try {
+    tsg::solve_device(*lv, df.get(), du.get(), du.get(), batch, *cfg, r, s);
+  } catch (const tsg::Error& e) {
+    rc = e.code;
+    msg = e.what();
+  }
+  if (rc == TS_OK || rc == TS_ERR_NO_CONVERGENCE)
+    TS_CUDA(cudaMemcpy(u_out, du.get(), bytes, cudaMemcpyDeviceToHost));
+  if (rc != TS_OK) tsg::fail(rc, msg);
+  TS_API_END
+}
+
+ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, double* u_out, int32_t batch, double tol,
+                        int32_t max_iter, ts_solve_report* rep) {
+  TS_API_BEGIN
+  if (!k || !f || !u0 || !u_out) tsg::validation("solve_pcge: null argument");
+  if (k->prec != 64 || k->order != 2) tsg::validation("solve_pcge: needs the 64-bit second-order operator");
+  if (batch < 1 || batch > tsg::kRedThreads) tsg::validation("solve_pcge: batch must be in [1, 256]");
+  ts_solve_report local{};
+  ts_solve_report& r = rep ? *rep : local;
+  tsg::report_reset(r, 1, 64);
+  const int32_t n = k->n_nodes;
+  const size_t len = 3 * size_t(n) * batch;
+  LevelVecs v;
+  for (auto* b : {&v.r, &v.q, &v.z, &v.p, &v.scratch, &v.f, &v.u}) b->alloc(len);
+  ColScalars cs;
+  cs.ensure(batch);
+  tsg::Workspace ws;
+  ws.ensure(batch);
+  DevBuf<double> m64(9 * size_t(n));
+  cudaStream_t s = nullptr;
+  tsg::ebe_block_jacobi(*k, m64.get(), s);
+  TS_CUDA(cudaMemcpyAsync(v.f.get(), f, len * sizeof(double), cudaMemcpyHostToDevice, s));
+  TS_CUDA(cudaMemcpyAsync(v.u.get(), u0, len * sizeof(double), cudaMemcpyHostToDevice, s));
+  auto precond = [&](const double* rr, double* z) { tsg::bj_apply<double>(m64.get(), rr, z, n, batch, s); };
+  ts_status rc = TS_OK;
+  std::string msg;
+  try {
+    tsg::run_outer_cg(*k, v.f.get(), v.u.get(), batch, tol, max_iter, 0, precond, v, cs, ws, r, s);
+  } catch (const tsg::Error& e) {
+    rc = e.code;
+    msg = e.what();
+  }
+  if (rc == TS_OK || rc == TS_ERR_NO_CONVERGENCE)
+    TS_CUDA(cudaMemcpy(u_out, v.u.get(), len * sizeof(double), cudaMemcpyDeviceToHost));
+  if (rc != TS_OK) tsg::fail(rc, msg);
+  TS_API_END
+}
+
+}  // extern "C"

@@ -301,7 +301,7 @@ class EbeOperator:
                  _borrowed=None):
         self._own = _borrowed is None
         if _borrowed is not None:
-            self._h = _borrowed
+            self._h = _borrowed if isinstance(_borrowed, C.c_void_p) else C.c_void_p(_borrowed)
         else:
             lam, mu = _lame(materials)
             mk = None if dof_mask is None or len(dof_mask) == 0 else np.ascontiguousarray(dof_mask, np.uint8)
@@ -367,3 +367,106 @@ class EbeOperator:
                 lib.ts_ebe_destroy(self._h)
             except Exception:
                 pass
+
+
+# ------------------------------------------------------------------ solver
+class SolverLevels:
+    """SolverLevels (adaptive_cg.hpp:27-37) built on the device by
+    build_solver_levels (adaptive_cg.hpp:39-67)."""
+
+    def __init__(self, handle, mesh: Mesh):
+        self._h = handle
+        self.mesh = mesh
+        n0, n1, n2, nz = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        _ck(lib.ts_levels_sizes(self._h, C.byref(n0), C.byref(n1), C.byref(n2), C.byref(nz)))
+        self.n0, self.n1, self.n2, self.nnzb2 = n0.value, n1.value, n2.value, nz.value
+        ops = []
+        for which in range(3):
+            h = C.c_void_p()
+            _ck(lib.ts_levels_operator(self._h, which, C.byref(h)))
+            ops.append(EbeOperator(None, 0, None, _borrowed=h))
+        self.outer, self.level0, self.level1 = ops
+
+    def export(self) -> dict:
+        """Setup introspection: aggregation, level-2 Galerkin matrix, masks, M2."""
+        agg = np.zeros(self.n1, np.int32)
+        rp = np.zeros(self.n2 + 1, np.int32)
+        ci = np.zeros(self.nnzb2, np.int32)
+        bl = np.zeros((self.nnzb2, 9), np.float32)
+        mk = np.zeros(3 * self.n2, np.uint8)
+        m2 = np.zeros((self.n2, 9), np.float32)
+        _ck(lib.ts_levels_export(self._h, _p(agg), _p(rp), _p(ci), _p(bl), _p(mk), _p(m2)))
+        return dict(agg=agg, row_ptr2=rp, col_idx2=ci, blocks2=bl, mask2=mk, m2=m2)
+
+    def __del__(self):
+        try:
+            # borrowed operators must not outlive the level set
+            for op in (self.outer, self.level0, self.level1):
+                op._own = False
+            lib.ts_levels_destroy(self._h)
+        except Exception:
+            pass
+
+
+def build_solver_levels(mesh: Mesh, materials, dof_mask=None, cfg: SolverConfig | None = None,
+                        workers: int = 1) -> SolverLevels:
+    """build_solver_levels (adaptive_cg.hpp:39-67); dof_mask None -> dirichlet_mask(mesh)."""
+    cfg = cfg or SolverConfig()
+    lam, mu = _lame(materials)
+    mk = None if dof_mask is None else np.ascontiguousarray(dof_mask, np.uint8)
+    c = cfg.to_c()
+    h = C.c_void_p()
+    _ck(lib.ts_levels_create(mesh._h, len(lam), _p(lam), _p(mu), _p(mk), C.byref(c), C.byref(h)))
+    return SolverLevels(h, mesh)
+
+
+@dataclass
+class CrustModel:
+    """CrustModel (model.hpp:14-19)."""
+
+    mesh: Mesh
+    materials: list
+    mask: np.ndarray
+    levels: SolverLevels
+
+
+def build_crust_model(mesh: Mesh, materials, cfg: SolverConfig | None = None, workers: int = 1) -> CrustModel:
+    """build_crust_model (model.hpp:21-29)."""
+    mask = mesh.dirichlet_mask()
+    return CrustModel(mesh, list(materials), mask, build_solver_levels(mesh, materials, mask, cfg, workers))
+
+
+def solve(levels: SolverLevels, f, u0, cfg: SolverConfig | None = None, history: int = 4096):
+    """solve (adaptive_cg.hpp:242-263). f, u0: (3N, batch) numpy (host path) or
+    CUDA float64 tensors (device path). Returns (u, SolveReport)."""
+    cfg = cfg or SolverConfig()
+    c = cfg.to_c()
+    batch = int(f.shape[1])
+    rb = _ReportBuf(batch, history if cfg.residual_history_stride > 0 else 0)
+    if _is_torch(f):
+        u = torch.empty_like(f)
+        rc = lib.ts_solve_device(levels._h, C.c_void_p(f.data_ptr()), C.c_void_p(u0.data_ptr()),
+                                 C.c_void_p(u.data_ptr()), batch, C.byref(c), C.byref(rb.c), _stream())
+    else:
+        f = np.ascontiguousarray(f, np.float64)
+        u0 = np.ascontiguousarray(u0, np.float64)
+        if f.shape != u0.shape:
+            raise ValidationError("solve: initial guess shape mismatch")
+        u = np.empty_like(f)
+        rc = lib.ts_solve(levels._h, _p(f), _p(u0), _p(u), batch, C.byref(c), C.byref(rb.c))
+    rep = rb.report(cfg.residual_history_stride)
+    _ck(rc, rep)
+    return u, rep
+
+
+def solve_pcge(k: EbeOperator, f, u0, tol: float, max_iter: int):
+    """solve_pcge (adaptive_cg.hpp:267-279): 64-bit CG + 3x3 block Jacobi."""
+    f = np.ascontiguousarray(f, np.float64)
+    u0 = np.ascontiguousarray(u0, np.float64)
+    batch = int(f.shape[1])
+    rb = _ReportBuf(batch, 0)
+    u = np.empty_like(f)
+    rc = lib.ts_solve_pcge(k._h, _p(f), _p(u0), _p(u), batch, tol, max_iter, C.byref(rb.c))
+    rep = rb.report(0)
+    _ck(rc, rep)
+    return u, rep
