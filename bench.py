@@ -111,6 +111,23 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def max_over_ranks(vals, device="cpu"):
+    """Max of each value over all ranks (the step time of a multi-GPU run is the
+    slowest rank's). Identity when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(v) for v in vals]
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def whole_job_gbps(world, alg_bytes_per_rank, step_ms):
+    """value = bytes processed by ALL ranks / the (max-over-ranks) step time."""
+    return world * alg_bytes_per_rank / (step_ms * 1e-3) / 1e9
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -136,7 +153,7 @@ def run_reference(args, world, rank):
     lam = [rho * (vp * vp - 2 * vs * vs) for vp, vs, rho in TWO_LAYER]
     mu = [rho * vs * vs for vp, vs, rho in TWO_LAYER]
     cores = ref.hw_threads()
-    r, prec = args.r, args.prec
+    r, prec = args.cases, args.prec
     steps = max(1, args.steps)
     sec, _ = ref.time_ebe_apply_box(ext, div, ifs, 1, 2, lam, mu, prec, cores, r, steps)
     E = 6 * cells[0] * cells[1] * cells[2]
@@ -172,7 +189,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cells", type=int, nargs=3, default=[82, 123, 41])
-    ap.add_argument("--r", type=int, default=16)
+    ap.add_argument("--cases", type=int, default=16, help="load cases r per GPU")
     ap.add_argument("--prec", type=int, default=32, choices=[32, 64])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
@@ -212,7 +229,7 @@ def main():
     op.set_timing(True)
     E, N = op.n_elements(), op.n_nodes()
     log(f"[rank {rank}] mesh {cells}: {E} tet10, {N} nodes ({3 * N} dof), setup {time.time() - t0:.1f}s")
-    r, s = args.r, args.prec // 8
+    r, s = args.cases, args.prec // 8
     B = alg_bytes(E, N, r, s)
     dt = torch.float32 if args.prec == 32 else torch.float64
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
@@ -241,14 +258,8 @@ def main():
             kernel_ms.append(op.last_kernel_ms())
         ev1.record(stream)
         barrier()
-    step_ms = ev0.elapsed_time(ev1) / args.steps
-    kms = float(np.mean(kernel_ms))
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([step_ms, kms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms, kms = float(t[0]), float(t[1])
-    value = world * B / (step_ms * 1e-3) / 1e9
+    step_ms, kms = max_over_ranks([ev0.elapsed_time(ev1) / args.steps, float(np.mean(kernel_ms))], "cuda")
+    value = whole_job_gbps(world, B, step_ms)
 
     # ---- end to end through the C ABI with pinned host buffers
     uh = torch.empty(u.shape, dtype=dt, pin_memory=True)
@@ -263,13 +274,8 @@ def main():
     for _ in range(e2e_steps):
         op.apply(uh_np, fh_np)  # ts_ebe_apply_host: H2D u, apply, D2H f
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - te) * 1e3 / e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t[0])
-    e2e_val = world * B / (e2e_ms * 1e-3) / 1e9
+    e2e_ms = max_over_ranks([(time.perf_counter() - te) * 1e3 / e2e_steps], "cuda")[0]
+    e2e_val = whole_job_gbps(world, B, e2e_ms)
     fd = torch.from_numpy(fh_np).cuda().double()
     ok = bool(torch.isfinite(fd).all()) and float((fd - f.double()).norm() / f.double().norm()) < 1e-5
 

@@ -1,0 +1,456 @@
+// tetsolve_b200/tetsolve.hpp — drop-in C++ mirror of the reference solve-path
+// interface (/root/reference/proj/include/tetsolve, namespace tetsolve), backed
+// by libtsgpu.so (include/tsgpu.h). A reference user replaces
+//   #include "tetsolve/adaptive_cg.hpp" / "tetsolve/model.hpp"
+// with
+//   #include "tetsolve_b200/tetsolve.hpp"
+// and links -ltsgpu. Types, signatures, ownership (value types, host
+// VectorBatch in/out) and exceptions follow the reference; each symbol cites
+// the reference declaration it replaces. All arithmetic runs on the GPU.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../tsgpu.h"
+
+namespace tetsolve {
+
+// ------------------------------------------------------------ errors.hpp:9-31
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+class ValidationError : public Error {
+ public:
+  explicit ValidationError(const std::string& m) : Error(m) {}
+};
+class SolverError : public Error {
+ public:
+  explicit SolverError(const std::string& m) : Error(m) {}
+};
+class DeviceError : public Error {  // no reference counterpart: CUDA failure / no device
+ public:
+  explicit DeviceError(const std::string& m) : Error(m) {}
+};
+
+// ---------------------------------------------------------- geometry / material
+using Vec3 = std::array<double, 3>;  // geometry.hpp:8
+
+struct Material {  // material.hpp:14-20
+  double vp = 0.0, vs = 0.0, rho = 0.0, lambda = 0.0, mu = 0.0;
+};
+
+// ------------------------------------------------------- solver_config.hpp:16-116
+struct InnerLoopConfig {
+  double tol = 0.1;
+  int max_iter = 30;
+};
+
+struct SolverConfig {
+  double outer_tol = 1e-8;
+  int outer_max_iter = 5000;
+  InnerLoopConfig level0 = {0.1, 30};
+  InnerLoopConfig level1 = {0.05, 300};
+  InnerLoopConfig level2 = {0.025, 3000};
+  int32_t batch_size = 16;
+  int32_t aggregate_target = 8;
+  int residual_history_stride = 1;
+
+  ts_solver_config to_c() const {
+    ts_solver_config c;
+    c.outer_tol = outer_tol;
+    c.outer_max_iter = outer_max_iter;
+    c.level_tol[0] = level0.tol;
+    c.level_tol[1] = level1.tol;
+    c.level_tol[2] = level2.tol;
+    c.level_max_iter[0] = level0.max_iter;
+    c.level_max_iter[1] = level1.max_iter;
+    c.level_max_iter[2] = level2.max_iter;
+    c.batch_size = batch_size;
+    c.aggregate_target = aggregate_target;
+    c.residual_history_stride = residual_history_stride;
+    return c;
+  }
+  void validate() const;
+};
+
+struct SolveReport {
+  bool converged = false;
+  int residual_history_stride = 0;
+  int outer_iterations = 0;
+  long inner_iterations[3] = {0, 0, 0};
+  std::vector<double> final_rel_residual;
+  std::vector<std::pair<int, std::vector<double>>> residual_history;
+  double time_setup_s = 0.0, time_outer_s = 0.0;
+  double time_inner_s[3] = {0.0, 0.0, 0.0};
+  double time_total_s = 0.0;
+  int32_t batch_size = 0;
+  std::string method = "amg";
+  std::string inner_precision = "float32";
+  double max_final_residual() const {
+    double m = 0.0;
+    for (double v : final_rel_residual) m = m > v ? m : v;
+    return m;
+  }
+};
+
+class ConvergenceError : public SolverError {
+ public:
+  ConvergenceError(const std::string& msg, SolveReport rep) : SolverError(msg), report(std::move(rep)) {}
+  SolveReport report;
+};
+
+namespace detail {
+inline void check(ts_status rc) {
+  if (rc == TS_OK) return;
+  const std::string msg = ts_last_error();
+  switch (rc) {
+    case TS_ERR_VALIDATION: throw ValidationError(msg);
+    case TS_ERR_BREAKDOWN:
+    case TS_ERR_NONFINITE: throw SolverError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+}  // namespace detail
+
+inline void SolverConfig::validate() const {
+  const ts_solver_config c = to_c();
+  detail::check(ts_config_validate(&c));
+}
+
+inline Material material_from_wavespeeds(double vp, double vs, double rho) {  // material.hpp:22-34
+  Material m;
+  m.vp = vp;
+  m.vs = vs;
+  m.rho = rho;
+  detail::check(ts_material_from_wavespeeds(vp, vs, rho, &m.lambda, &m.mu));
+  return m;
+}
+
+// ------------------------------------------------------------- mesh.hpp:19-156
+struct DirichletBc {
+  int32_t node = 0;
+  int8_t axis = 0;
+};
+
+struct Mesh {  // vertices first; tets10 = 4 vertices + 6 edge nodes
+  std::vector<Vec3> coords;
+  std::vector<std::array<int32_t, 10>> tets10;
+  std::vector<std::array<int32_t, 4>> tets4;
+  std::vector<int32_t> material_id;
+  std::map<std::pair<int32_t, int32_t>, int32_t> edge_map;
+  int32_t vertex_count = 0;
+  std::vector<DirichletBc> dirichlet;
+  int32_t node_count() const { return static_cast<int32_t>(coords.size()); }
+  int32_t element_count() const { return static_cast<int32_t>(tets10.size()); }
+};
+
+inline std::vector<uint8_t> dirichlet_mask(const Mesh& m) {  // mesh.hpp:150-154
+  std::vector<uint8_t> mask(3 * static_cast<size_t>(m.node_count()), 0);
+  for (const auto& bc : m.dirichlet) mask[3 * static_cast<size_t>(bc.node) + bc.axis] = 1;
+  return mask;
+}
+
+enum class FixedBoundary { none, bottom_and_sides, all_clamped };  // box_mesh.hpp:13-17
+
+struct BoxMeshSpec {  // box_mesh.hpp:23-28
+  Vec3 extents = {1.0, 1.0, 1.0};
+  std::array<int32_t, 3> divisions = {1, 1, 1};
+  std::vector<double> layer_interfaces;
+  FixedBoundary fixed_boundary = FixedBoundary::bottom_and_sides;
+};
+
+namespace detail {
+struct MeshHandle {
+  ts_mesh* h = nullptr;
+  explicit MeshHandle(const Mesh& m) {
+    std::vector<double> c(3 * m.coords.size());
+    for (size_t i = 0; i < m.coords.size(); ++i)
+      for (int k = 0; k < 3; ++k) c[3 * i + k] = m.coords[i][k];
+    std::vector<int32_t> t(10 * m.tets10.size());
+    for (size_t e = 0; e < m.tets10.size(); ++e)
+      for (int a = 0; a < 10; ++a) t[10 * e + a] = m.tets10[e][a];
+    std::vector<int32_t> bn(m.dirichlet.size());
+    std::vector<int8_t> ba(m.dirichlet.size());
+    for (size_t i = 0; i < m.dirichlet.size(); ++i) {
+      bn[i] = m.dirichlet[i].node;
+      ba[i] = m.dirichlet[i].axis;
+    }
+    check(ts_mesh_from_arrays(m.node_count(), m.vertex_count, c.data(), m.element_count(), t.data(),
+                              m.material_id.data(), static_cast<int32_t>(bn.size()), bn.data(), ba.data(), &h));
+  }
+  ~MeshHandle() { ts_mesh_destroy(h); }
+  MeshHandle(const MeshHandle&) = delete;
+  MeshHandle& operator=(const MeshHandle&) = delete;
+};
+
+inline std::pair<std::vector<double>, std::vector<double>> lame(const std::vector<Material>& mats) {
+  std::vector<double> l(mats.size()), m(mats.size());
+  for (size_t i = 0; i < mats.size(); ++i) {
+    l[i] = mats[i].lambda;
+    m[i] = mats[i].mu;
+  }
+  return {l, m};
+}
+}  // namespace detail
+
+// generate_box_mesh (box_mesh.hpp:55-157): identical node numbering
+inline Mesh generate_box_mesh(const BoxMeshSpec& spec) {
+  ts_mesh* h = nullptr;
+  detail::check(ts_box_mesh(spec.extents.data(), spec.divisions.data(),
+                            static_cast<int32_t>(spec.layer_interfaces.size()), spec.layer_interfaces.data(),
+                            static_cast<int32_t>(spec.fixed_boundary), &h));
+  int32_t nn, nv, ne, nbc;
+  ts_mesh_sizes(h, &nn, &nv, &ne, &nbc);
+  std::vector<double> c(3 * size_t(nn));
+  std::vector<int32_t> t(10 * size_t(ne)), mat(ne), bn(nbc);
+  std::vector<int8_t> ba(nbc);
+  ts_mesh_export(h, c.data(), t.data(), mat.data(), bn.data(), ba.data());
+  ts_mesh_destroy(h);
+  Mesh m;
+  m.vertex_count = nv;
+  m.coords.resize(nn);
+  for (int32_t i = 0; i < nn; ++i) m.coords[i] = {c[3 * size_t(i)], c[3 * size_t(i) + 1], c[3 * size_t(i) + 2]};
+  m.tets10.resize(ne);
+  m.tets4.resize(ne);
+  static constexpr int ee[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
+  for (int32_t e = 0; e < ne; ++e) {
+    for (int a = 0; a < 10; ++a) m.tets10[e][a] = t[10 * size_t(e) + a];
+    for (int a = 0; a < 4; ++a) m.tets4[e][a] = t[10 * size_t(e) + a];
+    for (int q = 0; q < 6; ++q) {
+      int32_t a = m.tets10[e][ee[q][0]], b = m.tets10[e][ee[q][1]];
+      if (a > b) std::swap(a, b);
+      m.edge_map[{a, b}] = m.tets10[e][4 + q];
+    }
+  }
+  m.material_id = std::move(mat);
+  for (int32_t i = 0; i < nbc; ++i) m.dirichlet.push_back({bn[i], ba[i]});
+  return m;
+}
+
+// ------------------------------------------------------- vector_batch.hpp:15-34
+template <typename T>
+struct VectorBatch {
+  int32_t n_nodes = 0;
+  int32_t batch = 0;
+  std::vector<T> data;
+  VectorBatch() = default;
+  VectorBatch(int32_t nodes, int32_t b) : n_nodes(nodes), batch(b) {
+    data.assign(static_cast<size_t>(3) * nodes * b, T(0));
+  }
+  int64_t n_dofs() const { return static_cast<int64_t>(3) * n_nodes; }
+  T& at(int64_t dof, int32_t b) { return data[dof * batch + b]; }
+  T at(int64_t dof, int32_t b) const { return data[dof * batch + b]; }
+  void set_zero() { std::memset(data.data(), 0, data.size() * sizeof(T)); }
+};
+using VectorBatch64 = VectorBatch<double>;
+using VectorBatch32 = VectorBatch<float>;
+
+template <typename T>
+struct BlockJacobi {  // block_jacobi.hpp:15-39 (host copy of the inverse blocks)
+  std::vector<std::array<T, 9>> inv_blocks;
+  int32_t n_nodes() const { return static_cast<int32_t>(inv_blocks.size()); }
+};
+
+// ----------------------------------------------------- ebe_operator.hpp:29-226
+template <typename T>
+class EbeOperator {
+ public:
+  EbeOperator() = default;
+  // EbeOperator(mesh, order, materials, dof_mask, workers) (ebe_operator.hpp:35-36);
+  // `workers` is accepted and ignored: the device sweep is order-independent.
+  EbeOperator(const Mesh& mesh, int order, const std::vector<Material>& materials, std::vector<uint8_t> dof_mask,
+              int workers = 1)
+      : order_(order), mask_(std::move(dof_mask)) {
+    (void)workers;
+    detail::MeshHandle mh(mesh);
+    auto [l, m] = detail::lame(materials);
+    ts_ebe* h = nullptr;
+    detail::check(ts_ebe_create(mh.h, order, static_cast<int32_t>(l.size()), l.data(), m.data(),
+                                mask_.empty() ? nullptr : mask_.data(), sizeof(T) == 4 ? 32 : 64, &h));
+    op_ = std::shared_ptr<ts_ebe>(h, ts_ebe_destroy);
+    int32_t nn, ne;
+    ts_ebe_info(h, &nn, &ne, nullptr, nullptr);
+    n_nodes_ = nn;
+    n_elems_ = ne;
+    conn_.resize(static_cast<size_t>(nodes_per_element()) * ne);
+    for (int32_t e = 0; e < ne; ++e)
+      for (int a = 0; a < nodes_per_element(); ++a)
+        conn_[static_cast<size_t>(nodes_per_element()) * e + a] = mesh.tets10[e][a];
+  }
+  // non-owning view of an operator inside a SolverLevels
+  EbeOperator(std::shared_ptr<ts_ebe> op, int32_t n_nodes, int32_t n_elems, int order)
+      : op_(std::move(op)), order_(order), n_nodes_(n_nodes), n_elems_(n_elems) {}
+
+  int32_t n_nodes() const { return n_nodes_; }
+  int32_t n_elements() const { return n_elems_; }
+  int order() const { return order_; }
+  int nodes_per_element() const { return order_ == 1 ? 4 : 10; }
+  const std::vector<uint8_t>& mask() const { return mask_; }
+  int32_t element_node(int32_t e, int a) const { return conn_[static_cast<size_t>(nodes_per_element()) * e + a]; }
+
+  // f = A u for all batch columns (ebe_operator.hpp:90-134): host buffers in/out
+  void apply(const VectorBatch<T>& u, VectorBatch<T>& f) const {
+    if (u.n_nodes != n_nodes_) throw ValidationError("ebe apply: dimension mismatch");
+    if (f.n_nodes != u.n_nodes || f.batch != u.batch) f = VectorBatch<T>(u.n_nodes, u.batch);
+    detail::check(ts_ebe_apply_host(op_.get(), u.data.data(), f.data.data(), u.batch));
+  }
+  // device-pointer entry for callers that keep vectors in HBM
+  void apply_device(const T* u, T* f, int32_t batch, void* stream = nullptr) const {
+    detail::check(ts_ebe_apply(op_.get(), u, f, batch, stream));
+  }
+  const ts_ebe* handle() const { return op_.get(); }
+
+ private:
+  std::shared_ptr<ts_ebe> op_;
+  int order_ = 2;
+  int32_t n_nodes_ = 0, n_elems_ = 0;
+  std::vector<uint8_t> mask_;
+  std::vector<int32_t> conn_;
+};
+
+// extract_block_jacobi(EbeOperator) (ebe_operator.hpp:288-313), computed on the GPU
+template <typename T>
+inline BlockJacobi<T> extract_block_jacobi(const EbeOperator<T>& op) {
+  BlockJacobi<T> m;
+  m.inv_blocks.resize(op.n_nodes());
+  detail::check(ts_ebe_block_jacobi_host(op.handle(), m.inv_blocks.data()));
+  return m;
+}
+
+// ------------------------------------------------------ adaptive_cg.hpp:27-67
+class SolverLevels {
+ public:
+  SolverLevels() = default;
+  explicit SolverLevels(ts_levels* h) : lv_(h, ts_levels_destroy) {
+    int32_t n0, n1, n2;
+    ts_levels_sizes(h, &n0, &n1, &n2, nullptr);
+    const ts_ebe* o;
+    ts_levels_operator(h, 0, &o);
+    int32_t ne;
+    ts_ebe_info(o, nullptr, &ne, nullptr, nullptr);
+    // operators are owned by the level set; views share its lifetime
+    auto keep = lv_;
+    auto view = [&](int which) {
+      const ts_ebe* p;
+      ts_levels_operator(h, which, &p);
+      return std::shared_ptr<ts_ebe>(keep, const_cast<ts_ebe*>(p));
+    };
+    outer = EbeOperator<double>(view(0), n0, ne, 2);
+    level0 = EbeOperator<float>(view(1), n0, ne, 2);
+    level1 = EbeOperator<float>(view(2), n1, ne, 1);
+    n2_ = n2;
+  }
+  EbeOperator<double> outer;
+  EbeOperator<float> level0, level1;
+  int32_t level2_rows() const { return n2_; }
+  ts_levels* handle() const { return lv_.get(); }
+
+ private:
+  std::shared_ptr<ts_levels> lv_;
+  int32_t n2_ = 0;
+};
+
+inline SolverLevels build_solver_levels(const Mesh& mesh, const std::vector<Material>& materials,
+                                        const std::vector<uint8_t>& dof_mask, const SolverConfig& cfg,
+                                        int workers = 1) {
+  (void)workers;
+  detail::MeshHandle mh(mesh);
+  auto [l, m] = detail::lame(materials);
+  const ts_solver_config c = cfg.to_c();
+  ts_levels* h = nullptr;
+  detail::check(ts_levels_create(mh.h, static_cast<int32_t>(l.size()), l.data(), m.data(),
+                                 dof_mask.empty() ? nullptr : dof_mask.data(), &c, &h));
+  return SolverLevels(h);
+}
+
+struct CrustModel {  // model.hpp:14-19
+  Mesh mesh;
+  std::vector<Material> materials;
+  std::vector<uint8_t> mask;
+  SolverLevels levels;
+};
+
+inline CrustModel build_crust_model(Mesh mesh, std::vector<Material> materials, const SolverConfig& cfg,
+                                    int workers = 1) {  // model.hpp:21-29
+  CrustModel model;
+  model.mask = dirichlet_mask(mesh);
+  model.levels = build_solver_levels(mesh, materials, model.mask, cfg, workers);
+  model.mesh = std::move(mesh);
+  model.materials = std::move(materials);
+  return model;
+}
+
+namespace detail {
+struct ReportBuf {
+  ts_solve_report c{};
+  std::vector<double> final_, hist;
+  std::vector<int32_t> hit;
+  ReportBuf(int32_t batch, int32_t cap) : final_(batch), hist(size_t(cap > 0 ? cap : 1) * batch), hit(cap > 0 ? cap : 1) {
+    c.final_rel_residual = final_.data();
+    c.history = hist.data();
+    c.history_iter = hit.data();
+    c.history_capacity = cap;
+  }
+  SolveReport report(int stride) const {
+    SolveReport r;
+    r.converged = c.converged != 0;
+    r.residual_history_stride = stride;
+    r.outer_iterations = c.outer_iterations;
+    for (int i = 0; i < 3; ++i) {
+      r.inner_iterations[i] = static_cast<long>(c.inner_iterations[i]);
+      r.time_inner_s[i] = c.time_inner_s[i];
+    }
+    r.final_rel_residual = final_;
+    const int32_t b = static_cast<int32_t>(final_.size());
+    for (int32_t i = 0; i < c.history_count; ++i)
+      r.residual_history.emplace_back(hit[i], std::vector<double>(hist.begin() + size_t(i) * b,
+                                                                   hist.begin() + size_t(i + 1) * b));
+    r.time_setup_s = c.time_setup_s;
+    r.time_outer_s = c.time_outer_s;
+    r.time_total_s = c.time_total_s;
+    r.batch_size = c.batch_size;
+    r.method = c.method == 1 ? "pcge" : "amg";
+    r.inner_precision = c.inner_precision == 64 ? "float64" : "float32";
+    return r;
+  }
+};
+inline void finish(ts_status rc, const ReportBuf& rb, int stride) {
+  if (rc == TS_ERR_NO_CONVERGENCE) throw ConvergenceError(ts_last_error(), rb.report(stride));
+  check(rc);
+}
+}  // namespace detail
+
+// solve (adaptive_cg.hpp:242-263): host VectorBatch in/out, GPU inside
+inline std::pair<VectorBatch64, SolveReport> solve(const SolverLevels& levels, const VectorBatch64& f,
+                                                   const VectorBatch64& u0, const SolverConfig& cfg) {
+  if (u0.n_nodes != f.n_nodes || u0.batch != f.batch) throw ValidationError("solve: initial guess shape mismatch");
+  const ts_solver_config c = cfg.to_c();
+  const int32_t cap = cfg.residual_history_stride > 0 ? cfg.outer_max_iter / cfg.residual_history_stride + 1 : 0;
+  detail::ReportBuf rb(f.batch, cap);
+  VectorBatch64 u(f.n_nodes, f.batch);
+  detail::finish(ts_solve(levels.handle(), f.data.data(), u0.data.data(), u.data.data(), f.batch, &c, &rb.c), rb,
+                 cfg.residual_history_stride);
+  return {std::move(u), rb.report(cfg.residual_history_stride)};
+}
+
+// solve_pcge (adaptive_cg.hpp:267-279)
+inline std::pair<VectorBatch64, SolveReport> solve_pcge(const EbeOperator<double>& k, const VectorBatch64& f,
+                                                        const VectorBatch64& u0, double tol, int max_iter) {
+  detail::ReportBuf rb(f.batch, 0);
+  VectorBatch64 u(f.n_nodes, f.batch);
+  detail::finish(ts_solve_pcge(k.handle(), f.data.data(), u0.data.data(), u.data.data(), f.batch, tol, max_iter,
+                               &rb.c),
+                 rb, 0);
+  return {std::move(u), rb.report(0)};
+}
+
+}  // namespace tetsolve

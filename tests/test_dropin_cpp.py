@@ -1,0 +1,34 @@
+"""The C++ drop-in headers (include/tetsolve_b200/tetsolve.hpp) compile against
+libtsgpu.so here (CPU), and the reference's manufactured-solution test written
+against them runs on the GPU."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "dropin_demo.cpp")
+BIN = os.path.join(ROOT, "tests", "cpp", "dropin_demo")
+LIBDIR = os.path.join(ROOT, "paper_1710_08679_b200")
+
+
+def build():
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SRC, "-L", LIBDIR, "-ltsgpu",
+                    f"-Wl,-rpath,{LIBDIR}", "-o", BIN], check=True)
+
+
+def test_dropin_header_compiles_and_links():
+    build()
+    assert os.path.exists(BIN)
+
+
+@pytest.mark.gpu
+def test_dropin_manufactured_solution_on_gpu():
+    build()
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["converged"] == 1 and res["rel_err"] < 1e-7 and res["max_final"] <= 1e-8
+    assert res["method"] == "pcge" and res["pcge_outer"] >= res["outer"]
+    assert res["history"] == res["outer"] and res["validation_throw"] == 1
