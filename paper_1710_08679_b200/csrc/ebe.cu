@@ -1116,7 +1116,12 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) 
     return;
   }
   bool done = false;
-  if (op.kernel == 3)
+  // Default dispatch (measured, profiles/r01_ebe_tile.txt): the chunk-tiled sweep
+  // wins for the tet4 level-1 operator and for narrow fp32 batches; the
+  // element-parallel RED sweep wins for wide tet10 batches.
+  if (op.kernel == 5 || (op.kernel == 6 && (op.order == 1 || (op.prec == 32 && batch <= 4))))
+    done = ebe_tile_apply(op, u, f, batch, s);
+  if (!done && op.kernel >= 3 && op.kernel != 4)
     done = (op.order == 2)
                ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s)
                                                    : launch_fast<T, T, 10, 12>(op, u, f, batch, s))
@@ -1313,7 +1318,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->coef64.swap(c642);
     coef.swap(coef2);
   }
-  if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : 3;
+  if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5 : 6;
   {
     // fast-kernel layout: 3*node per local node, then the dof-mask word (bit 3a+c)
     const int cs3 = order == 1 ? 8 : 12;
@@ -1364,6 +1369,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->slab_init_ptr_dev.upload(op->slab_init_ptr);
     op->slab_ready.alloc(S);
   }
+  build_tile_plan(*op, conn, cs);
   op->conn.upload(conn);
   op->coef.upload(coef);
   if (dof_mask) op->mask.upload(op->host_mask);

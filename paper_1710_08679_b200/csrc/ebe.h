@@ -20,6 +20,19 @@ struct EbeClusters {
   tsg::DevBuf<uint16_t> inc;       // slot * npe + local index, element order
 };
 
+// Chunk records for the tiled sweep (ebe_tile.cu): kChunk consecutive
+// elements per chunk; one 16-byte-aligned record per chunk holding its
+// distinct nodes, their incidence lists and the elements' local node slots.
+struct EbeTilePlan {
+  int chunk = 0;
+  int32_t n_chunks = 0;
+  int rec_max = 0;             // bytes of the largest record
+  int lmax = 0;                // most distinct nodes in a chunk (rounded up to 4)
+  double nodes_per_elem = 0.0; // chunk node rows moved per element
+  tsg::DevBuf<unsigned char> rec;
+  tsg::DevBuf<uint32_t> rec_off;  // [n_chunks + 1] in 16-byte units
+};
+
 struct ts_ebe {
   int order = 2;   // 1 = tet4 on the vertex grid, 2 = tet10
   int npe = 10;
@@ -42,7 +55,9 @@ struct ts_ebe {
   std::vector<uint8_t> host_mask;       // host [3N]
   mutable std::vector<std::unique_ptr<EbeClusters>> clusters;  // cached per W
   mutable std::mutex clusters_mu;
-  int kernel = 3;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised (default), 4 slab-gated
+  std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, the default kernel)
+  int kernel = 6;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised, 4 slab-gated,
+                   // 5 tiled, 6 auto (tiled for tet4 / narrow fp32 batches, else 3) = default
   mutable std::mutex host_mu;            // guards the host-entry staging buffers
   mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
   bool timing = false;
@@ -57,6 +72,9 @@ void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStre
 // inverse nodal diagonal blocks, fp64 math, rounded to prec (ebe_operator.hpp:288-313);
 // writes a DEVICE array [n_nodes][9] of the operator precision
 void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s);
+// tiled sweep (ebe_tile.cu); false when no instance covers this batch width
+bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s);
+void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int conn_stride);
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda,
                    const double* mu, const uint8_t* dof_mask, int prec);
 }  // namespace tsg

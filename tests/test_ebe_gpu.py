@@ -41,11 +41,16 @@ CASES = [
 ]
 
 
+KERNELS = ["auto", "fast", "tile"]  # TSGPU_EBE_KERNEL: default dispatch, element-parallel RED sweep, chunk-tiled sweep
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("prec", [32, 64])
 @pytest.mark.parametrize("order", [1, 2])
 @pytest.mark.parametrize("batch", [1, 3, 4, 16, 20])
-def test_ebe_matches_reference(checker, case, prec, order, batch):
+def test_ebe_matches_reference(checker, monkeypatch, kernel, case, prec, order, batch):
+    monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
     spec, table = case
     mesh = ts.generate_box_mesh(*spec)
     om = checker.box_mesh(*spec)
@@ -162,3 +167,25 @@ def test_full_size_properties(batch):
     vau = (v.double() * f64).sum(0)
     uav = (u.double() * op64.apply(v.double())).sum(0)
     assert ((vau - uav).abs().max() / vau.abs().max()).item() <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("prec,batch", [(32, 16), (32, 4), (64, 8)])
+@pytest.mark.parametrize("order", [1, 2])
+def test_ebe_many_chunks_per_block(checker, monkeypatch, kernel, prec, batch, order):
+    """A mesh with many more element chunks than resident blocks, so every
+    persistent block walks several chunks (pipelined tile / record prefetch)."""
+    monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
+    spec = ((6000.0, 5000.0, 4000.0), (24, 20, 16), (3000.0,), 1)
+    mesh = ts.generate_box_mesh(*spec)
+    om = checker.box_mesh(*spec)
+    nn = mesh.vertex_count if order == 1 else mesh.node_count()
+    mask = mesh.dirichlet_mask()[: 3 * nn]
+    lam, mu = lame(TWO_LAYER)
+    op = ts.EbeOperator(mesh, order, mats(TWO_LAYER), mask, prec=prec)
+    dt = np.float32 if prec == 32 else np.float64
+    u = checker.rng_sym(5 + batch, 3 * nn * batch).reshape(3 * nn, batch).astype(dt)
+    want = checker.ebe_apply(om, order, lam, mu, mask, prec, u)
+    got = op.apply(dev(u)).cpu().numpy()
+    assert rel_l2(got, want) <= TOL[prec]
+    assert np.array_equal(got[mask == 1], u[mask == 1])
