@@ -18,6 +18,13 @@ explicit flush is needed between steps.
   cpu_baseline: the UNMODIFIED reference (oracle/_ref/libtsref.so) timing the
            same apply on this host's cores (rank 0, N = 1).
   --impl reference: the reference's own CPU implementation as the arm.
+  solve  : BASELINE's other metric, time per case: the full multigrid solve
+           (build_crust_model + solve, adaptive_cg.hpp:242-263) of configs[2]
+           (50M-DOF 3-layer crust, 16 cases, mixed-precision PCG) through the
+           host-buffer entry ts_solve; manufactured right-hand sides
+           f = K u* (acceptance_main.cpp:82-102 fields). Beside it the
+           reference's own solve() and ours on a bounded same-workload sample
+           (16^3 cells, 16 cases) on this host's cores.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
        torchrun --nproc-per-node N bench.py --gpus N ...
@@ -65,50 +72,52 @@ def mesh_spec(cells):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every ~5 ms) DURING the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.rows = []
+        self._stop = None
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            return self
+        self._stop = threading.Event()
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4,
+                "hw_power_brake_slowdown": 0x80}
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, [k for k, v in bits.items() if rs & v]))
+                except Exception:
+                    pass
+                self._stop.wait(self.period)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *exc):
-        self.rows = []
-        if self.proc is None:
-            return False
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out = ""
-        for line in out.splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
         return False
 
     def summary(self):
-        rows = getattr(self, "rows", [])
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self._max,
+                "reasons": sorted({x for r in self.rows for x in r[1]}), "samples": len(self.rows)}
 
 
 def max_over_ranks(vals, device="cpu"):
@@ -154,7 +163,7 @@ def run_reference(args, world, rank):
     mu = [rho * vs * vs for vp, vs, rho in TWO_LAYER]
     cores = ref.hw_threads()
     r, prec = args.cases, args.prec
-    steps = max(1, args.steps)
+    steps = max(1, min(args.steps, 20))  # bounded CPU sample (~1.3 s per apply)
     sec, _ = ref.time_ebe_apply_box(ext, div, ifs, 1, 2, lam, mu, prec, cores, r, steps)
     E = 6 * cells[0] * cells[1] * cells[2]
     N = (2 * cells[0] + 1) * (2 * cells[1] + 1) * (2 * cells[2] + 1)
@@ -181,11 +190,111 @@ def config_dict(cells, r, prec, world, E, N):
             "l2_policy": "inputs larger than L2 (u, f = 650 MB each vs 126 MB L2); no flush"}
 
 
+# ---------------------------------------------------------------- solve leg
+THREE_LAYER = TWO_LAYER + [(6800.0, 3900.0, 2900.0)]  # 3rd layer invented (vp^2 > 2 vs^2)
+
+
+def manufactured(mesh, ext, mask, batch, seed, torch):
+    """acceptance_main.cpp:82-102 smooth fields, per-column amplitude / ky (device)."""
+    import numpy as np
+    N = mesh.node_count()
+    xyz = torch.from_numpy(np.asarray(mesh.coords).reshape(-1, 3)).cuda()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    amp = 0.05 * (1 + 0.2 * (torch.rand(batch, device="cuda", dtype=torch.float64, generator=g) * 2 - 1))
+    ky = 1.0 + (torch.rand(batch, device="cuda", dtype=torch.float64, generator=g) > 0.5).double()
+    X, Y, Z = [xyz[:, k:k + 1] / ext[k] for k in range(3)]
+    sz = torch.sin(0.5 * torch.pi * Z)
+    us = torch.stack([amp * torch.sin(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz,
+                      amp * torch.cos(torch.pi * X) * torch.sin(ky * torch.pi * Y) * sz,
+                      amp * torch.cos(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz], 1)
+    us = us.reshape(3 * N, batch).contiguous()
+    us[torch.from_numpy(mask).cuda().bool()] = 0
+    return us
+
+
+def gpu_solve(ts, torch, cells, table, batch, seed):
+    """build_crust_model + solve on (3N, batch) host buffers (ts_solve: H2D f/u0, solve, D2H u).
+    Returns a dict of times and iteration counts."""
+    ext = tuple(c * CELL_KM * 1e3 for c in cells)
+    ifs = (0.75 * ext[2],) if len(table) == 2 else (0.4 * ext[2], 0.75 * ext[2])
+    t0 = time.perf_counter()
+    mesh = ts.generate_box_mesh(ext, cells, ifs)
+    mats = [ts.material_from_wavespeeds(*t) for t in table]
+    cfg = ts.SolverConfig(batch_size=batch)
+    model = ts.build_crust_model(mesh, mats, cfg)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    us = manufactured(mesh, ext, model.mask, batch, seed, torch)
+    f = model.levels.outer.apply(us).cpu().numpy()
+    u0 = f * 0.0
+    t1 = time.perf_counter()
+    u, rep = ts.solve(model.levels, f, u0, cfg, history=0)
+    t_solve = time.perf_counter() - t1
+    ud = torch.from_numpy(u).cuda()
+    err = float((ud - us).norm() / us.norm())
+    return {"cells": list(cells), "dof": 3 * mesh.node_count(), "elements": mesh.element_count(), "cases": batch,
+            "setup_s": round(t_setup, 3), "solve_s": round(t_solve, 4), "s_per_case": t_solve / batch,
+            "outer_iterations": rep.outer_iterations, "inner_iterations": list(rep.inner_iterations),
+            "time_inner_s": [round(x, 4) for x in rep.time_inner_s], "time_outer_s": round(rep.time_outer_s, 4),
+            "max_final_rel_residual": rep.max_final_residual(), "rel_err_vs_manufactured": err,
+            "h2d_bytes": int(2 * f.nbytes), "d2h_bytes": int(u.nbytes)}
+
+
+def solve_leg(args, ts, torch, world, rank, local):
+    """BASELINE metric 'time per case (s)': configs[2] solve per rank (replicas:
+    each rank its own cases), max over ranks; plus the CPU reference on a
+    bounded same-workload sample (rank 0, N = 1)."""
+    cells, r = tuple(args.solve_cells), args.solve_cases
+    with ClockSampler(local) as clk:
+        g = gpu_solve(ts, torch, cells, THREE_LAYER, r, 31 + rank)
+    solve_s = max_over_ranks([g["solve_s"]], "cuda")[0]
+    out = {"metric": "time per case (s)", "higher_is_better": False,
+           "workload": f"configs[2]: {g['dof'] / 1e6:.1f}M-DOF 3-layer crust box {list(cells)}, {r} cases per GPU, "
+                       "mixed-precision multigrid PCG (fp32 inner, fp64 outer), manufactured RHS",
+           "value": round(solve_s / (r * world), 5), "unit": "s", "n_gpus": world,
+           "entry": "ts_solve (host f/u0/u; H2D + solve + D2H timed)", **g, "clocks": clk.summary()}
+    out["s_per_case"] = round(g["s_per_case"], 5)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            from oracle import Oracle, SolverConfig as OCfg, have_reference
+            if have_reference():
+                ref = Oracle("reference")
+                cores = ref.hw_threads()
+                sc = tuple(args.cpu_solve_cells)
+                ext = tuple(c * CELL_KM * 1e3 for c in sc)
+                om = ref.box_mesh(ext, sc, (0.4 * ext[2], 0.75 * ext[2]), 1)
+                lam = [rho * (vp * vp - 2 * vs * vs) for vp, vs, rho in THREE_LAYER]
+                mu = [rho * vs * vs for vp, vs, rho in THREE_LAYER]
+                t0 = time.perf_counter()
+                olv = ref.levels(om, lam, mu, OCfg.default(batch_size=r), workers=cores)
+                t_set = time.perf_counter() - t0
+                mesh = ts.generate_box_mesh(ext, sc, (0.4 * ext[2], 0.75 * ext[2]))
+                us = manufactured(mesh, ext, mesh.dirichlet_mask(), r, 31, torch).cpu().numpy()
+                fo = olv.outer_apply(us)
+                t0 = time.perf_counter()
+                uo, ro = olv.solve(fo)
+                t_ref = time.perf_counter() - t0
+                gs = gpu_solve(ts, torch, sc, THREE_LAYER, r, 31)
+                out["cpu_reference_sample"] = {
+                    "kind": "reference", "cores": cores,
+                    "sample": f"reference solve() on {list(sc)} cells ({3 * mesh.node_count()} DOF), {r} cases, "
+                              f"workers={cores}; same mesh/RHS solved here on the GPU through ts_solve",
+                    "reference_s_per_case": round(t_ref / r, 4), "reference_setup_s": round(t_set, 3),
+                    "reference_outer_iterations": ro["outer_iterations"],
+                    "reference_inner_iterations": list(ro["inner_iterations"]),
+                    "gpu_s_per_case": round(gs["s_per_case"], 5), "gpu_outer_iterations": gs["outer_iterations"],
+                    "gpu_inner_iterations": gs["inner_iterations"]}
+        except Exception as exc:  # reported, never fatal
+            out["cpu_reference_sample"] = {"failed": str(exc)}
+    return out
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cells", type=int, nargs=3, default=[82, 123, 41])
@@ -194,6 +303,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--solve-cells", type=int, nargs=3, default=[140, 210, 70], help="configs[2]: 50M DOF")
+    ap.add_argument("--solve-cases", type=int, default=16)
+    ap.add_argument("--cpu-solve-cells", type=int, nargs=3, default=[16, 16, 16])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -341,6 +454,14 @@ def main():
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"failed: {exc}"}
 
+    # ---- time per case: the full solve (configs[2]) through the host entry
+    solve = None
+    io_bytes = int(u.numel() * u.element_size())
+    if not args.no_solve:
+        del u, f, uh, fh, fd
+        torch.cuda.empty_cache()
+        solve = solve_leg(args, ts, torch, world, rank, local)
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -348,17 +469,18 @@ def main():
             "vs_baseline": None, "dtype": "f32" if args.prec == 32 else "f64", "data": "synthetic",
             "config": config_dict(cells, r, args.prec, world, E, N),
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
-                    "h2d_bytes_per_step": int(u.numel() * u.element_size()),
-                    "d2h_bytes_per_step": int(f.numel() * f.element_size()), "entry": "ts_ebe_apply_host"},
+                    "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes, "entry": "ts_ebe_apply_host"},
             "roofline": {"bound": "hbm", "achieved": round(B / kms / 1e6, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(B / kms / 1e6 / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": f"k_ebe_fast<{'float,float2' if args.prec == 32 else 'double,double'},10,12,{r}>",
+                         "kernel": (f"k_ebe_tile<float,float2,10,{r},32>" if args.prec == 32 and r <= 4 else
+                                    f"k_ebe_fast<{'float,float2' if args.prec == 32 else 'double,double'},10,12,{r}>"),
                          "kernel_ms": round(kms, 4), "alg_bytes_per_launch": int(B)},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": 2 * args.steps,
             "r_sweep": sweep,
             "e2e_result_matches_device": ok,
+            "solve": solve,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
