@@ -174,6 +174,65 @@ ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, doub
 ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, double* u_out,
                         int32_t batch, double tol, int32_t max_iter, ts_solve_report* rep);
 
+/* ------------------------------------------------ partitioned (multi-GPU) solve
+ *
+ * SURVEY.md §8e. The reference has no distributed path; these
+ * entries add the paper's one: the mesh is split into element partitions, one
+ * rank per GPU, interface-node partial sums travel between neighbouring
+ * partitions inside every EBE product (NCCL send/recv, overlapped with the
+ * interior elements) and dot products are all-reduced. Vectors are in each
+ * rank's LOCAL node order (ts_dist_local_nodes gives local -> global). */
+typedef struct ts_comm ts_comm;
+typedef struct ts_thread_world ts_thread_world;
+typedef struct ts_dist_levels ts_dist_levels;
+
+/* NCCL communicator, one process per GPU: rank 0 calls ts_comm_nccl_id and
+ * broadcasts the 128 bytes (any out-of-band channel, e.g. torch.distributed). */
+ts_status ts_comm_nccl_available(char* why, int32_t why_len);
+ts_status ts_comm_nccl_id(uint8_t id[128]);
+ts_status ts_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device,
+                              ts_comm** out);
+/* in-process ranks (one host thread each, any device incl. a shared one) */
+ts_status ts_thread_world_create(int32_t nranks, ts_thread_world** out);
+void ts_thread_world_destroy(ts_thread_world* w);
+ts_status ts_comm_create_thread(ts_thread_world* w, int32_t rank, int32_t device, ts_comm** out);
+void ts_comm_destroy(ts_comm* c);
+ts_status ts_comm_info(const ts_comm* c, int32_t* rank, int32_t* size, int32_t* device);
+
+/* recursive coordinate bisection of element centroids: part[E] in [0, nparts) */
+ts_status ts_partition_rcb(const ts_mesh* mesh, int32_t nparts, int32_t* part);
+
+/* host-only plan of one rank (no device needed): sizes, then arrays */
+ts_status ts_dist_plan_sizes(const ts_mesh* mesh, const uint8_t* dof_mask, const int32_t* part,
+                             int32_t nranks, int32_t rank, int32_t* n_local, int32_t* n_local_vertices,
+                             int32_t* n_elems, int32_t* n_nbr, int64_t* n_halo_rows);
+/* l2g [n_local], owned [n_local], elems [n_elems], nbr [n_nbr], nbr_rows [n_nbr]
+ * (rows per neighbour), halo_rows [n_halo_rows] (local ids, neighbour-major) */
+ts_status ts_dist_plan_export(const ts_mesh* mesh, const uint8_t* dof_mask, const int32_t* part,
+                              int32_t nranks, int32_t rank, int32_t* l2g, uint8_t* owned, int32_t* elems,
+                              int32_t* nbr, int32_t* nbr_rows, int32_t* halo_rows);
+
+/* build_solver_levels (adaptive_cg.hpp:39-67) for this rank's partition of the
+ * GLOBAL mesh (every rank passes the same mesh / part); dof_mask NULL =
+ * dirichlet_mask(mesh). The comm must outlive the level set. */
+ts_status ts_dist_levels_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda,
+                                const double* mu, const uint8_t* dof_mask, const int32_t* part,
+                                const ts_solver_config* cfg, ts_comm* comm, ts_dist_levels** out);
+void ts_dist_levels_destroy(ts_dist_levels* lv);
+ts_status ts_dist_levels_sizes(const ts_dist_levels* lv, int32_t* n_local, int32_t* n_local_vertices,
+                               int32_t* n2);
+ts_status ts_dist_local_nodes(const ts_dist_levels* lv, int32_t* l2g);
+/* solve (adaptive_cg.hpp:242-263) on local vectors; host or device buffers */
+ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, double* u_out,
+                        int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);
+ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double* u0, double* u_out,
+                               int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep,
+                               void* stream);
+/* one partitioned EBE product (device buffers, local order) incl. the halo
+ * exchange: which = 0 outer fp64 tet10, 1 level-0 fp32 tet10, 2 level-1 fp32 tet4 */
+ts_status ts_dist_ebe_apply(ts_dist_levels* lv, int32_t which, const void* u, void* f, int32_t batch,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

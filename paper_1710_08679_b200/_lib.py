@@ -95,6 +95,24 @@ _sig = {
     "ts_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
     "ts_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
     "ts_solve_pcge": (C.c_int, [vp, vp, vp, vp, i32, C.c_double, i32, vp]),
+    "ts_comm_nccl_available": (C.c_int, [vp, i32]),
+    "ts_comm_nccl_id": (C.c_int, [vp]),
+    "ts_comm_create_nccl": (C.c_int, [i32, i32, vp, i32, vp]),
+    "ts_thread_world_create": (C.c_int, [i32, vp]),
+    "ts_thread_world_destroy": (None, [vp]),
+    "ts_comm_create_thread": (C.c_int, [vp, i32, i32, vp]),
+    "ts_comm_destroy": (None, [vp]),
+    "ts_comm_info": (C.c_int, [vp, vp, vp, vp]),
+    "ts_partition_rcb": (C.c_int, [vp, i32, vp]),
+    "ts_dist_plan_sizes": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
+    "ts_dist_plan_export": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "ts_dist_levels_create": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "ts_dist_levels_destroy": (None, [vp]),
+    "ts_dist_levels_sizes": (C.c_int, [vp, vp, vp, vp]),
+    "ts_dist_local_nodes": (C.c_int, [vp, vp]),
+    "ts_dist_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
+    "ts_dist_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
+    "ts_dist_ebe_apply": (C.c_int, [vp, i32, vp, vp, i32, vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _fn = getattr(lib, _name, None)

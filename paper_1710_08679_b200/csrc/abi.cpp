@@ -3,6 +3,9 @@
 #include <cstring>
 #include <memory>
 
+#include "comm.h"
+#include "dist.h"
+#include "dist_api.h"
 #include "ebe.h"
 
 namespace tsg {
@@ -30,6 +33,13 @@ const std::string& last_error();
   do {                        \
     if (!(cond)) tsg::validation(msg); \
   } while (0)
+
+struct ts_comm {
+  std::unique_ptr<tsg::Comm> c;
+};
+struct ts_thread_world {
+  std::shared_ptr<tsg::ThreadWorld> w;
+};
 
 extern "C" {
 
@@ -235,6 +245,158 @@ ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t* n) {
   TS_API_BEGIN
   TS_REQUIRE(op && n, "ebe: null argument");
   *n = 2;  // masked-identity init (or memset) + one element sweep per 32 cases
+  TS_API_END
+}
+
+// ------------------------------------------------------------ partitioned solve
+ts_status ts_comm_nccl_available(char* why, int32_t why_len) {
+  TS_API_BEGIN
+  std::string w;
+  const bool ok = tsg::nccl_available(&w);
+  if (why && why_len > 0) {
+    std::strncpy(why, w.c_str(), size_t(why_len) - 1);
+    why[why_len - 1] = 0;
+  }
+  if (!ok) tsg::fail(TS_ERR_NCCL, "nccl unavailable: " + w);
+  TS_API_END
+}
+
+ts_status ts_comm_nccl_id(uint8_t id[128]) {
+  TS_API_BEGIN
+  TS_REQUIRE(id, "comm: null id");
+  tsg::nccl_unique_id(id);
+  TS_API_END
+}
+
+ts_status ts_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device, ts_comm** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(id && out, "comm: null argument");
+  auto h = std::make_unique<ts_comm>();
+  h->c = tsg::make_nccl_comm(nranks, rank, id, device);
+  *out = h.release();
+  TS_API_END
+}
+
+ts_status ts_thread_world_create(int32_t nranks, ts_thread_world** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(out, "comm: null argument");
+  auto h = std::make_unique<ts_thread_world>();
+  h->w = tsg::make_thread_world(nranks);
+  *out = h.release();
+  TS_API_END
+}
+
+void ts_thread_world_destroy(ts_thread_world* w) { delete w; }
+
+ts_status ts_comm_create_thread(ts_thread_world* w, int32_t rank, int32_t device, ts_comm** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(w && out, "comm: null argument");
+  auto h = std::make_unique<ts_comm>();
+  h->c = tsg::make_thread_comm(w->w, rank, device);
+  *out = h.release();
+  TS_API_END
+}
+
+void ts_comm_destroy(ts_comm* c) { delete c; }
+
+ts_status ts_comm_info(const ts_comm* c, int32_t* rank, int32_t* size, int32_t* device) {
+  TS_API_BEGIN
+  TS_REQUIRE(c, "comm: null handle");
+  if (rank) *rank = c->c->rank();
+  if (size) *size = c->c->size();
+  if (device) *device = c->c->device();
+  TS_API_END
+}
+
+ts_status ts_partition_rcb(const ts_mesh* mesh, int32_t nparts, int32_t* part) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && part, "partition: null argument");
+  const std::vector<int32_t> p = tsg::partition_rcb(mesh->m, nparts);
+  std::memcpy(part, p.data(), p.size() * sizeof(int32_t));
+  TS_API_END
+}
+
+ts_status ts_dist_plan_sizes(const ts_mesh* mesh, const uint8_t* dof_mask, const int32_t* part, int32_t nranks,
+                             int32_t rank, int32_t* n_local, int32_t* n_local_vertices, int32_t* n_elems,
+                             int32_t* n_nbr, int64_t* n_halo_rows) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && part, "dist plan: null argument");
+  const tsg::DistPlan p = tsg::build_dist_plan(mesh->m, dof_mask, part, nranks, rank);
+  if (n_local) *n_local = p.n_local;
+  if (n_local_vertices) *n_local_vertices = p.n_local_vertices;
+  if (n_elems) *n_elems = static_cast<int32_t>(p.elems.size());
+  if (n_nbr) *n_nbr = static_cast<int32_t>(p.halo0.nbr.size());
+  if (n_halo_rows) *n_halo_rows = p.halo0.rows_total();
+  TS_API_END
+}
+
+ts_status ts_dist_plan_export(const ts_mesh* mesh, const uint8_t* dof_mask, const int32_t* part, int32_t nranks,
+                              int32_t rank, int32_t* l2g, uint8_t* owned, int32_t* elems, int32_t* nbr,
+                              int32_t* nbr_rows, int32_t* halo_rows) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && part, "dist plan: null argument");
+  const tsg::DistPlan p = tsg::build_dist_plan(mesh->m, dof_mask, part, nranks, rank);
+  if (l2g) std::memcpy(l2g, p.l2g.data(), p.l2g.size() * sizeof(int32_t));
+  if (owned) std::memcpy(owned, p.owned.data(), p.owned.size());
+  if (elems) std::memcpy(elems, p.elems.data(), p.elems.size() * sizeof(int32_t));
+  int64_t o = 0;
+  for (size_t k = 0; k < p.halo0.nbr.size(); ++k) {
+    if (nbr) nbr[k] = p.halo0.nbr[k];
+    if (nbr_rows) nbr_rows[k] = static_cast<int32_t>(p.halo0.rows[k].size());
+    if (halo_rows) std::memcpy(halo_rows + o, p.halo0.rows[k].data(), p.halo0.rows[k].size() * sizeof(int32_t));
+    o += static_cast<int64_t>(p.halo0.rows[k].size());
+  }
+  TS_API_END
+}
+
+ts_status ts_dist_levels_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda, const double* mu,
+                                const uint8_t* dof_mask, const int32_t* part, const ts_solver_config* cfg,
+                                ts_comm* comm, ts_dist_levels** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && lambda && mu && part && cfg && comm && out, "dist levels: null argument");
+  TS_REQUIRE(n_materials >= 1, "dist levels: need at least one material");
+  *out = tsg::dist_levels_create(mesh->m, n_materials, lambda, mu, dof_mask, part, *cfg, comm->c.get());
+  TS_API_END
+}
+
+void ts_dist_levels_destroy(ts_dist_levels* lv) { tsg::dist_levels_destroy(lv); }
+
+ts_status ts_dist_levels_sizes(const ts_dist_levels* lv, int32_t* n_local, int32_t* n_local_vertices, int32_t* n2) {
+  TS_API_BEGIN
+  TS_REQUIRE(lv, "dist levels: null handle");
+  tsg::dist_levels_sizes(*lv, n_local, n_local_vertices, n2);
+  TS_API_END
+}
+
+ts_status ts_dist_local_nodes(const ts_dist_levels* lv, int32_t* l2g) {
+  TS_API_BEGIN
+  TS_REQUIRE(lv && l2g, "dist levels: null argument");
+  const auto& v = tsg::dist_local_nodes(*lv);
+  std::memcpy(l2g, v.data(), v.size() * sizeof(int32_t));
+  TS_API_END
+}
+
+ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
+                        const ts_solver_config* cfg, ts_solve_report* rep) {
+  TS_API_BEGIN
+  TS_REQUIRE(lv && f && u0 && u_out && cfg && rep, "solve: null argument");
+  tsg::dist_solve_host(*lv, f, u0, u_out, batch, *cfg, *rep);
+  TS_API_END
+}
+
+ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
+                               const ts_solver_config* cfg, ts_solve_report* rep, void* stream) {
+  TS_API_BEGIN
+  TS_REQUIRE(lv && f && u0 && u_out && cfg && rep, "solve: null argument");
+  tsg::dist_solve_device(*lv, f, u0, u_out, batch, *cfg, *rep, static_cast<cudaStream_t>(stream));
+  TS_API_END
+}
+
+ts_status ts_dist_ebe_apply(ts_dist_levels* lv, int32_t which, const void* u, void* f, int32_t batch, void* stream) {
+  TS_API_BEGIN
+  TS_REQUIRE(lv && u && f, "dist apply: null argument");
+  TS_REQUIRE(batch >= 1, "dist apply: batch must be >= 1");
+  tsg::dist_ebe_apply(*lv, which, u, f, batch, static_cast<cudaStream_t>(stream));
   TS_API_END
 }
 

@@ -16,8 +16,13 @@ namespace tsg {
 
 namespace {
 
+// Partial sums over a contiguous entry range per block. `owned` (nullable,
+// distributed solves): per-node flags; entries of nodes this rank does not own
+// are still visited (updates happen everywhere) but do not accumulate, so every
+// dof is counted once across ranks. Entry i belongs to node i / per_node.
 template <int ND, typename F>
-__device__ __forceinline__ void reduce_pass(int64_t len, int32_t B, double* __restrict__ partial, F&& f) {
+__device__ __forceinline__ void reduce_pass(int64_t len, int32_t B, double* __restrict__ partial,
+                                            const uint8_t* __restrict__ owned, int64_t per_node, F&& f) {
   __shared__ double sm[kRedThreads * 4];
   const int S = (kRedThreads / B) * B;
   const int t = threadIdx.x;
@@ -29,7 +34,11 @@ __device__ __forceinline__ void reduce_pass(int64_t len, int32_t B, double* __re
     const int64_t per = ((len + gridDim.x - 1) / gridDim.x + S - 1) / S * S;
     const int64_t lo = per * blockIdx.x;
     const int64_t hi = lo + per < len ? lo + per : len;
-    for (int64_t i = lo + t; i < hi; i += S) f(i, b, acc);
+    if (owned) {
+      for (int64_t i = lo + t; i < hi; i += S) f(i, b, acc, owned[i / per_node] != 0);
+    } else {
+      for (int64_t i = lo + t; i < hi; i += S) f(i, b, acc, true);
+    }
   }
 #pragma unroll
   for (int k = 0; k < ND; ++k) sm[k * kRedThreads + t] = acc[k];
@@ -44,11 +53,12 @@ __device__ __forceinline__ void reduce_pass(int64_t len, int32_t B, double* __re
   }
 }
 
-// column total of partial k
-__device__ __forceinline__ double col_total(const double* __restrict__ partial, int nd, int k, int32_t B,
-                                            int b) {
+// column total of partial k over nblk blocks (kRedBlocks, or 1 when the
+// partials were already summed and all-reduced across ranks)
+__device__ __forceinline__ double col_total(const double* __restrict__ partial, int nd, int k, int32_t B, int b,
+                                            int nblk) {
   double s = 0.0;
-  for (int blk = 0; blk < kRedBlocks; ++blk) s += partial[(static_cast<int64_t>(blk) * nd + k) * B + b];
+  for (int blk = 0; blk < nblk; ++blk) s += partial[(static_cast<int64_t>(blk) * nd + k) * B + b];
   return s;
 }
 
@@ -74,27 +84,33 @@ __device__ void write_ratio(const double* num, const double* den, int32_t B, Pcg
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_dot2(const T* __restrict__ x0, const T* __restrict__ y0,
                                                       const T* __restrict__ x1, const T* __restrict__ y1,
-                                                      int64_t len, int32_t B, double* partial) {
+                                                      int64_t len, int32_t B, double* partial,
+                                                      const uint8_t* __restrict__ owned) {
   if (x1) {
-    reduce_pass<2>(len, B, partial, [&](int64_t i, int, double* acc) {
+    reduce_pass<2>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
+      if (!own) return;
       acc[0] += double(x0[i]) * double(y0[i]);
       acc[1] += double(x1[i]) * double(y1[i]);
     });
   } else {
-    reduce_pass<1>(len, B, partial, [&](int64_t i, int, double* acc) { acc[0] += double(x0[i]) * double(y0[i]); });
+    reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
+      if (own) acc[0] += double(x0[i]) * double(y0[i]);
+    });
   }
 }
 
 __global__ void k_sum_partials(const double* partial, int nd, int32_t B, double* out) {
   const int t = threadIdx.x;
-  if (t < nd * B) out[t] = col_total(partial, nd, t / B, B, t % B);
+  if (t < nd * B) out[t] = col_total(partial, nd, t / B, B, t % B, kRedBlocks);
 }
 
 // z = M^-1 e (fp64 math, rounded to T), accumulate (z, e)
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_rho(const T* __restrict__ inv, const T* __restrict__ e,
-                                                     int32_t n, int32_t B, double* partial) {
-  reduce_pass<1>(int64_t(n) * B, B, partial, [&](int64_t it, int b, double* acc) {
+                                                     int32_t n, int32_t B, double* partial,
+                                                     const uint8_t* __restrict__ owned) {
+  reduce_pass<1>(int64_t(n) * B, B, partial, owned, int64_t(B), [&](int64_t it, int b, double* acc, bool own) {
+    if (!own) return;
     const int64_t node = it / B;
     const T* m = inv + 9 * node;
     const T* ev = e + 3 * node * B + b;
@@ -107,11 +123,11 @@ __global__ void __launch_bounds__(kRedThreads) k_rho(const T* __restrict__ inv, 
   });
 }
 
-__global__ void k_rho_final(const double* partial, int32_t B, int first, double* rho_a, const double* rho_b,
-                            double* beta) {
+__global__ void k_rho_final(const double* partial, int nblk, int32_t B, int first, double* rho_a,
+                            const double* rho_b, double* beta) {
   const int b = threadIdx.x;
   if (b >= B) return;
-  const double r = col_total(partial, 1, 0, B, b);
+  const double r = col_total(partial, 1, 0, B, b, nblk);
   rho_a[b] = r;
   beta[b] = first ? 0.0 : (rho_b[b] != 0.0 ? r / rho_b[b] : 0.0);  // pcg.hpp:74-80
 }
@@ -138,8 +154,9 @@ __global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, 
 
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_gamma(const T* __restrict__ p, const T* __restrict__ q, int64_t len,
-                                                       int32_t B, double* partial) {
-  reduce_pass<3>(len, B, partial, [&](int64_t i, int, double* acc) {
+                                                       int32_t B, double* partial, const uint8_t* __restrict__ owned) {
+  reduce_pass<3>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
+    if (!own) return;
     const double a = double(p[i]), c = double(q[i]);
     acc[0] += a * c;
     acc[1] += a * a;
@@ -149,7 +166,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gamma(const T* __restrict__ p, 
 
 // alpha with the reference's breakdown / stagnation rules (pcg.hpp:83-110)
 template <typename T>
-__global__ void k_gamma_final(const double* partial, int32_t B, const double* rho_a, double* rho_b,
+__global__ void k_gamma_final(const double* partial, int nblk, int32_t B, const double* rho_a, double* rho_b,
                               double* gamma, double* alpha, PcgStatus* st) {
   __shared__ int stag, brk;
   if (threadIdx.x == 0) {
@@ -159,7 +176,7 @@ __global__ void k_gamma_final(const double* partial, int32_t B, const double* rh
   __syncthreads();
   const int b = threadIdx.x;
   if (b < B) {
-    const double g = col_total(partial, 3, 0, B, b);
+    const double g = col_total(partial, 3, 0, B, b, nblk);
     gamma[b] = g;
     double a = 0.0;
     if (g > 0.0) {
@@ -167,7 +184,7 @@ __global__ void k_gamma_final(const double* partial, int32_t B, const double* rh
     } else if (g == 0.0 && rho_a[b] == 0.0) {
       a = 0.0;
     } else {
-      const double pn = col_total(partial, 3, 1, B, b), qn = col_total(partial, 3, 2, B, b);
+      const double pn = col_total(partial, 3, 1, B, b, nblk), qn = col_total(partial, 3, 2, B, b, nblk);
       const double scale = sqrt(pn) * sqrt(qn);
       const double eps16 = 16.0 * (sizeof(T) == 4 ? double(FLT_EPSILON) : DBL_EPSILON);
       if (fabs(g) <= eps16 * scale) atomicExch(&stag, 1);
@@ -189,9 +206,10 @@ template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_update(T* __restrict__ e, T* __restrict__ u,
                                                         const T* __restrict__ p, const T* __restrict__ q,
                                                         int64_t len, int32_t B, const double* __restrict__ alpha,
-                                                        const PcgStatus* __restrict__ st, double* partial) {
+                                                        const PcgStatus* __restrict__ st, double* partial,
+                                                        const uint8_t* __restrict__ owned) {
   const bool skip = st->stagnated || st->breakdown_col >= 0;
-  reduce_pass<1>(len, B, partial, [&](int64_t i, int b, double* acc) {
+  reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b, double* acc, bool own) {
     T ev = e[i];
     if (!skip) {
       const T a = static_cast<T>(alpha[b]);
@@ -200,13 +218,14 @@ __global__ void __launch_bounds__(kRedThreads) k_update(T* __restrict__ e, T* __
       e[i] = ev;
       u[i] = u[i] + a * p[i];
     }
-    acc[0] += double(ev) * double(ev);
+    if (own) acc[0] += double(ev) * double(ev);
   });
 }
 
-__global__ void k_ratio_final(const double* partial, int32_t B, double* num, const double* den, PcgStatus* st) {
+__global__ void k_ratio_final(const double* partial, int nblk, int32_t B, double* num, const double* den,
+                              PcgStatus* st) {
   const int b = threadIdx.x;
-  if (b < B) num[b] = col_total(partial, 1, 0, B, b);
+  if (b < B) num[b] = col_total(partial, 1, 0, B, b, nblk);
   __syncthreads();
   write_ratio(num, den, B, st);
 }
@@ -214,21 +233,22 @@ __global__ void k_ratio_final(const double* partial, int32_t B, double* num, con
 // e = r - e (e holds A u); partials: ||r||^2, ||e||^2 (pcg.hpp:59-65)
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_init(const T* __restrict__ r, T* __restrict__ e, int64_t len,
-                                                      int32_t B, double* partial) {
-  reduce_pass<2>(len, B, partial, [&](int64_t i, int, double* acc) {
+                                                      int32_t B, double* partial, const uint8_t* __restrict__ owned) {
+  reduce_pass<2>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
     const T rv = r[i];
     const T ev = rv - e[i];
     e[i] = ev;
+    if (!own) return;
     acc[0] += double(rv) * double(rv);
     acc[1] += double(ev) * double(ev);
   });
 }
 
-__global__ void k_init_final(const double* partial, int32_t B, double* rn2, double* en2, PcgStatus* st) {
+__global__ void k_init_final(const double* partial, int nblk, int32_t B, double* rn2, double* en2, PcgStatus* st) {
   const int b = threadIdx.x;
   if (b < B) {
-    rn2[b] = col_total(partial, 2, 0, B, b);
-    en2[b] = col_total(partial, 2, 1, B, b);
+    rn2[b] = col_total(partial, 2, 0, B, b, nblk);
+    en2[b] = col_total(partial, 2, 1, B, b, nblk);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -240,18 +260,19 @@ __global__ void k_init_final(const double* partial, int32_t B, double* rn2, doub
 
 // ---- outer CG (fp64) ----
 __global__ void __launch_bounds__(kRedThreads) k_true_res(const double* __restrict__ f, double* __restrict__ r,
-                                                          int64_t len, int32_t B, double* partial) {
-  reduce_pass<1>(len, B, partial, [&](int64_t i, int, double* acc) {
+                                                          int64_t len, int32_t B, double* partial,
+                                                          const uint8_t* __restrict__ owned) {
+  reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
     const double v = f[i] - r[i];
     r[i] = v;
-    acc[0] += v * v;
+    if (own) acc[0] += v * v;
   });
 }
 
-__global__ void k_cg_beta(const double* partial, int32_t B, const double* gprev, double* beta) {
+__global__ void k_cg_beta(const double* partial, int nblk, int32_t B, const double* gprev, double* beta) {
   const int b = threadIdx.x;
   if (b >= B) return;
-  const double zq = col_total(partial, 1, 0, B, b);
+  const double zq = col_total(partial, 1, 0, B, b, nblk);
   beta[b] = gprev[b] != 0.0 ? -zq / gprev[b] : 0.0;  // adaptive_cg.hpp:196-200
 }
 
@@ -262,14 +283,14 @@ __global__ void k_xpby(const double* __restrict__ z, double* __restrict__ p, int
   p[i] = first ? z[i] : z[i] + beta[i % B] * p[i];
 }
 
-__global__ void k_cg_alpha(const double* partial, int32_t B, double* rho, double* gamma, double* gprev,
+__global__ void k_cg_alpha(const double* partial, int nblk, int32_t B, double* rho, double* gamma, double* gprev,
                            double* alpha, PcgStatus* st) {
   __shared__ int brk;
   if (threadIdx.x == 0) brk = INT32_MAX;
   __syncthreads();
   const int b = threadIdx.x;
   if (b < B) {
-    const double r = col_total(partial, 2, 0, B, b), g = col_total(partial, 2, 1, B, b);
+    const double r = col_total(partial, 2, 0, B, b, nblk), g = col_total(partial, 2, 1, B, b, nblk);
     rho[b] = r;
     gamma[b] = g;
     double a = 0.0;
@@ -289,13 +310,14 @@ __global__ void k_cg_alpha(const double* partial, int32_t B, double* rho, double
 __global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ r, double* __restrict__ u,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ q, int64_t len, int32_t B,
-                                                           const double* __restrict__ alpha, double* partial) {
-  reduce_pass<1>(len, B, partial, [&](int64_t i, int b, double* acc) {
+                                                           const double* __restrict__ alpha, double* partial,
+                                                           const uint8_t* __restrict__ owned) {
+  reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b, double* acc, bool own) {
     const double a = alpha[b];
     const double rv = r[i] + (-a) * q[i];
     r[i] = rv;
     u[i] = u[i] + a * p[i];
-    acc[0] += rv * rv;
+    if (own) acc[0] += rv * rv;
   });
 }
 
@@ -376,14 +398,15 @@ __global__ void k_p1_apply(const float* __restrict__ c, float* __restrict__ fine
 
 __global__ void k_p1_restrict(const float* __restrict__ fine, float* __restrict__ coarse,
                               const int32_t* __restrict__ t_ptr, const int32_t* __restrict__ t_idx, int32_t nv,
-                              const uint8_t* __restrict__ mask, int32_t B) {
+                              const uint8_t* __restrict__ mask, int32_t B, const uint8_t* __restrict__ owned) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t len = 3 * int64_t(nv) * B;
   if (i >= len) return;
   const int64_t dof = i / B;
   const int64_t node = dof / 3;
   const int64_t rem = i - node * 3 * B;
-  float v = 0.0f + fine[i];  // fn = node itself first (weight 1)
+  // fn = node itself first (weight 1); a partition adds it only on the owner
+  float v = (owned && !owned[node]) ? 0.0f : 0.0f + fine[i];
   for (int32_t k = t_ptr[node]; k < t_ptr[node + 1]; ++k)
     v = __fadd_rn(v, __fmul_rn(0.5f, fine[3 * int64_t(t_idx[k]) * B + rem]));
   coarse[i] = (mask && mask[dof]) ? 0.0f : v;
@@ -415,6 +438,22 @@ __global__ void k_p2_restrict(const float* __restrict__ fine, float* __restrict_
   coarse[i] = (mask && mask[dof]) ? 0.0f : v;
 }
 
+// Partials of the last reduction -> (pointer, block count) for the finalize
+// kernels. Distributed solves (ws.comm set) first sum the block partials and
+// all-reduce the per-rank column sums, so every rank applies the reference's
+// scalar logic to the same global numbers.
+struct Partials {
+  const double* p;
+  int nblk;
+};
+Partials finish_partials(Workspace& ws, int nd, int32_t B, cudaStream_t s) {
+  if (!ws.comm) return {ws.partial.get(), kRedBlocks};
+  k_sum_partials<<<1, 1024, 0, s>>>(ws.partial.get(), nd, B, ws.summed.get());
+  TS_CUDA_LAUNCH();
+  ws.comm->allreduce_sum(ws.summed.get(), size_t(nd) * B, s);
+  return {ws.summed.get(), 1};
+}
+
 void check_batch(int32_t B) {
   if (B < 1 || B > kRedThreads) validation("batch must be in [1, 256]");
 }
@@ -423,6 +462,7 @@ void check_batch(int32_t B) {
 
 void Workspace::ensure(int32_t batch) {
   partial.ensure(static_cast<size_t>(kRedBlocks) * 4 * batch);
+  summed.ensure(static_cast<size_t>(4) * batch);
   if (!status.get()) {
     status.alloc(1);
     TS_CUDA(cudaMallocHost(&host_status, sizeof(PcgStatus)));
@@ -437,10 +477,11 @@ void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int3
           Workspace& ws, cudaStream_t s) {
   check_batch(batch);
   ws.ensure(batch);
-  k_dot2<T><<<kRedBlocks, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch, ws.partial.get());
+  k_dot2<T><<<kRedBlocks, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch, ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
   k_sum_partials<<<1, 512, 0, s>>>(ws.partial.get(), x1 ? 2 : 1, batch, out);
   TS_CUDA_LAUNCH();
+  if (ws.comm) ws.comm->allreduce_sum(out, size_t(x1 ? 2 : 1) * batch, s);
 }
 template void dot2<float>(const float*, const float*, const float*, const float*, int64_t, int32_t, double*,
                           Workspace&, cudaStream_t);
@@ -450,9 +491,10 @@ template void dot2<double>(const double*, const double*, const double*, const do
 template <typename T>
 void pcg_rho(const T* inv, const T* e, int32_t n, int32_t B, bool first, const ColScalars& cs, Workspace& ws,
              cudaStream_t s) {
-  k_rho<T><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, n, B, ws.partial.get());
+  k_rho<T><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, n, B, ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_rho_final<<<1, 256, 0, s>>>(ws.partial.get(), B, first ? 1 : 0, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+  const Partials pp = finish_partials(ws, 1, B, s);
+  k_rho_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, first ? 1 : 0, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
                                 cs[ColScalars::BETA]);
   TS_CUDA_LAUNCH();
 }
@@ -468,9 +510,10 @@ void pcg_direction(const T* inv, const T* e, T* p, int32_t n, int32_t B, bool fi
 template <typename T>
 void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                cudaStream_t s) {
-  k_gamma<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B, ws.partial.get());
+  k_gamma<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_gamma_final<T><<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+  const Partials pp = finish_partials(ws, 3, B, s);
+  k_gamma_final<T><<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
                                      cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get());
   TS_CUDA_LAUNCH();
 }
@@ -479,17 +522,19 @@ template <typename T>
 void pcg_update(T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                 cudaStream_t s) {
   k_update<T><<<kRedBlocks, kRedThreads, 0, s>>>(e, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
-                                                 ws.status.get(), ws.partial.get());
+                                                 ws.status.get(), ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_ratio_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::EN2], cs[ColScalars::RN2], ws.status.get());
+  const Partials pp = finish_partials(ws, 1, B, s);
+  k_ratio_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::EN2], cs[ColScalars::RN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
 template <typename T>
 void pcg_init(const T* r, T* e, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  k_init<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, e, 3 * int64_t(n) * B, B, ws.partial.get());
+  k_init<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, e, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_init_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RN2], cs[ColScalars::EN2], ws.status.get());
+  const Partials pp = finish_partials(ws, 2, B, s);
+  k_init_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::EN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
@@ -515,9 +560,10 @@ INST(double)
 
 void cg_true_residual(const double* f, double* r, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                       cudaStream_t s) {
-  k_true_res<<<kRedBlocks, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B, ws.partial.get());
+  k_true_res<<<kRedBlocks, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_ratio_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  const Partials pp = finish_partials(ws, 1, B, s);
+  k_ratio_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
@@ -525,9 +571,10 @@ void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_
                   const ColScalars& cs, Workspace& ws, cudaStream_t s) {
   const int64_t len = 3 * int64_t(n) * B;
   if (!first) {
-    k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B, ws.partial.get());
+    k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B, ws.partial.get(), ws.owned);
     TS_CUDA_LAUNCH();
-    k_cg_beta<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::GPREV], cs[ColScalars::BETA]);
+    const Partials pp = finish_partials(ws, 1, B, s);
+    k_cg_beta<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::GPREV], cs[ColScalars::BETA]);
     TS_CUDA_LAUNCH();
   }
   k_xpby<<<grid_for(len, 256), 256, 0, s>>>(z, p, len, B, first ? 1 : 0, cs[ColScalars::BETA]);
@@ -536,9 +583,10 @@ void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_
 
 void cg_alpha(const double* z, const double* r, const double* p, const double* q, int32_t n, int32_t B,
               const ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B, ws.partial.get());
+  k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_cg_alpha<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RHO_A], cs[ColScalars::GAMMA],
+  const Partials pp = finish_partials(ws, 2, B, s);
+  k_cg_alpha<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::GAMMA],
                                cs[ColScalars::GPREV], cs[ColScalars::ALPHA], ws.status.get());
   TS_CUDA_LAUNCH();
 }
@@ -546,9 +594,10 @@ void cg_alpha(const double* z, const double* r, const double* p, const double* q
 void cg_update(double* r, double* u, const double* p, const double* q, int32_t n, int32_t B, const ColScalars& cs,
                Workspace& ws, cudaStream_t s) {
   k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(r, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
-                                                 ws.partial.get());
+                                                 ws.partial.get(), ws.owned);
   TS_CUDA_LAUNCH();
-  k_ratio_final<<<1, 256, 0, s>>>(ws.partial.get(), B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  const Partials pp = finish_partials(ws, 1, B, s);
+  k_ratio_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
@@ -576,8 +625,9 @@ void p1_apply(const float* coarse, float* fine, const int32_t* edge_ends, int32_
   TS_CUDA_LAUNCH();
 }
 void p1_restrict(const float* fine, float* coarse, const int32_t* t_ptr, const int32_t* t_idx, int32_t nv,
-                 const uint8_t* coarse_mask, int32_t B, cudaStream_t s) {
-  k_p1_restrict<<<grid_for(3 * int64_t(nv) * B, 256), 256, 0, s>>>(fine, coarse, t_ptr, t_idx, nv, coarse_mask, B);
+                 const uint8_t* coarse_mask, int32_t B, cudaStream_t s, const uint8_t* owned) {
+  k_p1_restrict<<<grid_for(3 * int64_t(nv) * B, 256), 256, 0, s>>>(fine, coarse, t_ptr, t_idx, nv, coarse_mask, B,
+                                                                  owned);
   TS_CUDA_LAUNCH();
 }
 void p2_apply(const float* coarse, float* fine, const int32_t* agg, int32_t nf, const uint8_t* fine_mask, int32_t B,

@@ -1,6 +1,7 @@
 // blas.h — device vector / transfer / small-operator kernels of the solve path.
 // All vectors are [node][axis][case] with `batch` cases (vector_batch.hpp:12-28).
 #pragma once
+#include "comm.h"
 #include "ts_common.h"
 
 namespace tsg {
@@ -32,8 +33,14 @@ struct PcgStatus {
   int pad;
 };
 
+// Collective hooks of a distributed solve (comm.h); null on one device.
+struct Comm;
+
 struct Workspace {
   DevBuf<double> partial;  // [kRedBlocks][4][batch]
+  DevBuf<double> summed;   // [4][batch] per-rank column sums (distributed)
+  Comm* comm = nullptr;             // set: reductions are all-reduced across ranks
+  const uint8_t* owned = nullptr;   // set: per-node ownership flags of the current level's vectors
   DevBuf<PcgStatus> status;
   PcgStatus* host_status = nullptr;  // pinned
   void ensure(int32_t batch);
@@ -99,8 +106,10 @@ void p1_apply(const float* coarse, float* fine, const int32_t* edge_ends, int32_
               const uint8_t* fine_mask, int32_t batch, cudaStream_t s);
 // restriction P1^T as a gather over the transpose in ascending fine order (bit-exact
 // with the reference's serial scatter, prolongation.hpp:44-61), then zero_masked
+// (owned: nullable per-vertex flags; a partition counts the vertex's own row only on its owner)
 void p1_restrict(const float* fine, float* coarse, const int32_t* t_ptr, const int32_t* t_idx,
-                 int32_t n_vert, const uint8_t* coarse_mask, int32_t batch, cudaStream_t s);
+                 int32_t n_vert, const uint8_t* coarse_mask, int32_t batch, cudaStream_t s,
+                 const uint8_t* owned = nullptr);
 // aggregation P2: fine = coarse[agg]; restrict = ascending-member sums
 void p2_apply(const float* coarse, float* fine, const int32_t* agg, int32_t n_fine, const uint8_t* fine_mask,
               int32_t batch, cudaStream_t s);

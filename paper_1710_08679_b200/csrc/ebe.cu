@@ -24,6 +24,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <type_traits>
 
 #include "ebe.h"
@@ -165,7 +166,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // zero-filled by the copy engine (src-size 0) — no branches, no extra loads.
 template <typename T, typename V, int NPE, int CS>
 __global__ void __launch_bounds__(128, 3)
-k_ebe_pipe(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t n_elems,
+k_ebe_pipe(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t e_begin, int32_t n_elems,
            int tpe_shift, int32_t batch, int32_t col_base, const T* __restrict__ u, T* __restrict__ f) {
   using O = LaneOps<V>;
   constexpr int CPT = O::kCols;
@@ -185,7 +186,7 @@ k_ebe_pipe(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t
   const int G = gridDim.x * groups;
   const int col = col_base + lane * CPT;
   const bool colok = col < batch;
-  int e = blockIdx.x * groups + grp;
+  int e = e_begin + blockIdx.x * groups + grp;
 
   auto issue = [&](int ee, int stage) {
     if (ee < n_elems) {
@@ -940,7 +941,10 @@ void launch_cluster(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStrea
 }
 
 template <typename T, typename V, int NPE, int CS>
-void launch_pipe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
+void launch_pipe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t e0 = 0,
+                 int32_t e1 = -1) {
+  if (e1 < 0) e1 = op.n_elems;
+  if (e1 <= e0) return;
   constexpr int CPT = LaneOps<V>::kCols;
   constexpr int NT = 128;
   const int nct = (batch + CPT - 1) / CPT;
@@ -962,17 +966,17 @@ void launch_pipe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
   per_sm = std::max(per_sm, 1);
   const int nct_passes = (nct + tpe - 1) / tpe;
-  const int64_t need = (int64_t(op.n_elems) + groups - 1) / groups;
+  const int64_t need = (int64_t(e1 - e0) + groups - 1) / groups;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(cached_sms) * per_sm)));
   for (int p = 0; p < nct_passes; ++p) {
-    kern<<<grid, NT, smem, s>>>(op.conn.get(), reinterpret_cast<const T*>(op.coef.get()), op.n_elems,
+    kern<<<grid, NT, smem, s>>>(op.conn.get(), reinterpret_cast<const T*>(op.coef.get()), e0, e1,
                                  shift, batch, p * tpe * CPT, u, f);
     TS_CUDA_LAUNCH();
   }
 }
 
 template <typename T, typename V, int NPE, int CS, int B>
-bool launch_fast_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s) {
+bool launch_fast_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t e0, int32_t e1) {
   constexpr int CPT = LaneOps<V>::kCols;
   constexpr int NT = 128;
   constexpr int nct = (B + CPT - 1) / CPT;
@@ -993,9 +997,10 @@ bool launch_fast_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s) {
       TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
       per_sm = std::max(per_sm, 1);
     }
-    const int64_t need = (int64_t(op.n_elems) + GROUPS - 1) / GROUPS;
+    if (e1 <= e0) return true;
+    const int64_t need = (int64_t(e1 - e0) + GROUPS - 1) / GROUPS;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
-    kern<<<grid, NT, smem, s>>>(op.conn3.get(), reinterpret_cast<const T*>(op.coef.get()), 0, op.n_elems,
+    kern<<<grid, NT, smem, s>>>(op.conn3.get(), reinterpret_cast<const T*>(op.coef.get()), e0, e1,
                                 nullptr, 0, nullptr, u, f);
     TS_CUDA_LAUNCH();
     return true;
@@ -1003,15 +1008,15 @@ bool launch_fast_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s) {
 }
 
 template <typename T, typename V, int NPE, int CS>
-bool launch_fast(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
+bool launch_fast(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t e0, int32_t e1) {
   switch (batch) {
-    case 1: return launch_fast_b<T, V, NPE, CS, 1>(op, u, f, s);
-    case 2: return launch_fast_b<T, V, NPE, CS, 2>(op, u, f, s);
-    case 4: return launch_fast_b<T, V, NPE, CS, 4>(op, u, f, s);
-    case 8: return launch_fast_b<T, V, NPE, CS, 8>(op, u, f, s);
-    case 16: return launch_fast_b<T, V, NPE, CS, 16>(op, u, f, s);
-    case 20: return launch_fast_b<T, V, NPE, CS, 20>(op, u, f, s);
-    case 32: return launch_fast_b<T, V, NPE, CS, 32>(op, u, f, s);
+    case 1: return launch_fast_b<T, V, NPE, CS, 1>(op, u, f, s, e0, e1);
+    case 2: return launch_fast_b<T, V, NPE, CS, 2>(op, u, f, s, e0, e1);
+    case 4: return launch_fast_b<T, V, NPE, CS, 4>(op, u, f, s, e0, e1);
+    case 8: return launch_fast_b<T, V, NPE, CS, 8>(op, u, f, s, e0, e1);
+    case 16: return launch_fast_b<T, V, NPE, CS, 16>(op, u, f, s, e0, e1);
+    case 20: return launch_fast_b<T, V, NPE, CS, 20>(op, u, f, s, e0, e1);
+    case 32: return launch_fast_b<T, V, NPE, CS, 32>(op, u, f, s, e0, e1);
     default: return false;
   }
 }
@@ -1084,10 +1089,13 @@ void launch_sweep(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_
   }
 }
 
+// part: -1 = every element, 0 = boundary group [0, group_split), 1 = interior
+// group [group_split, E) (partitioned operators, dist_solver.cu); init: write
+// the masked identity into f first.
 template <typename T>
-void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
+void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int part, bool init) {
   const int64_t n = 3 * static_cast<int64_t>(op.n_nodes) * batch;
-  if (op.kernel == 4 && op.n_elems > 0) {
+  if (part < 0 && init && op.kernel == 4 && op.n_elems > 0) {
     if (op.timing) TS_CUDA(cudaEventRecord(op.ev0, s));
     const bool done = (op.order == 2)
                           ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_persist<T, float2_or<T>, 10, 12>(op, u, f, batch, s)
@@ -1100,18 +1108,21 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) 
     }
   }
   // identity rows for constrained dofs, zero elsewhere (ebe_operator.hpp:96-110)
-  if (!op.has_mask) {
-    TS_CUDA(cudaMemsetAsync(f, 0, n * sizeof(T), s));
-  } else {
-    constexpr int W = sizeof(typename Vec4Of<T>::type) / sizeof(T);
-    if (batch % W == 0)
-      k_masked_identity<T><<<grid_for(n / W, 256), 256, 0, s>>>(op.mask.get(), n / W, batch, u, f);
-    else
-      k_masked_identity_scalar<T><<<grid_for(n, 256), 256, 0, s>>>(op.mask.get(), n, batch, u, f);
-    TS_CUDA_LAUNCH();
+  if (init) {
+    if (!op.has_mask) {
+      TS_CUDA(cudaMemsetAsync(f, 0, n * sizeof(T), s));
+    } else {
+      constexpr int W = sizeof(typename Vec4Of<T>::type) / sizeof(T);
+      if (batch % W == 0)
+        k_masked_identity<T><<<grid_for(n / W, 256), 256, 0, s>>>(op.mask.get(), n / W, batch, u, f);
+      else
+        k_masked_identity_scalar<T><<<grid_for(n, 256), 256, 0, s>>>(op.mask.get(), n, batch, u, f);
+      TS_CUDA_LAUNCH();
+    }
   }
   if (op.timing) TS_CUDA(cudaEventRecord(op.ev0, s));  // times the element sweep only
-  if (op.n_elems == 0) {
+  const int32_t e0 = part == 1 ? op.group_split : 0, e1 = part == 0 ? op.group_split : op.n_elems;
+  if (e1 <= e0) {
     if (op.timing) TS_CUDA(cudaEventRecord(op.ev1, s));
     return;
   }
@@ -1120,13 +1131,23 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) 
   // wins for the tet4 level-1 operator and for narrow fp32 batches; the
   // element-parallel RED sweep wins for wide tet10 batches.
   if (op.kernel == 5 || (op.kernel == 6 && (op.order == 1 || (op.prec == 32 && batch <= 4))))
-    done = ebe_tile_apply(op, u, f, batch, s);
+    done = ebe_tile_apply(op, u, f, batch, s, part);
   if (!done && op.kernel >= 3 && op.kernel != 4)
     done = (op.order == 2)
-               ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s)
-                                                   : launch_fast<T, T, 10, 12>(op, u, f, batch, s))
-               : (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 4, 8>(op, u, f, batch, s)
-                                                   : launch_fast<T, T, 4, 8>(op, u, f, batch, s));
+               ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s, e0, e1)
+                                                   : launch_fast<T, T, 10, 12>(op, u, f, batch, s, e0, e1))
+               : (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 4, 8>(op, u, f, batch, s, e0, e1)
+                                                   : launch_fast<T, T, 4, 8>(op, u, f, batch, s, e0, e1));
+  if (!done && part >= 0) {  // any batch width: the generic pipelined sweep over the element range
+    if (op.order == 2) {
+      if (sizeof(T) == 4 && batch % 2 == 0) launch_pipe<float, float2, 10, 12>(op, reinterpret_cast<const float*>(u), reinterpret_cast<float*>(f), batch, s, e0, e1);
+      else launch_pipe<T, T, 10, 12>(op, u, f, batch, s, e0, e1);
+    } else {
+      if (sizeof(T) == 4 && batch % 2 == 0) launch_pipe<float, float2, 4, 4>(op, reinterpret_cast<const float*>(u), reinterpret_cast<float*>(f), batch, s, e0, e1);
+      else launch_pipe<T, T, 4, 4>(op, u, f, batch, s, e0, e1);
+    }
+    done = true;
+  }
   if (!done) {
     if (op.order == 2) launch_sweep<T, 10, 12, 12>(op, u, f, batch, s);
     else launch_sweep<T, 4, 4, 8>(op, u, f, batch, s);
@@ -1160,44 +1181,58 @@ void det_inv3(const double j[3][3], double inv[3][3], double* det) {
 void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s) {
   if (batch < 1) validation("ebe apply: batch must be >= 1");
   if (u == f) validation("ebe apply: input and output must not alias");
-  if (op.prec == 32) apply_t<float>(op, static_cast<const float*>(u), static_cast<float*>(f), batch, s);
-  else apply_t<double>(op, static_cast<const double*>(u), static_cast<double*>(f), batch, s);
+  if (op.prec == 32) apply_t<float>(op, static_cast<const float*>(u), static_cast<float*>(f), batch, s, -1, true);
+  else apply_t<double>(op, static_cast<const double*>(u), static_cast<double*>(f), batch, s, -1, true);
 }
 
-void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s) {
+void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part, bool init) {
+  if (batch < 1) validation("ebe apply: batch must be >= 1");
+  if (u == f) validation("ebe apply: input and output must not alias");
+  if (op.prec == 32) apply_t<float>(op, static_cast<const float*>(u), static_cast<float*>(f), batch, s, part, init);
+  else apply_t<double>(op, static_cast<const double*>(u), static_cast<double*>(f), batch, s, part, init);
+}
+
+void ebe_diag_blocks(const ts_ebe& op, double* diag, cudaStream_t s) {
   if (op.coef64.size() != 12 * static_cast<size_t>(op.n_elems))
     validation("block jacobi: operator setup data released (level-set inner operators keep only device state)");
-  DevBuf<double> diag(9 * static_cast<size_t>(op.n_nodes));
   DevBuf<double> c64;
-  DevBuf<int32_t> bad(1);
   c64.upload(op.coef64, s);
-  TS_CUDA(cudaMemsetAsync(diag.get(), 0, diag.size() * sizeof(double), s));
+  TS_CUDA(cudaMemsetAsync(diag, 0, 9 * static_cast<size_t>(op.n_nodes) * sizeof(double), s));
+  if (op.n_elems > 0) {
+    if (op.order == 2)
+      k_bj_diag<10><<<grid_for(op.n_elems, 128), 128, 0, s>>>(op.conn.get(), op.conn_stride, c64.get(), op.n_elems,
+                                                              diag);
+    else
+      k_bj_diag<4><<<grid_for(op.n_elems, 128), 128, 0, s>>>(op.conn.get(), op.conn_stride, c64.get(), op.n_elems,
+                                                             diag);
+    TS_CUDA_LAUNCH();
+  }
+  TS_CUDA(cudaStreamSynchronize(s));  // c64 is released on return
+}
+
+void bj_invert(const double* diag, const uint8_t* mask, int32_t n, int prec, void* inv_dev, cudaStream_t s) {
+  DevBuf<int32_t> bad(1);
   const int init = INT32_MAX;
   TS_CUDA(cudaMemcpyAsync(bad.get(), &init, sizeof(int), cudaMemcpyHostToDevice, s));
-  if (op.order == 2)
-    k_bj_diag<10><<<grid_for(op.n_elems, 128), 128, 0, s>>>(op.conn.get(), op.conn_stride, c64.get(),
-                                                            op.n_elems, diag.get());
+  if (prec == 32)
+    k_bj_invert<float><<<grid_for(n, 128), 128, 0, s>>>(diag, mask, n, static_cast<float*>(inv_dev), bad.get());
   else
-    k_bj_diag<4><<<grid_for(op.n_elems, 128), 128, 0, s>>>(op.conn.get(), op.conn_stride, c64.get(),
-                                                           op.n_elems, diag.get());
-  TS_CUDA_LAUNCH();
-  const uint8_t* mk = op.has_mask ? op.mask.get() : nullptr;
-  if (op.prec == 32)
-    k_bj_invert<float><<<grid_for(op.n_nodes, 128), 128, 0, s>>>(diag.get(), mk, op.n_nodes,
-                                                                 static_cast<float*>(inv_dev), bad.get());
-  else
-    k_bj_invert<double><<<grid_for(op.n_nodes, 128), 128, 0, s>>>(diag.get(), mk, op.n_nodes,
-                                                                  static_cast<double*>(inv_dev), bad.get());
+    k_bj_invert<double><<<grid_for(n, 128), 128, 0, s>>>(diag, mask, n, static_cast<double*>(inv_dev), bad.get());
   TS_CUDA_LAUNCH();
   int hb = 0;
   TS_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   TS_CUDA(cudaStreamSynchronize(s));
-  if (hb != INT32_MAX)
-    validation("block jacobi: singular diagonal block at node " + std::to_string(hb));
+  if (hb != INT32_MAX) validation("block jacobi: singular diagonal block at node " + std::to_string(hb));
+}
+
+void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s) {
+  DevBuf<double> diag(9 * static_cast<size_t>(op.n_nodes));
+  ebe_diag_blocks(op, diag.get(), s);
+  bj_invert(diag.get(), op.has_mask ? op.mask.get() : nullptr, op.n_nodes, op.prec, inv_dev, s);
 }
 
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda, const double* mu,
-                   const uint8_t* dof_mask, int prec) {
+                   const uint8_t* dof_mask, int prec, const uint8_t* elem_group) {
   if (order != 1 && order != 2) validation("ebe: order must be 1 or 2");
   if (prec != 32 && prec != 64) validation("ebe: precision must be 32 or 64");
   require_device();
@@ -1294,20 +1329,25 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     double ext = 0.0;
     for (int c = 0; c < 3; ++c) ext = std::max(ext, hi[c] - lo[c]);
     const double scale = ext > 0.0 ? double((1 << 20) - 1) / ext : 0.0;
-    std::vector<std::pair<uint64_t, int32_t>> key(E);
+    // (group, Morton key, id): a partitioned operator keeps its boundary elements
+    // (group 0) ahead of the interior ones so the two sweep separately
+    std::vector<std::tuple<uint8_t, uint64_t, int32_t>> key(E);
     for (size_t e = 0; e < E; ++e) {
       uint64_t k = 0;
       for (int c = 0; c < 3; ++c)
         k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
-      key[e] = {k, static_cast<int32_t>(e)};
+      key[e] = {elem_group ? elem_group[e] : uint8_t(0), k, static_cast<int32_t>(e)};
     }
     std::sort(key.begin(), key.end());
+    op->group_split = 0;
+    for (size_t i = 0; i < E; ++i)
+      if (std::get<0>(key[i]) == 0) op->group_split = static_cast<int32_t>(i + 1);
     std::vector<int32_t> conn2(conn.size());
     std::vector<int32_t> hconn2(op->host_conn.size());
     std::vector<double> c642(op->coef64.size());
     std::vector<unsigned char> coef2(coef.size());
     for (size_t i = 0; i < E; ++i) {
-      const size_t e = static_cast<size_t>(key[i].second);
+      const size_t e = static_cast<size_t>(std::get<2>(key[i]));
       std::memcpy(&conn2[i * cs], &conn[e * cs], cs * sizeof(int32_t));
       std::memcpy(&hconn2[i * npe], &op->host_conn[e * npe], npe * sizeof(int32_t));
       std::memcpy(&c642[i * 12], &op->coef64[e * 12], 12 * sizeof(double));

@@ -26,6 +26,7 @@ struct EbeClusters {
 struct EbeTilePlan {
   int chunk = 0;
   int32_t n_chunks = 0;
+  int32_t group_chunk_split = 0;  // chunks [0, split) cover element group 0
   int rec_max = 0;             // bytes of the largest record
   int lmax = 0;                // most distinct nodes in a chunk (rounded up to 4)
   double nodes_per_elem = 0.0; // chunk node rows moved per element
@@ -56,6 +57,7 @@ struct ts_ebe {
   mutable std::vector<std::unique_ptr<EbeClusters>> clusters;  // cached per W
   mutable std::mutex clusters_mu;
   std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, the default kernel)
+  int32_t group_split = 0;              // elements [0, split) = group 0 (partition boundary), rest group 1
   int kernel = 6;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised, 4 slab-gated,
                    // 5 tiled, 6 auto (tiled for tet4 / narrow fp32 batches, else 3) = default
   mutable std::mutex host_mu;            // guards the host-entry staging buffers
@@ -72,9 +74,16 @@ void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStre
 // inverse nodal diagonal blocks, fp64 math, rounded to prec (ebe_operator.hpp:288-313);
 // writes a DEVICE array [n_nodes][9] of the operator precision
 void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s);
+// the two halves of ebe_block_jacobi: fp64 nodal diagonal blocks [n][9] of sum_e K_e,
+// then invert_node_block per node (block_jacobi.hpp:45-66) rounded to prec
+void ebe_diag_blocks(const ts_ebe& op, double* diag_dev, cudaStream_t s);
+void bj_invert(const double* diag_dev, const uint8_t* mask_dev, int32_t n, int prec, void* inv_dev, cudaStream_t s);
 // tiled sweep (ebe_tile.cu); false when no instance covers this batch width
-bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s);
+bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part = -1);
+// element-group sweep of a partitioned operator (part -1 all, 0 boundary, 1 interior)
+void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part, bool init);
 void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int conn_stride);
+// elem_group (nullable, [E] in {0,1}): group-0 elements sweep separately (boundary first)
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda,
-                   const double* mu, const uint8_t* dof_mask, int prec);
+                   const double* mu, const uint8_t* dof_mask, int prec, const uint8_t* elem_group = nullptr);
 }  // namespace tsg

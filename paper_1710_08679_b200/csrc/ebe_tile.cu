@@ -165,7 +165,7 @@ __device__ __forceinline__ RecView rec_view(const unsigned char* base) {
 
 template <typename T, typename V, int NPE, int B, int kChunk, bool ROWRED>
 __global__ void __launch_bounds__(TileCfg<T, V, NPE, B, kChunk>::NT)
-k_ebe_tile(const uint4* __restrict__ rec, const uint32_t* __restrict__ rec_off, int32_t n_chunks,
+k_ebe_tile(const uint4* __restrict__ rec, const uint32_t* __restrict__ rec_off, int32_t c_begin, int32_t n_chunks,
            int rec_max, int lmax, const T* __restrict__ coef, const T* __restrict__ u, T* __restrict__ f) {
   using Cfg = TileCfg<T, V, NPE, B, kChunk>;
   using O = LaneOps<V>;
@@ -215,7 +215,7 @@ k_ebe_tile(const uint4* __restrict__ rec, const uint32_t* __restrict__ rec_off, 
     (void)CB;
   };
 
-  int c = blockIdx.x;
+  int c = c_begin + blockIdx.x;
   if (c >= n_chunks) return;
   load_rec(c, 0);
   cpa_commit();
@@ -316,7 +316,8 @@ k_ebe_tile(const uint4* __restrict__ rec, const uint32_t* __restrict__ rec_off, 
 
 
 template <typename T, typename V, int NPE, int B, int kChunk, bool ROWRED>
-bool launch_tile_c(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, cudaStream_t s) {
+bool launch_tile_c(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, cudaStream_t s, int32_t c0,
+                   int32_t c1) {
   using Cfg = TileCfg<T, V, NPE, B, kChunk>;
   const size_t smem = sizeof(T) * (size_t(kChunk) * Cfg::ES + size_t(plan.lmax) * Cfg::ROW + kChunk * 12) +
                       sizeof(int) * kChunk * NPE + 3 * size_t(plan.rec_max);
@@ -339,37 +340,39 @@ bool launch_tile_c(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, 
     TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::NT, smem));
     if (per_sm < 1) return false;
   }
-  const int grid = std::max(1, std::min(plan.n_chunks, sms * per_sm));
-  kern<<<grid, Cfg::NT, smem, s>>>(reinterpret_cast<const uint4*>(plan.rec.get()), plan.rec_off.get(),
-                                   plan.n_chunks, plan.rec_max, plan.lmax, reinterpret_cast<const T*>(op.coef.get()),
+  if (c1 <= c0) return true;
+  const int grid = std::max(1, std::min(c1 - c0, sms * per_sm));
+  kern<<<grid, Cfg::NT, smem, s>>>(reinterpret_cast<const uint4*>(plan.rec.get()), plan.rec_off.get(), c0,
+                                   c1, plan.rec_max, plan.lmax, reinterpret_cast<const T*>(op.coef.get()),
                                    u, f);
   TS_CUDA_LAUNCH();
   return true;
 }
 
 template <typename T, typename V, int NPE, int B>
-bool launch_tile_b(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, cudaStream_t s) {
+bool launch_tile_b(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, cudaStream_t s, int32_t c0,
+                   int32_t c1) {
   static const bool rowred = [] { const char* e = std::getenv("TSGPU_TILE_ROWRED"); return e && e[0] == '1'; }();
   if (plan.chunk == 16)
-    return rowred ? launch_tile_c<T, V, NPE, B, 16, true>(op, plan, u, f, s)
-                  : launch_tile_c<T, V, NPE, B, 16, false>(op, plan, u, f, s);
+    return rowred ? launch_tile_c<T, V, NPE, B, 16, true>(op, plan, u, f, s, c0, c1)
+                  : launch_tile_c<T, V, NPE, B, 16, false>(op, plan, u, f, s, c0, c1);
   if (plan.chunk == 32)
-    return rowred ? launch_tile_c<T, V, NPE, B, 32, true>(op, plan, u, f, s)
-                  : launch_tile_c<T, V, NPE, B, 32, false>(op, plan, u, f, s);
+    return rowred ? launch_tile_c<T, V, NPE, B, 32, true>(op, plan, u, f, s, c0, c1)
+                  : launch_tile_c<T, V, NPE, B, 32, false>(op, plan, u, f, s, c0, c1);
   return false;
 }
 
 template <typename T, typename V, int NPE>
-bool launch_tile_npe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
+bool launch_tile_npe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t c0, int32_t c1) {
   const EbeTilePlan& plan = *op.tile;
   switch (batch) {
-    case 1: return launch_tile_b<T, T, NPE, 1>(op, plan, u, f, s);
-    case 2: return launch_tile_b<T, V, NPE, 2>(op, plan, u, f, s);
-    case 4: return launch_tile_b<T, V, NPE, 4>(op, plan, u, f, s);
-    case 8: return launch_tile_b<T, V, NPE, 8>(op, plan, u, f, s);
-    case 16: return launch_tile_b<T, V, NPE, 16>(op, plan, u, f, s);
+    case 1: return launch_tile_b<T, T, NPE, 1>(op, plan, u, f, s, c0, c1);
+    case 2: return launch_tile_b<T, V, NPE, 2>(op, plan, u, f, s, c0, c1);
+    case 4: return launch_tile_b<T, V, NPE, 4>(op, plan, u, f, s, c0, c1);
+    case 8: return launch_tile_b<T, V, NPE, 8>(op, plan, u, f, s, c0, c1);
+    case 16: return launch_tile_b<T, V, NPE, 16>(op, plan, u, f, s, c0, c1);
     case 32:
-      if constexpr (sizeof(T) == 4) return launch_tile_b<T, V, NPE, 32>(op, plan, u, f, s);
+      if constexpr (sizeof(T) == 4) return launch_tile_b<T, V, NPE, 32>(op, plan, u, f, s, c0, c1);
       return false;
     default: return false;
   }
@@ -377,18 +380,20 @@ bool launch_tile_npe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStre
 
 }  // namespace
 
-bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s) {
+bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part) {
   if (!op.tile || op.tile->n_chunks == 0) return false;
+  const int32_t c0 = part == 1 ? op.tile->group_chunk_split : 0;
+  const int32_t c1 = part == 0 ? op.tile->group_chunk_split : op.tile->n_chunks;
   if (op.prec == 32) {
     const float* uu = static_cast<const float*>(u);
     float* ff = static_cast<float*>(f);
-    return op.order == 2 ? launch_tile_npe<float, float2, 10>(op, uu, ff, batch, s)
-                         : launch_tile_npe<float, float2, 4>(op, uu, ff, batch, s);
+    return op.order == 2 ? launch_tile_npe<float, float2, 10>(op, uu, ff, batch, s, c0, c1)
+                         : launch_tile_npe<float, float2, 4>(op, uu, ff, batch, s, c0, c1);
   }
   const double* uu = static_cast<const double*>(u);
   double* ff = static_cast<double*>(f);
-  return op.order == 2 ? launch_tile_npe<double, double, 10>(op, uu, ff, batch, s)
-                       : launch_tile_npe<double, double, 4>(op, uu, ff, batch, s);
+  return op.order == 2 ? launch_tile_npe<double, double, 10>(op, uu, ff, batch, s, c0, c1)
+                       : launch_tile_npe<double, double, 4>(op, uu, ff, batch, s, c0, c1);
 }
 
 // Chunk records from the Morton-ordered connectivity words (node | mask << 28).
@@ -399,14 +404,20 @@ void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int con
   int kChunk = kChunkDefault;
   if (const char* e = std::getenv("TSGPU_TILE_CHUNK")) kChunk = std::atoi(e) == 16 ? 16 : 32;
   plan->chunk = kChunk;
-  plan->n_chunks = static_cast<int32_t>((E + kChunk - 1) / kChunk);
+  // chunks never straddle the element-group boundary (boundary / interior sweeps)
+  std::vector<int64_t> cstart;
+  for (int64_t e = 0; e < op.group_split; e += kChunk) cstart.push_back(e);
+  plan->group_chunk_split = static_cast<int32_t>(cstart.size());
+  for (int64_t e = op.group_split; e < E; e += kChunk) cstart.push_back(e);
+  plan->n_chunks = static_cast<int32_t>(cstart.size());
   const int32_t nc = plan->n_chunks;
   std::vector<std::vector<uint32_t>> recs(nc);
   std::vector<int> lmax_t(nc, 0);
 #pragma omp parallel for schedule(static)
   for (int32_t c = 0; c < nc; ++c) {
-    const int64_t e0 = int64_t(c) * kChunk;
-    const int ne = static_cast<int>(std::min<int64_t>(kChunk, E - e0));
+    const int64_t e0 = cstart[c];
+    const int64_t gend = e0 < op.group_split ? op.group_split : E;
+    const int ne = static_cast<int>(std::min<int64_t>(kChunk, gend - e0));
     // distinct nodes in ascending id order (adjacent ids -> adjacent rows in HBM)
     std::vector<uint32_t> nodes(ne * npe);
     std::vector<uint16_t> lconn(ne * npe);

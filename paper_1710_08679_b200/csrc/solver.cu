@@ -19,6 +19,7 @@
 #include "blas.h"
 #include "ebe.h"
 #include "setup.h"
+#include "solver_core.h"
 
 using tsg::ColScalars;
 using tsg::DevBuf;
@@ -51,52 +52,7 @@ struct ts_levels {
 
 namespace tsg {
 namespace {
-
-using clk = std::chrono::steady_clock;
-double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
-
-const PcgStatus& read_status(Workspace& ws, cudaStream_t s) {
-  TS_CUDA(cudaMemcpyAsync(ws.host_status, ws.status.get(), sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
-  TS_CUDA(cudaStreamSynchronize(s));
-  return *ws.host_status;
-}
-
-struct InnerStats {
-  int iterations = 0;
-  bool converged = false;
-};
-
-// inner_pcg (pcg.hpp:52-124). A(x, y): y = A x on the stream.
-template <typename T, typename Op>
-InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t B, double tol, int max_iter, T* e,
-                     T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  if (max_iter < 1) validation("inner_pcg: max_iter must be >= 1");
-  A(u, e);
-  pcg_init<T>(r, e, n, B, cs, ws, s);
-  InnerStats st;
-  const double tol2 = tol * tol;
-  double ratio = read_status(ws, s).ratio;
-  if (std::isnan(ratio)) fail(TS_ERR_NONFINITE, "inner_pcg: non-finite initial residual");
-  while (ratio > tol2 && st.iterations < max_iter) {
-    const bool first = st.iterations == 0;
-    pcg_rho<T>(inv, e, n, B, first, cs, ws, s);
-    pcg_direction<T>(inv, e, p, n, B, first, cs, s);
-    A(p, q);
-    pcg_gamma<T>(p, q, n, B, cs, ws, s);
-    pcg_update<T>(e, u, p, q, n, B, cs, ws, s);
-    const PcgStatus& ps = read_status(ws, s);
-    if (ps.breakdown_col >= 0)
-      fail(TS_ERR_BREAKDOWN, "inner_pcg: breakdown (p,Ap) <= 0 at iteration " + std::to_string(st.iterations + 1) +
-                                 ", column " + std::to_string(ps.breakdown_col));
-    if (ps.stagnated) break;
-    ++st.iterations;
-    ratio = ps.ratio;
-    if (std::isnan(ratio))
-      fail(TS_ERR_NONFINITE, "inner_pcg: non-finite residual at iteration " + std::to_string(st.iterations));
-  }
-  st.converged = ratio <= tol2;
-  return st;
-}
+using namespace core;
 
 void ensure_vecs(ts_levels& lv, int32_t B) {
   LevelVecs& v = lv.v;
@@ -150,96 +106,6 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
   cast_f2d(v.u0.get(), z, len0, s);
 }
 
-void report_reset(ts_solve_report& rep, int method, int prec) {
-  rep.converged = 0;
-  rep.outer_iterations = 0;
-  for (int i = 0; i < 3; ++i) {
-    rep.inner_iterations[i] = 0;
-    rep.time_inner_s[i] = 0.0;
-  }
-  rep.time_setup_s = rep.time_outer_s = rep.time_total_s = 0.0;
-  rep.history_count = 0;
-  rep.method = method;
-  rep.inner_precision = prec;
-}
-
-// run_outer_cg (adaptive_cg.hpp:126-233); vectors r,q,z,p,scratch of `lv.v`.
-template <typename Precond>
-void run_outer_cg(const ts_ebe& k, const double* f, double* u, int32_t B, double tol, int max_iter, int stride,
-                  Precond&& precond, LevelVecs& v, ColScalars& cs, Workspace& ws, ts_solve_report& rep,
-                  cudaStream_t s) {
-  const auto t_start = clk::now();
-  const int32_t n = k.n_nodes;
-  std::vector<double> fn2(B), rn2(B);
-  dot2<double>(f, f, nullptr, nullptr, 3 * int64_t(n), B, cs[ColScalars::FN2], ws, s);
-  TS_CUDA(cudaMemcpyAsync(fn2.data(), cs[ColScalars::FN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
-  auto true_residual = [&]() -> double {
-    ebe_apply(k, u, v.r.get(), B, s);
-    cg_true_residual(f, v.r.get(), n, B, cs, ws, s);
-    return read_status(ws, s).ratio;
-  };
-  auto finalize = [&]() {
-    TS_CUDA(cudaMemcpyAsync(rn2.data(), cs[ColScalars::RN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
-    TS_CUDA(cudaStreamSynchronize(s));
-    rep.batch_size = B;
-    if (rep.final_rel_residual)
-      for (int b = 0; b < B; ++b)
-        rep.final_rel_residual[b] = fn2[b] > 0.0 ? std::sqrt(rn2[b] / fn2[b])
-                                                 : (rn2[b] > 0.0 ? std::numeric_limits<double>::infinity() : 0.0);
-    rep.time_total_s = secs(t_start, clk::now());
-    rep.time_outer_s = rep.time_total_s - rep.time_inner_s[0] - rep.time_inner_s[1] - rep.time_inner_s[2];
-  };
-  double ratio = true_residual();
-  const double tol2 = tol * tol;
-  rep.batch_size = B;
-  int it = 0;
-  bool r_is_true = true, first = true;
-  while (true) {
-    if (std::isnan(ratio)) fail(TS_ERR_NONFINITE, "solve: non-finite residual");
-    if (ratio <= tol2) {
-      if (r_is_true) break;
-      ratio = true_residual();
-      r_is_true = true;
-      if (ratio <= tol2) break;
-    }
-    if (it >= max_iter) {
-      if (!r_is_true) ratio = true_residual();
-      rep.outer_iterations = it;
-      rep.converged = 0;
-      finalize();
-      char buf[64];
-      std::snprintf(buf, sizeof buf, "%f", std::sqrt(ratio));
-      fail(TS_ERR_NO_CONVERGENCE, "solve: outer loop did not converge within " + std::to_string(max_iter) +
-                                      " iterations (max residual " + buf + ")");
-    }
-    precond(v.r.get(), v.z.get());
-    cg_direction(v.z.get(), v.q.get(), v.p.get(), n, B, first, cs, ws, s);
-    first = false;
-    ebe_apply(k, v.p.get(), v.q.get(), B, s);
-    cg_alpha(v.z.get(), v.r.get(), v.p.get(), v.q.get(), n, B, cs, ws, s);
-    cg_update(v.r.get(), u, v.p.get(), v.q.get(), n, B, cs, ws, s);
-    const PcgStatus& ps = read_status(ws, s);
-    if (ps.breakdown_col >= 0)
-      fail(TS_ERR_BREAKDOWN, "solve: breakdown (p,Kp) <= 0 at outer iteration " + std::to_string(it + 1) +
-                                 ", column " + std::to_string(ps.breakdown_col));
-    ratio = ps.ratio;
-    r_is_true = false;
-    ++it;
-    if (stride > 0 && it % stride == 0 && rep.history_count < rep.history_capacity) {
-      TS_CUDA(cudaMemcpyAsync(rn2.data(), cs[ColScalars::RN2], B * sizeof(double), cudaMemcpyDeviceToHost, s));
-      TS_CUDA(cudaStreamSynchronize(s));
-      const int32_t row = rep.history_count++;
-      if (rep.history_iter) rep.history_iter[row] = it;
-      if (rep.history)
-        for (int b = 0; b < B; ++b)
-          rep.history[size_t(row) * B + b] = fn2[b] > 0.0 ? std::sqrt(rn2[b] / fn2[b]) : 0.0;
-    }
-  }
-  rep.outer_iterations = it;
-  rep.converged = 1;
-  finalize();
-}
-
 void check_cfg(const ts_solver_config* c) {
   const ts_status rc = ts_config_validate(c);
   if (rc != TS_OK) fail(rc, ts_last_error());
@@ -263,7 +129,8 @@ void solve_device(ts_levels& lv, const double* f, const double* u0, double* u, i
   if (u != u0)
     TS_CUDA(cudaMemcpyAsync(u, u0, 3 * size_t(lv.n0) * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
   auto precond = [&](const double* r, double* z) { mg_precond(lv, cfg, r, z, B, rep, s); };
-  run_outer_cg(*lv.outer, f, u, B, cfg.outer_tol, cfg.outer_max_iter, cfg.residual_history_stride, precond, lv.v,
+  auto kop = [&](const double* x, double* y) { ebe_apply(*lv.outer, x, y, B, s); };
+  run_outer_cg(kop, lv.n0, f, u, B, cfg.outer_tol, cfg.outer_max_iter, cfg.residual_history_stride, precond, lv.v,
                lv.cs, lv.ws, rep, s);
 }
 
@@ -494,7 +361,8 @@ ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, doub
   ts_status rc = TS_OK;
   std::string msg;
   try {
-    tsg::run_outer_cg(*k, v.f.get(), v.u.get(), batch, tol, max_iter, 0, precond, v, cs, ws, r, s);
+    auto kop = [&](const double* x, double* y) { tsg::ebe_apply(*k, x, y, batch, s); };
+    tsg::core::run_outer_cg(kop, k->n_nodes, v.f.get(), v.u.get(), batch, tol, max_iter, 0, precond, v, cs, ws, r, s);
   } catch (const tsg::Error& e) {
     rc = e.code;
     msg = e.what();
