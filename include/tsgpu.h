@@ -233,6 +233,20 @@ ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double
 ts_status ts_dist_ebe_apply(ts_dist_levels* lv, int32_t which, const void* u, void* f, int32_t batch,
                             void* stream);
 
+/* a partitioned EBE operator alone (no level hierarchy), e.g. for the
+ * partitioned matvec benchmark: order 1|2, prec 32|64, this rank's partition */
+typedef struct ts_dist_ebe ts_dist_ebe;
+ts_status ts_dist_ebe_create(const ts_mesh* mesh, int32_t order, int32_t n_materials, const double* lambda,
+                             const double* mu, const uint8_t* dof_mask, const int32_t* part, int32_t prec,
+                             ts_comm* comm, ts_dist_ebe** out);
+void ts_dist_ebe_destroy(ts_dist_ebe* op);
+ts_status ts_dist_ebe_info(const ts_dist_ebe* op, int32_t* n_local, int32_t* n_elements, int64_t* halo_rows,
+                           int32_t* n_neighbours);
+ts_status ts_dist_ebe_local_nodes(const ts_dist_ebe* op, int32_t* l2g);
+ts_status ts_dist_ebe_op_apply(ts_dist_ebe* op, const void* u, void* f, int32_t batch, void* stream);
+/* the partition's local operator (borrowed; timing controls via ts_ebe_set_timing) */
+ts_status ts_dist_ebe_local_operator(ts_dist_ebe* op, ts_ebe** local);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,12 @@ _sig = {
     "ts_dist_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
     "ts_dist_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
     "ts_dist_ebe_apply": (C.c_int, [vp, i32, vp, vp, i32, vp]),
+    "ts_dist_ebe_create": (C.c_int, [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp]),
+    "ts_dist_ebe_destroy": (None, [vp]),
+    "ts_dist_ebe_info": (C.c_int, [vp, vp, vp, vp, vp]),
+    "ts_dist_ebe_local_nodes": (C.c_int, [vp, vp]),
+    "ts_dist_ebe_op_apply": (C.c_int, [vp, vp, vp, i32, vp]),
+    "ts_dist_ebe_local_operator": (C.c_int, [vp, vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _fn = getattr(lib, _name, None)

@@ -400,4 +400,48 @@ ts_status ts_dist_ebe_apply(ts_dist_levels* lv, int32_t which, const void* u, vo
   TS_API_END
 }
 
+ts_status ts_dist_ebe_create(const ts_mesh* mesh, int32_t order, int32_t n_materials, const double* lambda,
+                             const double* mu, const uint8_t* dof_mask, const int32_t* part, int32_t prec,
+                             ts_comm* comm, ts_dist_ebe** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && lambda && mu && part && comm && out, "dist ebe: null argument");
+  TS_REQUIRE(order == 1 || order == 2, "dist ebe: order must be 1 or 2");
+  TS_REQUIRE(prec == 32 || prec == 64, "dist ebe: precision must be 32 or 64");
+  *out = tsg::dist_ebe_create(mesh->m, order, n_materials, lambda, mu, dof_mask, part, prec, comm->c.get());
+  TS_API_END
+}
+
+void ts_dist_ebe_destroy(ts_dist_ebe* op) { tsg::dist_ebe_destroy(op); }
+
+ts_status ts_dist_ebe_info(const ts_dist_ebe* op, int32_t* n_local, int32_t* n_elements, int64_t* halo_rows,
+                           int32_t* n_neighbours) {
+  TS_API_BEGIN
+  TS_REQUIRE(op, "dist ebe: null handle");
+  tsg::dist_ebe_info(*op, n_local, n_elements, halo_rows, n_neighbours);
+  TS_API_END
+}
+
+ts_status ts_dist_ebe_local_nodes(const ts_dist_ebe* op, int32_t* l2g) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && l2g, "dist ebe: null argument");
+  const auto& v = tsg::dist_ebe_local_nodes(*op);
+  std::memcpy(l2g, v.data(), v.size() * sizeof(int32_t));
+  TS_API_END
+}
+
+ts_status ts_dist_ebe_op_apply(ts_dist_ebe* op, const void* u, void* f, int32_t batch, void* stream) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && u && f, "dist ebe: null argument");
+  TS_REQUIRE(batch >= 1, "dist ebe: batch must be >= 1");
+  tsg::dist_ebe_apply_op(*op, u, f, batch, static_cast<cudaStream_t>(stream));
+  TS_API_END
+}
+
+ts_status ts_dist_ebe_local_operator(ts_dist_ebe* op, ts_ebe** local) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && local, "dist ebe: null argument");
+  *local = tsg::dist_ebe_local(*op);
+  TS_API_END
+}
+
 }  // extern "C"

@@ -15,4 +15,11 @@ void dist_solve_device(ts_dist_levels& L, const double* f, const double* u0, dou
 void dist_solve_host(ts_dist_levels& L, const double* f, const double* u0, double* u, int32_t B,
                      const ts_solver_config& cfg, ts_solve_report& rep);
 void dist_ebe_apply(ts_dist_levels& L, int which, const void* u, void* f, int32_t B, cudaStream_t s);
+ts_dist_ebe* dist_ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lam, const double* mu,
+                             const uint8_t* dof_mask, const int32_t* part, int prec, Comm* comm);
+void dist_ebe_destroy(ts_dist_ebe* D);
+void dist_ebe_info(const ts_dist_ebe& D, int32_t* n_local, int32_t* n_elems, int64_t* halo_rows, int32_t* n_nbr);
+const std::vector<int32_t>& dist_ebe_local_nodes(const ts_dist_ebe& D);
+void dist_ebe_apply_op(ts_dist_ebe& D, const void* u, void* f, int32_t B, cudaStream_t s);
+ts_ebe* dist_ebe_local(ts_dist_ebe& D);
 }  // namespace tsg

@@ -466,4 +466,61 @@ void dist_solve_host(ts_dist_levels& L, const double* f, const double* u0, doubl
   if (rc != TS_OK) fail(rc, msg);
 }
 
+// ---- a standalone partitioned EBE operator (no level hierarchy): bench / users
+// that only need K u on a partitioned mesh
+}  // namespace tsg
+
+struct ts_dist_ebe {
+  tsg::DistPlan plan;
+  tsg::DistEbe d;
+  tsg::DevBuf<uint8_t> mask;
+};
+
+namespace tsg {
+
+ts_dist_ebe* dist_ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lam, const double* mu,
+                             const uint8_t* dof_mask, const int32_t* part, int prec, Comm* comm) {
+  if (!comm) validation("dist ebe: communicator required");
+  require_device();
+  TS_CUDA(cudaSetDevice(comm->device()));
+  auto D = std::make_unique<ts_dist_ebe>();
+  const std::vector<uint8_t> gmask = dof_mask ? std::vector<uint8_t>(dof_mask, dof_mask + 3 * size_t(m.n_nodes()))
+                                              : m.dirichlet_mask();
+  D->plan = build_dist_plan(m, gmask.data(), part, comm->size(), comm->rank());
+  const DistPlan& P = D->plan;
+  std::vector<uint8_t> group(P.elems.size());
+  for (size_t k = 0; k < group.size(); ++k) group[k] = P.elem_boundary[k] ? 0 : 1;
+  const int32_t nn = order == 1 ? P.n_local_vertices : P.n_local;
+  const std::vector<uint8_t> mk(P.mask.begin(), P.mask.begin() + 3 * size_t(nn));
+  D->d.op.reset(ebe_create(P.local, order, n_mat, lam, mu, mk.data(), prec, group.data()));
+  std::vector<double>().swap(D->d.op->coef64);
+  D->mask.upload(mk);
+  D->d.halo.build(order == 1 ? P.halo1 : P.halo0);
+  D->d.mask = D->mask.get();
+  D->d.comm = comm;
+  if (const char* e = std::getenv("TSGPU_DIST_OVERLAP")) D->d.overlap = e[0] != '0';
+  TS_CUDA(cudaDeviceSynchronize());
+  comm->barrier();
+  return D.release();
+}
+
+void dist_ebe_destroy(ts_dist_ebe* D) { delete D; }
+
+void dist_ebe_info(const ts_dist_ebe& D, int32_t* n_local, int32_t* n_elems, int64_t* halo_rows, int32_t* n_nbr) {
+  if (n_local) *n_local = D.d.op->n_nodes;
+  if (n_elems) *n_elems = D.d.op->n_elems;
+  if (halo_rows) *halo_rows = D.d.halo.roff.empty() ? 0 : D.d.halo.roff.back();
+  if (n_nbr) *n_nbr = static_cast<int32_t>(D.d.halo.nbr.size());
+}
+
+const std::vector<int32_t>& dist_ebe_local_nodes(const ts_dist_ebe& D) { return D.plan.l2g; }
+
+void dist_ebe_apply_op(ts_dist_ebe& D, const void* u, void* f, int32_t B, cudaStream_t s) {
+  TS_CUDA(cudaSetDevice(D.d.comm->device()));
+  if (D.d.op->prec == 64) D.d.apply<double>(static_cast<const double*>(u), static_cast<double*>(f), B, s);
+  else D.d.apply<float>(static_cast<const float*>(u), static_cast<float*>(f), B, s);
+}
+
+ts_ebe* dist_ebe_local(ts_dist_ebe& D) { return D.d.op.get(); }
+
 }  // namespace tsg

@@ -180,3 +180,38 @@ class DistLevels:
             lib.ts_dist_levels_destroy(self._h)
         except Exception:
             pass
+
+
+class DistEbeOperator:
+    """A partitioned EBE operator alone (ts_dist_ebe): this rank's elements of
+    the global mesh, K u with the interface exchange inside (local node order)."""
+
+    def __init__(self, mesh: Mesh, order: int, materials, part, comm: Comm, prec: int = 32, dof_mask=None):
+        lam, mu = _lame(materials)
+        part = np.ascontiguousarray(part, np.int32)
+        mk = None if dof_mask is None else np.ascontiguousarray(dof_mask, np.uint8)
+        h = C.c_void_p()
+        _ck(lib.ts_dist_ebe_create(mesh._h, int(order), len(lam), _p(lam), _p(mu), _p(mk), _p(part), int(prec),
+                                   comm._h, C.byref(h)))
+        self._h, self.comm, self.prec, self.order = h, comm, int(prec), int(order)
+        nl, ne, nn = C.c_int32(), C.c_int32(), C.c_int32()
+        hr = C.c_int64()
+        _ck(lib.ts_dist_ebe_info(self._h, C.byref(nl), C.byref(ne), C.byref(hr), C.byref(nn)))
+        self.n_local, self.n_elements, self.halo_rows, self.n_neighbours = nl.value, ne.value, hr.value, nn.value
+
+    def local_nodes(self) -> np.ndarray:
+        l2g = np.zeros(self.n_local, np.int32)
+        _ck(lib.ts_dist_ebe_local_nodes(self._h, _p(l2g)))
+        return l2g
+
+    def apply(self, u, f, stream=None):
+        st = _stream() if stream is None else stream
+        _ck(lib.ts_dist_ebe_op_apply(self._h, C.c_void_p(u.data_ptr()), C.c_void_p(f.data_ptr()), int(u.shape[1]),
+                                     st))
+        return f
+
+    def __del__(self):
+        try:
+            lib.ts_dist_ebe_destroy(self._h)
+        except Exception:
+            pass
