@@ -16,50 +16,96 @@ namespace tsg {
 
 namespace {
 
-// Partial sums over a contiguous entry range per block. `owned` (nullable,
-// distributed solves): per-node flags; entries of nodes this rank does not own
-// are still visited (updates happen everywhere) but do not accumulate, so every
-// dof is counted once across ranks. Entry i belongs to node i / per_node.
-template <int ND, typename F>
+// W consecutive scalars (one 16 / 8-byte access), W | B so a pack never
+// straddles two dof rows and its columns are b0 .. b0+W-1.
+template <typename T, int W>
+struct alignas(sizeof(T) * W) Pack {
+  T v[W];
+};
+template <typename T, int W>
+__device__ __forceinline__ Pack<T, W> ld(const T* p) {
+  return *reinterpret_cast<const Pack<T, W>*>(p);
+}
+template <typename T, int W>
+__device__ __forceinline__ void st(T* p, const Pack<T, W>& x) {
+  *reinterpret_cast<Pack<T, W>*>(p) = x;
+}
+
+// Partial sums over a contiguous entry range per block. Each thread walks
+// packs of W entries with a stride of S entries (S = largest multiple of B
+// <= kRedThreads * W), so its columns b0..b0+W-1 never change; the block then
+// sums each column's slots in fixed order, so results are reproducible and
+// identical columns stay identical. `owned` (nullable, distributed solves):
+// per-node flags; entries of nodes this rank does not own are visited
+// (updates happen everywhere) but do not accumulate. Entry i belongs to node
+// i / per_node. f(i0, b0, acc[ND][W], own) handles entries i0..i0+W-1.
+template <int ND, int W, typename F>
 __device__ __forceinline__ void reduce_pass(int64_t len, int32_t B, double* __restrict__ partial,
                                             const uint8_t* __restrict__ owned, int64_t per_node, F&& f) {
-  __shared__ double sm[kRedThreads * 4];
-  const int S = (kRedThreads / B) * B;
+  __shared__ double sm[ND * kRedThreads * W];
+  const int S = (kRedThreads * W / B) * B;
   const int t = threadIdx.x;
-  double acc[ND];
+  double acc[ND][W];
 #pragma unroll
-  for (int k = 0; k < ND; ++k) acc[k] = 0.0;
-  if (t < S) {
-    const int b = t % B;
+  for (int k = 0; k < ND; ++k)
+#pragma unroll
+    for (int c = 0; c < W; ++c) acc[k][c] = 0.0;
+  if (t * W < S) {
+    const int b0 = (t * W) % B;
     const int64_t per = ((len + gridDim.x - 1) / gridDim.x + S - 1) / S * S;
     const int64_t lo = per * blockIdx.x;
     const int64_t hi = lo + per < len ? lo + per : len;
     if (owned) {
-      for (int64_t i = lo + t; i < hi; i += S) f(i, b, acc, owned[i / per_node] != 0);
+#pragma unroll 2
+      for (int64_t i = lo + int64_t(t) * W; i < hi; i += S) f(i, b0, acc, owned[i / per_node] != 0);
     } else {
-      for (int64_t i = lo + t; i < hi; i += S) f(i, b, acc, true);
+#pragma unroll 2
+      for (int64_t i = lo + int64_t(t) * W; i < hi; i += S) f(i, b0, acc, true);
     }
   }
 #pragma unroll
-  for (int k = 0; k < ND; ++k) sm[k * kRedThreads + t] = acc[k];
+  for (int k = 0; k < ND; ++k)
+#pragma unroll
+    for (int c = 0; c < W; ++c) sm[k * kRedThreads * W + t * W + c] = acc[k][c];
   __syncthreads();
   if (t < B) {
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       double s = 0.0;
-      for (int j = t; j < S; j += B) s += sm[k * kRedThreads + j];
+      for (int j = t; j < S; j += B) s += sm[k * kRedThreads * W + j];
       partial[(static_cast<int64_t>(blockIdx.x) * ND + k) * B + t] = s;
     }
   }
 }
 
-// column total of partial k over nblk blocks (kRedBlocks, or 1 when the
-// partials were already summed and all-reduced across ranks)
-__device__ __forceinline__ double col_total(const double* __restrict__ partial, int nd, int k, int32_t B, int b,
-                                            int nblk) {
-  double s = 0.0;
-  for (int blk = 0; blk < nblk; ++blk) s += partial[(static_cast<int64_t>(blk) * nd + k) * B + b];
-  return s;
+// Column totals of the nd x B partials over nblk blocks into shared memory,
+// with every thread of the block: thread t sums the blocks t/P, t/P + T/P, ...
+// of pair t % P (P = nd*B) in ascending order, then pair p's slots are added in
+// slot order — a fixed order, so the totals are reproducible. tot[k*B + b].
+__device__ void block_totals(const double* __restrict__ partial, int nd, int32_t B, int nblk,
+                             double* __restrict__ tot, double* __restrict__ scratch) {
+  const int P = nd * B, t = threadIdx.x;
+  const int slots = blockDim.x / P;  // >= 1: P <= 4 * 256 and blockDim = 1024
+  if (t < slots * P) {
+    const int pr = t % P, s0 = t / P;
+    double s = 0.0;
+#pragma unroll 4
+    for (int blk = s0; blk < nblk; blk += slots) s += partial[int64_t(blk) * P + pr];
+    scratch[t] = s;
+  }
+  __syncthreads();
+  if (t < P) {
+    double s = 0.0;
+    for (int j = 0; j < slots; ++j) s += scratch[j * P + t];
+    tot[t] = s;
+  }
+  __syncthreads();
+}
+constexpr int kFinThreads = 1024;
+
+// column total of partial k, read from block_totals' result
+__device__ __forceinline__ double col_total(const double* __restrict__ tot, int k, int32_t B, int b) {
+  return tot[k * B + b];
 }
 
 // max_rel_ratio (pcg.hpp:32-42): max_b num/den; 0/0 converged; x/0 -> inf
@@ -81,102 +127,135 @@ __device__ void write_ratio(const double* num, const double* den, int32_t B, Pcg
 }
 
 // ---------------------------------------------------------------- kernels
-template <typename T>
+template <typename T, int W>
 __global__ void __launch_bounds__(kRedThreads) k_dot2(const T* __restrict__ x0, const T* __restrict__ y0,
                                                       const T* __restrict__ x1, const T* __restrict__ y1,
                                                       int64_t len, int32_t B, double* partial,
                                                       const uint8_t* __restrict__ owned) {
   if (x1) {
-    reduce_pass<2>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
+    reduce_pass<2, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double(&acc)[2][W], bool own) {
       if (!own) return;
-      acc[0] += double(x0[i]) * double(y0[i]);
-      acc[1] += double(x1[i]) * double(y1[i]);
+      const Pack<T, W> a = ld<T, W>(x0 + i), c = ld<T, W>(y0 + i), d = ld<T, W>(x1 + i), e = ld<T, W>(y1 + i);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        acc[0][k] += double(a.v[k]) * double(c.v[k]);
+        acc[1][k] += double(d.v[k]) * double(e.v[k]);
+      }
     });
   } else {
-    reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
-      if (own) acc[0] += double(x0[i]) * double(y0[i]);
+    reduce_pass<1, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double(&acc)[1][W], bool own) {
+      if (!own) return;
+      const Pack<T, W> a = ld<T, W>(x0 + i), c = ld<T, W>(y0 + i);
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[0][k] += double(a.v[k]) * double(c.v[k]);
     });
   }
 }
 
-__global__ void k_sum_partials(const double* partial, int nd, int32_t B, double* out) {
+__global__ void __launch_bounds__(kFinThreads) k_sum_partials(const double* partial, int nd, int32_t B, double* out) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
+  block_totals(partial, nd, B, kRedBlocks, tot, scr);
   const int t = threadIdx.x;
-  if (t < nd * B) out[t] = col_total(partial, nd, t / B, B, t % B, kRedBlocks);
+  if (t < nd * B) out[t] = tot[t];
 }
 
-// z = M^-1 e (fp64 math, rounded to T), accumulate (z, e)
-template <typename T>
+// z = M^-1 e per node (fp64 math, rounded to T); entries are (node, case)
+template <typename T, int W>
+__device__ __forceinline__ void bj_pack(const T* __restrict__ m, const Pack<T, W> (&ev)[3], Pack<T, W> (&z)[3]) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const double e0 = double(ev[0].v[k]), e1 = double(ev[1].v[k]), e2 = double(ev[2].v[k]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      z[i].v[k] = static_cast<T>(double(m[3 * i]) * e0 + double(m[3 * i + 1]) * e1 + double(m[3 * i + 2]) * e2);
+  }
+}
+
+// accumulate (M^-1 e, e)
+template <typename T, int W>
 __global__ void __launch_bounds__(kRedThreads) k_rho(const T* __restrict__ inv, const T* __restrict__ e,
                                                      int32_t n, int32_t B, double* partial,
                                                      const uint8_t* __restrict__ owned) {
-  reduce_pass<1>(int64_t(n) * B, B, partial, owned, int64_t(B), [&](int64_t it, int b, double* acc, bool own) {
+  reduce_pass<1, W>(int64_t(n) * B, B, partial, owned, int64_t(B), [&](int64_t it, int b0, double(&acc)[1][W], bool own) {
     if (!own) return;
     const int64_t node = it / B;
-    const T* m = inv + 9 * node;
-    const T* ev = e + 3 * node * B + b;
-    const double e0 = double(ev[0]), e1 = double(ev[B]), e2 = double(ev[2 * B]);
+    const T* ev = e + 3 * node * B + b0;
+    const Pack<T, W> x[3] = {ld<T, W>(ev), ld<T, W>(ev + B), ld<T, W>(ev + 2 * B)};
+    Pack<T, W> z[3];
+    bj_pack<T, W>(inv + 9 * node, x, z);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const T z = static_cast<T>(double(m[3 * i]) * e0 + double(m[3 * i + 1]) * e1 + double(m[3 * i + 2]) * e2);
-      acc[0] += double(z) * double(ev[i * B]);
-    }
+    for (int k = 0; k < W; ++k)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) acc[0][k] += double(z[i].v[k]) * double(x[i].v[k]);
   });
 }
 
-__global__ void k_rho_final(const double* partial, int nblk, int32_t B, int first, double* rho_a,
-                            const double* rho_b, double* beta) {
+__global__ void __launch_bounds__(kFinThreads) k_rho_final(const double* partial, int nblk, int32_t B, int first,
+                                                           double* rho_a, const double* rho_b, double* beta) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
+  block_totals(partial, 1, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b >= B) return;
-  const double r = col_total(partial, 1, 0, B, b, nblk);
+  const double r = tot[b];
   rho_a[b] = r;
   beta[b] = first ? 0.0 : (rho_b[b] != 0.0 ? r / rho_b[b] : 0.0);  // pcg.hpp:74-80
 }
 
 // p = z + (T)beta p, z = M^-1 e (xpby_columns, vector_batch.hpp:86-97); first: p = z
-template <typename T>
+template <typename T, int W>
 __global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, T* __restrict__ p, int32_t n,
                             int32_t B, int first, const double* __restrict__ beta) {
-  const int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * W;
   if (it >= int64_t(n) * B) return;
   const int64_t node = it / B;
-  const int b = static_cast<int>(it % B);
-  const T* m = inv + 9 * node;
-  const T* ev = e + 3 * node * B + b;
-  T* pv = p + 3 * node * B + b;
-  const double e0 = double(ev[0]), e1 = double(ev[B]), e2 = double(ev[2 * B]);
-  const T bt = static_cast<T>(beta[b]);
+  const int b0 = static_cast<int>(it - node * B);
+  const T* ev = e + 3 * node * B + b0;
+  T* pv = p + 3 * node * B + b0;
+  const Pack<T, W> x[3] = {ld<T, W>(ev), ld<T, W>(ev + B), ld<T, W>(ev + 2 * B)};
+  Pack<T, W> z[3];
+  bj_pack<T, W>(inv + 9 * node, x, z);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const T z = static_cast<T>(double(m[3 * i]) * e0 + double(m[3 * i + 1]) * e1 + double(m[3 * i + 2]) * e2);
-    pv[i * B] = first ? z : z + bt * pv[i * B];
+    if (!first) {
+      const Pack<T, W> pp = ld<T, W>(pv + i * B);
+#pragma unroll
+      for (int k = 0; k < W; ++k) z[i].v[k] = z[i].v[k] + static_cast<T>(beta[b0 + k]) * pp.v[k];
+    }
+    st<T, W>(pv + i * B, z[i]);
   }
 }
 
-template <typename T>
+template <typename T, int W>
 __global__ void __launch_bounds__(kRedThreads) k_gamma(const T* __restrict__ p, const T* __restrict__ q, int64_t len,
                                                        int32_t B, double* partial, const uint8_t* __restrict__ owned) {
-  reduce_pass<3>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
+  reduce_pass<3, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double(&acc)[3][W], bool own) {
     if (!own) return;
-    const double a = double(p[i]), c = double(q[i]);
-    acc[0] += a * c;
-    acc[1] += a * a;
-    acc[2] += c * c;
+    const Pack<T, W> a = ld<T, W>(p + i), c = ld<T, W>(q + i);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const double x = double(a.v[k]), y = double(c.v[k]);
+      acc[0][k] += x * y;
+      acc[1][k] += x * x;
+      acc[2][k] += y * y;
+    }
   });
 }
 
 // alpha with the reference's breakdown / stagnation rules (pcg.hpp:83-110)
 template <typename T>
-__global__ void k_gamma_final(const double* partial, int nblk, int32_t B, const double* rho_a, double* rho_b,
-                              double* gamma, double* alpha, PcgStatus* st) {
+__global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* partial, int nblk, int32_t B,
+                                                             const double* rho_a, double* rho_b, double* gamma,
+                                                             double* alpha, PcgStatus* st) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
   __shared__ int stag, brk;
   if (threadIdx.x == 0) {
     stag = 0;
     brk = INT32_MAX;
   }
-  __syncthreads();
+  block_totals(partial, 3, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b < B) {
-    const double g = col_total(partial, 3, 0, B, b, nblk);
+    const double g = tot[b];
     gamma[b] = g;
     double a = 0.0;
     if (g > 0.0) {
@@ -184,7 +263,7 @@ __global__ void k_gamma_final(const double* partial, int nblk, int32_t B, const 
     } else if (g == 0.0 && rho_a[b] == 0.0) {
       a = 0.0;
     } else {
-      const double pn = col_total(partial, 3, 1, B, b, nblk), qn = col_total(partial, 3, 2, B, b, nblk);
+      const double pn = tot[B + b], qn = tot[2 * B + b];
       const double scale = sqrt(pn) * sqrt(qn);
       const double eps16 = 16.0 * (sizeof(T) == 4 ? double(FLT_EPSILON) : DBL_EPSILON);
       if (fabs(g) <= eps16 * scale) atomicExch(&stag, 1);
@@ -202,53 +281,71 @@ __global__ void k_gamma_final(const double* partial, int nblk, int32_t B, const 
 }
 
 // e += (T)(-alpha) q ; u += (T)alpha p ; ||e||^2  (axpy_columns, vector_batch.hpp:72-83)
-template <typename T>
+template <typename T, int W>
 __global__ void __launch_bounds__(kRedThreads) k_update(T* __restrict__ e, T* __restrict__ u,
                                                         const T* __restrict__ p, const T* __restrict__ q,
                                                         int64_t len, int32_t B, const double* __restrict__ alpha,
-                                                        const PcgStatus* __restrict__ st, double* partial,
+                                                        const PcgStatus* __restrict__ st_, double* partial,
                                                         const uint8_t* __restrict__ owned) {
-  const bool skip = st->stagnated || st->breakdown_col >= 0;
-  reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b, double* acc, bool own) {
-    T ev = e[i];
+  const bool skip = st_->stagnated || st_->breakdown_col >= 0;
+  reduce_pass<1, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b0, double(&acc)[1][W], bool own) {
+    Pack<T, W> ev = ld<T, W>(e + i);
     if (!skip) {
-      const T a = static_cast<T>(alpha[b]);
-      const T na = static_cast<T>(-alpha[b]);
-      ev = ev + na * q[i];
-      e[i] = ev;
-      u[i] = u[i] + a * p[i];
+      const Pack<T, W> qv = ld<T, W>(q + i), pv = ld<T, W>(p + i);
+      Pack<T, W> uv = ld<T, W>(u + i);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const T a = static_cast<T>(alpha[b0 + k]);
+        const T na = static_cast<T>(-alpha[b0 + k]);
+        ev.v[k] = ev.v[k] + na * qv.v[k];
+        uv.v[k] = uv.v[k] + a * pv.v[k];
+      }
+      st<T, W>(e + i, ev);
+      st<T, W>(u + i, uv);
     }
-    if (own) acc[0] += double(ev) * double(ev);
+    if (own)
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[0][k] += double(ev.v[k]) * double(ev.v[k]);
   });
 }
 
-__global__ void k_ratio_final(const double* partial, int nblk, int32_t B, double* num, const double* den,
-                              PcgStatus* st) {
+__global__ void __launch_bounds__(kFinThreads) k_ratio_final(const double* partial, int nblk, int32_t B, double* num,
+                                                             const double* den, PcgStatus* st) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
+  block_totals(partial, 1, B, nblk, tot, scr);
   const int b = threadIdx.x;
-  if (b < B) num[b] = col_total(partial, 1, 0, B, b, nblk);
+  if (b < B) num[b] = tot[b];
   __syncthreads();
   write_ratio(num, den, B, st);
 }
 
 // e = r - e (e holds A u); partials: ||r||^2, ||e||^2 (pcg.hpp:59-65)
-template <typename T>
+template <typename T, int W>
 __global__ void __launch_bounds__(kRedThreads) k_init(const T* __restrict__ r, T* __restrict__ e, int64_t len,
                                                       int32_t B, double* partial, const uint8_t* __restrict__ owned) {
-  reduce_pass<2>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
-    const T rv = r[i];
-    const T ev = rv - e[i];
-    e[i] = ev;
+  reduce_pass<2, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double(&acc)[2][W], bool own) {
+    const Pack<T, W> rv = ld<T, W>(r + i);
+    Pack<T, W> ev = ld<T, W>(e + i);
+#pragma unroll
+    for (int k = 0; k < W; ++k) ev.v[k] = rv.v[k] - ev.v[k];
+    st<T, W>(e + i, ev);
     if (!own) return;
-    acc[0] += double(rv) * double(rv);
-    acc[1] += double(ev) * double(ev);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      acc[0][k] += double(rv.v[k]) * double(rv.v[k]);
+      acc[1][k] += double(ev.v[k]) * double(ev.v[k]);
+    }
   });
 }
 
-__global__ void k_init_final(const double* partial, int nblk, int32_t B, double* rn2, double* en2, PcgStatus* st) {
+__global__ void __launch_bounds__(kFinThreads) k_init_final(const double* partial, int nblk, int32_t B, double* rn2,
+                                                            double* en2, PcgStatus* st) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
+  block_totals(partial, 2, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b < B) {
-    rn2[b] = col_total(partial, 2, 0, B, b, nblk);
-    en2[b] = col_total(partial, 2, 1, B, b, nblk);
+    rn2[b] = tot[b];
+    en2[b] = tot[B + b];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -259,20 +356,29 @@ __global__ void k_init_final(const double* partial, int nblk, int32_t B, double*
 }
 
 // ---- outer CG (fp64) ----
+template <int W>
 __global__ void __launch_bounds__(kRedThreads) k_true_res(const double* __restrict__ f, double* __restrict__ r,
                                                           int64_t len, int32_t B, double* partial,
                                                           const uint8_t* __restrict__ owned) {
-  reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double* acc, bool own) {
-    const double v = f[i] - r[i];
-    r[i] = v;
-    if (own) acc[0] += v * v;
+  reduce_pass<1, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double(&acc)[1][W], bool own) {
+    const Pack<double, W> fv = ld<double, W>(f + i);
+    Pack<double, W> rv = ld<double, W>(r + i);
+#pragma unroll
+    for (int k = 0; k < W; ++k) rv.v[k] = fv.v[k] - rv.v[k];
+    st<double, W>(r + i, rv);
+    if (own)
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[0][k] += rv.v[k] * rv.v[k];
   });
 }
 
-__global__ void k_cg_beta(const double* partial, int nblk, int32_t B, const double* gprev, double* beta) {
+__global__ void __launch_bounds__(kFinThreads) k_cg_beta(const double* partial, int nblk, int32_t B,
+                                                         const double* gprev, double* beta) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
+  block_totals(partial, 1, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b >= B) return;
-  const double zq = col_total(partial, 1, 0, B, b, nblk);
+  const double zq = tot[b];
   beta[b] = gprev[b] != 0.0 ? -zq / gprev[b] : 0.0;  // adaptive_cg.hpp:196-200
 }
 
@@ -283,14 +389,15 @@ __global__ void k_xpby(const double* __restrict__ z, double* __restrict__ p, int
   p[i] = first ? z[i] : z[i] + beta[i % B] * p[i];
 }
 
-__global__ void k_cg_alpha(const double* partial, int nblk, int32_t B, double* rho, double* gamma, double* gprev,
-                           double* alpha, PcgStatus* st) {
+__global__ void __launch_bounds__(kFinThreads) k_cg_alpha(const double* partial, int nblk, int32_t B, double* rho,
+                                                          double* gamma, double* gprev, double* alpha, PcgStatus* st) {
+  __shared__ double tot[kFinThreads], scr[kFinThreads];
   __shared__ int brk;
   if (threadIdx.x == 0) brk = INT32_MAX;
-  __syncthreads();
+  block_totals(partial, 2, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b < B) {
-    const double r = col_total(partial, 2, 0, B, b, nblk), g = col_total(partial, 2, 1, B, b, nblk);
+    const double r = tot[b], g = tot[B + b];
     rho[b] = r;
     gamma[b] = g;
     double a = 0.0;
@@ -307,17 +414,26 @@ __global__ void k_cg_alpha(const double* partial, int nblk, int32_t B, double* r
   }
 }
 
+template <int W>
 __global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ r, double* __restrict__ u,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ q, int64_t len, int32_t B,
                                                            const double* __restrict__ alpha, double* partial,
                                                            const uint8_t* __restrict__ owned) {
-  reduce_pass<1>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b, double* acc, bool own) {
-    const double a = alpha[b];
-    const double rv = r[i] + (-a) * q[i];
-    r[i] = rv;
-    u[i] = u[i] + a * p[i];
-    if (own) acc[0] += rv * rv;
+  reduce_pass<1, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b0, double(&acc)[1][W], bool own) {
+    Pack<double, W> rv = ld<double, W>(r + i), uv = ld<double, W>(u + i);
+    const Pack<double, W> pv = ld<double, W>(p + i), qv = ld<double, W>(q + i);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const double a = alpha[b0 + k];
+      rv.v[k] = rv.v[k] + (-a) * qv.v[k];
+      uv.v[k] = uv.v[k] + a * pv.v[k];
+    }
+    st<double, W>(r + i, rv);
+    st<double, W>(u + i, uv);
+    if (own)
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[0][k] += rv.v[k] * rv.v[k];
   });
 }
 
@@ -438,6 +554,21 @@ __global__ void k_p2_restrict(const float* __restrict__ fine, float* __restrict_
   coarse[i] = (mask && mask[dof]) ? 0.0f : v;
 }
 
+// pack width for batch B: 16-byte packs for fp32 (B % 4 == 0), else 8 / 4 bytes
+template <typename T>
+int pack_width(int32_t B) {
+  if (sizeof(T) == 4) return B % 4 == 0 ? 4 : (B % 2 == 0 ? 2 : 1);
+  return B % 2 == 0 ? 2 : 1;
+}
+#define TS_WIDTH_DISPATCH(T, B, CALL)           \
+  do {                                          \
+    switch (pack_width<T>(B)) {                 \
+      case 4: { constexpr int W = 4; CALL; } break; \
+      case 2: { constexpr int W = 2; CALL; } break; \
+      default: { constexpr int W = 1; CALL; } break; \
+    }                                           \
+  } while (0)
+
 // Partials of the last reduction -> (pointer, block count) for the finalize
 // kernels. Distributed solves (ws.comm set) first sum the block partials and
 // all-reduce the per-rank column sums, so every rank applies the reference's
@@ -448,7 +579,7 @@ struct Partials {
 };
 Partials finish_partials(Workspace& ws, int nd, int32_t B, cudaStream_t s) {
   if (!ws.comm) return {ws.partial.get(), kRedBlocks};
-  k_sum_partials<<<1, 1024, 0, s>>>(ws.partial.get(), nd, B, ws.summed.get());
+  k_sum_partials<<<1, kFinThreads, 0, s>>>(ws.partial.get(), nd, B, ws.summed.get());
   TS_CUDA_LAUNCH();
   ws.comm->allreduce_sum(ws.summed.get(), size_t(nd) * B, s);
   return {ws.summed.get(), 1};
@@ -477,9 +608,10 @@ void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int3
           Workspace& ws, cudaStream_t s) {
   check_batch(batch);
   ws.ensure(batch);
-  k_dot2<T><<<kRedBlocks, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch, ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(T, batch, (k_dot2<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch,
+                                                                          ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
-  k_sum_partials<<<1, 512, 0, s>>>(ws.partial.get(), x1 ? 2 : 1, batch, out);
+  k_sum_partials<<<1, kFinThreads, 0, s>>>(ws.partial.get(), x1 ? 2 : 1, batch, out);
   TS_CUDA_LAUNCH();
   if (ws.comm) ws.comm->allreduce_sum(out, size_t(x1 ? 2 : 1) * batch, s);
 }
@@ -491,10 +623,10 @@ template void dot2<double>(const double*, const double*, const double*, const do
 template <typename T>
 void pcg_rho(const T* inv, const T* e, int32_t n, int32_t B, bool first, const ColScalars& cs, Workspace& ws,
              cudaStream_t s) {
-  k_rho<T><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, n, B, ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(T, B, (k_rho<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, n, B, ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
-  k_rho_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, first ? 1 : 0, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+  k_rho_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, first ? 1 : 0, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
                                 cs[ColScalars::BETA]);
   TS_CUDA_LAUNCH();
 }
@@ -502,18 +634,19 @@ void pcg_rho(const T* inv, const T* e, int32_t n, int32_t B, bool first, const C
 template <typename T>
 void pcg_direction(const T* inv, const T* e, T* p, int32_t n, int32_t B, bool first, const ColScalars& cs,
                    cudaStream_t s) {
-  k_direction<T><<<grid_for(int64_t(n) * B, 256), 256, 0, s>>>(inv, e, p, n, B, first ? 1 : 0,
-                                                               cs[ColScalars::BETA]);
+  TS_WIDTH_DISPATCH(T, B, (k_direction<T, W><<<grid_for(int64_t(n) * B / W, 256), 256, 0, s>>>(
+                               inv, e, p, n, B, first ? 1 : 0, cs[ColScalars::BETA])));
   TS_CUDA_LAUNCH();
 }
 
 template <typename T>
 void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                cudaStream_t s) {
-  k_gamma<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(T, B, (k_gamma<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B,
+                                                                          ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 3, B, s);
-  k_gamma_final<T><<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+  k_gamma_final<T><<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
                                      cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get());
   TS_CUDA_LAUNCH();
 }
@@ -521,20 +654,22 @@ void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& c
 template <typename T>
 void pcg_update(T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                 cudaStream_t s) {
-  k_update<T><<<kRedBlocks, kRedThreads, 0, s>>>(e, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
-                                                 ws.status.get(), ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(e, u, p, q, 3 * int64_t(n) * B, B,
+                                                                           cs[ColScalars::ALPHA], ws.status.get(),
+                                                                           ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
-  k_ratio_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::EN2], cs[ColScalars::RN2], ws.status.get());
+  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::EN2], cs[ColScalars::RN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
 template <typename T>
 void pcg_init(const T* r, T* e, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  k_init<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, e, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(T, B, (k_init<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(r, e, 3 * int64_t(n) * B, B,
+                                                                         ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 2, B, s);
-  k_init_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::EN2], ws.status.get());
+  k_init_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::EN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
@@ -560,10 +695,11 @@ INST(double)
 
 void cg_true_residual(const double* f, double* r, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                       cudaStream_t s) {
-  k_true_res<<<kRedBlocks, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(double, B, (k_true_res<W><<<kRedBlocks, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B,
+                                                                               ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
-  k_ratio_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
@@ -571,10 +707,11 @@ void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_
                   const ColScalars& cs, Workspace& ws, cudaStream_t s) {
   const int64_t len = 3 * int64_t(n) * B;
   if (!first) {
-    k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B, ws.partial.get(), ws.owned);
+    TS_WIDTH_DISPATCH(double, B, (k_dot2<double, W><<<kRedBlocks, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B,
+                                                                                     ws.partial.get(), ws.owned)));
     TS_CUDA_LAUNCH();
     const Partials pp = finish_partials(ws, 1, B, s);
-    k_cg_beta<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::GPREV], cs[ColScalars::BETA]);
+    k_cg_beta<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::GPREV], cs[ColScalars::BETA]);
     TS_CUDA_LAUNCH();
   }
   k_xpby<<<grid_for(len, 256), 256, 0, s>>>(z, p, len, B, first ? 1 : 0, cs[ColScalars::BETA]);
@@ -583,21 +720,22 @@ void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_
 
 void cg_alpha(const double* z, const double* r, const double* p, const double* q, int32_t n, int32_t B,
               const ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  k_dot2<double><<<kRedBlocks, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B, ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(double, B, (k_dot2<double, W><<<kRedBlocks, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B,
+                                                                                   ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 2, B, s);
-  k_cg_alpha<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::GAMMA],
+  k_cg_alpha<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::GAMMA],
                                cs[ColScalars::GPREV], cs[ColScalars::ALPHA], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
 void cg_update(double* r, double* u, const double* p, const double* q, int32_t n, int32_t B, const ColScalars& cs,
                Workspace& ws, cudaStream_t s) {
-  k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(r, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
-                                                 ws.partial.get(), ws.owned);
+  TS_WIDTH_DISPATCH(double, B, (k_cg_update<W><<<kRedBlocks, kRedThreads, 0, s>>>(r, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
+                                                 ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
-  k_ratio_final<<<1, 256, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
