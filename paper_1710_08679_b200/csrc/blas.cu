@@ -190,13 +190,14 @@ __global__ void __launch_bounds__(kRedThreads) k_rho(const T* __restrict__ inv, 
   });
 }
 
-__global__ void __launch_bounds__(kFinThreads) k_rho_final(const double* partial, int nblk, int32_t B, int first,
-                                                           double* rho_a, const double* rho_b, double* beta) {
+__global__ void __launch_bounds__(kFinThreads) k_rho_final(const double* partial, int nd, int slot, int nblk,
+                                                           int32_t B, int first, double* rho_a, const double* rho_b,
+                                                           double* beta) {
   __shared__ double tot[kFinThreads], scr[kFinThreads];
-  block_totals(partial, 1, B, nblk, tot, scr);
+  block_totals(partial, nd, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b >= B) return;
-  const double r = tot[b];
+  const double r = tot[slot * B + b];
   rho_a[b] = r;
   beta[b] = first ? 0.0 : (rho_b[b] != 0.0 ? r / rho_b[b] : 0.0);  // pcg.hpp:74-80
 }
@@ -280,68 +281,97 @@ __global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* parti
   }
 }
 
-// e += (T)(-alpha) q ; u += (T)alpha p ; ||e||^2  (axpy_columns, vector_batch.hpp:72-83)
+// e += (T)(-alpha) q ; u += (T)alpha p (axpy_columns, vector_batch.hpp:72-83);
+// partials ||e||^2 and — for the next iteration's beta — (M^-1 e, e)
+// (pcg.hpp:72-73,116), one pass over the node's 3 dofs x W cases.
 template <typename T, int W>
-__global__ void __launch_bounds__(kRedThreads) k_update(T* __restrict__ e, T* __restrict__ u,
-                                                        const T* __restrict__ p, const T* __restrict__ q,
-                                                        int64_t len, int32_t B, const double* __restrict__ alpha,
+__global__ void __launch_bounds__(kRedThreads) k_update(const T* __restrict__ inv, T* __restrict__ e,
+                                                        T* __restrict__ u, const T* __restrict__ p,
+                                                        const T* __restrict__ q, int32_t n, int32_t B,
+                                                        const double* __restrict__ alpha,
                                                         const PcgStatus* __restrict__ st_, double* partial,
                                                         const uint8_t* __restrict__ owned) {
   const bool skip = st_->stagnated || st_->breakdown_col >= 0;
-  reduce_pass<1, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int b0, double(&acc)[1][W], bool own) {
-    Pack<T, W> ev = ld<T, W>(e + i);
+  reduce_pass<2, W>(int64_t(n) * B, B, partial, owned, int64_t(B), [&](int64_t it, int b0, double(&acc)[2][W], bool own) {
+    const int64_t node = it / B;
+    const int64_t base = 3 * node * B + b0;
+    Pack<T, W> ev[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) ev[i] = ld<T, W>(e + base + i * B);
     if (!skip) {
-      const Pack<T, W> qv = ld<T, W>(q + i), pv = ld<T, W>(p + i);
-      Pack<T, W> uv = ld<T, W>(u + i);
 #pragma unroll
-      for (int k = 0; k < W; ++k) {
-        const T a = static_cast<T>(alpha[b0 + k]);
-        const T na = static_cast<T>(-alpha[b0 + k]);
-        ev.v[k] = ev.v[k] + na * qv.v[k];
-        uv.v[k] = uv.v[k] + a * pv.v[k];
+      for (int i = 0; i < 3; ++i) {
+        const Pack<T, W> qv = ld<T, W>(q + base + i * B), pv = ld<T, W>(p + base + i * B);
+        Pack<T, W> uv = ld<T, W>(u + base + i * B);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          const T a = static_cast<T>(alpha[b0 + k]);
+          const T na = static_cast<T>(-alpha[b0 + k]);
+          ev[i].v[k] = ev[i].v[k] + na * qv.v[k];
+          uv.v[k] = uv.v[k] + a * pv.v[k];
+        }
+        st<T, W>(e + base + i * B, ev[i]);
+        st<T, W>(u + base + i * B, uv);
       }
-      st<T, W>(e + i, ev);
-      st<T, W>(u + i, uv);
     }
-    if (own)
+    if (!own) return;
+    Pack<T, W> z[3];
+    bj_pack<T, W>(inv + 9 * node, ev, z);
 #pragma unroll
-      for (int k = 0; k < W; ++k) acc[0][k] += double(ev.v[k]) * double(ev.v[k]);
+    for (int k = 0; k < W; ++k)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        acc[0][k] += double(ev[i].v[k]) * double(ev[i].v[k]);
+        acc[1][k] += double(z[i].v[k]) * double(ev[i].v[k]);
+      }
   });
 }
 
-__global__ void __launch_bounds__(kFinThreads) k_ratio_final(const double* partial, int nblk, int32_t B, double* num,
-                                                             const double* den, PcgStatus* st) {
+__global__ void __launch_bounds__(kFinThreads) k_ratio_final(const double* partial, int nd, int nblk, int32_t B,
+                                                             double* num, const double* den, PcgStatus* st) {
   __shared__ double tot[kFinThreads], scr[kFinThreads];
-  block_totals(partial, 1, B, nblk, tot, scr);
+  block_totals(partial, nd, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b < B) num[b] = tot[b];
   __syncthreads();
   write_ratio(num, den, B, st);
 }
 
-// e = r - e (e holds A u); partials: ||r||^2, ||e||^2 (pcg.hpp:59-65)
+// e = r - e (e holds A u); partials ||r||^2, ||e||^2 (pcg.hpp:59-65) and (M^-1 e, e)
 template <typename T, int W>
-__global__ void __launch_bounds__(kRedThreads) k_init(const T* __restrict__ r, T* __restrict__ e, int64_t len,
-                                                      int32_t B, double* partial, const uint8_t* __restrict__ owned) {
-  reduce_pass<2, W>(len, B, partial, owned, 3 * int64_t(B), [&](int64_t i, int, double(&acc)[2][W], bool own) {
-    const Pack<T, W> rv = ld<T, W>(r + i);
-    Pack<T, W> ev = ld<T, W>(e + i);
+__global__ void __launch_bounds__(kRedThreads) k_init(const T* __restrict__ inv, const T* __restrict__ r,
+                                                      T* __restrict__ e, int32_t n, int32_t B, double* partial,
+                                                      const uint8_t* __restrict__ owned) {
+  reduce_pass<3, W>(int64_t(n) * B, B, partial, owned, int64_t(B), [&](int64_t it, int b0, double(&acc)[3][W], bool own) {
+    const int64_t node = it / B;
+    const int64_t base = 3 * node * B + b0;
+    Pack<T, W> rv[3], ev[3];
 #pragma unroll
-    for (int k = 0; k < W; ++k) ev.v[k] = rv.v[k] - ev.v[k];
-    st<T, W>(e + i, ev);
-    if (!own) return;
+    for (int i = 0; i < 3; ++i) {
+      rv[i] = ld<T, W>(r + base + i * B);
+      ev[i] = ld<T, W>(e + base + i * B);
 #pragma unroll
-    for (int k = 0; k < W; ++k) {
-      acc[0][k] += double(rv.v[k]) * double(rv.v[k]);
-      acc[1][k] += double(ev.v[k]) * double(ev.v[k]);
+      for (int k = 0; k < W; ++k) ev[i].v[k] = rv[i].v[k] - ev[i].v[k];
+      st<T, W>(e + base + i * B, ev[i]);
     }
+    if (!own) return;
+    Pack<T, W> z[3];
+    bj_pack<T, W>(inv + 9 * node, ev, z);
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        acc[0][k] += double(rv[i].v[k]) * double(rv[i].v[k]);
+        acc[1][k] += double(ev[i].v[k]) * double(ev[i].v[k]);
+        acc[2][k] += double(z[i].v[k]) * double(ev[i].v[k]);
+      }
   });
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_init_final(const double* partial, int nblk, int32_t B, double* rn2,
                                                             double* en2, PcgStatus* st) {
   __shared__ double tot[kFinThreads], scr[kFinThreads];
-  block_totals(partial, 2, B, nblk, tot, scr);
+  block_totals(partial, 3, B, nblk, tot, scr);
   const int b = threadIdx.x;
   if (b < B) {
     rn2[b] = tot[b];
@@ -620,15 +650,13 @@ template void dot2<float>(const float*, const float*, const float*, const float*
 template void dot2<double>(const double*, const double*, const double*, const double*, int64_t, int32_t, double*,
                            Workspace&, cudaStream_t);
 
-template <typename T>
-void pcg_rho(const T* inv, const T* e, int32_t n, int32_t B, bool first, const ColScalars& cs, Workspace& ws,
-             cudaStream_t s) {
-  TS_WIDTH_DISPATCH(T, B, (k_rho<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, n, B, ws.partial.get(), ws.owned)));
+// beta from the (M^-1 e, e) partials the last init / update pass left behind
+void pcg_rho(int32_t B, bool first, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
+  if (!ws.last_p) validation("pcg_rho: no (M^-1 e, e) partials pending");
+  k_rho_final<<<1, kFinThreads, 0, s>>>(ws.last_p, ws.last_nd, ws.last_nd - 1, ws.last_nblk, B, first ? 1 : 0,
+                                        cs[ColScalars::RHO_A], cs[ColScalars::RHO_B], cs[ColScalars::BETA]);
   TS_CUDA_LAUNCH();
-  const Partials pp = finish_partials(ws, 1, B, s);
-  k_rho_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, first ? 1 : 0, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
-                                cs[ColScalars::BETA]);
-  TS_CUDA_LAUNCH();
+  ws.last_p = nullptr;
 }
 
 template <typename T>
@@ -652,37 +680,44 @@ void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& c
 }
 
 template <typename T>
-void pcg_update(T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
-                cudaStream_t s) {
-  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(e, u, p, q, 3 * int64_t(n) * B, B,
+void pcg_update(const T* inv, T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs,
+                Workspace& ws, cudaStream_t s) {
+  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, u, p, q, n, B,
                                                                            cs[ColScalars::ALPHA], ws.status.get(),
                                                                            ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
-  const Partials pp = finish_partials(ws, 1, B, s);
-  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::EN2], cs[ColScalars::RN2], ws.status.get());
+  const Partials pp = finish_partials(ws, 2, B, s);
+  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, 2, pp.nblk, B, cs[ColScalars::EN2], cs[ColScalars::RN2],
+                                          ws.status.get());
   TS_CUDA_LAUNCH();
+  ws.last_p = pp.p;
+  ws.last_nblk = pp.nblk;
+  ws.last_nd = 2;
 }
 
 template <typename T>
-void pcg_init(const T* r, T* e, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  TS_WIDTH_DISPATCH(T, B, (k_init<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(r, e, 3 * int64_t(n) * B, B,
-                                                                         ws.partial.get(), ws.owned)));
+void pcg_init(const T* inv, const T* r, T* e, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
+              cudaStream_t s) {
+  TS_WIDTH_DISPATCH(T, B, (k_init<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(inv, r, e, n, B, ws.partial.get(),
+                                                                         ws.owned)));
   TS_CUDA_LAUNCH();
-  const Partials pp = finish_partials(ws, 2, B, s);
+  const Partials pp = finish_partials(ws, 3, B, s);
   k_init_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::EN2], ws.status.get());
   TS_CUDA_LAUNCH();
+  ws.last_p = pp.p;
+  ws.last_nblk = pp.nblk;
+  ws.last_nd = 3;
 }
 
 #define INST(T)                                                                                              \
-  template void pcg_rho<T>(const T*, const T*, int32_t, int32_t, bool, const ColScalars&, Workspace&,       \
-                           cudaStream_t);                                                                    \
   template void pcg_direction<T>(const T*, const T*, T*, int32_t, int32_t, bool, const ColScalars&,         \
                                  cudaStream_t);                                                              \
   template void pcg_gamma<T>(const T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,           \
                              cudaStream_t);                                                                  \
-  template void pcg_update<T>(T*, T*, const T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,  \
-                              cudaStream_t);                                                                 \
-  template void pcg_init<T>(const T*, T*, int32_t, int32_t, const ColScalars&, Workspace&, cudaStream_t);    \
+  template void pcg_update<T>(const T*, T*, T*, const T*, const T*, int32_t, int32_t, const ColScalars&,     \
+                              Workspace&, cudaStream_t);                                                     \
+  template void pcg_init<T>(const T*, const T*, T*, int32_t, int32_t, const ColScalars&, Workspace&,         \
+                            cudaStream_t);                                                                   \
   template void bj_apply<T>(const T*, const T*, T*, int32_t, int32_t, cudaStream_t);
 template <typename T>
 void bj_apply(const T* inv, const T* r, T* z, int32_t n, int32_t B, cudaStream_t s) {
@@ -699,7 +734,7 @@ void cg_true_residual(const double* f, double* r, int32_t n, int32_t B, const Co
                                                                                ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
-  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, 1, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 
@@ -735,7 +770,7 @@ void cg_update(double* r, double* u, const double* p, const double* q, int32_t n
                                                  ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
-  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
+  k_ratio_final<<<1, kFinThreads, 0, s>>>(pp.p, 1, pp.nblk, B, cs[ColScalars::RN2], cs[ColScalars::FN2], ws.status.get());
   TS_CUDA_LAUNCH();
 }
 

@@ -43,6 +43,9 @@ struct Workspace {
   const uint8_t* owned = nullptr;   // set: per-node ownership flags of the current level's vectors
   DevBuf<PcgStatus> status;
   PcgStatus* host_status = nullptr;  // pinned
+  // (M^-1 e, e) partials left by the last pcg_init / pcg_update (slot nd-1), consumed by pcg_rho
+  const double* last_p = nullptr;
+  int last_nblk = 0, last_nd = 0;
   void ensure(int32_t batch);
   ~Workspace();
 };
@@ -54,10 +57,9 @@ void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int3
           Workspace& ws, cudaStream_t s);
 
 // ---- inner PCG steps (pcg.hpp:52-124), T = float | double --------------------
-// rho_a = (M^-1 e, e); beta = first ? 0 : (rho_b != 0 ? rho_a / rho_b : 0)
-template <typename T>
-void pcg_rho(const T* inv, const T* e, int32_t n_nodes, int32_t batch, bool first, const ColScalars& cs,
-             Workspace& ws, cudaStream_t s);
+// rho_a = (M^-1 e, e) from the partials of the last pcg_init / pcg_update;
+// beta = first ? 0 : (rho_b != 0 ? rho_a / rho_b : 0)
+void pcg_rho(int32_t batch, bool first, const ColScalars& cs, Workspace& ws, cudaStream_t s);
 // p = M^-1 e + beta p  (first: p = M^-1 e)
 template <typename T>
 void pcg_direction(const T* inv, const T* e, T* p, int32_t n_nodes, int32_t batch, bool first,
@@ -66,13 +68,14 @@ void pcg_direction(const T* inv, const T* e, T* p, int32_t n_nodes, int32_t batc
 template <typename T>
 void pcg_gamma(const T* p, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,
                cudaStream_t s);
-// unless stagnated/broken: e -= alpha q ; u += alpha p ; en2 = ||e||^2 ; ratio
+// unless stagnated/broken: e -= alpha q ; u += alpha p ; en2 = ||e||^2 ; ratio;
+// also the (M^-1 e, e) partials of the next iteration (pcg_rho)
 template <typename T>
-void pcg_update(T* e, T* u, const T* p, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs,
-                Workspace& ws, cudaStream_t s);
-// e = r - Au (Au in e on entry); rn2 = ||r||^2, en2 = ||e||^2, ratio
+void pcg_update(const T* inv, T* e, T* u, const T* p, const T* q, int32_t n_nodes, int32_t batch,
+                const ColScalars& cs, Workspace& ws, cudaStream_t s);
+// e = r - Au (Au in e on entry); rn2 = ||r||^2, en2 = ||e||^2, ratio; (M^-1 e, e) partials
 template <typename T>
-void pcg_init(const T* r, T* e, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,
+void pcg_init(const T* inv, const T* r, T* e, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,
               cudaStream_t s);
 
 // ---- outer CG steps (adaptive_cg.hpp:126-233), fp64 -------------------------

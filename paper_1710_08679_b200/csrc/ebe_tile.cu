@@ -43,6 +43,7 @@ namespace tsg {
 namespace {
 
 constexpr int kChunkDefault = 32;  // elements per chunk (one lane group each)
+constexpr int kChunkTet4 = 32;  // 64 and 128 measured slower (profiles/r01_ebe_tile.txt)
 
 __device__ __forceinline__ void cpa16(void* s, const void* g, int src) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(s));
@@ -352,14 +353,18 @@ bool launch_tile_c(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, 
 template <typename T, typename V, int NPE, int B>
 bool launch_tile_b(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, cudaStream_t s, int32_t c0,
                    int32_t c1) {
-  static const bool rowred = [] { const char* e = std::getenv("TSGPU_TILE_ROWRED"); return e && e[0] == '1'; }();
-  if (plan.chunk == 16)
-    return rowred ? launch_tile_c<T, V, NPE, B, 16, true>(op, plan, u, f, s, c0, c1)
-                  : launch_tile_c<T, V, NPE, B, 16, false>(op, plan, u, f, s, c0, c1);
-  if (plan.chunk == 32)
-    return rowred ? launch_tile_c<T, V, NPE, B, 32, true>(op, plan, u, f, s, c0, c1)
-                  : launch_tile_c<T, V, NPE, B, 32, false>(op, plan, u, f, s, c0, c1);
-  return false;
+  constexpr int TPE = TileCfg<T, V, NPE, B, 1>::TPE;
+  switch (plan.chunk) {
+    case 16: return launch_tile_c<T, V, NPE, B, 16, false>(op, plan, u, f, s, c0, c1);
+    case 32: return launch_tile_c<T, V, NPE, B, 32, false>(op, plan, u, f, s, c0, c1);
+    case 64:
+      if constexpr (64 * TPE <= 1024) return launch_tile_c<T, V, NPE, B, 64, false>(op, plan, u, f, s, c0, c1);
+      return false;
+    case 128:
+      if constexpr (128 * TPE <= 1024) return launch_tile_c<T, V, NPE, B, 128, false>(op, plan, u, f, s, c0, c1);
+      return false;
+    default: return false;
+  }
 }
 
 template <typename T, typename V, int NPE>
@@ -401,8 +406,13 @@ void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int con
   const int npe = op.npe;
   const int64_t E = op.n_elems;
   auto plan = std::make_unique<EbeTilePlan>();
-  int kChunk = kChunkDefault;
-  if (const char* e = std::getenv("TSGPU_TILE_CHUNK")) kChunk = std::atoi(e) == 16 ? 16 : 32;
+  // elements per chunk: tet10 32 (one 256-thread block at r = 16); the light tet4
+  // product amortises the per-chunk pipeline over more elements
+  int kChunk = npe == 4 ? kChunkTet4 : kChunkDefault;
+  if (const char* e = std::getenv(npe == 4 ? "TSGPU_TILE_CHUNK4" : "TSGPU_TILE_CHUNK")) {
+    const int c = std::atoi(e);
+    kChunk = (c == 16 || c == 32 || c == 64 || c == 128) ? c : kChunk;
+  }
   plan->chunk = kChunk;
   // chunks never straddle the element-group boundary (boundary / interior sweeps)
   std::vector<int64_t> cstart;

@@ -37,18 +37,18 @@ InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t 
                      T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s) {
   if (max_iter < 1) validation("inner_pcg: max_iter must be >= 1");
   A(u, e);
-  pcg_init<T>(r, e, n, B, cs, ws, s);
+  pcg_init<T>(inv, r, e, n, B, cs, ws, s);
   InnerStats st;
   const double tol2 = tol * tol;
   double ratio = read_status(ws, s).ratio;
   if (std::isnan(ratio)) fail(TS_ERR_NONFINITE, "inner_pcg: non-finite initial residual");
   while (ratio > tol2 && st.iterations < max_iter) {
     const bool first = st.iterations == 0;
-    pcg_rho<T>(inv, e, n, B, first, cs, ws, s);
+    pcg_rho(B, first, cs, ws, s);
     pcg_direction<T>(inv, e, p, n, B, first, cs, s);
     A(p, q);
     pcg_gamma<T>(p, q, n, B, cs, ws, s);
-    pcg_update<T>(e, u, p, q, n, B, cs, ws, s);
+    pcg_update<T>(inv, e, u, p, q, n, B, cs, ws, s);
     const PcgStatus& ps = read_status(ws, s);
     if (ps.breakdown_col >= 0)
       fail(TS_ERR_BREAKDOWN, "inner_pcg: breakdown (p,Ap) <= 0 at iteration " + std::to_string(st.iterations + 1) +
