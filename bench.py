@@ -589,7 +589,8 @@ def main():
                     "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes, "entry": "ts_ebe_apply_host"},
             "roofline": {"bound": "hbm", "achieved": round(B / kms / 1e6, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(B / kms / 1e6 / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": (f"k_ebe_tile<float,float2,10,{r},32>" if args.prec == 32 and r <= 4 else
+                         "kernel": (f"k_ebe_pair<{'float,float2' if args.prec == 32 else 'double,double'},10,{r}>"
+                                    if r in (1, 2, 4, 8, 16) else
                                     f"k_ebe_fast<{'float,float2' if args.prec == 32 else 'double,double'},10,12,{r}>"),
                          "kernel_ms": round(kms, 4), "alg_bytes_per_launch": int(B)},
             "cpu_baseline": cpu,

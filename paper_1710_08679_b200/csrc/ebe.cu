@@ -19,6 +19,7 @@
 //  * f starts as the masked identity (ebe_operator.hpp:96-110) and element
 //    contributions land through fire-and-forget vector REDs in L2.
 #include <algorithm>
+#include <parallel/algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1130,7 +1131,9 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
   // Default dispatch (measured, profiles/r01_ebe_tile.txt): the chunk-tiled sweep
   // wins for the tet4 level-1 operator and for narrow fp32 batches; the
   // element-parallel RED sweep wins for wide tet10 batches.
-  if (op.kernel == 5 || (op.kernel == 6 && (op.order == 1 || (op.prec == 32 && batch <= 4))))
+  // default (6): face-pair sweep (ebe_pair.cu) — measured fastest for every order / batch it covers
+  if (op.kernel == 7 || op.kernel == 6) done = ebe_pair_apply(op, u, f, batch, s, part);
+  if (!done && (op.kernel == 5 || (op.kernel == 6 && (op.order == 1 || (op.prec == 32 && batch <= 4)))))
     done = ebe_tile_apply(op, u, f, batch, s, part);
   if (!done && op.kernel >= 3 && op.kernel != 4)
     done = (op.order == 2)
@@ -1254,17 +1257,24 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   std::vector<unsigned char> coef(E * 12 * ts, 0);
   if (dof_mask) op->host_mask.assign(dof_mask, dof_mask + 3 * static_cast<size_t>(op->n_nodes));
   auto rnd = [prec](double x) { return prec == 32 ? static_cast<double>(static_cast<float>(x)) : x; };
-  for (size_t e = 0; e < E; ++e) {
+  for (size_t e = 0; e < E; ++e) {  // validation first (exceptions stay out of the parallel loop)
     const int32_t mid = m.material_id[e];
     if (mid < 0 || mid >= n_mat)
       validation("ebe: element " + std::to_string(e) + " references material " + std::to_string(mid) +
                  " but only " + std::to_string(n_mat) + " defined");
-    const int32_t* t = m.tets10.data() + 10 * e;
     for (int a = 0; a < npe; ++a) {
-      const int32_t node = t[a];
+      const int32_t node = m.tets10[10 * e + a];
       if (node < 0 || node >= op->n_nodes)
         validation("ebe: element " + std::to_string(e) + " references node " + std::to_string(node) +
                    " out of range");
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (size_t e = 0; e < E; ++e) {
+    const int32_t mid = m.material_id[e];
+    const int32_t* t = m.tets10.data() + 10 * e;
+    for (int a = 0; a < npe; ++a) {
+      const int32_t node = t[a];
       int32_t word = node;
       if (dof_mask)
         for (int c = 0; c < 3; ++c)
@@ -1303,17 +1313,22 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
       }
     }
   }
+  setup_mark("ebe: element records");
   // Morton (Z-order) element ordering of centroids: consecutive elements — and
   // so each block's cluster — are spatially compact, which minimises the
   // cluster node count (scatter traffic) and keeps gathers L2-local.
   {
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     std::vector<double> cen(3 * E);
+#pragma omp parallel for schedule(static)
     for (size_t e = 0; e < E; ++e)
       for (int c = 0; c < 3; ++c) {
         double x = 0.0;
         for (int a = 0; a < 4; ++a) x += m.coords[3 * static_cast<size_t>(m.tets10[10 * e + a]) + c];
         cen[3 * e + c] = 0.25 * x;
+      }
+    for (size_t e = 0; e < E; ++e)
+      for (int c = 0; c < 3; ++c) {
         lo[c] = std::min(lo[c], cen[3 * e + c]);
         hi[c] = std::max(hi[c], cen[3 * e + c]);
       }
@@ -1332,13 +1347,14 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     // (group, Morton key, id): a partitioned operator keeps its boundary elements
     // (group 0) ahead of the interior ones so the two sweep separately
     std::vector<std::tuple<uint8_t, uint64_t, int32_t>> key(E);
+#pragma omp parallel for schedule(static)
     for (size_t e = 0; e < E; ++e) {
       uint64_t k = 0;
       for (int c = 0; c < 3; ++c)
         k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
       key[e] = {elem_group ? elem_group[e] : uint8_t(0), k, static_cast<int32_t>(e)};
     }
-    std::sort(key.begin(), key.end());
+    __gnu_parallel::sort(key.begin(), key.end());
     op->group_split = 0;
     for (size_t i = 0; i < E; ++i)
       if (std::get<0>(key[i]) == 0) op->group_split = static_cast<int32_t>(i + 1);
@@ -1346,6 +1362,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     std::vector<int32_t> hconn2(op->host_conn.size());
     std::vector<double> c642(op->coef64.size());
     std::vector<unsigned char> coef2(coef.size());
+#pragma omp parallel for schedule(static)
     for (size_t i = 0; i < E; ++i) {
       const size_t e = static_cast<size_t>(std::get<2>(key[i]));
       std::memcpy(&conn2[i * cs], &conn[e * cs], cs * sizeof(int32_t));
@@ -1358,11 +1375,12 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->coef64.swap(c642);
     coef.swap(coef2);
   }
-  if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5 : 6;
+  if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5 : std::string(k) == "pair" ? 7 : 6;
   {
     // fast-kernel layout: 3*node per local node, then the dof-mask word (bit 3a+c)
     const int cs3 = order == 1 ? 8 : 12;
     std::vector<int32_t> conn3(E * cs3, 0);
+#pragma omp parallel for schedule(static)
     for (size_t e = 0; e < E; ++e) {
       uint32_t mw = 0;
       for (int a = 0; a < npe; ++a) {
@@ -1374,6 +1392,10 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
       conn3[e * cs3 + npe] = static_cast<int32_t>(mw);
     }
     op->conn3.upload(conn3);
+  }
+  if (op->kernel == 4) {  // slab-gated persistent sweep only
+    const int cs3 = order == 1 ? 8 : 12;
+    (void)cs3;
     // slabs of consecutive (Morton) elements and the nodes each slab touches
     // first: the fast kernel initialises slab j+1's nodes while sweeping slab j
     const int64_t f_bytes = 3 * int64_t(op->n_nodes) * 16 * ts;  // sized for 16 cases
@@ -1409,7 +1431,12 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->slab_init_ptr_dev.upload(op->slab_init_ptr);
     op->slab_ready.alloc(S);
   }
-  build_tile_plan(*op, conn, cs);
+  setup_mark("ebe: morton + conn3");
+  // the tiled sweep's chunk records serve kernel 5, and kernel 6 batch widths the pair sweep does not cover
+  if (op->kernel == 5 || op->kernel == 6) build_tile_plan(*op, conn, cs);
+  setup_mark("ebe: tile plan");
+  if (op->kernel == 7 || op->kernel == 6) build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32);
+  setup_mark("ebe: pair plan");
   op->conn.upload(conn);
   op->coef.upload(coef);
   if (dof_mask) op->mask.upload(op->host_mask);

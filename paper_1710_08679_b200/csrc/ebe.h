@@ -34,6 +34,15 @@ struct EbeTilePlan {
   tsg::DevBuf<uint32_t> rec_off;  // [n_chunks + 1] in 16-byte units
 };
 
+// Face-sharing element pairs for the pair sweep (ebe_pair.cu).
+struct EbePairPlan {
+  int32_t n_units = 0;           // pairs, then singles, per element group
+  int32_t group_split = 0;       // units [0, split) cover element group 0
+  double paired_fraction = 0.0;  // elements that are in a pair
+  tsg::DevBuf<int32_t> conn;     // [units][16 | 8]: A's slots, B's own slots (3*node), mask words
+  tsg::DevBuf<unsigned char> coef;  // [units][24] of T: A and B coefficient records
+};
+
 struct ts_ebe {
   int order = 2;   // 1 = tet4 on the vertex grid, 2 = tet10
   int npe = 10;
@@ -58,8 +67,9 @@ struct ts_ebe {
   mutable std::mutex clusters_mu;
   std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, the default kernel)
   int32_t group_split = 0;              // elements [0, split) = group 0 (partition boundary), rest group 1
+  std::unique_ptr<EbePairPlan> pair;    // face-sharing pairs (kernel 7)
   int kernel = 6;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised, 4 slab-gated,
-                   // 5 tiled, 6 auto (tiled for tet4 / narrow fp32 batches, else 3) = default
+                   // 5 tiled, 6 auto (tiled for tet4 / narrow fp32 batches, else 3) = default, 7 pairs
   mutable std::mutex host_mu;            // guards the host-entry staging buffers
   mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
   bool timing = false;
@@ -83,6 +93,10 @@ bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cud
 // element-group sweep of a partitioned operator (part -1 all, 0 boundary, 1 interior)
 void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part, bool init);
 void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int conn_stride);
+// pair sweep (ebe_pair.cu); false when no instance covers this batch width
+bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
+void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn_words, int cs,
+                     const std::vector<double>& coef64, bool fp32);
 // elem_group (nullable, [E] in {0,1}): group-0 elements sweep separately (boundary first)
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda,
                    const double* mu, const uint8_t* dof_mask, int prec, const uint8_t* elem_group = nullptr);

@@ -1,0 +1,503 @@
+// ebe_pair.cu — EBE sweep over face-sharing element pairs (tet10).
+//
+// Same product as k_ebe_fast (ebe_operator.hpp:143-188 semantics, lean exact
+// element math of element_kernels.cuh) but the unit of work is a PAIR of
+// tetrahedra that share a face. The setup renumbers both elements' local nodes
+// (a relabelling leaves K_e unchanged up to the same permutation of rows and
+// columns; gradients are taken in the new order, the volume keeps the original
+// orientation) so that the shared face is A's vertices (1,2,3) and B's vertices
+// (0,1,2): the 6 shared nodes (3 vertices + 3 edge midpoints) then occupy fixed
+// register slots. A lane group gathers 14 node rows instead of 20, computes A,
+// reduces A's 4 unshared rows, keeps A's 6 face rows in registers, computes B,
+// adds them and reduces B's 10 rows: 14 vector-RED node rows per pair instead
+// of 20 — the L2 atomic traffic that bounds the element-parallel sweep drops by
+// 30 % (profiles/r01_ebe_memory_paths.txt). Unpaired elements run as singles.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <tuple>
+#include <vector>
+
+#include "ebe.h"
+#include "element_kernels.cuh"
+
+namespace tsg {
+namespace {
+
+constexpr int kHasB = 1 << 31;
+
+// Slot geometry of a pair, per element order. A's shared face is its vertices
+// (1,2,3) (+ edges 5, 9, 8 for tet10); B's is (0,1,2) (+ edges 4, 5, 6).
+template <int NPE> struct PairGeo;
+template <> struct PairGeo<10> {
+  static constexpr int NR = 14;        // gathered node rows: A's 10, B's own 3,7,8,9
+  static constexpr int WORDS = 16;     // NR node words, A mask bits, B own mask bits | hasB
+  static constexpr int NA_OWN = 4, NFACE = 6, NB_OWN = 4;
+  __host__ __device__ static constexpr int a_own(int k) { return k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : 7; }
+  __host__ __device__ static constexpr int a_face(int k) { return k < 3 ? k + 1 : k == 3 ? 5 : k == 4 ? 9 : 8; }
+  __host__ __device__ static constexpr int b_face(int k) { return k < 3 ? k : k + 1; }
+  __host__ __device__ static constexpr int b_own(int k) { return k == 0 ? 3 : k + 6; }
+  // gathered-row index of B's slot s
+  __host__ __device__ static constexpr int b_row(int s) {
+    return s == 0 ? 1 : s == 1 ? 2 : s == 2 ? 3 : s == 3 ? 10 : s == 4 ? 5 : s == 5 ? 9 : s == 6 ? 8 : s == 7 ? 11 : s == 8 ? 12 : 13;
+  }
+};
+template <> struct PairGeo<4> {
+  static constexpr int NR = 5;
+  static constexpr int WORDS = 8;
+  static constexpr int NA_OWN = 1, NFACE = 3, NB_OWN = 1;
+  __host__ __device__ static constexpr int a_own(int) { return 0; }
+  __host__ __device__ static constexpr int a_face(int k) { return k + 1; }
+  __host__ __device__ static constexpr int b_face(int k) { return k; }
+  __host__ __device__ static constexpr int b_own(int) { return 3; }
+  __host__ __device__ static constexpr int b_row(int s) { return s < 3 ? s + 1 : 4; }
+};
+
+__device__ __forceinline__ void cpa(void* s, const void* g, int src, int bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(s));
+  if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a), "l"(g), "r"(src) : "memory");
+  else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(a), "l"(g), "r"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(a), "l"(g), "r"(src) : "memory");
+}
+
+__device__ __forceinline__ void red_p(float2* p, float2 v, unsigned skip) {
+  asm volatile("{ .reg .pred q; setp.eq.u32 q, %3, 0; @q red.global.add.v2.f32 [%0], {%1, %2}; }" ::"l"(p),
+               "f"(v.x), "f"(v.y), "r"(skip)
+               : "memory");
+}
+__device__ __forceinline__ void red_p(float* p, float v, unsigned skip) {
+  asm volatile("{ .reg .pred q; setp.eq.u32 q, %2, 0; @q red.global.add.f32 [%0], %1; }" ::"l"(p), "f"(v), "r"(skip)
+               : "memory");
+}
+__device__ __forceinline__ void red_p(double* p, double v, unsigned skip) {
+  asm volatile("{ .reg .pred q; setp.eq.u32 q, %2, 0; @q red.global.add.f64 [%0], %1; }" ::"l"(p), "d"(v), "r"(skip)
+               : "memory");
+}
+
+template <typename T, typename V, int NPE, int B>
+__global__ void __launch_bounds__(128, 2)
+k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32_t p_begin, int32_t p_end,
+           const T* __restrict__ u, T* __restrict__ f) {
+  using O = LaneOps<V>;
+  using Geo = PairGeo<NPE>;
+  constexpr int CPT = O::kCols;
+  constexpr int NR = Geo::NR, NIN = NR * 3;  // gathered node rows / dofs per pair
+  constexpr int kPairWords = Geo::WORDS;
+  constexpr int MW = NR;                     // index of A's mask word (B's own follows)
+  constexpr int NT = 128;
+  constexpr int TPE = (B + CPT - 1) / CPT;
+  static_assert(NT % TPE == 0, "lane groups must tile the block");
+  constexpr int GROUPS = NT / TPE;
+  constexpr int TPC = 16 / sizeof(T);
+  constexpr int CHUNKS = 24 / TPC;  // two 12-scalar coefficient records
+  extern __shared__ __align__(16) unsigned char smem[];
+  V* ubuf = reinterpret_cast<V*>(smem);                                    // [2][NIN][NT]
+  T* cbuf = reinterpret_cast<T*>(smem + 2 * NIN * NT * sizeof(V));          // [2][GROUPS][24]
+  int32_t* nbuf = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(cbuf) +
+                                             2 * GROUPS * 24 * sizeof(T));  // [2][GROUPS][16]
+  const int grp = threadIdx.x / TPE;
+  const int lane = threadIdx.x % TPE;
+  const int G = gridDim.x * GROUPS;
+  const int col = lane * CPT;
+  int e = p_begin + blockIdx.x * GROUPS + grp;
+
+  int32_t nd[kPairWords];
+  auto load_conn = [&](int ee) {
+    if (ee < p_end) {
+      const int4* c4 = reinterpret_cast<const int4*>(pconn + static_cast<size_t>(ee) * kPairWords);
+#pragma unroll
+      for (int q = 0; q < kPairWords / 4; ++q) {
+        const int4 v = __ldg(c4 + q);
+        nd[4 * q] = v.x; nd[4 * q + 1] = v.y; nd[4 * q + 2] = v.z; nd[4 * q + 3] = v.w;
+      }
+    }
+  };
+  auto issue = [&](int ee, int stage) {
+    if (ee < p_end) {
+      if (lane == 0) {
+        int4* dst = reinterpret_cast<int4*>(nbuf + (stage * GROUPS + grp) * kPairWords);
+#pragma unroll
+        for (int q = 0; q < kPairWords / 4; ++q)
+          dst[q] = make_int4(nd[4 * q], nd[4 * q + 1], nd[4 * q + 2], nd[4 * q + 3]);
+      }
+      for (int q = lane; q < CHUNKS; q += TPE)
+        cpa(cbuf + (stage * GROUPS + grp) * 24 + q * TPC, pcoef + static_cast<size_t>(ee) * 24 + q * TPC, 16, 16);
+      V* dst = ubuf + stage * NIN * NT + threadIdx.x;
+      const unsigned ma = static_cast<unsigned>(nd[MW]), mb = static_cast<unsigned>(nd[MW + 1]);
+      const int nrows = (mb & unsigned(kHasB)) ? NR : NPE;
+#pragma unroll
+      for (int a = 0; a < NR; ++a) {
+        if (a >= nrows) break;
+        const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const unsigned m = a < NPE ? (ma >> (3 * a + c)) & 1u : (mb >> (3 * (a - NPE) + c)) & 1u;
+          cpa(dst + (a * 3 + c) * NT, row + c * B, m ? 0 : int(sizeof(V)), sizeof(V));
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  load_conn(e);
+  issue(e, 0);
+  load_conn(e + G);
+  int s = 0;
+  while (__any_sync(0xffffffffu, e < p_end)) {
+    const int en = e + G;
+    issue(en, s ^ 1);
+    load_conn(en + G);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    if (e < p_end) {
+      const T* cf = cbuf + (s * GROUPS + grp) * 24;
+      const int32_t* w = nbuf + (s * GROUPS + grp) * kPairWords;
+      const V* src = ubuf + s * NIN * NT + threadIdx.x;
+      const unsigned ma = static_cast<unsigned>(w[MW]), mb = static_cast<unsigned>(w[MW + 1]);
+      const bool hasB = (mb & unsigned(kHasB)) != 0;
+      V carry[Geo::NFACE][3];  // A's face rows (= B's face rows)
+      {
+        V b[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cf[3 * k + d]);
+        const V lp = O::splat(cf[9]), mp = O::splat(cf[10]);
+        V uu[NPE][3];
+#pragma unroll
+        for (int a = 0; a < NPE; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) uu[a][c] = src[(a * 3 + c) * NT];
+        V ff[NPE][3];
+        if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
+        else tet4_product<V>(uu, b, lp, mp, ff);
+#pragma unroll
+        for (int k = 0; k < Geo::NA_OWN; ++k) {
+          const int a = Geo::a_own(k);
+          T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], (ma >> (3 * a + c)) & 1u);
+        }
+#pragma unroll
+        for (int k = 0; k < Geo::NFACE; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) carry[k][c] = ff[Geo::a_face(k)][c];
+      }
+      if (hasB) {
+        const T* cfb = cf + 12;
+        V b[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cfb[3 * k + d]);
+        const V lp = O::splat(cfb[9]), mp = O::splat(cfb[10]);
+        V uu[NPE][3];
+#pragma unroll
+        for (int a = 0; a < NPE; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) uu[a][c] = src[(Geo::b_row(a) * 3 + c) * NT];
+        V ff[NPE][3];
+        if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
+        else tet4_product<V>(uu, b, lp, mp, ff);
+#pragma unroll
+        for (int k = 0; k < Geo::NFACE; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ff[Geo::b_face(k)][c] = O::add(ff[Geo::b_face(k)][c], carry[k][c]);
+#pragma unroll
+        for (int a = 0; a < NPE; ++a) {
+          const int r = Geo::b_row(a);
+          T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[r])) * B + col;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const unsigned m = r < NPE ? (ma >> (3 * r + c)) & 1u : (mb >> (3 * (r - NPE) + c)) & 1u;
+            red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], m);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < Geo::NFACE; ++k) {
+          const int a = Geo::a_face(k);
+          T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(row + c * B), carry[k][c], (ma >> (3 * a + c)) & 1u);
+        }
+      }
+    }
+    __syncwarp();
+    e = en;
+    s ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename T, typename V, int NPE, int B>
+bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p0, int32_t p1) {
+  constexpr int CPT = LaneOps<V>::kCols;
+  constexpr int TPE = (B + CPT - 1) / CPT;
+  if constexpr (128 % TPE != 0 || TPE * CPT != B) {
+    return false;
+  } else {
+    using Geo = PairGeo<NPE>;
+    constexpr int NT = 128, GROUPS = NT / TPE;
+    const size_t smem = 2 * (size_t(Geo::NR) * 3 * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
+                             size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
+    auto kern = k_ebe_pair<T, V, NPE, B>;
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+      int dev = 0;
+      TS_CUDA(cudaGetDevice(&dev));
+      TS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+      per_sm = std::max(per_sm, 1);
+    }
+    if (p1 <= p0) return true;
+    const int64_t need = (int64_t(p1 - p0) + GROUPS - 1) / GROUPS;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
+    kern<<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()), p0, p1, u, f);
+    TS_CUDA_LAUNCH();
+    return true;
+  }
+}
+
+template <typename T, typename V, int NPE>
+bool launch_pair_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t p0, int32_t p1) {
+  switch (batch) {
+    case 1: return launch_pair_b<T, T, NPE, 1>(op, u, f, s, p0, p1);
+    case 2: return launch_pair_b<T, V, NPE, 2>(op, u, f, s, p0, p1);
+    case 4: return launch_pair_b<T, V, NPE, 4>(op, u, f, s, p0, p1);
+    case 8: return launch_pair_b<T, V, NPE, 8>(op, u, f, s, p0, p1);
+    case 16: return launch_pair_b<T, V, NPE, 16>(op, u, f, s, p0, p1);
+    default: return false;
+  }
+}
+
+bool inv3(const double j[3][3], double inv[3][3]) {
+  const double d = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) - j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
+                   j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
+  if (d == 0.0) return false;
+  const double id = 1.0 / d;
+  inv[0][0] = (j[1][1] * j[2][2] - j[1][2] * j[2][1]) * id;
+  inv[0][1] = (j[0][2] * j[2][1] - j[0][1] * j[2][2]) * id;
+  inv[0][2] = (j[0][1] * j[1][2] - j[0][2] * j[1][1]) * id;
+  inv[1][0] = (j[1][2] * j[2][0] - j[1][0] * j[2][2]) * id;
+  inv[1][1] = (j[0][0] * j[2][2] - j[0][2] * j[2][0]) * id;
+  inv[1][2] = (j[0][2] * j[1][0] - j[0][0] * j[1][2]) * id;
+  inv[2][0] = (j[1][0] * j[2][1] - j[1][1] * j[2][0]) * id;
+  inv[2][1] = (j[0][1] * j[2][0] - j[0][0] * j[2][1]) * id;
+  inv[2][2] = (j[0][0] * j[1][1] - j[0][1] * j[1][0]) * id;
+  return true;
+}
+
+}  // namespace
+
+bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part) {
+  if (!op.pair) return false;
+  const int32_t p0 = part == 1 ? op.pair->group_split : 0;
+  const int32_t p1 = part == 0 ? op.pair->group_split : op.pair->n_units;
+  if (op.prec == 32) {
+    const float* uu = static_cast<const float*>(u);
+    float* ff = static_cast<float*>(f);
+    return op.order == 2 ? launch_pair_t<float, float2, 10>(op, uu, ff, batch, s, p0, p1)
+                         : launch_pair_t<float, float2, 4>(op, uu, ff, batch, s, p0, p1);
+  }
+  const double* uu = static_cast<const double*>(u);
+  double* ff = static_cast<double*>(f);
+  return op.order == 2 ? launch_pair_t<double, double, 10>(op, uu, ff, batch, s, p0, p1)
+                       : launch_pair_t<double, double, 4>(op, uu, ff, batch, s, p0, p1);
+}
+
+// Pair plan: greedy face matching in (group, Morton) order, then per unit the
+// permuted connectivity words (3*node), mask bits and coefficient records.
+//   conn_words: Morton-ordered [E][cs] node | mask << 28; coef64: Morton-ordered
+//   [E][12] fp64 (b rows, lambda V, mu V, V); vrnd: T-rounded vertex coordinates.
+void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn_words, int cs,
+                     const std::vector<double>& coef64, bool fp32) {
+  const int npe = op.npe;
+  const int NR = npe == 10 ? PairGeo<10>::NR : PairGeo<4>::NR;
+  const int kPairWords = npe == 10 ? PairGeo<10>::WORDS : PairGeo<4>::WORDS;
+  const int64_t E = op.n_elems;
+  static constexpr int ev[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
+  auto node = [&](int64_t e, int a) { return static_cast<int32_t>(conn_words[e * cs + a] & 0x0FFFFFFF); };
+  auto mbits = [&](int64_t e, int a) { return (static_cast<uint32_t>(conn_words[e * cs + a]) >> 28) & 7u; };
+  auto edge_slot = [&](int p, int q) {
+    for (int k = 0; k < 6; ++k)
+      if ((ev[k][0] == p && ev[k][1] == q) || (ev[k][0] == q && ev[k][1] == p)) return 4 + k;
+    return -1;
+  };
+  // face adjacency through the vertex -> element incidence: the element across
+  // face k (opposite local vertex k) is the other element containing its 3 vertices
+  int32_t nv = 0;
+  for (int64_t e = 0; e < E; ++e)
+    for (int a = 0; a < 4; ++a) nv = std::max(nv, node(e, a) + 1);
+  std::vector<int32_t> vptr(size_t(nv) + 1, 0), velem(size_t(E) * 4);
+  for (int64_t e = 0; e < E; ++e)
+    for (int a = 0; a < 4; ++a) ++vptr[node(e, a) + 1];
+  for (int32_t v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
+  {
+    std::vector<int32_t> cur(vptr.begin(), vptr.end() - 1);
+    for (int64_t e = 0; e < E; ++e)
+      for (int a = 0; a < 4; ++a) velem[cur[node(e, a)]++] = static_cast<int32_t>(e);
+  }
+  std::vector<std::array<int32_t, 4>> nbr(E);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < E; ++e)
+    for (int k = 0; k < 4; ++k) {
+      int32_t f3[3], n = 0;
+      for (int a = 0; a < 4; ++a)
+        if (a != k) f3[n++] = node(e, a);
+      int32_t found = -1;
+      for (int32_t p = vptr[f3[0]]; p < vptr[f3[0] + 1] && found < 0; ++p) {
+        const int32_t j = velem[p];
+        if (j == e) continue;
+        int hits = 0;
+        for (int a = 0; a < 4; ++a) {
+          const int32_t x = node(j, a);
+          hits += (x == f3[1]) + (x == f3[2]);
+        }
+        if (hits == 2) found = j;
+      }
+      nbr[e][k] = found;
+    }
+  auto group_of = [&](int64_t e) { return e < op.group_split ? 0 : 1; };
+  std::vector<int32_t> mate(E, -1);
+  std::vector<int8_t> mate_k(E, -1);
+  for (int64_t e = 0; e < E; ++e) {
+    if (mate[e] >= 0) continue;
+    int best = -1;
+    int64_t bd = 0;
+    for (int k = 0; k < 4; ++k) {
+      const int32_t j = nbr[e][k];
+      if (j < 0 || j == e || mate[j] >= 0 || group_of(j) != group_of(e)) continue;
+      const int64_t d = std::llabs(int64_t(j) - e);
+      if (best < 0 || d < bd) {
+        best = k;
+        bd = d;
+      }
+    }
+    if (best >= 0) {
+      const int32_t j = nbr[e][best];
+      mate[e] = j;
+      mate[j] = static_cast<int32_t>(e);
+      mate_k[e] = static_cast<int8_t>(best);
+    }
+  }
+  // units in group order: pairs (led by the lower index), then singles
+  std::vector<int32_t> units;  // leader element; singles encoded as ~e
+  int32_t split = 0;
+  for (int g = 0; g < 2; ++g) {
+    const int64_t lo = g == 0 ? 0 : op.group_split, hi = g == 0 ? op.group_split : E;
+    for (int64_t e = lo; e < hi; ++e)
+      if (mate[e] > e) units.push_back(static_cast<int32_t>(e));
+    for (int64_t e = lo; e < hi; ++e)
+      if (mate[e] < 0) units.push_back(~static_cast<int32_t>(e));
+    if (g == 0) split = static_cast<int32_t>(units.size());
+  }
+  const int32_t U = static_cast<int32_t>(units.size());
+  std::vector<int32_t> pc(size_t(U) * kPairWords, 0);
+  const size_t ts = fp32 ? 4 : 8;
+  std::vector<unsigned char> pcf(size_t(U) * 24 * ts, 0);
+  auto rnd = [fp32](double x) { return fp32 ? static_cast<double>(static_cast<float>(x)) : x; };
+  // coefficient record of element e with local vertex order perm (orientation from the original order)
+  auto record = [&](int64_t e, const int perm[4], unsigned char* dst) -> bool {
+    double v[4][3], j[3][3], inv[3][3];
+    for (int a = 0; a < 4; ++a)
+      for (int c = 0; c < 3; ++c) v[a][c] = rnd(m.coords[3 * size_t(op.host_conn[e * npe + perm[a]]) + c]);
+    for (int c = 0; c < 3; ++c)
+      for (int r = 0; r < 3; ++r) j[r][c] = v[c + 1][r] - v[0][r];
+    if (!inv3(j, inv)) return false;
+    double rec[12];
+    for (int k = 0; k < 3; ++k)
+      for (int d = 0; d < 3; ++d) rec[3 * k + d] = inv[k][d];
+    const double scale = npe == 10 ? 1.0 / 20.0 : 1.0;
+    rec[9] = coef64[12 * e + 9] * scale;   // lambda V (/ 20 for tet10), original orientation
+    rec[10] = coef64[12 * e + 10] * scale; // mu V
+    rec[11] = 0.0;
+    for (int q = 0; q < 12; ++q) {
+      if (fp32) {
+        const float x = static_cast<float>(rec[q]);
+        std::memcpy(dst + q * 4, &x, 4);
+      } else {
+        std::memcpy(dst + q * 8, &rec[q], 8);
+      }
+    }
+    return true;
+  };
+  auto slot_node = [&](int64_t e, const int perm[4], int s) -> std::pair<int32_t, uint32_t> {
+    const int a = s < 4 ? perm[s] : edge_slot(perm[ev[s - 4][0]], perm[ev[s - 4][1]]);
+    return {node(e, a), mbits(e, a)};
+  };
+  bool bad = false;
+#pragma omp parallel for schedule(static) reduction(|| : bad)
+  for (int32_t i = 0; i < U; ++i) {
+    int32_t* w = pc.data() + size_t(i) * kPairWords;
+    unsigned char* cf = pcf.data() + size_t(i) * 24 * ts;
+    const bool single = units[i] < 0;
+    const int64_t a = single ? ~units[i] : units[i];
+    int pa[4] = {0, 1, 2, 3};
+    uint32_t ma = 0, mb = 0;
+    if (!single) {
+      const int k = mate_k[a];
+      const int64_t b = mate[a];
+      // A: (opposite vertex k, then the face vertices in A's order); B: the face vertices in A's order, then its 4th
+      int n = 1;
+      pa[0] = k;
+      for (int q = 0; q < 4; ++q)
+        if (q != k) pa[n++] = q;
+      int pb[4];
+      for (int q = 1; q < 4; ++q) {
+        pb[q - 1] = -1;
+        for (int r = 0; r < 4; ++r)
+          if (node(b, r) == node(a, pa[q])) pb[q - 1] = r;
+        if (pb[q - 1] < 0) bad = true;
+      }
+      if (pb[0] < 0 || pb[1] < 0 || pb[2] < 0) continue;
+      for (int r = 0; r < 4; ++r)
+        if (r != pb[0] && r != pb[1] && r != pb[2]) pb[3] = r;
+      for (int s = 0; s < npe; ++s) {
+        const auto [nd, mk] = slot_node(a, pa, s);
+        w[s] = 3 * nd;
+        ma |= mk << (3 * s);
+      }
+      const int nbown = NR - npe;
+      for (int q = 0; q < nbown; ++q) {
+        const int sl = npe == 10 ? PairGeo<10>::b_own(q) : PairGeo<4>::b_own(q);
+        const auto [nd, mk] = slot_node(b, pb, sl);
+        w[npe + q] = 3 * nd;
+        mb |= mk << (3 * q);
+      }
+      // the shared face: B's face slots are A's face slots
+      const int nface = npe == 10 ? PairGeo<10>::NFACE : PairGeo<4>::NFACE;
+      for (int q = 0; q < nface; ++q) {
+        const int bs = npe == 10 ? PairGeo<10>::b_face(q) : PairGeo<4>::b_face(q);
+        const int as = npe == 10 ? PairGeo<10>::a_face(q) : PairGeo<4>::a_face(q);
+        if (slot_node(b, pb, bs).first * 3 != w[as]) bad = true;
+      }
+      mb |= uint32_t(kHasB);
+      bad = bad || !record(a, pa, cf) || !record(b, pb, cf + 12 * ts);
+    } else {
+      for (int s = 0; s < npe; ++s) {
+        const auto [nd, mk] = slot_node(a, pa, s);
+        w[s] = 3 * nd;
+        ma |= mk << (3 * s);
+      }
+      bad = bad || !record(a, pa, cf);
+    }
+    w[NR] = static_cast<int32_t>(ma);
+    w[NR + 1] = static_cast<int32_t>(mb);
+  }
+  if (bad) validation("pair plan: inconsistent face pairing or degenerate element");
+  auto plan = std::make_unique<EbePairPlan>();
+  plan->n_units = U;
+  plan->group_split = split;
+  int64_t paired = 0;
+  for (int32_t x : units) paired += x >= 0 ? 2 : 0;
+  plan->paired_fraction = E ? double(paired) / double(E) : 0.0;
+  plan->conn.upload(pc);
+  plan->coef.upload(pcf);
+  op.pair = std::move(plan);
+}
+
+}  // namespace tsg

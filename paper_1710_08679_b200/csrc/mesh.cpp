@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // mesh.cpp — host mesh container and the layered box generator.
 //
 // generate_box_mesh reproduces the reference numbering exactly
@@ -160,6 +163,15 @@ Mesh generate_box_mesh(const double ext[3], const int32_t div[3],
     }
   }
   return m;
+}
+
+void setup_mark(const char* what) {
+  static const bool on = std::getenv("TSGPU_SETUP_PROFILE") != nullptr;
+  if (!on) return;
+  static thread_local auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - last).count());
+  last = now;
 }
 
 }  // namespace tsg

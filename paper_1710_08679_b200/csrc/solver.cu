@@ -157,9 +157,12 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   std::vector<uint8_t> mask1(mask0.begin(), mask0.begin() + 3 * size_t(V));
   lv->n0 = N;
   lv->n1 = V;
+  setup_mark("levels: start");
   lv->outer.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 64));
+  setup_mark("levels: outer operator");
   lv->l0.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 32));
   lv->l1.reset(ebe_create(m, 1, n_mat, lam, mu, mask1.data(), 32));
+  setup_mark("levels: l0 + l1 operators");
   // geometric P1 (prolongation.hpp:67-98): edge endpoints (vmin, vmax) + transpose
   {
     static constexpr int ee[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
@@ -195,9 +198,13 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   }
   // K1 -> aggregation -> Galerkin level 2 (adaptive_cg.hpp:53-60)
   const std::vector<double> lam_e = lame_per_element(m, n_mat, lam), mu_e = lame_per_element(m, n_mat, mu);
+  setup_mark("levels: P1");
   const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1);
+  setup_mark("levels: K1 assembly");
   Aggregation agg = aggregate_p1(k1, cfg.aggregate_target);
+  setup_mark("levels: aggregation");
   const BcsrD a2 = build_level2(k1, agg, mask1);
+  setup_mark("levels: Galerkin level 2");
   lv->n2 = agg.n_aggregates;
   lv->h_mask2 = coarse_mask(agg, mask1);
   lv->h_m2 = bcsr_block_jacobi_f32(a2);
@@ -225,6 +232,7 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   lv->mask2.upload(lv->h_mask2);
   lv->m0.alloc(9 * size_t(N));
   lv->m1.alloc(9 * size_t(V));
+  setup_mark("levels: uploads");
   ebe_block_jacobi(*lv->l0, lv->m0.get(), nullptr);
   ebe_block_jacobi(*lv->l1, lv->m1.get(), nullptr);
   // host setup copies no longer needed by the operators
@@ -232,6 +240,7 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
     std::vector<double>().swap(op->coef64);
   }
   TS_CUDA(cudaDeviceSynchronize());
+  setup_mark("levels: block Jacobi");
   lv->setup_s = secs(t0, clk::now());
   return lv.release();
 }

@@ -81,6 +81,9 @@ class DevBuf {
   size_t n_ = 0;
 };
 
+// setup phase timing to stderr when TSGPU_SETUP_PROFILE is set
+void setup_mark(const char* what);
+
 inline unsigned grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
   return static_cast<unsigned>(g < 1 ? 1 : g);

@@ -41,7 +41,7 @@ CASES = [
 ]
 
 
-KERNELS = ["auto", "fast", "tile"]  # TSGPU_EBE_KERNEL: default dispatch, element-parallel RED sweep, chunk-tiled sweep
+KERNELS = ["auto", "fast", "tile", "pair"]  # TSGPU_EBE_KERNEL: default dispatch, element-parallel RED sweep, chunk-tiled sweep
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
