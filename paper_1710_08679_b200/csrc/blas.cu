@@ -202,10 +202,14 @@ __global__ void __launch_bounds__(kFinThreads) k_rho_final(const double* partial
   beta[b] = first ? 0.0 : (rho_b[b] != 0.0 ? r / rho_b[b] : 0.0);  // pcg.hpp:74-80
 }
 
-// p = z + (T)beta p, z = M^-1 e (xpby_columns, vector_batch.hpp:86-97); first: p = z
+// p = z + (T)beta p, z = M^-1 e (xpby_columns, vector_batch.hpp:86-97); first: p = z.
+// q (optional): the next EBE product's starting value, the masked identity of
+// the new p (ebe_operator.hpp:96-110), written here so the product skips its own
+// initialisation pass (mask null: zeros).
 template <typename T, int W>
 __global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, T* __restrict__ p, int32_t n,
-                            int32_t B, int first, const double* __restrict__ beta) {
+                            int32_t B, int first, const double* __restrict__ beta, T* __restrict__ q,
+                            const uint8_t* __restrict__ mask) {
   const int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * W;
   if (it >= int64_t(n) * B) return;
   const int64_t node = it / B;
@@ -223,6 +227,13 @@ __global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, 
       for (int k = 0; k < W; ++k) z[i].v[k] = z[i].v[k] + static_cast<T>(beta[b0 + k]) * pp.v[k];
     }
     st<T, W>(pv + i * B, z[i]);
+    if (q) {
+      Pack<T, W> qi;
+      const bool keep = mask && mask[3 * node + i];
+#pragma unroll
+      for (int k = 0; k < W; ++k) qi.v[k] = keep ? z[i].v[k] : T(0);
+      st<T, W>(q + 3 * node * B + b0 + i * B, qi);
+    }
   }
 }
 
@@ -661,9 +672,9 @@ void pcg_rho(int32_t B, bool first, const ColScalars& cs, Workspace& ws, cudaStr
 
 template <typename T>
 void pcg_direction(const T* inv, const T* e, T* p, int32_t n, int32_t B, bool first, const ColScalars& cs,
-                   cudaStream_t s) {
+                   cudaStream_t s, T* q_init, const uint8_t* mask) {
   TS_WIDTH_DISPATCH(T, B, (k_direction<T, W><<<grid_for(int64_t(n) * B / W, 256), 256, 0, s>>>(
-                               inv, e, p, n, B, first ? 1 : 0, cs[ColScalars::BETA])));
+                               inv, e, p, n, B, first ? 1 : 0, cs[ColScalars::BETA], q_init, mask)));
   TS_CUDA_LAUNCH();
 }
 
@@ -711,7 +722,7 @@ void pcg_init(const T* inv, const T* r, T* e, int32_t n, int32_t B, const ColSca
 
 #define INST(T)                                                                                              \
   template void pcg_direction<T>(const T*, const T*, T*, int32_t, int32_t, bool, const ColScalars&,         \
-                                 cudaStream_t);                                                              \
+                                 cudaStream_t, T*, const uint8_t*);                                          \
   template void pcg_gamma<T>(const T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,           \
                              cudaStream_t);                                                                  \
   template void pcg_update<T>(const T*, T*, T*, const T*, const T*, int32_t, int32_t, const ColScalars&,     \

@@ -60,10 +60,11 @@ void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int3
 // rho_a = (M^-1 e, e) from the partials of the last pcg_init / pcg_update;
 // beta = first ? 0 : (rho_b != 0 ? rho_a / rho_b : 0)
 void pcg_rho(int32_t batch, bool first, const ColScalars& cs, Workspace& ws, cudaStream_t s);
-// p = M^-1 e + beta p  (first: p = M^-1 e)
+// p = M^-1 e + beta p  (first: p = M^-1 e); q_init (optional): masked identity of the new p
+// (zeros where mask is null), the starting value of the following EBE product
 template <typename T>
 void pcg_direction(const T* inv, const T* e, T* p, int32_t n_nodes, int32_t batch, bool first,
-                   const ColScalars& cs, cudaStream_t s);
+                   const ColScalars& cs, cudaStream_t s, T* q_init = nullptr, const uint8_t* mask = nullptr);
 // gamma = (p,q), plus ||p||^2, ||q||^2; alpha + stagnation/breakdown flags
 template <typename T>
 void pcg_gamma(const T* p, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,

@@ -133,9 +133,9 @@ struct DistEbe {
     if (side) cudaStreamDestroy(side);
   }
   template <typename T>
-  void apply(const T* u, T* f, int32_t B, cudaStream_t s) {
+  void apply(const T* u, T* f, int32_t B, cudaStream_t s, bool init = true) {
     const bool split = overlap && !halo.nbr.empty() && op->group_split < op->n_elems;
-    ebe_apply_part(*op, u, f, B, s, 0, true);  // masked identity + boundary elements
+    ebe_apply_part(*op, u, f, B, s, 0, init);  // masked identity (unless written by the caller) + boundary elements
     if (!split) {
       ebe_apply_part(*op, u, f, B, s, 1, false);
       halo.run<T>(f, 3 * B, B, mask, *comm, s);
@@ -220,7 +220,7 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
   const auto t0 = clk::now();
   L.ws.comm = nullptr;  // level 2 is replicated: identical on every rank, no collectives
   L.ws.owned = nullptr;
-  auto a2 = [&](const float* x, float* y) {
+  auto a2 = [&](const float* x, float* y, bool) {
     bcsr_apply_f32(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s);
   };
   const InnerStats s2 = inner_pcg<float>(a2, L.m2.get(), v.r2.get(), v.u2.get(), L.n2, B, cfg.level_tol[2],
@@ -229,14 +229,16 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
   L.ws.comm = L.comm;
   L.ws.owned = L.owned0.get();  // the vertex prefix of the level-0 flags
   p2_apply(v.u2.get(), v.u1.get(), L.agg.get(), L.n1, L.mask1.get(), B, s);
-  auto a1 = [&](const float* x, float* y) { L.l1.apply<float>(x, y, B, s); };
+  auto a1 = [&](const float* x, float* y, bool init) { L.l1.apply<float>(x, y, B, s, init); };
   const InnerStats s1 = inner_pcg<float>(a1, L.m1.get(), v.r1.get(), v.u1.get(), L.n1, B, cfg.level_tol[1],
-                                         cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), L.cs, L.ws, s);
+                                         cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), L.cs, L.ws, s,
+                                         true, L.mask1.get());
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), L.p1_ends.get(), L.n1, L.n0, L.mask0.get(), B, s);
-  auto a0 = [&](const float* x, float* y) { L.l0.apply<float>(x, y, B, s); };
+  auto a0 = [&](const float* x, float* y, bool init) { L.l0.apply<float>(x, y, B, s, init); };
   const InnerStats s0 = inner_pcg<float>(a0, L.m0.get(), v.r0.get(), v.u0.get(), L.n0, B, cfg.level_tol[0],
-                                         cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), L.cs, L.ws, s);
+                                         cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), L.cs, L.ws, s,
+                                         true, L.mask0.get());
   const auto t3 = clk::now();
   rep.inner_iterations[2] += s2.iterations;
   rep.inner_iterations[1] += s1.iterations;

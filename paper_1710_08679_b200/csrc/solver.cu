@@ -81,21 +81,23 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
   p2_restrict(v.r1.get(), v.r2.get(), lv.p2t_ptr.get(), lv.p2t_idx.get(), lv.n2, lv.mask2.get(), B, s);
   p2_restrict(v.u1.get(), v.u2.get(), lv.p2t_ptr.get(), lv.p2t_idx.get(), lv.n2, lv.mask2.get(), B, s);
   const auto t0 = clk::now();
-  auto a2 = [&](const float* x, float* y) {
+  auto a2 = [&](const float* x, float* y, bool) {
     bcsr_apply_f32(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s);
   };
   const InnerStats s2 = inner_pcg<float>(a2, lv.m2.get(), v.r2.get(), v.u2.get(), lv.n2, B, cfg.level_tol[2],
                                          cfg.level_max_iter[2], v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s);
   const auto t1 = clk::now();
   p2_apply(v.u2.get(), v.u1.get(), lv.agg.get(), lv.n1, lv.mask1.get(), B, s);
-  auto a1 = [&](const float* x, float* y) { ebe_apply(*lv.l1, x, y, B, s); };
+  auto a1 = [&](const float* x, float* y, bool init) { ebe_apply_part(*lv.l1, x, y, B, s, -1, init); };
   const InnerStats s1 = inner_pcg<float>(a1, lv.m1.get(), v.r1.get(), v.u1.get(), lv.n1, B, cfg.level_tol[1],
-                                         cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s);
+                                         cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s,
+                                         true, lv.mask1.get());
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), lv.p1_ends.get(), lv.n1, lv.n0, lv.mask0.get(), B, s);
-  auto a0 = [&](const float* x, float* y) { ebe_apply(*lv.l0, x, y, B, s); };
+  auto a0 = [&](const float* x, float* y, bool init) { ebe_apply_part(*lv.l0, x, y, B, s, -1, init); };
   const InnerStats s0 = inner_pcg<float>(a0, lv.m0.get(), v.r0.get(), v.u0.get(), lv.n0, B, cfg.level_tol[0],
-                                         cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s);
+                                         cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s,
+                                         true, lv.mask0.get());
   const auto t3 = clk::now();
   rep.inner_iterations[2] += s2.iterations;
   rep.inner_iterations[1] += s1.iterations;

@@ -31,12 +31,15 @@ struct InnerStats {
   bool converged = false;
 };
 
-// inner_pcg (pcg.hpp:52-124). A(x, y): y = A x on the stream.
+// inner_pcg (pcg.hpp:52-124). A(x, y, init): y = A x on the stream; with
+// fuse_init the direction pass writes A's starting value (the masked identity
+// of p, op_mask = the operator's dof mask) and A is called with init = false.
 template <typename T, typename Op>
 InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t B, double tol, int max_iter, T* e,
-                     T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s) {
+                     T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s, bool fuse_init = false,
+                     const uint8_t* op_mask = nullptr) {
   if (max_iter < 1) validation("inner_pcg: max_iter must be >= 1");
-  A(u, e);
+  A(u, e, true);
   pcg_init<T>(inv, r, e, n, B, cs, ws, s);
   InnerStats st;
   const double tol2 = tol * tol;
@@ -45,8 +48,8 @@ InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t 
   while (ratio > tol2 && st.iterations < max_iter) {
     const bool first = st.iterations == 0;
     pcg_rho(B, first, cs, ws, s);
-    pcg_direction<T>(inv, e, p, n, B, first, cs, s);
-    A(p, q);
+    pcg_direction<T>(inv, e, p, n, B, first, cs, s, fuse_init ? q : nullptr, op_mask);
+    A(p, q, !fuse_init);
     pcg_gamma<T>(p, q, n, B, cs, ws, s);
     pcg_update<T>(inv, e, u, p, q, n, B, cs, ws, s);
     const PcgStatus& ps = read_status(ws, s);

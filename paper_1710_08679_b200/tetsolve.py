@@ -436,9 +436,10 @@ def build_crust_model(mesh: Mesh, materials, cfg: SolverConfig | None = None, wo
     return CrustModel(mesh, list(materials), mask, build_solver_levels(mesh, materials, mask, cfg, workers))
 
 
-def solve(levels: SolverLevels, f, u0, cfg: SolverConfig | None = None, history: int = 4096):
+def solve(levels: SolverLevels, f, u0, cfg: SolverConfig | None = None, history: int = 4096, out=None):
     """solve (adaptive_cg.hpp:242-263). f, u0: (3N, batch) numpy (host path) or
-    CUDA float64 tensors (device path). Returns (u, SolveReport)."""
+    CUDA float64 tensors (device path); `out` optionally receives u (e.g. a
+    pinned host array). Returns (u, SolveReport)."""
     cfg = cfg or SolverConfig()
     c = cfg.to_c()
     batch = int(f.shape[1])
@@ -452,7 +453,7 @@ def solve(levels: SolverLevels, f, u0, cfg: SolverConfig | None = None, history:
         u0 = np.ascontiguousarray(u0, np.float64)
         if f.shape != u0.shape:
             raise ValidationError("solve: initial guess shape mismatch")
-        u = np.empty_like(f)
+        u = out if out is not None and out.shape == f.shape and out.dtype == np.float64 else np.empty_like(f)
         rc = lib.ts_solve(levels._h, _p(f), _p(u0), _p(u), batch, C.byref(c), C.byref(rb.c))
     rep = rb.report(cfg.residual_history_stride)
     _ck(rc, rep)
