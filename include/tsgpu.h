@@ -163,6 +163,11 @@ ts_status ts_levels_export(const ts_levels* lv, int32_t* agg_of_node, int32_t* r
 ts_status ts_levels_operator(const ts_levels* lv, int32_t which /*0 outer,1 level0,2 level1*/,
                              const ts_ebe** op);
 
+/* the level operator the solve applies (device buffers): 0 outer fp64 tet10, 1 level-0
+ * fp32 tet10, 2 level-1 fp32 tet4 — the assembled K1 (float-rounded inputs, fp32 sums)
+ * unless TSGPU_L1=ebe; same product as EbeOperator<float> order 1 (ebe_operator.hpp:90) */
+ts_status ts_levels_apply(ts_levels* lv, int32_t which, const void* u, void* f, int32_t batch, void* stream);
+
 /* solve (adaptive_cg.hpp:242-263) with host buffers; u_out may alias u0. */
 ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_out,
                    int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);

@@ -92,6 +92,7 @@ _sig = {
     "ts_levels_sizes": (C.c_int, [vp, vp, vp, vp, vp]),
     "ts_levels_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "ts_levels_operator": (C.c_int, [vp, i32, vp]),
+    "ts_levels_apply": (C.c_int, [vp, i32, vp, vp, i32, vp]),
     "ts_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
     "ts_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
     "ts_solve_pcge": (C.c_int, [vp, vp, vp, vp, i32, C.c_double, i32, vp]),

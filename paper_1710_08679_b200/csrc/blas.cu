@@ -519,6 +519,47 @@ __global__ void k_bcsr(const int32_t* __restrict__ row_ptr, const int32_t* __res
   fr[2 * B] = static_cast<float>(a2);
 }
 
+// Assembled level-1 operator (K1 of the fp32 tier, setup.cpp assemble_tet4):
+// W cases of one block row per thread, fp32 accumulation of ~14 blocks — the
+// EbeOperator<float> order-1 product (fp32 cross-element sums) without atomics.
+template <int W>
+__global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                            const float* __restrict__ blocks, int32_t n, const float* __restrict__ u,
+                            float* __restrict__ f, int32_t B) {
+  const int qpr = B / W;
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r = t / qpr;
+  if (r >= n) return;
+  const int b0 = static_cast<int>(t - r * qpr) * W;
+  float acc[3][W];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc[i][k] = 0.f;
+  const int32_t e1 = __ldg(row_ptr + r + 1);
+  for (int32_t e = __ldg(row_ptr + r); e < e1; ++e) {
+    const float* blk = blocks + 9 * int64_t(e);
+    float m[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) m[q] = __ldg(blk + q);
+    const float* uc = u + 3 * int64_t(__ldg(col_idx + e)) * B + b0;
+    const Pack<float, W> x0 = ld<float, W>(uc), x1 = ld<float, W>(uc + B), x2 = ld<float, W>(uc + 2 * B);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        acc[i][k] = fmaf(m[3 * i + 2], x2.v[k], fmaf(m[3 * i + 1], x1.v[k], fmaf(m[3 * i], x0.v[k], acc[i][k])));
+  }
+  float* fr = f + 3 * r * B + b0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    Pack<float, W> o;
+#pragma unroll
+    for (int k = 0; k < W; ++k) o.v[k] = acc[i][k];
+    st<float, W>(fr + i * B, o);
+  }
+}
+
 __global__ void k_cast_d2f(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) y[i] = static_cast<float>(x[i]);
@@ -788,6 +829,12 @@ void cg_update(double* r, double* u, const double* p, const double* q, int32_t n
 void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
                     float* f, int32_t B, cudaStream_t s) {
   k_bcsr<<<grid_for(int64_t(n) * B, 128), 128, 0, s>>>(row_ptr, col_idx, blocks, n, u, f, B);
+  TS_CUDA_LAUNCH();
+}
+void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
+                   float* f, int32_t B, cudaStream_t s) {
+  TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
+                                   row_ptr, col_idx, blocks, n, u, f, B)));
   TS_CUDA_LAUNCH();
 }
 void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s) {

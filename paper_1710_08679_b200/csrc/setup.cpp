@@ -49,7 +49,10 @@ int32_t find_col(const BcsrD& a, int32_t r, int32_t c) {
 // assemble_bcsr(EbeOperator<double>(mesh, 1, ...)) (ebe_operator.hpp:230-284)
 // for the first-order vertex grid with the level-1 mask.
 BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
-                    const std::vector<uint8_t>& mask1) {
+                    const std::vector<uint8_t>& mask1, bool round32) {
+  // round32: float-rounded vertices and Lame values, as the fp32 EbeOperator
+  // stores them (ebe_operator.hpp:54-62) — the assembled image of the level-1 operator
+  auto rnd = [round32](double x) { return round32 ? static_cast<double>(static_cast<float>(x)) : x; };
   const int32_t n = m.vertex_count;
   const int64_t E = m.n_elems();
   // node -> elements CSR
@@ -91,7 +94,7 @@ BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::
       const int32_t* t = m.tets10.data() + 10 * e;
       double v[4][3];
       for (int a = 0; a < 4; ++a)
-        for (int c = 0; c < 3; ++c) v[a][c] = m.coords[3 * size_t(t[a]) + c];
+        for (int c = 0; c < 3; ++c) v[a][c] = rnd(m.coords[3 * size_t(t[a]) + c]);
       double j[3][3], inv[3][3];
       for (int c = 0; c < 3; ++c)
         for (int q = 0; q < 3; ++q) j[q][c] = v[c + 1][q] - v[0][q];
@@ -107,7 +110,7 @@ BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::
         g[3][d] = inv[2][d];
         g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
       }
-      const double wl = vol * lam_e[e], wm = vol * mu_e[e];
+      const double wl = vol * rnd(lam_e[e]), wm = vol * rnd(mu_e[e]);
       int a = 0;
       while (t[a] != r) ++a;
       for (int b = 0; b < 4; ++b) {

@@ -19,7 +19,7 @@ struct Aggregation {  // aggregation.hpp:13-17
 };
 
 BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
-                    const std::vector<uint8_t>& mask1);
+                    const std::vector<uint8_t>& mask1, bool round32 = false);
 Aggregation aggregate_p1(const BcsrD& a, int32_t target);
 BcsrD build_level2(const BcsrD& k1, const Aggregation& agg, const std::vector<uint8_t>& fine_mask);
 std::vector<uint8_t> coarse_mask(const Aggregation& agg, const std::vector<uint8_t>& fine_mask);

@@ -8,6 +8,7 @@
 // kernels and reads one 24-byte status record per iteration (the reference's
 // convergence test is a host-side max over columns, pcg.hpp:71,116-117).
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -37,6 +38,11 @@ struct ts_levels {
   std::unique_ptr<ts_ebe> outer, l0, l1;
   DevBuf<int32_t> l2_row_ptr, l2_col_idx;
   DevBuf<float> l2_blocks;
+  // level 1 as an assembled BCSR (float-rounded assembly of the fp32 tet4 operator):
+  // tet4's ~21 elements per vertex make the EBE scatter L2-atomic bound
+  bool l1_assembled = false;
+  DevBuf<int32_t> l1_row_ptr, l1_col_idx;
+  DevBuf<float> l1_blocks;
   DevBuf<int32_t> p1_ends, p1t_ptr, p1t_idx, agg, p2t_ptr, p2t_idx;
   DevBuf<float> m0, m1, m2;
   DevBuf<uint8_t> mask0, mask1, mask2;
@@ -88,10 +94,15 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
                                          cfg.level_max_iter[2], v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s);
   const auto t1 = clk::now();
   p2_apply(v.u2.get(), v.u1.get(), lv.agg.get(), lv.n1, lv.mask1.get(), B, s);
-  auto a1 = [&](const float* x, float* y, bool init) { ebe_apply_part(*lv.l1, x, y, B, s, -1, init); };
+  auto a1 = [&](const float* x, float* y, bool init) {
+    if (lv.l1_assembled)
+      bcsr_rows_f32(lv.l1_row_ptr.get(), lv.l1_col_idx.get(), lv.l1_blocks.get(), lv.n1, x, y, B, s);
+    else
+      ebe_apply_part(*lv.l1, x, y, B, s, -1, init);
+  };
   const InnerStats s1 = inner_pcg<float>(a1, lv.m1.get(), v.r1.get(), v.u1.get(), lv.n1, B, cfg.level_tol[1],
                                          cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s,
-                                         true, lv.mask1.get());
+                                         !lv.l1_assembled, lv.mask1.get());
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), lv.p1_ends.get(), lv.n1, lv.n0, lv.mask0.get(), B, s);
   auto a0 = [&](const float* x, float* y, bool init) { ebe_apply_part(*lv.l0, x, y, B, s, -1, init); };
@@ -203,6 +214,20 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   setup_mark("levels: P1");
   const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1);
   setup_mark("levels: K1 assembly");
+  {
+    const char* e = std::getenv("TSGPU_L1");
+    lv->l1_assembled = !(e && std::string(e) == "ebe");
+  }
+  if (lv->l1_assembled) {
+    const BcsrD k1f = assemble_tet4(m, lam_e, mu_e, mask1, true);
+    std::vector<float> bl(k1f.blocks.size());
+#pragma omp parallel for schedule(static)
+    for (size_t q = 0; q < bl.size(); ++q) bl[q] = static_cast<float>(k1f.blocks[q]);
+    lv->l1_row_ptr.upload(k1f.row_ptr);
+    lv->l1_col_idx.upload(k1f.col_idx);
+    lv->l1_blocks.upload(bl);
+    setup_mark("levels: K1 fp32 operator");
+  }
   Aggregation agg = aggregate_p1(k1, cfg.aggregate_target);
   setup_mark("levels: aggregation");
   const BcsrD a2 = build_level2(k1, agg, mask1);
@@ -305,6 +330,21 @@ ts_status ts_levels_operator(const ts_levels* lv, int32_t which, const ts_ebe** 
   else if (which == 1) *op = lv->l0.get();
   else if (which == 2) *op = lv->l1.get();
   else tsg::validation("levels: operator index must be 0 (outer), 1 (level0) or 2 (level1)");
+  TS_API_END
+}
+
+ts_status ts_levels_apply(ts_levels* lv, int32_t which, const void* u, void* f, int32_t batch, void* stream) {
+  TS_API_BEGIN
+  if (!lv || !u || !f) tsg::validation("levels apply: null argument");
+  if (batch < 1) tsg::validation("levels apply: batch must be >= 1");
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (which == 0) tsg::ebe_apply(*lv->outer, u, f, batch, s);
+  else if (which == 1) tsg::ebe_apply(*lv->l0, u, f, batch, s);
+  else if (which == 2 && lv->l1_assembled)
+    tsg::bcsr_rows_f32(lv->l1_row_ptr.get(), lv->l1_col_idx.get(), lv->l1_blocks.get(), lv->n1,
+                       static_cast<const float*>(u), static_cast<float*>(f), batch, s);
+  else if (which == 2) tsg::ebe_apply(*lv->l1, u, f, batch, s);
+  else tsg::validation("levels apply: operator index must be 0 (outer), 1 (level0) or 2 (level1)");
   TS_API_END
 }
 

@@ -387,6 +387,14 @@ class SolverLevels:
             ops.append(EbeOperator(None, 0, None, _borrowed=h))
         self.outer, self.level0, self.level1 = ops
 
+    def apply(self, which: int, u, f=None):
+        """The level operator the solve applies (CUDA tensors): 0 outer fp64, 1 level-0
+        fp32 tet10, 2 level-1 fp32 tet4 (assembled K1 unless TSGPU_L1=ebe)."""
+        f = torch.empty_like(u) if f is None else f
+        _ck(lib.ts_levels_apply(self._h, int(which), C.c_void_p(u.data_ptr()), C.c_void_p(f.data_ptr()),
+                                int(u.shape[1]), _stream()))
+        return f
+
     def export(self) -> dict:
         """Setup introspection: aggregation, level-2 Galerkin matrix, masks, M2."""
         agg = np.zeros(self.n1, np.int32)

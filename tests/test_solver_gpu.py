@@ -164,3 +164,26 @@ def test_convergence_error_carries_report():
         ts.solve(model.levels, f, np.zeros_like(f), cfg)
     rep = ei.value.report
     assert rep.outer_iterations == 1 and not rep.converged and len(rep.final_rel_residual) == 1
+
+
+@pytest.mark.parametrize("which", [0, 1, 2])
+@pytest.mark.parametrize("batch", [1, 3, 16])
+def test_level_operators_match_reference(checker, which, batch):
+    """The operators the solve applies (ts_levels_apply) against the reference's
+    EbeOperator<double> order 2 (outer), <float> order 2 (level 0) and <float>
+    order 1 (level 1 — assembled K1 on the device) on the same inputs."""
+    import torch
+    ext, div, ifs = (16000.0, 20000.0, 10000.0), (6, 7, 4), (7000.0,)
+    mesh = ts.generate_box_mesh(ext, div, ifs)
+    om = checker.box_mesh(ext, div, ifs, 1)
+    lam, mu = lame(TWO_LAYER)
+    lv = ts.build_crust_model(mesh, mats(TWO_LAYER), ts.SolverConfig(batch_size=batch)).levels
+    order, prec = [(2, 64), (2, 32), (1, 32)][which]
+    nn = mesh.vertex_count if order == 1 else mesh.node_count()
+    mask = mesh.dirichlet_mask()[: 3 * nn]
+    dt = np.float64 if prec == 64 else np.float32
+    u = checker.rng_sym(40 + batch, 3 * nn * batch).reshape(3 * nn, batch).astype(dt)
+    want = checker.ebe_apply(om, order, lam, mu, mask, prec, u)
+    got = lv.apply(which, torch.from_numpy(u).cuda()).cpu().numpy()
+    assert rel(got.astype(np.float64), want.astype(np.float64)) <= (1e-12 if prec == 64 else 1e-5)
+    assert np.array_equal(got[mask == 1], u[mask == 1])
