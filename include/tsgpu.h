@@ -252,6 +252,32 @@ ts_status ts_dist_ebe_op_apply(ts_dist_ebe* op, const void* u, void* f, int32_t 
 /* the partition's local operator (borrowed; timing controls via ts_ebe_set_timing) */
 ts_status ts_dist_ebe_local_operator(ts_dist_ebe* op, ts_ebe** local);
 
+/* ------------------------------------------------ Green's-function sweep
+ *
+ * find_plane_fault_faces (fault.hpp:86-118) -> build_faulted_model (model.hpp:41-51,
+ * split_nodes fault.hpp:140-302) -> compute_greens_bank (greens.hpp:114-145): per batch of
+ * cfg->batch_size unit slips (unit_slip_basis fault.hpp:325-343; direction 0 = dip, 1 =
+ * strike), slip_to_rhs (fault.hpp:363-388) as ONE multi-case fp64 EBE product on the split
+ * mesh, solve() on the base hierarchy, sample_displacement (greens.hpp:50-76). */
+typedef struct ts_faulted ts_faulted;
+/* faces: NULL to query *n_faces, else [*n_faces][3] base-mesh vertex ids */
+ts_status ts_fault_plane_faces(const ts_mesh* mesh, int32_t axis, double coord, const double lo[3],
+                               const double hi[3], int32_t* n_faces, int32_t* faces);
+ts_status ts_faulted_model_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda,
+                                  const double* mu, const int32_t* faces, int32_t n_faces,
+                                  const ts_solver_config* cfg, ts_faulted** out);
+void ts_faulted_model_destroy(ts_faulted* fm);
+ts_status ts_faulted_info(const ts_faulted* fm, int32_t* n_split_nodes, int32_t* split_mesh_nodes,
+                          int32_t* n_faces);
+/* right-hand sides of n_slips unit slips: f_host [3N][n_slips] (base mesh) */
+ts_status ts_slip_to_rhs(ts_faulted* fm, int32_t n_slips, const double* centers /*[n][3]*/,
+                         const int32_t* directions, const double* radii, double* f_host);
+/* bank [n_obs][n_slips] row-major; points [n_obs][3], axes 0..2 */
+ts_status ts_greens_bank(ts_faulted* fm, int32_t n_slips, const double* centers, const int32_t* directions,
+                         const double* radii, int32_t n_obs, const double* points, const int32_t* axes,
+                         const ts_solver_config* cfg, double* bank, int32_t* solver_calls,
+                         int64_t* outer_iterations);
+
 #ifdef __cplusplus
 }
 #endif

@@ -367,6 +367,60 @@ class Oracle:
             self._f("mesh_destroy")(h)
         return sec.value, chk.value
 
+    # ---- Green's-function sweep (reference only: fault.hpp / greens.hpp)
+    def fault_plane_faces(self, m: MeshArrays, axis, coord, lo, hi) -> np.ndarray:
+        assert self.kind == "reference"
+        h = self._mesh(m)
+        try:
+            n = C.c_int32(0)
+            lo = np.ascontiguousarray(lo, np.float64)
+            hi = np.ascontiguousarray(hi, np.float64)
+            self._check(self.lib.ref_fault_plane_faces(h, axis, C.c_double(coord), _p(lo), _p(hi), C.byref(n), None))
+            out = np.zeros((n.value, 3), np.int32)
+            self._check(self.lib.ref_fault_plane_faces(h, axis, C.c_double(coord), _p(lo), _p(hi), C.byref(n), _p(out)))
+        finally:
+            self._f("mesh_destroy")(h)
+        return out
+
+    def slip_to_rhs(self, m: MeshArrays, lam, mu, faces, centers, dirs, radii):
+        assert self.kind == "reference"
+        lam = np.ascontiguousarray(lam, np.float64)
+        mu = np.ascontiguousarray(mu, np.float64)
+        faces = np.ascontiguousarray(faces, np.int32)
+        centers = np.ascontiguousarray(centers, np.float64)
+        dirs = np.ascontiguousarray(dirs, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        f = np.zeros((3 * m.n_nodes, len(dirs)), np.float64)
+        info = np.zeros(2, np.int32)
+        h = self._mesh(m)
+        try:
+            self._check(self.lib.ref_slip_to_rhs(h, len(lam), _p(lam), _p(mu), _p(faces), len(faces), len(dirs),
+                                                 _p(centers), _p(dirs), _p(radii), _p(f), _p(info)))
+        finally:
+            self._f("mesh_destroy")(h)
+        return f, info
+
+    def greens_bank(self, m: MeshArrays, lam, mu, faces, centers, dirs, radii, points, axes, cfg: SolverConfig):
+        assert self.kind == "reference"
+        lam = np.ascontiguousarray(lam, np.float64)
+        mu = np.ascontiguousarray(mu, np.float64)
+        faces = np.ascontiguousarray(faces, np.int32)
+        centers = np.ascontiguousarray(centers, np.float64)
+        dirs = np.ascontiguousarray(dirs, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        points = np.ascontiguousarray(points, np.float64)
+        axes = np.ascontiguousarray(axes, np.int32)
+        bank = np.zeros((len(axes), len(dirs)), np.float64)
+        calls, outer = C.c_int32(), C.c_int64()
+        h = self._mesh(m)
+        try:
+            self._check(self.lib.ref_greens_bank(h, len(lam), _p(lam), _p(mu), _p(faces), len(faces), len(dirs),
+                                                 _p(centers), _p(dirs), _p(radii), len(axes), _p(points), _p(axes),
+                                                 C.byref(cfg), _p(bank), C.byref(calls), C.byref(outer)))
+        finally:
+            self._f("mesh_destroy")(h)
+        return bank, calls.value, outer.value
+
     def hw_threads(self) -> int:
         return int(self.lib.ref_hw_threads()) if self.kind == "reference" else 1
 

@@ -18,6 +18,8 @@
 
 #include "tetsolve/adaptive_cg.hpp"
 #include "tetsolve/box_mesh.hpp"
+#include "tetsolve/fault.hpp"
+#include "tetsolve/greens.hpp"
 #include "tetsolve/model.hpp"
 #include "tetsolve/verification.hpp"
 
@@ -496,5 +498,74 @@ void ref_rng_sym(uint64_t seed, int64_t n, double* out) {
 }
 
 int ref_hw_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+// ---- Green's-function sweep (fault.hpp / model.hpp / greens.hpp), for parity tests
+int ref_fault_plane_faces(const void* mh, int32_t axis, double coord, const double* lo, const double* hi,
+                          int32_t* n_faces, int32_t* faces) {
+  REF_TRY
+  const auto f = find_plane_fault_faces(*static_cast<const Mesh*>(mh), axis, coord, {lo[0], lo[1], lo[2]},
+                                        {hi[0], hi[1], hi[2]});
+  if (faces)
+    for (size_t i = 0; i < f.size() && int32_t(i) < *n_faces; ++i)
+      for (int k = 0; k < 3; ++k) faces[3 * i + k] = f[i][k];
+  *n_faces = static_cast<int32_t>(f.size());
+  REF_CATCH
+}
+
+namespace {
+std::vector<std::array<int32_t, 3>> tris_of(const int32_t* faces, int32_t n) {
+  std::vector<std::array<int32_t, 3>> t(n);
+  for (int32_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) t[i][k] = faces[3 * i + k];
+  return t;
+}
+std::vector<UnitSlip> slips_of(const FaultedModel& fm, int32_t n, const double* c, const int32_t* d, const double* r) {
+  std::vector<UnitSlip> s;
+  for (int32_t j = 0; j < n; ++j)
+    s.push_back(unit_slip_basis(fm.patch, fm.base.mesh, {c[3 * j], c[3 * j + 1], c[3 * j + 2]},
+                                d[j] == 0 ? SlipDirection::dip : SlipDirection::strike, r[j]));
+  return s;
+}
+}  // namespace
+
+int ref_slip_to_rhs(const void* mh, int32_t n_mat, const double* lam, const double* mu, const int32_t* faces,
+                    int32_t n_faces, int32_t n_slips, const double* centers, const int32_t* dirs, const double* radii,
+                    double* f_out, int32_t* split_info /*[2]: split nodes, split mesh nodes*/) {
+  REF_TRY
+  const FaultedModel fm = build_faulted_model(*static_cast<const Mesh*>(mh), mats_of(n_mat, lam, mu),
+                                              tris_of(faces, n_faces), SolverConfig{});
+  const auto slips = slips_of(fm, n_slips, centers, dirs, radii);
+  const int32_t N = fm.base.mesh.node_count();
+  for (int32_t j = 0; j < n_slips; ++j) {
+    const VectorBatch64 col = slip_to_rhs(fm, slips[j]);
+    for (int64_t d = 0; d < 3 * int64_t(N); ++d) f_out[d * n_slips + j] = col.at(d, 0);
+  }
+  if (split_info) {
+    split_info[0] = static_cast<int32_t>(fm.patch.split_nodes.size());
+    split_info[1] = fm.split_mesh.node_count();
+  }
+  REF_CATCH
+}
+
+int ref_greens_bank(const void* mh, int32_t n_mat, const double* lam, const double* mu, const int32_t* faces,
+                    int32_t n_faces, int32_t n_slips, const double* centers, const int32_t* dirs, const double* radii,
+                    int32_t n_obs, const double* points, const int32_t* axes, const ts_solver_config* cfg,
+                    double* bank, int32_t* solver_calls, int64_t* outer_iterations) {
+  REF_TRY
+  const SolverConfig c = cfg_of(cfg);
+  const FaultedModel fm = build_faulted_model(*static_cast<const Mesh*>(mh), mats_of(n_mat, lam, mu),
+                                              tris_of(faces, n_faces), c);
+  const auto slips = slips_of(fm, n_slips, centers, dirs, radii);
+  std::vector<ObservationComponent> obs(n_obs);
+  for (int32_t r = 0; r < n_obs; ++r) {
+    obs[r].point = {points[3 * r], points[3 * r + 1], points[3 * r + 2]};
+    obs[r].axis = axes[r];
+  }
+  auto [b, rep] = compute_greens_bank(fm, slips, obs, c);
+  std::memcpy(bank, b.values.data(), b.values.size() * sizeof(double));
+  *solver_calls = rep.solver_calls;
+  *outer_iterations = rep.outer_iterations;
+  REF_CATCH
+}
 
 }  // extern "C"

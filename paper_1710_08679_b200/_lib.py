@@ -120,6 +120,12 @@ _sig = {
     "ts_dist_ebe_local_nodes": (C.c_int, [vp, vp]),
     "ts_dist_ebe_op_apply": (C.c_int, [vp, vp, vp, i32, vp]),
     "ts_dist_ebe_local_operator": (C.c_int, [vp, vp]),
+    "ts_fault_plane_faces": (C.c_int, [vp, i32, C.c_double, vp, vp, vp, vp]),
+    "ts_faulted_model_create": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp]),
+    "ts_faulted_model_destroy": (None, [vp]),
+    "ts_faulted_info": (C.c_int, [vp, vp, vp, vp]),
+    "ts_slip_to_rhs": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+    "ts_greens_bank": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _fn = getattr(lib, _name, None)

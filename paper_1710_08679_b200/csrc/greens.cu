@@ -1,0 +1,268 @@
+// greens.cu — the Green's-function bank on the device:
+// compute_greens_bank (greens.hpp:114-145) = for each batch of B unit slips
+// (greens_batch_plan, greens.hpp:102-110): lift the slips to right-hand sides
+// (slip_to_rhs, fault.hpp:363-388: ONE multi-case fp64 EBE product on the
+// split mesh for the whole batch), solve the batch (adaptive_cg.hpp:242-263),
+// sample every observation (greens.hpp:50-76: first containing element, tet10
+// shape values — located once, then a device gather for all columns).
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ebe.h"
+#include "fault.h"
+#include "levels_api.h"
+
+#include <algorithm>
+
+namespace tsg {
+namespace {
+
+// g[plus][a][j] = +delta/2, g[minus][a][j] = -delta/2 (fault.hpp:370-376); d: [ns][3][W]
+__global__ void k_slip_jump(const int32_t* __restrict__ plus, const int32_t* __restrict__ minus, int32_t ns, int32_t W,
+                            const double* __restrict__ d, double* __restrict__ g) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(ns) * 3 * W) return;
+  const int64_t k = i / (3 * W), rem = i - k * 3 * W;
+  g[3 * int64_t(plus[k]) * W + rem] = 0.5 * d[i];
+  g[3 * int64_t(minus[k]) * W + rem] = -0.5 * d[i];
+}
+
+// f[base] = -(w[first copy]) - w[second copy]; constrained base dofs zeroed (fault.hpp:380-386)
+__global__ void k_lift(const double* __restrict__ w, const int32_t* __restrict__ s1, const int32_t* __restrict__ s2,
+                       const uint8_t* __restrict__ mask, int32_t n, int32_t W, double* __restrict__ f) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(n) * 3 * W) return;
+  const int64_t node = i / (3 * W), rem = i - node * 3 * W;
+  double v = 0.0 - w[3 * int64_t(s1[node]) * W + rem];
+  if (s2[node] >= 0) v -= w[3 * int64_t(s2[node]) * W + rem];
+  f[i] = (mask && mask[3 * node + rem / W]) ? 0.0 : v;
+}
+
+// bank[r][col0 + j] = sum_a n_a u[3 node_a + axis][j] (greens.hpp:70-73)
+__global__ void k_sample(const double* __restrict__ u, const int32_t* __restrict__ nodes, const double* __restrict__ sh,
+                         const int32_t* __restrict__ axis, int32_t n_obs, int32_t W, int32_t n_cols, int32_t col0,
+                         double* __restrict__ bank) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(n_obs) * W) return;
+  const int32_t r = static_cast<int32_t>(i / W), j = static_cast<int32_t>(i - int64_t(r) * W);
+  double v = 0.0;
+  for (int a = 0; a < 10; ++a) v += sh[10 * r + a] * u[(3 * int64_t(nodes[10 * r + a]) + axis[r]) * W + j];
+  bank[int64_t(r) * n_cols + col0 + j] = v;
+}
+
+}  // namespace
+}  // namespace tsg
+
+// FaultedModel (model.hpp:34-56) on the device
+struct ts_faulted {
+  tsg::Mesh base;        // host copy for point location
+  tsg::Mesh split;
+  tsg::FaultPatch patch;
+  ts_levels* levels = nullptr;
+  std::unique_ptr<ts_ebe> split_raw;  // unmasked fp64 tet10 on the split mesh
+  tsg::DevBuf<int32_t> plus, minus, s1, s2;
+  ~ts_faulted() { tsg::levels_free(levels); }
+};
+
+namespace tsg {
+
+ts_faulted* faulted_create(const Mesh& m, int32_t n_mat, const double* lam, const double* mu,
+                           const std::vector<std::array<int32_t, 3>>& tris, const ts_solver_config& cfg) {
+  auto F = std::make_unique<ts_faulted>();
+  F->base = m;
+  split_nodes(m, tris, F->split, F->patch);
+  F->split_raw.reset(ebe_create(F->split, 2, n_mat, lam, mu, nullptr, 64));
+  F->levels = levels_build(m, n_mat, lam, mu, nullptr, cfg);
+  const size_t ns = F->patch.split_nodes.size();
+  std::vector<int32_t> pl(ns), mi(ns), s1(m.n_nodes()), s2(m.n_nodes(), -1);
+  for (size_t k = 0; k < ns; ++k) {
+    pl[k] = F->patch.split_nodes[k].plus;
+    mi[k] = F->patch.split_nodes[k].minus;
+  }
+  // base node -> its split copies in ascending split id (the reference's accumulation order)
+  std::vector<int32_t> seen(m.n_nodes(), 0);
+  for (size_t s = 0; s < F->patch.to_base.size(); ++s) {
+    const int32_t b = F->patch.to_base[s];
+    if (seen[b]++ == 0) s1[b] = static_cast<int32_t>(s);
+    else s2[b] = static_cast<int32_t>(s);
+  }
+  F->plus.upload(pl);
+  F->minus.upload(mi);
+  F->s1.upload(s1);
+  F->s2.upload(s2);
+  TS_CUDA(cudaDeviceSynchronize());
+  return F.release();
+}
+
+// delta (device [ns][3][W]) of W unit slips (slip_vectors, fault.hpp:347-361)
+void slip_deltas(const ts_faulted& F, int32_t W, const double* centers, const int32_t* dirs, const double* radii,
+                 DevBuf<double>& d) {
+  const size_t ns = F.patch.split_nodes.size();
+  std::vector<double> h(ns * 3 * W);
+  for (int32_t j = 0; j < W; ++j) {
+    const V3 c = {centers[3 * j], centers[3 * j + 1], centers[3 * j + 2]};
+    if (dirs[j] != 0 && dirs[j] != 1) validation("unit slip: direction must be 0 (dip) or 1 (strike)");
+    const std::vector<double> mag = unit_slip_magnitudes(F.patch, F.base, c, radii[j]);
+    for (size_t k = 0; k < ns; ++k) {
+      const V3& dir = dirs[j] == 0 ? F.patch.split_nodes[k].dip : F.patch.split_nodes[k].strike;
+      for (int a = 0; a < 3; ++a) h[(3 * k + a) * W + j] = mag[k] * dir[a];
+    }
+  }
+  d.upload(h);
+}
+
+// f (device [N][3][W]) = slip_to_rhs of W unit slips
+void slips_to_rhs(ts_faulted& F, int32_t W, const double* centers, const int32_t* dirs, const double* radii, double* f,
+                  cudaStream_t s) {
+  const int32_t ns = static_cast<int32_t>(F.patch.split_nodes.size());
+  const int32_t NS = F.split.n_nodes(), N = F.base.n_nodes();
+  DevBuf<double> d, g(3 * size_t(NS) * W), w(3 * size_t(NS) * W);
+  slip_deltas(F, W, centers, dirs, radii, d);
+  TS_CUDA(cudaMemsetAsync(g.get(), 0, g.size() * sizeof(double), s));
+  k_slip_jump<<<grid_for(int64_t(ns) * 3 * W, 256), 256, 0, s>>>(F.plus.get(), F.minus.get(), ns, W, d.get(), g.get());
+  TS_CUDA_LAUNCH();
+  ebe_apply(*F.split_raw, g.get(), w.get(), W, s);
+  k_lift<<<grid_for(int64_t(N) * 3 * W, 256), 256, 0, s>>>(w.get(), F.s1.get(), F.s2.get(), levels_mask0(*F.levels), N,
+                                                             W, f);
+  TS_CUDA_LAUNCH();
+  TS_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace tsg
+
+extern "C" {
+
+ts_status ts_fault_plane_faces(const ts_mesh* mesh, int32_t axis, double coord, const double lo[3], const double hi[3],
+                               int32_t* n_faces, int32_t* faces) {
+  try {
+    if (!mesh || !lo || !hi || !n_faces) tsg::validation("fault plane: null argument");
+    const auto f = tsg::find_plane_fault_faces(mesh->m, axis, coord, {lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]});
+    if (faces) {
+      if (*n_faces < static_cast<int32_t>(f.size())) tsg::validation("fault plane: faces buffer too small");
+      for (size_t i = 0; i < f.size(); ++i)
+        for (int k = 0; k < 3; ++k) faces[3 * i + k] = f[i][k];
+    }
+    *n_faces = static_cast<int32_t>(f.size());
+  } catch (const tsg::Error& e) {
+    tsg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    tsg::set_last_error(e.what());
+    return TS_ERR_VALIDATION;
+  }
+  return TS_OK;
+}
+
+ts_status ts_faulted_model_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda, const double* mu,
+                                  const int32_t* faces, int32_t n_faces, const ts_solver_config* cfg,
+                                  ts_faulted** out) {
+  try {
+    if (!mesh || !lambda || !mu || !faces || !cfg || !out) tsg::validation("faulted model: null argument");
+    if (n_faces < 1) tsg::validation("split_nodes: empty fault surface");
+    if (ts_config_validate(cfg) != TS_OK) tsg::fail(TS_ERR_VALIDATION, ts_last_error());
+    std::vector<std::array<int32_t, 3>> tris(n_faces);
+    for (int32_t i = 0; i < n_faces; ++i)
+      for (int k = 0; k < 3; ++k) tris[i][k] = faces[3 * i + k];
+    *out = tsg::faulted_create(mesh->m, n_materials, lambda, mu, tris, *cfg);
+  } catch (const tsg::Error& e) {
+    tsg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    tsg::set_last_error(e.what());
+    return TS_ERR_VALIDATION;
+  }
+  return TS_OK;
+}
+
+void ts_faulted_model_destroy(ts_faulted* fm) { delete fm; }
+
+ts_status ts_faulted_info(const ts_faulted* fm, int32_t* n_split_nodes, int32_t* split_mesh_nodes, int32_t* n_faces) {
+  if (!fm) {
+    tsg::set_last_error("faulted model: null handle");
+    return TS_ERR_VALIDATION;
+  }
+  if (n_split_nodes) *n_split_nodes = static_cast<int32_t>(fm->patch.split_nodes.size());
+  if (split_mesh_nodes) *split_mesh_nodes = fm->split.n_nodes();
+  if (n_faces) *n_faces = static_cast<int32_t>(fm->patch.faces.size());
+  return TS_OK;
+}
+
+ts_status ts_slip_to_rhs(ts_faulted* fm, int32_t n_slips, const double* centers, const int32_t* directions,
+                         const double* radii, double* f_host) {
+  try {
+    if (!fm || !centers || !directions || !radii || !f_host) tsg::validation("slip_to_rhs: null argument");
+    if (n_slips < 1) tsg::validation("slip_to_rhs: need at least one slip");
+    const size_t len = 3 * size_t(fm->base.n_nodes()) * n_slips;
+    tsg::DevBuf<double> f(len);
+    tsg::slips_to_rhs(*fm, n_slips, centers, directions, radii, f.get(), nullptr);
+    TS_CUDA(cudaMemcpy(f_host, f.get(), len * sizeof(double), cudaMemcpyDeviceToHost));
+  } catch (const tsg::Error& e) {
+    tsg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    tsg::set_last_error(e.what());
+    return TS_ERR_VALIDATION;
+  }
+  return TS_OK;
+}
+
+ts_status ts_greens_bank(ts_faulted* fm, int32_t n_slips, const double* centers, const int32_t* directions,
+                         const double* radii, int32_t n_obs, const double* points, const int32_t* axes,
+                         const ts_solver_config* cfg, double* bank, int32_t* solver_calls, int64_t* outer_iterations) {
+  try {
+    if (!fm || !centers || !directions || !radii || !points || !axes || !cfg || !bank)
+      tsg::validation("greens: null argument");
+    if (n_slips < 1) tsg::validation("greens: need at least one unit slip");
+    if (cfg->batch_size < 1) tsg::validation("greens: batch size must be >= 1");
+    if (n_obs < 1) tsg::validation("greens: no observation components");
+    const int32_t N = fm->base.n_nodes();
+    // locate every observation once (the reference re-scans per column; same element, same values)
+    std::vector<int32_t> nodes(10 * size_t(n_obs)), ax(n_obs);
+    std::vector<double> sh(10 * size_t(n_obs));
+    for (int32_t r = 0; r < n_obs; ++r) {
+      if (axes[r] < 0 || axes[r] > 2) tsg::validation("greens: observation axis must be 0..2");
+      int32_t e = -1;
+      const tsg::V3 p = {points[3 * r], points[3 * r + 1], points[3 * r + 2]};
+      if (!tsg::locate_point(fm->base, p, &e, sh.data() + 10 * r))
+        tsg::validation("observation point (" + std::to_string(p[0]) + ", " + std::to_string(p[1]) + ", " +
+                        std::to_string(p[2]) + ") lies outside the mesh");
+      for (int a = 0; a < 10; ++a) nodes[10 * r + a] = fm->base.tets10[10 * size_t(e) + a];
+      ax[r] = axes[r];
+    }
+    tsg::DevBuf<int32_t> dn, da;
+    tsg::DevBuf<double> ds, dbank(size_t(n_obs) * n_slips);
+    dn.upload(nodes);
+    da.upload(ax);
+    ds.upload(sh);
+    const int32_t B = cfg->batch_size;
+    tsg::DevBuf<double> f(3 * size_t(N) * B), u0(3 * size_t(N) * B), u(3 * size_t(N) * B);
+    int32_t calls = 0;
+    int64_t outer = 0;
+    for (int32_t lo = 0; lo < n_slips; lo += B) {  // greens_batch_plan (greens.hpp:102-110)
+      const int32_t W = std::min(n_slips, lo + B) - lo;
+      tsg::slips_to_rhs(*fm, W, centers + 3 * lo, directions + lo, radii + lo, f.get(), nullptr);
+      TS_CUDA(cudaMemset(u0.get(), 0, 3 * size_t(N) * W * sizeof(double)));
+      ts_solve_report rep{};
+      tsg::levels_solve_device(*fm->levels, f.get(), u0.get(), u.get(), W, *cfg, rep, nullptr);
+      ++calls;
+      outer += rep.outer_iterations;
+      tsg::k_sample<<<tsg::grid_for(int64_t(n_obs) * W, 256), 256>>>(u.get(), dn.get(), ds.get(), da.get(), n_obs, W,
+                                                                      n_slips, lo, dbank.get());
+      TS_CUDA(cudaGetLastError());
+    }
+    TS_CUDA(cudaMemcpy(bank, dbank.get(), dbank.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (solver_calls) *solver_calls = calls;
+    if (outer_iterations) *outer_iterations = outer;
+  } catch (const tsg::Error& e) {
+    tsg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    tsg::set_last_error(e.what());
+    return TS_ERR_VALIDATION;
+  }
+  return TS_OK;
+}
+
+}  // extern "C"

@@ -273,6 +273,20 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
 }
 
 }  // namespace
+
+// entry points for other translation units (greens.cu)
+ts_levels* levels_build(const Mesh& m, int32_t n_mat, const double* lam, const double* mu, const uint8_t* dof_mask,
+                        const ts_solver_config& cfg) {
+  return levels_create(m, n_mat, lam, mu, dof_mask, cfg);
+}
+void levels_free(ts_levels* lv) { delete lv; }
+void levels_solve_device(ts_levels& lv, const double* f, const double* u0, double* u, int32_t B,
+                         const ts_solver_config& cfg, ts_solve_report& rep, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(lv.mu);
+  solve_device(lv, f, u0, u, B, cfg, rep, s);
+}
+int32_t levels_nodes(const ts_levels& lv) { return lv.n0; }
+const uint8_t* levels_mask0(const ts_levels& lv) { return lv.mask0.get(); }
 }  // namespace tsg
 
 #define TS_API_BEGIN try {

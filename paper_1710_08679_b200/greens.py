@@ -1,0 +1,71 @@
+"""Green's-function sweep — Python mirror of include/tsgpu.h's ts_fault_* /
+ts_faulted_* / ts_greens_bank (reference fault.hpp,
+model.hpp:34-56, greens.hpp:114-145)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import lib
+from .tetsolve import Mesh, SolverConfig, _ck, _lame, _p
+
+DIP, STRIKE = 0, 1  # SlipDirection (fault.hpp:304)
+
+
+def find_plane_fault_faces(mesh: Mesh, axis: int, coord: float, lo, hi) -> np.ndarray:
+    """find_plane_fault_faces (fault.hpp:86-118): [F, 3] base-mesh vertex ids."""
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    n = C.c_int32(0)
+    _ck(lib.ts_fault_plane_faces(mesh._h, int(axis), float(coord), _p(lo), _p(hi), C.byref(n), None))
+    out = np.zeros((n.value, 3), np.int32)
+    _ck(lib.ts_fault_plane_faces(mesh._h, int(axis), float(coord), _p(lo), _p(hi), C.byref(n), _p(out)))
+    return out
+
+
+class FaultedModel:
+    """build_faulted_model (model.hpp:41-51): split mesh + base crust hierarchy on the device."""
+
+    def __init__(self, mesh: Mesh, materials, faces, cfg: SolverConfig | None = None):
+        cfg = cfg or SolverConfig()
+        lam, mu = _lame(materials)
+        faces = np.ascontiguousarray(faces, np.int32)
+        c = cfg.to_c()
+        h = C.c_void_p()
+        _ck(lib.ts_faulted_model_create(mesh._h, len(lam), _p(lam), _p(mu), _p(faces), len(faces), C.byref(c),
+                                        C.byref(h)))
+        self._h, self.mesh = h, mesh
+        ns, nsm, nf = C.c_int32(), C.c_int32(), C.c_int32()
+        _ck(lib.ts_faulted_info(self._h, C.byref(ns), C.byref(nsm), C.byref(nf)))
+        self.n_split_nodes, self.split_mesh_nodes, self.n_faces = ns.value, nsm.value, nf.value
+
+    def slip_to_rhs(self, centers, directions, radii) -> np.ndarray:
+        """slip_to_rhs (fault.hpp:363-388) of each unit slip: [3N, n_slips]."""
+        centers = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        directions = np.ascontiguousarray(directions, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        f = np.zeros((3 * self.mesh.node_count(), len(directions)), np.float64)
+        _ck(lib.ts_slip_to_rhs(self._h, len(directions), _p(centers), _p(directions), _p(radii), _p(f)))
+        return f
+
+    def greens_bank(self, centers, directions, radii, points, axes, cfg: SolverConfig | None = None):
+        """compute_greens_bank (greens.hpp:114-145): (bank [n_obs, n_slips], solver_calls, outer_iterations)."""
+        cfg = cfg or SolverConfig()
+        c = cfg.to_c()
+        centers = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        directions = np.ascontiguousarray(directions, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        points = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        axes = np.ascontiguousarray(axes, np.int32)
+        bank = np.zeros((len(axes), len(directions)), np.float64)
+        calls, outer = C.c_int32(), C.c_int64()
+        _ck(lib.ts_greens_bank(self._h, len(directions), _p(centers), _p(directions), _p(radii), len(axes), _p(points),
+                               _p(axes), C.byref(c), _p(bank), C.byref(calls), C.byref(outer)))
+        return bank, calls.value, outer.value
+
+    def __del__(self):
+        try:
+            lib.ts_faulted_model_destroy(self._h)
+        except Exception:
+            pass
