@@ -18,6 +18,9 @@ explicit flush is needed between steps.
   cpu_baseline: the UNMODIFIED reference (oracle/_ref/libtsref.so) timing the
            same apply on this host's cores (rank 0, N = 1).
   --impl reference: the reference's own CPU implementation as the arm.
+  greens : the Green's-function bank (configs[4] workflow at one-GPU scale):
+           48 unit slips on a vertical fault in the configs[1] box, batch 16,
+           through ts_greens_bank; total sweep time and time per case.
   solve  : BASELINE's other metric, time per case: the full multigrid solve
            (build_crust_model + solve, adaptive_cg.hpp:242-263) of configs[2]
            (50M-DOF 3-layer crust, 16 cases, mixed-precision PCG) through the
@@ -411,6 +414,56 @@ def main_partitioned(args, world, rank, local):
     dist.destroy_process_group()
 
 
+# ------------------------------------------------------------ Green's sweep leg
+def greens_leg(args, ts, torch, world, rank, local):
+    """configs[4]-style workload at one-GPU scale: the Green's-function bank
+    (compute_greens_bank, greens.hpp:114-145) of n unit slips (dip + strike on a
+    grid of centres on a vertical fault) on the configs[1] layered box, batched
+    r = 16 per solve; total wall time and time per case (setup reported apart).
+    Replicas for N > 1 (each rank its own sweep)."""
+    import numpy as np
+    from paper_1710_08679_b200.greens import DIP, STRIKE, FaultedModel, find_plane_fault_faces
+
+    cells = tuple(args.cells)
+    ext, div, ifs = mesh_spec(cells)
+    h = CELL_KM * 1e3
+    xm = (cells[0] // 2) * h
+    t0 = time.perf_counter()
+    mesh = ts.generate_box_mesh(ext, div, ifs)
+    lo = (xm, 4 * h, 4 * h)
+    hi = (xm, (cells[1] - 4) * h, (cells[2] - 8) * h)
+    faces = find_plane_fault_faces(mesh, 0, xm, lo, hi)
+    cfg = ts.SolverConfig(batch_size=16)
+    fm = FaultedModel(mesh, [ts.material_from_wavespeeds(*t) for t in TWO_LAYER], faces, cfg)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    ny, nz = 6, 4
+    ys = np.linspace(lo[1] + 0.15 * (hi[1] - lo[1]), hi[1] - 0.15 * (hi[1] - lo[1]), ny)
+    zs = np.linspace(lo[2] + 0.2 * (hi[2] - lo[2]), hi[2] - 0.2 * (hi[2] - lo[2]), nz)
+    centers = np.array([[xm, y, z] for y in ys for z in zs for _ in (DIP, STRIKE)])
+    dirs = np.array([d for _ in ys for _ in zs for d in (DIP, STRIKE)], np.int32)
+    radii = np.full(len(dirs), 0.6 * (hi[1] - lo[1]) / ny)
+    gx, gy = np.meshgrid(np.linspace(0.1, 0.9, 10) * ext[0], np.linspace(0.1, 0.9, 10) * ext[1])
+    pts = np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, ext[2])], 1)
+    axes = (np.arange(len(pts)) % 3).astype(np.int32)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        bank, calls, outer = fm.greens_bank(centers, dirs, radii, pts, axes, cfg)
+        t_sweep = time.perf_counter() - t1
+    t_sweep = max_over_ranks([t_sweep], "cuda")[0]
+    n = len(dirs)
+    return {"metric": "Green's sweep time per case (s)", "higher_is_better": False,
+            "workload": f"configs[4] at one-GPU scale: {n} unit slips (dip+strike, {ny}x{nz} centres) on a vertical "
+                        f"fault ({len(faces)} faces, {fm.n_split_nodes} split nodes) in the configs[1] box "
+                        f"{list(cells)}, batch 16, {len(pts)} surface observations",
+            "value": round(t_sweep / (n * world), 5), "unit": "s", "n_gpus": world, "cases_per_rank": n,
+            "sweep_s": round(t_sweep, 3), "setup_s": round(t_setup, 3), "solver_calls": calls,
+            "outer_iterations": outer, "bank_shape": list(bank.shape), "bank_finite": bool(np.isfinite(bank).all()),
+            "entry": "ts_greens_bank (slip_to_rhs + solve + sampling per batch, host bank out)",
+            "clocks": clk.summary()}
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -425,6 +478,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-greens", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of the partitioned mesh")
     ap.add_argument("--partitioned", action="store_true", help="N=1: run the partitioned (N>1) path with one rank")
     ap.add_argument("--solve-cells", type=int, nargs=3, default=[140, 210, 70], help="configs[2]: 50M DOF")
@@ -593,6 +647,10 @@ def main():
         del u, f, uh, fh, fd
         torch.cuda.empty_cache()
         solve = solve_leg(args, ts, torch, world, rank, local)
+    greens = None
+    if not args.no_greens:
+        torch.cuda.empty_cache()
+        greens = greens_leg(args, ts, torch, world, rank, local)
 
     if rank == 0:
         out = {
@@ -614,6 +672,7 @@ def main():
             "r_sweep": sweep,
             "e2e_result_matches_device": ok,
             "solve": solve,
+            "greens": greens,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
