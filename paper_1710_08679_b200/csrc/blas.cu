@@ -522,7 +522,9 @@ __global__ void k_bcsr(const int32_t* __restrict__ row_ptr, const int32_t* __res
 // Assembled level-1 operator (K1 of the fp32 tier, setup.cpp assemble_tet4):
 // W cases of one block row per thread, fp32 accumulation of ~14 blocks — the
 // EbeOperator<float> order-1 product (fp32 cross-element sums) without atomics.
-template <int W>
+// ACC = float: the level-1 operator (fp32 sums); ACC = double: level 2 with the
+// reference's fp64 row accumulation in stored-block order (block_csr.hpp:40-54)
+template <int W, typename ACC>
 __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                             const float* __restrict__ blocks, int32_t n, const float* __restrict__ u,
                             float* __restrict__ f, int32_t B) {
@@ -531,11 +533,11 @@ __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* 
   const int64_t r = t / qpr;
   if (r >= n) return;
   const int b0 = static_cast<int>(t - r * qpr) * W;
-  float acc[3][W];
+  ACC acc[3][W];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int k = 0; k < W; ++k) acc[i][k] = 0.f;
+    for (int k = 0; k < W; ++k) acc[i][k] = ACC(0);
   const int32_t e1 = __ldg(row_ptr + r + 1);
   for (int32_t e = __ldg(row_ptr + r); e < e1; ++e) {
     const float* blk = blocks + 9 * int64_t(e);
@@ -547,15 +549,20 @@ __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* 
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int k = 0; k < W; ++k)
-        acc[i][k] = fmaf(m[3 * i + 2], x2.v[k], fmaf(m[3 * i + 1], x1.v[k], fmaf(m[3 * i], x0.v[k], acc[i][k])));
+      for (int k = 0; k < W; ++k) {
+        if constexpr (sizeof(ACC) == 4)
+          acc[i][k] = fmaf(m[3 * i + 2], x2.v[k], fmaf(m[3 * i + 1], x1.v[k], fmaf(m[3 * i], x0.v[k], acc[i][k])));
+        else  // a[b] += b0 u0 + b1 u1 + b2 u2 (block_csr.hpp:50)
+          acc[i][k] += double(m[3 * i]) * double(x0.v[k]) + double(m[3 * i + 1]) * double(x1.v[k]) +
+                       double(m[3 * i + 2]) * double(x2.v[k]);
+      }
   }
   float* fr = f + 3 * r * B + b0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     Pack<float, W> o;
 #pragma unroll
-    for (int k = 0; k < W; ++k) o.v[k] = acc[i][k];
+    for (int k = 0; k < W; ++k) o.v[k] = static_cast<float>(acc[i][k]);
     st<float, W>(fr + i * B, o);
   }
 }
@@ -828,12 +835,14 @@ void cg_update(double* r, double* u, const double* p, const double* q, int32_t n
 
 void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
                     float* f, int32_t B, cudaStream_t s) {
-  k_bcsr<<<grid_for(int64_t(n) * B, 128), 128, 0, s>>>(row_ptr, col_idx, blocks, n, u, f, B);
+  // fp64 row sums as the reference; W cases of a block row per thread, 16-byte u packs
+  TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W, double><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
+                                   row_ptr, col_idx, blocks, n, u, f, B)));
   TS_CUDA_LAUNCH();
 }
 void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
                    float* f, int32_t B, cudaStream_t s) {
-  TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
+  TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W, float><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
                                    row_ptr, col_idx, blocks, n, u, f, B)));
   TS_CUDA_LAUNCH();
 }

@@ -1128,13 +1128,11 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
     return;
   }
   bool done = false;
-  // Default dispatch (measured, profiles/r01_ebe_tile.txt): the chunk-tiled sweep
-  // wins for the tet4 level-1 operator and for narrow fp32 batches; the
-  // element-parallel RED sweep wins for wide tet10 batches.
-  // default (6): face-pair sweep (ebe_pair.cu) — measured fastest for every order / batch it covers
+  // Default dispatch (6, measured: profiles/r01_ebe_tile.txt, r01_ebe_pair_ncu.txt): the face-pair sweep
+  // (ebe_pair.cu) for every batch width it covers (1, 2, 4, 8, 16), else the element-parallel sweep;
+  // the chunk-tiled sweep on request (5).
   if (op.kernel == 7 || op.kernel == 6) done = ebe_pair_apply(op, u, f, batch, s, part);
-  if (!done && (op.kernel == 5 || (op.kernel == 6 && (op.order == 1 || (op.prec == 32 && batch <= 4)))))
-    done = ebe_tile_apply(op, u, f, batch, s, part);
+  if (!done && op.kernel == 5) done = ebe_tile_apply(op, u, f, batch, s, part);
   if (!done && op.kernel >= 3 && op.kernel != 4)
     done = (op.order == 2)
                ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s, e0, e1)
@@ -1235,7 +1233,8 @@ void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s) {
 }
 
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda, const double* mu,
-                   const uint8_t* dof_mask, int prec, const uint8_t* elem_group) {
+                   const uint8_t* dof_mask, int prec, const uint8_t* elem_group, int kernel_override,
+                   std::vector<int32_t>* element_order) {
   if (order != 1 && order != 2) validation("ebe: order must be 1 or 2");
   if (prec != 32 && prec != 64) validation("ebe: precision must be 32 or 64");
   require_device();
@@ -1319,15 +1318,16 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   // cluster node count (scatter traffic) and keeps gathers L2-local.
   {
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    std::vector<double> cen(3 * E);
-#pragma omp parallel for schedule(static)
-    for (size_t e = 0; e < E; ++e)
+    const bool reuse = element_order && element_order->size() == E;
+    std::vector<double> cen(reuse ? 0 : 3 * E);
+#pragma omp parallel for schedule(static) if (!reuse)
+    for (size_t e = 0; e < (reuse ? 0 : E); ++e)
       for (int c = 0; c < 3; ++c) {
         double x = 0.0;
         for (int a = 0; a < 4; ++a) x += m.coords[3 * static_cast<size_t>(m.tets10[10 * e + a]) + c];
         cen[3 * e + c] = 0.25 * x;
       }
-    for (size_t e = 0; e < E; ++e)
+    for (size_t e = 0; e < (reuse ? 0 : E); ++e)
       for (int c = 0; c < 3; ++c) {
         lo[c] = std::min(lo[c], cen[3 * e + c]);
         hi[c] = std::max(hi[c], cen[3 * e + c]);
@@ -1347,14 +1347,26 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     // (group, Morton key, id): a partitioned operator keeps its boundary elements
     // (group 0) ahead of the interior ones so the two sweep separately
     std::vector<std::tuple<uint8_t, uint64_t, int32_t>> key(E);
+    if (reuse) {  // the level set's other operators share one element order
 #pragma omp parallel for schedule(static)
-    for (size_t e = 0; e < E; ++e) {
-      uint64_t k = 0;
-      for (int c = 0; c < 3; ++c)
-        k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
-      key[e] = {elem_group ? elem_group[e] : uint8_t(0), k, static_cast<int32_t>(e)};
+      for (size_t i = 0; i < E; ++i) {
+        const int32_t e = (*element_order)[i];
+        key[i] = {elem_group ? elem_group[e] : uint8_t(0), 0, e};
+      }
+    } else {
+#pragma omp parallel for schedule(static)
+      for (size_t e = 0; e < E; ++e) {
+        uint64_t k = 0;
+        for (int c = 0; c < 3; ++c)
+          k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
+        key[e] = {elem_group ? elem_group[e] : uint8_t(0), k, static_cast<int32_t>(e)};
+      }
+      __gnu_parallel::sort(key.begin(), key.end());
+      if (element_order) {
+        element_order->resize(E);
+        for (size_t i = 0; i < E; ++i) (*element_order)[i] = std::get<2>(key[i]);
+      }
     }
-    __gnu_parallel::sort(key.begin(), key.end());
     op->group_split = 0;
     for (size_t i = 0; i < E; ++i)
       if (std::get<0>(key[i]) == 0) op->group_split = static_cast<int32_t>(i + 1);
@@ -1375,7 +1387,8 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->coef64.swap(c642);
     coef.swap(coef2);
   }
-  if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5 : std::string(k) == "pair" ? 7 : 6;
+  if (kernel_override >= 0) op->kernel = kernel_override;
+  else if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5 : std::string(k) == "pair" ? 7 : 6;
   {
     // fast-kernel layout: 3*node per local node, then the dof-mask word (bit 3a+c)
     const int cs3 = order == 1 ? 8 : 12;
@@ -1432,8 +1445,9 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->slab_ready.alloc(S);
   }
   setup_mark("ebe: morton + conn3");
-  // the tiled sweep's chunk records serve kernel 5, and kernel 6 batch widths the pair sweep does not cover
-  if (op->kernel == 5 || op->kernel == 6) build_tile_plan(*op, conn, cs);
+  // the tiled sweep's chunk records serve kernel 5 only (in the default mode the pair sweep covers the
+  // common batch widths and the element-parallel sweeps the rest)
+  if (op->kernel == 5) build_tile_plan(*op, conn, cs);
   setup_mark("ebe: tile plan");
   if (op->kernel == 7 || op->kernel == 6) build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32);
   setup_mark("ebe: pair plan");

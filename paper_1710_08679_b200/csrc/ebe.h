@@ -97,7 +97,10 @@ void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int con
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
 void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn_words, int cs,
                      const std::vector<double>& coef64, bool fp32);
-// elem_group (nullable, [E] in {0,1}): group-0 elements sweep separately (boundary first)
+// elem_group (nullable, [E] in {0,1}): group-0 elements sweep separately (boundary first);
+// kernel_override >= 0 fixes the sweep kernel (and so which plans are built);
+// element_order (nullable): empty -> receives the Morton order, filled -> reused
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda,
-                   const double* mu, const uint8_t* dof_mask, int prec, const uint8_t* elem_group = nullptr);
+                   const double* mu, const uint8_t* dof_mask, int prec, const uint8_t* elem_group = nullptr,
+                   int kernel_override = -1, std::vector<int32_t>* element_order = nullptr);
 }  // namespace tsg

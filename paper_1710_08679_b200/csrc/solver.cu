@@ -171,10 +171,17 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   lv->n0 = N;
   lv->n1 = V;
   setup_mark("levels: start");
-  lv->outer.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 64));
+  {
+    const char* e = std::getenv("TSGPU_L1");
+    lv->l1_assembled = !(e && std::string(e) == "ebe");
+  }
+  std::vector<int32_t> eorder;  // one Morton element order for the three operators
+  lv->outer.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 64, nullptr, -1, &eorder));
   setup_mark("levels: outer operator");
-  lv->l0.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 32));
-  lv->l1.reset(ebe_create(m, 1, n_mat, lam, mu, mask1.data(), 32));
+  lv->l0.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 32, nullptr, -1, &eorder));
+  // with the assembled level 1 the tet4 EBE operator only serves the API and its
+  // block-Jacobi diagonal: no sweep plans
+  lv->l1.reset(ebe_create(m, 1, n_mat, lam, mu, mask1.data(), 32, nullptr, lv->l1_assembled ? 3 : -1, &eorder));
   setup_mark("levels: l0 + l1 operators");
   // geometric P1 (prolongation.hpp:67-98): edge endpoints (vmin, vmax) + transpose
   {
@@ -214,10 +221,6 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   setup_mark("levels: P1");
   const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1);
   setup_mark("levels: K1 assembly");
-  {
-    const char* e = std::getenv("TSGPU_L1");
-    lv->l1_assembled = !(e && std::string(e) == "ebe");
-  }
   if (lv->l1_assembled) {
     const BcsrD k1f = assemble_tet4(m, lam_e, mu_e, mask1, true);
     std::vector<float> bl(k1f.blocks.size());
