@@ -740,6 +740,18 @@ __global__ void k_masked_identity(const uint8_t* __restrict__ mask, int64_t n_ve
   else std::memset(&v, 0, sizeof v);
   reinterpret_cast<V4*>(f)[i] = v;
 }
+// f[dof][*] = u[dof][*] for the listed constrained dofs (after a memset of f):
+// the identity rows of ebe_operator.hpp:96-110 without reading the whole of u
+template <typename T>
+__global__ void k_identity_rows(const int32_t* __restrict__ dofs, int32_t n_dofs, int32_t batch,
+                                const T* __restrict__ u, T* __restrict__ f) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(n_dofs) * batch) return;
+  const int64_t k = i / batch;
+  const int64_t at = int64_t(dofs[k]) * batch + (i - k * batch);
+  f[at] = u[at];
+}
+
 template <typename T>
 __global__ void k_masked_identity_scalar(const uint8_t* __restrict__ mask, int64_t n, int32_t batch,
                                          const T* __restrict__ u, T* __restrict__ f) {
@@ -1110,8 +1122,14 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
   }
   // identity rows for constrained dofs, zero elsewhere (ebe_operator.hpp:96-110)
   if (init) {
-    if (!op.has_mask) {
+    if (!op.has_mask || op.n_masked_dofs * 10 < 3 * int64_t(op.n_nodes)) {
+      // write-only zero fill, then the (few) constrained rows copied from u
       TS_CUDA(cudaMemsetAsync(f, 0, n * sizeof(T), s));
+      if (op.has_mask && op.n_masked_dofs > 0) {
+        k_identity_rows<T><<<grid_for(int64_t(op.n_masked_dofs) * batch, 256), 256, 0, s>>>(
+            op.masked_dofs.get(), op.n_masked_dofs, batch, u, f);
+        TS_CUDA_LAUNCH();
+      }
     } else {
       constexpr int W = sizeof(typename Vec4Of<T>::type) / sizeof(T);
       if (batch % W == 0)
@@ -1453,7 +1471,14 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   setup_mark("ebe: pair plan");
   op->conn.upload(conn);
   op->coef.upload(coef);
-  if (dof_mask) op->mask.upload(op->host_mask);
+  if (dof_mask) {
+    op->mask.upload(op->host_mask);
+    std::vector<int32_t> md;
+    for (size_t d = 0; d < op->host_mask.size(); ++d)
+      if (op->host_mask[d]) md.push_back(static_cast<int32_t>(d));
+    op->n_masked_dofs = static_cast<int32_t>(md.size());
+    op->masked_dofs.upload(md);
+  }
   TS_CUDA(cudaDeviceSynchronize());
   return op.release();
 }

@@ -60,6 +60,8 @@ struct ts_ebe {
   tsg::DevBuf<int> slab_ready;          // per-slab arrival counters (persistent kernel gates)
   tsg::DevBuf<unsigned char> coef;      // [E][12] of T: b_1,b_2,b_3, lp, mp, 0
   tsg::DevBuf<unsigned char> mask;      // [3N] uint8 (empty if unconstrained)
+  tsg::DevBuf<int32_t> masked_dofs;     // constrained dof indices (identity rows)
+  int32_t n_masked_dofs = 0;
   std::vector<double> coef64;           // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
   std::vector<int32_t> host_conn;       // host [E][npe] (setup only)
   std::vector<uint8_t> host_mask;       // host [3N]
