@@ -35,113 +35,10 @@ namespace tsg {
 
 namespace {
 
-constexpr int kBlock = 128;
-
 template <typename T> struct Vec4Of;
 template <typename T> using float2_or = typename std::conditional<sizeof(T) == 4, float2, T>::type;
 template <> struct Vec4Of<float> { using type = float4; };
 template <> struct Vec4Of<double> { using type = double2; };
-
-template <typename T>
-__device__ __forceinline__ void load_coef(const T* __restrict__ p, T (&c)[12]);
-template <>
-__device__ __forceinline__ void load_coef<float>(const float* __restrict__ p, float (&c)[12]) {
-  const float4* q = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const float4 v = __ldg(q + i);
-    c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
-  }
-}
-template <>
-__device__ __forceinline__ void load_coef<double>(const double* __restrict__ p, double (&c)[12]) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    const double2 v = __ldg(q + i);
-    c[2 * i] = v.x; c[2 * i + 1] = v.y;
-  }
-}
-
-// ---- reduction-width helpers for the cluster scatter --------------------------
-template <typename VR, typename T>
-__device__ __forceinline__ VR vr_load(const T* eo, int idx, bool zero) {
-  if (zero) { VR z; memset(&z, 0, sizeof z); return z; }
-  return *reinterpret_cast<const VR*>(eo + idx);
-}
-__device__ __forceinline__ float4 vr_add(float4 a, float4 b) {
-  const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
-  const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
-  return make_float4(lo.x, lo.y, hi.x, hi.y);
-}
-__device__ __forceinline__ float2 vr_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float vr_add(float a, float b) { return a + b; }
-__device__ __forceinline__ double vr_add(double a, double b) { return a + b; }
-__device__ __forceinline__ void red_vr(float* p, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void red_vr(float* p, float2 v) { red_lane(reinterpret_cast<float2*>(p), v); }
-__device__ __forceinline__ void red_vr(float* p, float v) { atomicAdd(p, v); }
-__device__ __forceinline__ void red_vr(double* p, double v) { atomicAdd(p, v); }
-
-// Direct element-parallel product: gather from L2, exact lean element product,
-// vector RED scatter. T = storage scalar, V = lane vector, NPE = 10 | 4.
-template <typename T, typename V, int NPE, int CS>
-__global__ void __launch_bounds__(kBlock)
-k_ebe_direct(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t n_elems,
-             int tpe_shift, int32_t batch, int32_t col_base, const T* __restrict__ u,
-             T* __restrict__ f) {
-  using O = LaneOps<V>;
-  constexpr int CPT = O::kCols;
-  const int64_t gt = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
-  const int64_t e = gt >> tpe_shift;
-  if (e >= n_elems) return;
-  const int col = col_base + static_cast<int>(gt & ((1 << tpe_shift) - 1)) * CPT;
-  if (col >= batch) return;
-
-  int32_t nd[CS];
-  const int4* c4 = reinterpret_cast<const int4*>(conn + static_cast<size_t>(e) * CS);
-#pragma unroll
-  for (int q = 0; q < CS / 4; ++q) {
-    const int4 v = __ldg(c4 + q);
-    nd[4 * q] = v.x; nd[4 * q + 1] = v.y; nd[4 * q + 2] = v.z; nd[4 * q + 3] = v.w;
-  }
-  T cf[12];
-  load_coef<T>(coef + static_cast<size_t>(e) * 12, cf);
-  V b[3][3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cf[3 * k + d]);
-  const V lp = O::splat(cf[9]), mp = O::splat(cf[10]);
-
-  V uu[NPE][3];
-#pragma unroll
-  for (int a = 0; a < NPE; ++a) {
-    const int64_t node = nd[a] & 0x0FFFFFFF;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const bool masked = (nd[a] >> (28 + c)) & 1;
-      const T* src = u + (3 * node + c) * static_cast<int64_t>(batch) + col;
-      uu[a][c] = masked ? O::zero() : ld_lane(reinterpret_cast<const V*>(src));
-    }
-  }
-  V ff[NPE][3];
-  if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
-  else tet4_product<V>(uu, b, lp, mp, ff);
-#pragma unroll
-  for (int a = 0; a < NPE; ++a) {
-    const int64_t node = nd[a] & 0x0FFFFFFF;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      if ((nd[a] >> (28 + c)) & 1) continue;
-      T* dst = f + (3 * node + c) * static_cast<int64_t>(batch) + col;
-      red_lane(reinterpret_cast<V*>(dst), ff[a][c]);
-    }
-  }
-}
 
 // ---- cp.async helpers (Ampere+ LDGSTS; zero-fill when src_size == 0) --------
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int src_size, int bytes) {
@@ -157,7 +54,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Persistent, software-pipelined element sweep (default kernel).
+// Persistent, software-pipelined element sweep (generic: any batch width, multi-pass beyond 32 cases).
 // Each lane group (TPE threads, CPT cases each) walks elements e, e+G, e+2G..
 // (G = all groups of the grid, so the grid sweeps a contiguous, L2-resident
 // window of the Morton-ordered mesh). While element e is computed from shared
@@ -282,7 +179,6 @@ __device__ __forceinline__ void red_pred(double* p, double v, unsigned skip) {
 template <typename T, typename V, int NPE, int CS, int B>
 __global__ void __launch_bounds__(128, 3)
 k_ebe_fast(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t e_begin, int32_t n_elems,
-           const int32_t* __restrict__ init_nodes, int32_t n_init, const uint8_t* __restrict__ mask,
            const T* __restrict__ u, T* __restrict__ f) {
   using O = LaneOps<V>;
   constexpr int CPT = O::kCols;
@@ -303,40 +199,6 @@ k_ebe_fast(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t
   const int col = lane * CPT;
   const bool colok = col < B;
   constexpr bool kFull = TPE * CPT == B;  // every lane's columns exist
-  // First-touch initialisation of the NEXT slab's nodes (f = mask ? u : 0,
-  // ebe_operator.hpp:96-110): plain stores of rows that no element of this
-  // slab touches, so they land in L2 just before the next slab RED-accumulates
-  // into them and f is never read back from DRAM.
-  {
-    // a node's 3*B values are contiguous: threads own consecutive W-wide chunks
-    constexpr int W = (B * sizeof(T)) % 16 == 0 ? 16 / sizeof(T) : ((B * sizeof(T)) % 8 == 0 ? 8 / sizeof(T) : 1);
-    using VW = typename std::conditional<W * sizeof(T) == 16, int4,
-                                         typename std::conditional<W * sizeof(T) == 8, int2, T>::type>::type;
-    constexpr int CH = 3 * B / W;  // chunks per node
-    // entries carry the node's dof-mask bits in bits 28..30; 4 independent
-    // items per trip so the entry loads overlap (this loop is latency-bound)
-    const int64_t total = int64_t(n_init) * CH, stride = int64_t(gridDim.x) * NT;
-    for (int64_t it0 = int64_t(blockIdx.x) * NT + threadIdx.x; it0 < total; it0 += 4 * stride) {
-      int32_t ent[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t it = it0 + q * stride;
-        ent[q] = it < total ? __ldg(init_nodes + it / CH) : -1;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t it = it0 + q * stride;
-        if (it >= total) break;
-        const int k = static_cast<int>(it % CH);
-        const int c = (k * W) / B;
-        const size_t off = 3 * static_cast<size_t>(ent[q] & 0x0FFFFFFF) * B + static_cast<size_t>(k) * W;
-        VW v;
-        if ((ent[q] >> (28 + c)) & 1) v = *reinterpret_cast<const VW*>(u + off);
-        else memset(&v, 0, sizeof v);
-        *reinterpret_cast<VW*>(f + off) = v;
-      }
-    }
-  }
   int e = e_begin + blockIdx.x * GROUPS + grp;
 
   int32_t nd[CS];  // connectivity of the element whose gathers issue next
@@ -437,293 +299,6 @@ k_ebe_fast(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t
     s ^= 1;
   }
   cp_async_wait<0>();
-}
-
-template <typename T, typename V, int NPE, int CS, int B>
-__global__ void __launch_bounds__(128, 3)
-k_ebe_persist(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t n_elems,
-              const int32_t* __restrict__ slab_ptr, const int32_t* __restrict__ init_ptr, int n_slabs,
-              const int32_t* __restrict__ init_nodes, int* __restrict__ slab_ready,
-              const T* __restrict__ u, T* __restrict__ f) {
-  const int32_t e_begin = 0;
-  using O = LaneOps<V>;
-  constexpr int CPT = O::kCols;
-  constexpr int NIN = NPE * 3;
-  constexpr int NT = 128;
-  constexpr int TPE = (B + CPT - 1) / CPT <= 1 ? 1 : ((B + CPT - 1) / CPT <= 2 ? 2 : ((B + CPT - 1) / CPT <= 4 ? 4 : ((B + CPT - 1) / CPT <= 8 ? 8 : 16)));
-  constexpr int GROUPS = NT / TPE;
-  constexpr int TPC = 16 / sizeof(T);
-  constexpr int CHUNKS = 12 / TPC;
-  extern __shared__ __align__(16) unsigned char smem[];
-  V* ubuf = reinterpret_cast<V*>(smem);                                  // [2][NIN][NT]
-  T* cbuf = reinterpret_cast<T*>(smem + 2 * NIN * NT * sizeof(V));        // [2][GROUPS][12]
-  int32_t* nbuf = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(cbuf) +
-                                             2 * GROUPS * 12 * sizeof(T));  // [2][GROUPS][CS]
-  const int grp = threadIdx.x / TPE;
-  const int lane = threadIdx.x % TPE;
-  const int G = gridDim.x * GROUPS;
-  const int col = lane * CPT;
-  const bool colok = col < B;
-  constexpr bool kFull = TPE * CPT == B;  // every lane's columns exist
-  // First-touch initialisation of the NEXT slab's nodes (f = mask ? u : 0,
-  // ebe_operator.hpp:96-110): plain stores of rows that no element of this
-  // slab touches, so they land in L2 just before the next slab RED-accumulates
-  // into them and f is never read back from DRAM.
-  // block's share of one slab's first-touch init, then publish it
-  auto init_share = [&](int j) {
-    constexpr int W = (B * sizeof(T)) % 16 == 0 ? 16 / sizeof(T) : ((B * sizeof(T)) % 8 == 0 ? 8 / sizeof(T) : 1);
-    using VW = typename std::conditional<W * sizeof(T) == 16, int4,
-                                         typename std::conditional<W * sizeof(T) == 8, int2, T>::type>::type;
-    constexpr int CH = 3 * B / W;
-    const int64_t lo = int64_t(__ldg(init_ptr + j)) * CH, hi = int64_t(__ldg(init_ptr + j + 1)) * CH;
-    const int64_t per = (hi - lo + gridDim.x - 1) / gridDim.x;
-    const int64_t b0 = lo + per * blockIdx.x, b1 = min(hi, b0 + per);
-    for (int64_t it0 = b0 + threadIdx.x; it0 < b1; it0 += 4 * NT) {
-      int32_t ent[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t it = it0 + q * NT;
-        ent[q] = it < b1 ? __ldg(init_nodes + it / CH) : 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t it = it0 + q * NT;
-        if (it >= b1) break;
-        const int kk = static_cast<int>(it % CH);
-        const int c = (kk * W) / B;
-        const size_t off = 3 * static_cast<size_t>(ent[q] & 0x0FFFFFFF) * B + static_cast<size_t>(kk) * W;
-        VW v;
-        if ((ent[q] >> (28 + c)) & 1) v = *reinterpret_cast<const VW*>(u + off);
-        else memset(&v, 0, sizeof v);
-        *reinterpret_cast<VW*>(f + off) = v;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(slab_ready + j, 1);
-    }
-  };
-  int next_init = 0;   // next slab whose init share this block owes
-  int ready = -1;      // highest slab known fully initialised
-  int js = 0;          // slab of the block's current chunk
-  init_share(next_init++);
-  int e = e_begin + blockIdx.x * GROUPS + grp;
-
-  int32_t nd[CS];  // connectivity of the element whose gathers issue next
-  auto load_conn = [&](int ee) {
-    if (ee < n_elems) {
-      const int4* c4 = reinterpret_cast<const int4*>(conn + static_cast<size_t>(ee) * CS);
-#pragma unroll
-      for (int q = 0; q < CS / 4; ++q) {
-        const int4 v = __ldg(c4 + q);
-        nd[4 * q] = v.x; nd[4 * q + 1] = v.y; nd[4 * q + 2] = v.z; nd[4 * q + 3] = v.w;
-      }
-    }
-  };
-  auto issue = [&](int ee, int stage) {
-    if (ee < n_elems) {
-      if (lane == 0) {
-        int4* dst = reinterpret_cast<int4*>(nbuf + (stage * GROUPS + grp) * CS);
-#pragma unroll
-        for (int q = 0; q < CS / 4; ++q) dst[q] = make_int4(nd[4 * q], nd[4 * q + 1], nd[4 * q + 2], nd[4 * q + 3]);
-      }
-      for (int q = lane; q < CHUNKS; q += TPE)
-        cp_async(cbuf + (stage * GROUPS + grp) * 12 + q * TPC, coef + static_cast<size_t>(ee) * 12 + q * TPC, 16, 16);
-      V* dst = ubuf + stage * NIN * NT + 2 * threadIdx.x;  // dof q at [q/2][tid][q%2]
-      const unsigned mw = static_cast<unsigned>(nd[NPE]);
-      if (kFull && mw == 0u) {  // interior element, all columns live: no per-dof predicates
-#pragma unroll
-        for (int a = 0; a < NPE; ++a) {
-          const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            cp_async(dst + ((a * 3 + c) >> 1) * 2 * NT + ((a * 3 + c) & 1), row + c * B, int(sizeof(V)), sizeof(V));
-        }
-      } else {
-        const unsigned live = colok ? ~mw : 0u;
-#pragma unroll
-        for (int a = 0; a < NPE; ++a) {
-          const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            cp_async(dst + ((a * 3 + c) >> 1) * 2 * NT + ((a * 3 + c) & 1), row + c * B,
-                     ((live >> (3 * a + c)) & 1u) * int(sizeof(V)), sizeof(V));
-        }
-      }
-    }
-    cp_async_commit();
-  };
-
-  load_conn(e);
-  issue(e, 0);
-  load_conn(e + G);
-  int s = 0;
-  int chunk = blockIdx.x * GROUPS;  // first element of the block's current chunk
-  while (chunk < n_elems) {
-    const int en = e + G;
-    {  // block-uniform slab bookkeeping
-      const int last = min(chunk + GROUPS, n_elems) - 1;
-      while (js + 1 < n_slabs && last >= __ldg(slab_ptr + js + 1)) ++js;
-      while (next_init < n_slabs && next_init <= js + 1) init_share(next_init++);
-      if (ready < js) {
-        if (threadIdx.x == 0) {
-          const int want = gridDim.x;
-          for (int j = ready + 1; j <= js; ++j) {
-            int v;
-            do {
-              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(slab_ready + j) : "memory");
-              if (v < want) __nanosleep(64);
-            } while (v < want);
-          }
-        }
-        __syncthreads();
-        ready = js;
-      }
-    }
-    issue(en, s ^ 1);
-    load_conn(en + G);  // consumed by the next iteration's issue
-    cp_async_wait<1>();
-    __syncwarp();
-    if (e < n_elems && colok) {
-      const T* cf = cbuf + (s * GROUPS + grp) * 12;
-      V b[3][3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cf[3 * k + d]);
-      const V lp = O::splat(cf[9]), mp = O::splat(cf[10]);
-      V uu[NPE][3];
-      const V* src = ubuf + s * NIN * NT + 2 * threadIdx.x;
-#pragma unroll
-      for (int q = 0; q < NIN; q += 2) {
-        V2Of<V> pr = *reinterpret_cast<const V2Of<V>*>(src + (q >> 1) * 2 * NT);
-        uu[q / 3][q % 3] = pr.a;
-        uu[(q + 1) / 3][(q + 1) % 3] = pr.b;
-      }
-      V ff[NPE][3];
-      if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
-      else tet4_product<V>(uu, b, lp, mp, ff);
-      const int32_t* ndc = nbuf + (s * GROUPS + grp) * CS;
-      const unsigned mk = static_cast<unsigned>(ndc[NPE]);
-      if (mk == 0u) {
-#pragma unroll
-        for (int a = 0; a < NPE; ++a) {
-          T* row = f + static_cast<size_t>(static_cast<uint32_t>(ndc[a])) * B + col;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(row + c * B), ff[a][c]);
-        }
-      } else {
-#pragma unroll
-        for (int a = 0; a < NPE; ++a) {
-          T* row = f + static_cast<size_t>(static_cast<uint32_t>(ndc[a])) * B + col;
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            red_pred(reinterpret_cast<V*>(row + c * B), ff[a][c], (mk >> (3 * a + c)) & 1u);
-        }
-      }
-    }
-    __syncwarp();
-    e = en;
-    s ^= 1;
-    chunk += G;
-  }
-  cp_async_wait<0>();
-  while (next_init < n_slabs) init_share(next_init++);  // never owed in practice; keeps counts complete
-}
-
-// Cluster-aggregated product. A block owns a cluster of W consecutive
-// (Morton-ordered) elements and one chunk of RB = TPE*CPT cases.
-//  phase 1: lane groups compute their element (as in k_ebe_direct) and park the
-//           30 (or 12) per-node outputs in shared memory (plain stores);
-//  phase 2: threads own (cluster node, axis, RW-case quad) items, sum the
-//           node's incidences in element order from shared memory, and issue
-//           ONE vector RED per item — ~PN/W (~3.4 for W=16) node updates per
-//           element instead of 10, at 4 cases per RED.
-template <typename T, typename V, typename VR, int NPE, int CS>
-__global__ void __launch_bounds__(128)
-k_ebe_cluster(const int32_t* __restrict__ conn, const T* __restrict__ coef, int32_t n_elems,
-              int tpe_shift, const int32_t* __restrict__ node_ptr, const int32_t* __restrict__ nodes,
-              const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ inc, int32_t batch,
-              const T* __restrict__ u, T* __restrict__ f) {
-  using O = LaneOps<V>;
-  constexpr int CPT = O::kCols;
-  constexpr int RW = sizeof(VR) / sizeof(T);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* eo = reinterpret_cast<T*>(smem_raw);
-  const int TPE = 1 << tpe_shift;
-  const int RB = TPE * CPT;
-  const int W = blockDim.x >> tpe_shift;
-  const int slot_stride = (NPE * 3 + 1) * RB;  // +RB pad: conflict-free STS across slots
-  const int col0 = blockIdx.y * RB;
-  const int32_t cl = blockIdx.x;
-
-  {
-    const int slot = threadIdx.x >> tpe_shift;
-    const int lane = threadIdx.x & (TPE - 1);
-    const int64_t e = static_cast<int64_t>(cl) * W + slot;
-    const int col = col0 + lane * CPT;
-    if (e < n_elems && col < batch) {
-      int32_t nd[CS];
-      const int4* c4 = reinterpret_cast<const int4*>(conn + static_cast<size_t>(e) * CS);
-#pragma unroll
-      for (int q = 0; q < CS / 4; ++q) {
-        const int4 v = __ldg(c4 + q);
-        nd[4 * q] = v.x; nd[4 * q + 1] = v.y; nd[4 * q + 2] = v.z; nd[4 * q + 3] = v.w;
-      }
-      T cf[12];
-      load_coef<T>(coef + static_cast<size_t>(e) * 12, cf);
-      V b[3][3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cf[3 * k + d]);
-      const V lp = O::splat(cf[9]), mp = O::splat(cf[10]);
-      V uu[NPE][3];
-#pragma unroll
-      for (int a = 0; a < NPE; ++a) {
-        const int64_t node = nd[a] & 0x0FFFFFFF;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const bool masked = (nd[a] >> (28 + c)) & 1;
-          const T* src = u + (3 * node + c) * static_cast<int64_t>(batch) + col;
-          uu[a][c] = masked ? O::zero() : ld_lane(reinterpret_cast<const V*>(src));
-        }
-      }
-      V ff[NPE][3];
-      if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
-      else tet4_product<V>(uu, b, lp, mp, ff);
-      T* dst = eo + slot * slot_stride + lane * CPT;
-#pragma unroll
-      for (int a = 0; a < NPE; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) *reinterpret_cast<V*>(dst + (a * 3 + c) * RB) = ff[a][c];
-    }
-  }
-  __syncthreads();
-  const int nb = node_ptr[cl];
-  const int pn = node_ptr[cl + 1] - nb;
-  const int qpr = RB / RW;
-  const int items = pn * 3 * qpr;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int n = it / (3 * qpr);
-    const int rem = it - n * 3 * qpr;
-    const int c = rem / qpr;
-    const int q = rem - c * qpr;
-    const int colq = col0 + q * RW;
-    if (colq >= batch) continue;
-    const int32_t g = __ldg(nodes + nb + n);
-    if ((g >> (28 + c)) & 1) continue;  // constrained dof: contributions discarded
-    const int k0 = __ldg(inc_ptr + nb + n), k1 = __ldg(inc_ptr + nb + n + 1);
-    VR acc = vr_load<VR>(eo, 0, true);
-    for (int k = k0; k < k1; ++k) {
-      const int s = __ldg(inc + k);
-      const int slot = s / NPE, a = s - slot * NPE;
-      acc = vr_add(acc, vr_load<VR>(eo, slot * slot_stride + (a * 3 + c) * RB + q * RW, false));
-    }
-    const int64_t node = g & 0x0FFFFFFF;
-    red_vr(f + (3 * node + c) * static_cast<int64_t>(batch) + colq, acc);
-  }
 }
 
 // f = mask ? u : 0, vectorised over the contiguous [dof][case] array.
@@ -860,100 +435,6 @@ int pow2ceil(int x) {
 }
 
 template <typename T, typename V, int NPE, int CS>
-void launch_direct(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
-  constexpr int CPT = LaneOps<V>::kCols;
-  const int nct = (batch + CPT - 1) / CPT;  // column threads needed
-  const int tpe = std::min(pow2ceil(nct), 16);
-  int shift = 0;
-  while ((1 << shift) < tpe) ++shift;
-  const int passes = (nct + tpe - 1) / tpe;
-  const int64_t threads = static_cast<int64_t>(op.n_elems) << shift;
-  for (int p = 0; p < passes; ++p) {
-    k_ebe_direct<T, V, NPE, CS><<<grid_for(threads, kBlock), kBlock, 0, s>>>(
-        op.conn.get(), reinterpret_cast<const T*>(op.coef.get()), op.n_elems, shift, batch,
-        p * tpe * CPT, u, f);
-    TS_CUDA_LAUNCH();
-  }
-}
-
-
-// Build (once per W) the cluster node tables: for each block of W consecutive
-// elements, its unique nodes (with mask bits) and each node's incidences
-// (slot * npe + local index) in element order.
-const EbeClusters& get_clusters(const ts_ebe& op, int W) {
-  std::lock_guard<std::mutex> lock(op.clusters_mu);
-  for (const auto& c : op.clusters)
-    if (c->W == W) return *c;
-  auto cl = std::make_unique<EbeClusters>();
-  cl->W = W;
-  const int npe = op.npe;
-  const int64_t E = op.n_elems;
-  const int32_t C = static_cast<int32_t>((E + W - 1) / W);
-  cl->n_clusters = C;
-  std::vector<int32_t> node_ptr(C + 1, 0), nodes, inc_ptr, stamp(op.n_nodes, -1), loc(op.n_nodes, 0);
-  std::vector<uint16_t> inc;
-  nodes.reserve(static_cast<size_t>(E) * 4);
-  inc_ptr.reserve(static_cast<size_t>(E) * 4 + 1);
-  inc.reserve(static_cast<size_t>(E) * npe);
-  std::vector<int32_t> cnt;
-  std::vector<std::vector<uint16_t>> lists;
-  for (int32_t c = 0; c < C; ++c) {
-    const int64_t e0 = int64_t(c) * W, e1 = std::min<int64_t>(E, e0 + W);
-    int32_t pn = 0;
-    lists.clear();
-    for (int64_t e = e0; e < e1; ++e)
-      for (int a = 0; a < npe; ++a) {
-        const int32_t g = op.host_conn[e * npe + a];
-        if (stamp[g] != c) {
-          stamp[g] = c;
-          loc[g] = pn++;
-          int32_t word = g;
-          if (op.has_mask)
-            for (int k = 0; k < 3; ++k)
-              if (op.host_mask[3 * size_t(g) + k]) word |= 1 << (28 + k);
-          nodes.push_back(word);
-          lists.emplace_back();
-        }
-        lists[loc[g]].push_back(static_cast<uint16_t>((e - e0) * npe + a));
-      }
-    for (int32_t n = 0; n < pn; ++n) {
-      inc_ptr.push_back(static_cast<int32_t>(inc.size()));
-      inc.insert(inc.end(), lists[n].begin(), lists[n].end());
-    }
-    node_ptr[c + 1] = node_ptr[c] + pn;
-    cl->max_nodes = std::max(cl->max_nodes, pn);
-  }
-  inc_ptr.push_back(static_cast<int32_t>(inc.size()));
-  cl->nodes_per_elem = E ? double(nodes.size()) / double(E) : 0.0;
-  cl->node_ptr.upload(node_ptr);
-  cl->nodes.upload(nodes);
-  cl->inc_ptr.upload(inc_ptr);
-  cl->inc.upload(inc);
-  TS_CUDA(cudaDeviceSynchronize());
-  op.clusters.push_back(std::move(cl));
-  return *op.clusters.back();
-}
-
-template <typename T, typename V, typename VR, int NPE, int CS>
-void launch_cluster(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
-  constexpr int CPT = LaneOps<V>::kCols;
-  constexpr int NT = 128;
-  const int nct = (batch + CPT - 1) / CPT;
-  const int tpe = std::min(pow2ceil(nct), 16);
-  int shift = 0;
-  while ((1 << shift) < tpe) ++shift;
-  const int RB = tpe * CPT;
-  const int W = NT / tpe;
-  const EbeClusters& cl = get_clusters(op, W);
-  const size_t smem = static_cast<size_t>(W) * (NPE * 3 + 1) * RB * sizeof(T);
-  dim3 grid(cl.n_clusters, (batch + RB - 1) / RB);
-  k_ebe_cluster<T, V, VR, NPE, CS><<<grid, NT, smem, s>>>(
-      op.conn.get(), reinterpret_cast<const T*>(op.coef.get()), op.n_elems, shift, cl.node_ptr.get(),
-      cl.nodes.get(), cl.inc_ptr.get(), cl.inc.get(), batch, u, f);
-  TS_CUDA_LAUNCH();
-}
-
-template <typename T, typename V, int NPE, int CS>
 void launch_pipe(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t e0 = 0,
                  int32_t e1 = -1) {
   if (e1 < 0) e1 = op.n_elems;
@@ -1013,8 +494,7 @@ bool launch_fast_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t e
     if (e1 <= e0) return true;
     const int64_t need = (int64_t(e1 - e0) + GROUPS - 1) / GROUPS;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
-    kern<<<grid, NT, smem, s>>>(op.conn3.get(), reinterpret_cast<const T*>(op.coef.get()), e0, e1,
-                                nullptr, 0, nullptr, u, f);
+    kern<<<grid, NT, smem, s>>>(op.conn3.get(), reinterpret_cast<const T*>(op.coef.get()), e0, e1, u, f);
     TS_CUDA_LAUNCH();
     return true;
   }
@@ -1034,92 +514,12 @@ bool launch_fast(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t
   }
 }
 
-template <typename T, typename V, int NPE, int CS, int B>
-bool launch_persist_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s) {
-  constexpr int CPT = LaneOps<V>::kCols;
-  constexpr int NT = 128;
-  constexpr int nct = (B + CPT - 1) / CPT;
-  if constexpr (nct > 16) {
-    return false;
-  } else {
-    constexpr int TPE = nct <= 1 ? 1 : nct <= 2 ? 2 : nct <= 4 ? 4 : nct <= 8 ? 8 : 16;
-    constexpr int GROUPS = NT / TPE;
-    const size_t smem = 2 * size_t(NPE) * 3 * NT * sizeof(V) + 2 * size_t(GROUPS) * 12 * sizeof(T) +
-                        2 * size_t(GROUPS) * CS * sizeof(int32_t);
-    auto kern = k_ebe_persist<T, V, NPE, CS, B>;
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
-      int dev = 0;
-      TS_CUDA(cudaGetDevice(&dev));
-      TS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-      per_sm = std::max(per_sm, 1);
-    }
-    const int S = static_cast<int>(op.slab_ptr.size()) - 1;
-    const int64_t need = (int64_t(op.n_elems) + GROUPS - 1) / GROUPS;
-    // persistent grid: every block co-resident (required by the slab gates)
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
-    TS_CUDA(cudaMemsetAsync(op.slab_ready.get(), 0, S * sizeof(int), s));
-    kern<<<grid, NT, smem, s>>>(op.conn3.get(), reinterpret_cast<const T*>(op.coef.get()), op.n_elems,
-                                op.slab_ptr_dev.get(), op.slab_init_ptr_dev.get(), S, op.slab_init.get(),
-                                op.slab_ready.get(), u, f);
-    TS_CUDA_LAUNCH();
-    return true;
-  }
-}
-
-template <typename T, typename V, int NPE, int CS>
-bool launch_persist(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
-  switch (batch) {
-    case 1: return launch_persist_b<T, V, NPE, CS, 1>(op, u, f, s);
-    case 2: return launch_persist_b<T, V, NPE, CS, 2>(op, u, f, s);
-    case 4: return launch_persist_b<T, V, NPE, CS, 4>(op, u, f, s);
-    case 8: return launch_persist_b<T, V, NPE, CS, 8>(op, u, f, s);
-    case 16: return launch_persist_b<T, V, NPE, CS, 16>(op, u, f, s);
-    case 20: return launch_persist_b<T, V, NPE, CS, 20>(op, u, f, s);
-    case 32: return launch_persist_b<T, V, NPE, CS, 32>(op, u, f, s);
-    default: return false;
-  }
-}
-
-template <typename T, int NPE, int CS, int CS3>
-void launch_sweep(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s) {
-  if constexpr (sizeof(T) == 4) {
-    if (batch % 2 == 0) {
-      if (op.kernel >= 2) return launch_pipe<float, float2, NPE, CS>(op, u, f, batch, s);
-      if (op.kernel == 0) return launch_direct<float, float2, NPE, CS>(op, u, f, batch, s);
-      if (batch % 4 == 0) return launch_cluster<float, float2, float4, NPE, CS>(op, u, f, batch, s);
-      return launch_cluster<float, float2, float2, NPE, CS>(op, u, f, batch, s);
-    }
-    if (op.kernel >= 2) return launch_pipe<float, float, NPE, CS>(op, u, f, batch, s);
-    if (op.kernel == 0) return launch_direct<float, float, NPE, CS>(op, u, f, batch, s);
-    return launch_cluster<float, float, float, NPE, CS>(op, u, f, batch, s);
-  } else {
-    if (op.kernel >= 2) return launch_pipe<double, double, NPE, CS>(op, u, f, batch, s);
-    if (op.kernel == 0) return launch_direct<double, double, NPE, CS>(op, u, f, batch, s);
-    return launch_cluster<double, double, double, NPE, CS>(op, u, f, batch, s);
-  }
-}
-
 // part: -1 = every element, 0 = boundary group [0, group_split), 1 = interior
 // group [group_split, E) (partitioned operators, dist_solver.cu); init: write
 // the masked identity into f first.
 template <typename T>
 void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int part, bool init) {
   const int64_t n = 3 * static_cast<int64_t>(op.n_nodes) * batch;
-  if (part < 0 && init && op.kernel == 4 && op.n_elems > 0) {
-    if (op.timing) TS_CUDA(cudaEventRecord(op.ev0, s));
-    const bool done = (op.order == 2)
-                          ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_persist<T, float2_or<T>, 10, 12>(op, u, f, batch, s)
-                                                              : launch_persist<T, T, 10, 12>(op, u, f, batch, s))
-                          : (sizeof(T) == 4 && batch % 2 == 0 ? launch_persist<T, float2_or<T>, 4, 8>(op, u, f, batch, s)
-                                                              : launch_persist<T, T, 4, 8>(op, u, f, batch, s));
-    if (done) {
-      if (op.timing) TS_CUDA(cudaEventRecord(op.ev1, s));
-      return;
-    }
-  }
   // identity rows for constrained dofs, zero elsewhere (ebe_operator.hpp:96-110)
   if (init) {
     if (!op.has_mask || op.n_masked_dofs * 10 < 3 * int64_t(op.n_nodes)) {
@@ -1151,13 +551,13 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
   // the chunk-tiled sweep on request (5).
   if (op.kernel == 7 || op.kernel == 6) done = ebe_pair_apply(op, u, f, batch, s, part);
   if (!done && op.kernel == 5) done = ebe_tile_apply(op, u, f, batch, s, part);
-  if (!done && op.kernel >= 3 && op.kernel != 4)
+  if (!done && op.kernel >= 3)
     done = (op.order == 2)
                ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s, e0, e1)
                                                    : launch_fast<T, T, 10, 12>(op, u, f, batch, s, e0, e1))
                : (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 4, 8>(op, u, f, batch, s, e0, e1)
                                                    : launch_fast<T, T, 4, 8>(op, u, f, batch, s, e0, e1));
-  if (!done && part >= 0) {  // any batch width: the generic pipelined sweep over the element range
+  if (!done) {  // any batch width: the generic pipelined sweep over the element range
     if (op.order == 2) {
       if (sizeof(T) == 4 && batch % 2 == 0) launch_pipe<float, float2, 10, 12>(op, reinterpret_cast<const float*>(u), reinterpret_cast<float*>(f), batch, s, e0, e1);
       else launch_pipe<T, T, 10, 12>(op, u, f, batch, s, e0, e1);
@@ -1165,11 +565,6 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
       if (sizeof(T) == 4 && batch % 2 == 0) launch_pipe<float, float2, 4, 4>(op, reinterpret_cast<const float*>(u), reinterpret_cast<float*>(f), batch, s, e0, e1);
       else launch_pipe<T, T, 4, 4>(op, u, f, batch, s, e0, e1);
     }
-    done = true;
-  }
-  if (!done) {
-    if (op.order == 2) launch_sweep<T, 10, 12, 12>(op, u, f, batch, s);
-    else launch_sweep<T, 4, 4, 8>(op, u, f, batch, s);
   }
   if (op.timing) TS_CUDA(cudaEventRecord(op.ev1, s));
 }
@@ -1406,7 +801,9 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     coef.swap(coef2);
   }
   if (kernel_override >= 0) op->kernel = kernel_override;
-  else if (const char* k = std::getenv("TSGPU_EBE_KERNEL")) op->kernel = std::string(k) == "direct" ? 0 : std::string(k) == "cluster" ? 1 : std::string(k) == "pipe" ? 2 : std::string(k) == "persist" ? 4 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5 : std::string(k) == "pair" ? 7 : 6;
+  else if (const char* k = std::getenv("TSGPU_EBE_KERNEL"))
+    op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5
+               : std::string(k) == "pair" ? 7 : 6;
   {
     // fast-kernel layout: 3*node per local node, then the dof-mask word (bit 3a+c)
     const int cs3 = order == 1 ? 8 : 12;
@@ -1423,44 +820,6 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
       conn3[e * cs3 + npe] = static_cast<int32_t>(mw);
     }
     op->conn3.upload(conn3);
-  }
-  if (op->kernel == 4) {  // slab-gated persistent sweep only
-    const int cs3 = order == 1 ? 8 : 12;
-    (void)cs3;
-    // slabs of consecutive (Morton) elements and the nodes each slab touches
-    // first: the fast kernel initialises slab j+1's nodes while sweeping slab j
-    const int64_t f_bytes = 3 * int64_t(op->n_nodes) * 16 * ts;  // sized for 16 cases
-    const int64_t target = 24ll << 20;
-    const int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (f_bytes + target - 1) / target)));
-    op->slab_ptr.resize(S + 1);
-    for (int j = 0; j <= S; ++j) op->slab_ptr[j] = static_cast<int32_t>((int64_t(E) * j) / S);
-    std::vector<int32_t> first(op->n_nodes, -1);
-    std::vector<int32_t> cnt(S + 1, 0);
-    int slab = 0;
-    for (size_t e = 0; e < E; ++e) {
-      while (static_cast<int64_t>(e) >= op->slab_ptr[slab + 1]) ++slab;
-      for (int a = 0; a < npe; ++a) {
-        const int32_t g = conn[e * cs + a] & 0x0FFFFFFF;
-        if (first[g] < 0) { first[g] = slab; ++cnt[slab + 1]; }
-      }
-    }
-    for (int32_t g = 0; g < op->n_nodes; ++g)
-      if (first[g] < 0) { first[g] = 0; ++cnt[1]; }  // untouched nodes: identity/zero rows in slab 0's init
-    for (int j = 0; j < S; ++j) cnt[j + 1] += cnt[j];
-    op->slab_init_ptr.assign(cnt.begin(), cnt.end());
-    std::vector<int32_t> init(cnt[S]);
-    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
-    for (int32_t g = 0; g < op->n_nodes; ++g) {
-      int32_t w = g;
-      if (dof_mask)
-        for (int c = 0; c < 3; ++c)
-          if (dof_mask[3 * static_cast<size_t>(g) + c]) w |= 1 << (28 + c);
-      init[cur[first[g]]++] = w;
-    }
-    op->slab_init.upload(init);
-    op->slab_ptr_dev.upload(op->slab_ptr);
-    op->slab_init_ptr_dev.upload(op->slab_init_ptr);
-    op->slab_ready.alloc(S);
   }
   setup_mark("ebe: morton + conn3");
   // the tiled sweep's chunk records serve kernel 5 only (in the default mode the pair sweep covers the

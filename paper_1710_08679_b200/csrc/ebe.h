@@ -6,20 +6,6 @@
 
 #include "ts_common.h"
 
-// Element clusters for the aggregated scatter (one cluster = the W elements a
-// thread block processes; W = block threads / threads per element). Built
-// lazily per W on the host from the Morton-ordered element list.
-struct EbeClusters {
-  int W = 0;
-  int32_t n_clusters = 0;
-  int32_t max_nodes = 0;
-  double nodes_per_elem = 0.0;
-  tsg::DevBuf<int32_t> node_ptr;   // [C+1]
-  tsg::DevBuf<int32_t> nodes;      // [sum PN]: global node | (dof-mask bits << 28)
-  tsg::DevBuf<int32_t> inc_ptr;    // [sum PN + 1] into inc
-  tsg::DevBuf<uint16_t> inc;       // slot * npe + local index, element order
-};
-
 // Chunk records for the tiled sweep (ebe_tile.cu): kChunk consecutive
 // elements per chunk; one 16-byte-aligned record per chunk holding its
 // distinct nodes, their incidence lists and the elements' local node slots.
@@ -53,11 +39,6 @@ struct ts_ebe {
   int conn_stride = 12;                 // int32 per element (npe padded to 4)
   tsg::DevBuf<int32_t> conn;            // [E][conn_stride]: node | (dof-mask bits << 28)
   tsg::DevBuf<int32_t> conn3;           // [E][12|8]: 3*node per local node, then dof-mask word
-  std::vector<int32_t> slab_ptr;        // element range of each slab (fast kernel)
-  std::vector<int32_t> slab_init_ptr;   // offsets into slab_init per slab
-  tsg::DevBuf<int32_t> slab_init;       // nodes first touched by each slab (| mask bits << 28)
-  tsg::DevBuf<int32_t> slab_ptr_dev, slab_init_ptr_dev;
-  tsg::DevBuf<int> slab_ready;          // per-slab arrival counters (persistent kernel gates)
   tsg::DevBuf<unsigned char> coef;      // [E][12] of T: b_1,b_2,b_3, lp, mp, 0
   tsg::DevBuf<unsigned char> mask;      // [3N] uint8 (empty if unconstrained)
   tsg::DevBuf<int32_t> masked_dofs;     // constrained dof indices (identity rows)
@@ -65,13 +46,11 @@ struct ts_ebe {
   std::vector<double> coef64;           // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
   std::vector<int32_t> host_conn;       // host [E][npe] (setup only)
   std::vector<uint8_t> host_mask;       // host [3N]
-  mutable std::vector<std::unique_ptr<EbeClusters>> clusters;  // cached per W
-  mutable std::mutex clusters_mu;
-  std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, the default kernel)
+  std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, kernel 5)
   int32_t group_split = 0;              // elements [0, split) = group 0 (partition boundary), rest group 1
   std::unique_ptr<EbePairPlan> pair;    // face-sharing pairs (kernel 7)
-  int kernel = 6;  // 0 direct, 1 cluster, 2 pipelined generic, 3 pipelined batch-specialised, 4 slab-gated,
-                   // 5 tiled, 6 auto (tiled for tet4 / narrow fp32 batches, else 3) = default, 7 pairs
+  int kernel = 6;  // 2 pipelined generic, 3 pipelined batch-specialised, 5 tiled, 6 = 7 = face pairs (default);
+                   // each falls back to 3, then 2, for batch widths it does not cover
   mutable std::mutex host_mu;            // guards the host-entry staging buffers
   mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
   bool timing = false;

@@ -41,7 +41,8 @@ CASES = [
 ]
 
 
-KERNELS = ["auto", "fast", "tile", "pair"]  # TSGPU_EBE_KERNEL: default dispatch, element-parallel RED sweep, chunk-tiled sweep
+KERNELS = ["auto", "pipe", "fast", "tile", "pair"]  # TSGPU_EBE_KERNEL: default dispatch, generic and batch-specialised
+# element-parallel RED sweeps, chunk-tiled sweep, face-pair sweep
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
