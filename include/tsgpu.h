@@ -39,7 +39,8 @@ typedef enum {
   TS_ERR_NONFINITE = 3,      /* SolverError: NaN residual            pcg.hpp:70,118-120, adaptive_cg.hpp:171 */
   TS_ERR_NO_CONVERGENCE = 4, /* ConvergenceError (carries report)    adaptive_cg.hpp:179-188 */
   TS_ERR_CUDA = 5,
-  TS_ERR_NCCL = 6
+  TS_ERR_NCCL = 6,
+  TS_ERR_PARSE = 7           /* ParseError (a ValidationError): "file:line: msg"  errors.hpp:21-25 */
 } ts_status;
 
 const char* ts_last_error(void);
@@ -107,6 +108,35 @@ ts_status ts_mesh_export(const ts_mesh* m, double* coords, int32_t* tets10,
 /* dirichlet_mask (mesh.hpp:150-154): 3*n_nodes bytes */
 ts_status ts_mesh_dirichlet_mask(const ts_mesh* m, uint8_t* mask);
 void ts_mesh_destroy(ts_mesh* m);
+
+/* ------------------------------------------------------------ file formats */
+
+/* TSMESH 1 text mesh. write: byte-identical to write_mesh (mesh_io.hpp:20-36),
+ * through a temporary file renamed over `path` (atomic_write, io_util.hpp:21-49).
+ * read: read_mesh (mesh_io.hpp:44-96) — TS_ERR_PARSE "path:line: msg" on a
+ * malformed line (same line numbers and messages), then validate_mesh
+ * (mesh.hpp:75-113, TS_ERR_VALIDATION naming the first bad element). The read
+ * mesh has no Dirichlet entries (they live in the sidecar). */
+ts_status ts_mesh_write_tsmesh(const ts_mesh* m, const char* path);
+ts_status ts_mesh_read_tsmesh(const char* path, ts_mesh** out);
+/* Dirichlet sidecar, "node axis" lines: write_dirichlet / read_dirichlet
+ * (mesh_io.hpp:38-42, 98-115); read REPLACES m's Dirichlet list. */
+ts_status ts_mesh_write_dirichlet(const ts_mesh* m, const char* path);
+ts_status ts_mesh_read_dirichlet(ts_mesh* m, const char* path);
+/* TSBMESH 1 binary mesh (this library's format: text header, then raw
+ * little-endian coords f64[N][3], tets10 i32[T][10], material i32[T],
+ * bc_node i32[D], bc_axis i8[D]); read validates like ts_mesh_read_tsmesh. */
+ts_status ts_mesh_write_tsbmesh(const ts_mesh* m, const char* path);
+ts_status ts_mesh_read_tsbmesh(const char* path, ts_mesh** out);
+
+/* TSVEC 1 solution file (solution_io.hpp:12-84): u = fp64 [nodes][3][batch].
+ * on_device != 0: u is a DEVICE pointer, streamed through pinned staging
+ * (PCIe copy of one 64 MB chunk overlapping the file I/O of the next). */
+ts_status ts_tsvec_write(const char* path, const double* u, int64_t nodes, int32_t batch, int32_t on_device);
+/* header only: dimensions (TS_ERR_PARSE on a bad header, read_solution's checks) */
+ts_status ts_tsvec_info(const char* path, int64_t* nodes, int32_t* batch);
+/* payload into u (sized by the caller from ts_tsvec_info; mismatch = TS_ERR_VALIDATION) */
+ts_status ts_tsvec_read(const char* path, double* u, int64_t nodes, int32_t batch, int32_t on_device);
 
 /* material_from_wavespeeds (material.hpp:22-34) */
 ts_status ts_material_from_wavespeeds(double vp, double vs, double rho, double* lambda,

@@ -421,6 +421,68 @@ class Oracle:
             self._f("mesh_destroy")(h)
         return bank, calls.value, outer.value
 
+    # ------------------------------------------------------ file formats (reference only)
+    def _io(self):
+        if self.kind != "reference":
+            raise OracleError(9, "file formats are checked against the reference itself (mesh_io.hpp, solution_io.hpp)")
+        L = self.lib
+        vp, cp = C.c_void_p, C.c_char_p
+        L.ref_write_mesh.argtypes = [vp, cp]
+        L.ref_read_mesh.argtypes = [cp, vp]
+        L.ref_write_dirichlet.argtypes = [vp, cp]
+        L.ref_read_dirichlet.argtypes = [vp, cp]
+        L.ref_write_solution.argtypes = [cp, vp, C.c_int32, C.c_int32]
+        L.ref_read_solution.argtypes = [cp, vp, vp, vp]
+        return L
+
+    def write_mesh(self, m: MeshArrays, path) -> None:
+        L = self._io()
+        h = self._mesh(m)
+        try:
+            self._check(L.ref_write_mesh(h, os.fsencode(path)))
+        finally:
+            self._f("mesh_destroy")(h)
+
+    def read_mesh(self, path) -> MeshArrays:
+        L = self._io()
+        h = C.c_void_p()
+        self._check(L.ref_read_mesh(os.fsencode(path), C.byref(h)))
+        try:
+            return self._export(h)
+        finally:
+            self._f("mesh_destroy")(h)
+
+    def write_dirichlet(self, m: MeshArrays, path) -> None:
+        L = self._io()
+        h = self._mesh(m)
+        try:
+            self._check(L.ref_write_dirichlet(h, os.fsencode(path)))
+        finally:
+            self._f("mesh_destroy")(h)
+
+    def read_dirichlet(self, m: MeshArrays, path) -> MeshArrays:
+        """read_dirichlet applied to a copy of m; returns the updated arrays."""
+        L = self._io()
+        h = self._mesh(m)
+        try:
+            self._check(L.ref_read_dirichlet(h, os.fsencode(path)))
+            return self._export(h)
+        finally:
+            self._f("mesh_destroy")(h)
+
+    def write_solution(self, path, u: np.ndarray) -> None:
+        L = self._io()
+        a = np.ascontiguousarray(u, np.float64)
+        self._check(L.ref_write_solution(os.fsencode(path), _p(a), a.shape[0] // 3, a.shape[1]))
+
+    def read_solution(self, path) -> np.ndarray:
+        L = self._io()
+        n, b = C.c_int32(), C.c_int32()
+        self._check(L.ref_read_solution(os.fsencode(path), C.byref(n), C.byref(b), None))
+        out = np.empty((3 * n.value, b.value), np.float64)
+        self._check(L.ref_read_solution(os.fsencode(path), C.byref(n), C.byref(b), _p(out)))
+        return out
+
     def hw_threads(self) -> int:
         return int(self.lib.ref_hw_threads()) if self.kind == "reference" else 1
 

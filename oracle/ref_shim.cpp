@@ -20,7 +20,9 @@
 #include "tetsolve/box_mesh.hpp"
 #include "tetsolve/fault.hpp"
 #include "tetsolve/greens.hpp"
+#include "tetsolve/mesh_io.hpp"
 #include "tetsolve/model.hpp"
+#include "tetsolve/solution_io.hpp"
 #include "tetsolve/verification.hpp"
 
 #include "../include/tsgpu.h"  // shared POD structs (ts_solver_config, ts_solve_report)
@@ -40,6 +42,7 @@ int fail(const std::exception& e, int code) {
   }                                                                    \
   catch (const ConvergenceError& e) { return fail(e, 4); }             \
   catch (const SolverError& e) { return fail(e, 2); }                  \
+  catch (const ParseError& e) { return fail(e, 7); }                   \
   catch (const ValidationError& e) { return fail(e, 1); }              \
   catch (const std::exception& e) { return fail(e, 9); }               \
   return 0;
@@ -565,6 +568,51 @@ int ref_greens_bank(const void* mh, int32_t n_mat, const double* lam, const doub
   std::memcpy(bank, b.values.data(), b.values.size() * sizeof(double));
   *solver_calls = rep.solver_calls;
   *outer_iterations = rep.outer_iterations;
+  REF_CATCH
+}
+
+// ------------------------------------------------------------ file formats
+// write_mesh / read_mesh / write_dirichlet / read_dirichlet (mesh_io.hpp),
+// write_solution / read_solution (solution_io.hpp)
+int ref_write_mesh(const void* mh, const char* path) {
+  REF_TRY
+  write_mesh(*static_cast<const Mesh*>(mh), path);
+  REF_CATCH
+}
+
+int ref_read_mesh(const char* path, void** out) {
+  REF_TRY
+  *out = new Mesh(read_mesh(path));
+  REF_CATCH
+}
+
+int ref_write_dirichlet(const void* mh, const char* path) {
+  REF_TRY
+  write_dirichlet(*static_cast<const Mesh*>(mh), path);
+  REF_CATCH
+}
+
+int ref_read_dirichlet(void* mh, const char* path) {
+  REF_TRY
+  read_dirichlet(*static_cast<Mesh*>(mh), path);
+  REF_CATCH
+}
+
+int ref_write_solution(const char* path, const double* u, int32_t nodes, int32_t batch) {
+  REF_TRY
+  VectorBatch64 v(nodes, batch);
+  std::memcpy(v.data.data(), u, v.data.size() * sizeof(double));
+  write_solution(v, path);
+  REF_CATCH
+}
+
+// out == nullptr: dimensions only
+int ref_read_solution(const char* path, int32_t* nodes, int32_t* batch, double* out) {
+  REF_TRY
+  const VectorBatch64 v = read_solution(path);
+  *nodes = v.n_nodes;
+  *batch = v.batch;
+  if (out) std::memcpy(out, v.data.data(), v.data.size() * sizeof(double));
   REF_CATCH
 }
 

@@ -12,6 +12,7 @@ from .tetsolve import (  # noqa: F401
     InnerLoopConfig,
     Material,
     Mesh,
+    ParseError,
     CrustModel,
     SolveReport,
     SolverLevels,
@@ -25,4 +26,12 @@ from .tetsolve import (  # noqa: F401
     dirichlet_mask,
     generate_box_mesh,
     material_from_wavespeeds,
+    read_dirichlet,
+    read_mesh,
+    read_mesh_binary,
+    read_solution,
+    write_dirichlet,
+    write_mesh,
+    write_mesh_binary,
+    write_solution,
 )

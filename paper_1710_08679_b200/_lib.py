@@ -21,6 +21,7 @@ TS_ERR_NONFINITE = 3
 TS_ERR_NO_CONVERGENCE = 4
 TS_ERR_CUDA = 5
 TS_ERR_NCCL = 6
+TS_ERR_PARSE = 7
 
 
 class SolverConfig(C.Structure):
@@ -77,6 +78,15 @@ _sig = {
     "ts_mesh_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "ts_mesh_dirichlet_mask": (C.c_int, [vp, vp]),
     "ts_mesh_destroy": (None, [vp]),
+    "ts_mesh_write_tsmesh": (C.c_int, [vp, C.c_char_p]),
+    "ts_mesh_read_tsmesh": (C.c_int, [C.c_char_p, vp]),
+    "ts_mesh_write_dirichlet": (C.c_int, [vp, C.c_char_p]),
+    "ts_mesh_read_dirichlet": (C.c_int, [vp, C.c_char_p]),
+    "ts_mesh_write_tsbmesh": (C.c_int, [vp, C.c_char_p]),
+    "ts_mesh_read_tsbmesh": (C.c_int, [C.c_char_p, vp]),
+    "ts_tsvec_write": (C.c_int, [C.c_char_p, vp, C.c_int64, i32, i32]),
+    "ts_tsvec_info": (C.c_int, [C.c_char_p, vp, vp]),
+    "ts_tsvec_read": (C.c_int, [C.c_char_p, vp, C.c_int64, i32, i32]),
     "ts_material_from_wavespeeds": (C.c_int, [C.c_double, C.c_double, C.c_double, vp, vp]),
     "ts_ebe_create": (C.c_int, [vp, i32, i32, vp, vp, vp, i32, vp]),
     "ts_ebe_destroy": (None, [vp]),

@@ -7,6 +7,7 @@
 #include "dist.h"
 #include "dist_api.h"
 #include "ebe.h"
+#include "mesh_io.h"
 
 namespace tsg {
 const std::string& last_error();
@@ -120,6 +121,78 @@ ts_status ts_mesh_from_arrays(int32_t n_nodes, int32_t vertex_count, const doubl
                "mesh: element " + std::to_string(q / 10) + " references node " +
                    std::to_string(m.tets10[q]) + " out of range");
   *out = h.release();
+  TS_API_END
+}
+
+// ------------------------------------------------------------ file formats
+ts_status ts_mesh_write_tsmesh(const ts_mesh* m, const char* path) {
+  TS_API_BEGIN
+  TS_REQUIRE(m && path, "mesh io: null argument");
+  tsg::write_tsmesh(m->m, path);
+  TS_API_END
+}
+
+ts_status ts_mesh_read_tsmesh(const char* path, ts_mesh** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && out, "mesh io: null argument");
+  auto h = std::make_unique<ts_mesh>();
+  h->m = tsg::read_tsmesh(path);
+  *out = h.release();
+  TS_API_END
+}
+
+ts_status ts_mesh_write_dirichlet(const ts_mesh* m, const char* path) {
+  TS_API_BEGIN
+  TS_REQUIRE(m && path, "mesh io: null argument");
+  tsg::write_dirichlet(m->m, path);
+  TS_API_END
+}
+
+ts_status ts_mesh_read_dirichlet(ts_mesh* m, const char* path) {
+  TS_API_BEGIN
+  TS_REQUIRE(m && path, "mesh io: null argument");
+  tsg::read_dirichlet(m->m, path);
+  TS_API_END
+}
+
+ts_status ts_mesh_write_tsbmesh(const ts_mesh* m, const char* path) {
+  TS_API_BEGIN
+  TS_REQUIRE(m && path, "mesh io: null argument");
+  tsg::write_tsbmesh(m->m, path);
+  TS_API_END
+}
+
+ts_status ts_mesh_read_tsbmesh(const char* path, ts_mesh** out) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && out, "mesh io: null argument");
+  auto h = std::make_unique<ts_mesh>();
+  h->m = tsg::read_tsbmesh(path);
+  *out = h.release();
+  TS_API_END
+}
+
+ts_status ts_tsvec_write(const char* path, const double* u, int64_t nodes, int32_t batch, int32_t on_device) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && (u || nodes == 0), "solution io: null argument");
+  tsg::write_tsvec(path, u, nodes, batch, on_device != 0);
+  TS_API_END
+}
+
+ts_status ts_tsvec_info(const char* path, int64_t* nodes, int32_t* batch) {
+  TS_API_BEGIN
+  TS_REQUIRE(path, "solution io: null argument");
+  int64_t n, b, off;
+  tsg::tsvec_info(path, &n, &b, &off);
+  TS_REQUIRE(b <= INT32_MAX, "solution io: batch out of range");
+  if (nodes) *nodes = n;
+  if (batch) *batch = static_cast<int32_t>(b);
+  TS_API_END
+}
+
+ts_status ts_tsvec_read(const char* path, double* u, int64_t nodes, int32_t batch, int32_t on_device) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && (u || nodes == 0), "solution io: null argument");
+  tsg::read_tsvec(path, u, nodes, batch, on_device != 0);
   TS_API_END
 }
 

@@ -1,0 +1,22 @@
+// mesh_io.h — TSMESH / Dirichlet sidecar / TSVEC (mesh_io.hpp, solution_io.hpp)
+// and the binary TSBMESH mesh; host-side, parallel (mesh_io.cc).
+#pragma once
+#include <string>
+
+#include "ts_common.h"
+
+namespace tsg {
+
+void validate_mesh(const Mesh& m);                            // mesh.hpp:75-113
+void write_tsmesh(const Mesh& m, const std::string& path);    // mesh_io.hpp:20-36
+Mesh read_tsmesh(const std::string& path);                    // mesh_io.hpp:44-96
+void write_dirichlet(const Mesh& m, const std::string& path); // mesh_io.hpp:38-42
+void read_dirichlet(Mesh& m, const std::string& path);        // mesh_io.hpp:98-115
+void write_tsbmesh(const Mesh& m, const std::string& path);
+Mesh read_tsbmesh(const std::string& path);
+// solution_io.hpp:14-27 / 29-84; u = [nodes][3][batch] fp64 on the host or device
+void write_tsvec(const std::string& path, const double* u, int64_t nodes, int64_t batch, bool on_device);
+void tsvec_info(const std::string& path, int64_t* nodes, int64_t* batch, int64_t* data_offset);
+void read_tsvec(const std::string& path, double* u, int64_t nodes, int64_t batch, bool on_device);
+
+}  // namespace tsg

@@ -38,6 +38,10 @@ class ValidationError(Error):
     """tetsolve::ValidationError (errors.hpp:15-18)."""
 
 
+class ParseError(ValidationError):
+    """tetsolve::ParseError (errors.hpp:21-25): message "file:line: msg"."""
+
+
 class SolverError(Error):
     """tetsolve::SolverError (errors.hpp:27-30)."""
 
@@ -56,6 +60,8 @@ class DeviceError(Error):
 
 def _raise(rc: int, report=None):
     msg = lib.ts_last_error().decode()
+    if rc == _lib.TS_ERR_PARSE:
+        raise ParseError(msg)
     if rc == _lib.TS_ERR_VALIDATION:
         raise ValidationError(msg)
     if rc == _lib.TS_ERR_NO_CONVERGENCE:
@@ -278,6 +284,81 @@ def generate_box_mesh(extents, divisions, layer_interfaces=(), fixed_boundary="b
 def dirichlet_mask(mesh: Mesh) -> np.ndarray:
     """dirichlet_mask (mesh.hpp:150-154)."""
     return mesh.dirichlet_mask()
+
+
+# ------------------------------------------------------------ file formats
+def _path(p) -> bytes:
+    import os
+
+    return os.fsencode(p)
+
+
+def write_mesh(mesh: Mesh, path) -> None:
+    """write_mesh (mesh_io.hpp:20-36): TSMESH 1 text, byte-identical, atomic replace."""
+    _ck(lib.ts_mesh_write_tsmesh(mesh._h, _path(path)))
+
+
+def read_mesh(path) -> Mesh:
+    """read_mesh (mesh_io.hpp:44-96): ParseError on a malformed line, then
+    validate_mesh (ValidationError naming the first bad element). No Dirichlet
+    entries (see read_dirichlet)."""
+    h = C.c_void_p()
+    _ck(lib.ts_mesh_read_tsmesh(_path(path), C.byref(h)))
+    return Mesh(h)
+
+
+def write_dirichlet(mesh: Mesh, path) -> None:
+    """write_dirichlet (mesh_io.hpp:38-42): one "node axis" line per entry."""
+    _ck(lib.ts_mesh_write_dirichlet(mesh._h, _path(path)))
+
+
+def read_dirichlet(mesh: Mesh, path) -> None:
+    """read_dirichlet (mesh_io.hpp:98-115): replaces the mesh's Dirichlet list in place."""
+    _ck(lib.ts_mesh_read_dirichlet(mesh._h, _path(path)))
+    mesh.__init__(mesh._h)
+
+
+def write_mesh_binary(mesh: Mesh, path) -> None:
+    """TSBMESH 1 (this library's binary mesh, Dirichlet list included)."""
+    _ck(lib.ts_mesh_write_tsbmesh(mesh._h, _path(path)))
+
+
+def read_mesh_binary(path) -> Mesh:
+    """Read a TSBMESH 1 file; validated like read_mesh."""
+    h = C.c_void_p()
+    _ck(lib.ts_mesh_read_tsbmesh(_path(path), C.byref(h)))
+    return Mesh(h)
+
+
+def write_solution(u, path) -> None:
+    """write_solution (solution_io.hpp:14-27) of a (3 * n_nodes, batch) fp64
+    VectorBatch: numpy (host) or a CUDA tensor (streamed from the device)."""
+    if _is_torch(u):
+        if u.dtype != torch.float64 or u.dim() != 2 or u.shape[0] % 3 or not u.is_contiguous():
+            raise ValidationError("write_solution: expected a contiguous float64 tensor of shape (3 * n_nodes, batch)")
+        if u.is_cuda:
+            torch.cuda.current_stream().synchronize()
+            _ck(lib.ts_tsvec_write(_path(path), C.c_void_p(u.data_ptr()), u.shape[0] // 3, u.shape[1], 1))
+            return
+        u = u.numpy()
+    a = np.ascontiguousarray(u, np.float64)
+    if a.ndim != 2 or a.shape[0] % 3:
+        raise ValidationError("write_solution: expected shape (3 * n_nodes, batch)")
+    _ck(lib.ts_tsvec_write(_path(path), _p(a), a.shape[0] // 3, a.shape[1], 0))
+
+
+def read_solution(path, device=None):
+    """read_solution (solution_io.hpp:29-84) -> (3 * n_nodes, batch) fp64;
+    numpy, or a CUDA tensor on ``device`` (streamed to the device)."""
+    n, b = C.c_int64(), C.c_int32()
+    _ck(lib.ts_tsvec_info(_path(path), C.byref(n), C.byref(b)))
+    if device is not None:
+        out = torch.empty((3 * n.value, b.value), dtype=torch.float64, device=device)
+        _ck(lib.ts_tsvec_read(_path(path), C.c_void_p(out.data_ptr()), n.value, b.value, 1))
+        return out
+    out = np.empty((3 * n.value, b.value), np.float64)
+    _ck(lib.ts_tsvec_read(_path(path), _p(out), n.value, b.value, 0))
+    return out
 
 
 # -------------------------------------------------------------- operators

@@ -132,7 +132,7 @@ def _worker(rank, world, port, out):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_partitioned_ebe_product_over_gloo(world):
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # no fork of a process that holds OpenMP threads
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     for r in range(world):
