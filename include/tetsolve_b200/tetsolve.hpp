@@ -32,6 +32,13 @@ class ValidationError : public Error {
  public:
   explicit ValidationError(const std::string& m) : Error(m) {}
 };
+class ParseError : public ValidationError {  // errors.hpp:21-25: "file:line: msg"
+ public:
+  explicit ParseError(const std::string& msg) : ValidationError(msg) {}
+  ParseError(const std::string& file, long line, const std::string& msg)
+      : ValidationError(file + ":" + std::to_string(line) + ": " + msg) {}
+};
+
 class SolverError : public Error {
  public:
   explicit SolverError(const std::string& m) : Error(m) {}
@@ -113,6 +120,7 @@ inline void check(ts_status rc) {
   if (rc == TS_OK) return;
   const std::string msg = ts_last_error();
   switch (rc) {
+    case TS_ERR_PARSE: throw ParseError(msg);
     case TS_ERR_VALIDATION: throw ValidationError(msg);
     case TS_ERR_BREAKDOWN:
     case TS_ERR_NONFINITE: throw SolverError(msg);
@@ -202,12 +210,9 @@ inline std::pair<std::vector<double>, std::vector<double>> lame(const std::vecto
 }
 }  // namespace detail
 
-// generate_box_mesh (box_mesh.hpp:55-157): identical node numbering
-inline Mesh generate_box_mesh(const BoxMeshSpec& spec) {
-  ts_mesh* h = nullptr;
-  detail::check(ts_box_mesh(spec.extents.data(), spec.divisions.data(),
-                            static_cast<int32_t>(spec.layer_interfaces.size()), spec.layer_interfaces.data(),
-                            static_cast<int32_t>(spec.fixed_boundary), &h));
+namespace detail {
+// copy a library mesh handle into the reference's Mesh (edge_map rebuilt as rebuild_edge_map, mesh.hpp:61-71)
+inline Mesh take_mesh(ts_mesh* h) {
   int32_t nn, nv, ne, nbc;
   ts_mesh_sizes(h, &nn, &nv, &ne, &nbc);
   std::vector<double> c(3 * size_t(nn));
@@ -235,6 +240,54 @@ inline Mesh generate_box_mesh(const BoxMeshSpec& spec) {
   for (int32_t i = 0; i < nbc; ++i) m.dirichlet.push_back({bn[i], ba[i]});
   return m;
 }
+}  // namespace detail
+
+// generate_box_mesh (box_mesh.hpp:55-157): identical node numbering
+inline Mesh generate_box_mesh(const BoxMeshSpec& spec) {
+  ts_mesh* h = nullptr;
+  detail::check(ts_box_mesh(spec.extents.data(), spec.divisions.data(),
+                            static_cast<int32_t>(spec.layer_interfaces.size()), spec.layer_interfaces.data(),
+                            static_cast<int32_t>(spec.fixed_boundary), &h));
+  return detail::take_mesh(h);
+}
+
+// ------------------------------------------------------------ mesh_io.hpp:13-115
+// TSMESH 1 text (byte-identical to the reference writer, atomic replace) and the
+// Dirichlet sidecar; read_mesh throws ParseError / ValidationError like the reference.
+inline void write_mesh(const Mesh& m, const std::string& path) {
+  detail::MeshHandle h(m);
+  detail::check(ts_mesh_write_tsmesh(h.h, path.c_str()));
+}
+inline void write_dirichlet(const Mesh& m, const std::string& path) {
+  detail::MeshHandle h(m);
+  detail::check(ts_mesh_write_dirichlet(h.h, path.c_str()));
+}
+inline Mesh read_mesh(const std::string& path) {
+  ts_mesh* h = nullptr;
+  detail::check(ts_mesh_read_tsmesh(path.c_str(), &h));
+  return detail::take_mesh(h);
+}
+inline void read_dirichlet(Mesh& m, const std::string& path) {
+  detail::MeshHandle h(m);
+  detail::check(ts_mesh_read_dirichlet(h.h, path.c_str()));
+  int32_t nn, nv, ne, nbc;
+  ts_mesh_sizes(h.h, &nn, &nv, &ne, &nbc);
+  std::vector<int32_t> bn(nbc);
+  std::vector<int8_t> ba(nbc);
+  ts_mesh_export(h.h, nullptr, nullptr, nullptr, bn.data(), ba.data());
+  m.dirichlet.clear();
+  for (int32_t i = 0; i < nbc; ++i) m.dirichlet.push_back({bn[i], ba[i]});
+}
+// TSBMESH 1: binary mesh including the Dirichlet list (no reference counterpart)
+inline void write_mesh_binary(const Mesh& m, const std::string& path) {
+  detail::MeshHandle h(m);
+  detail::check(ts_mesh_write_tsbmesh(h.h, path.c_str()));
+}
+inline Mesh read_mesh_binary(const std::string& path) {
+  ts_mesh* h = nullptr;
+  detail::check(ts_mesh_read_tsbmesh(path.c_str(), &h));
+  return detail::take_mesh(h);
+}
 
 // ------------------------------------------------------- vector_batch.hpp:15-34
 template <typename T>
@@ -253,6 +306,19 @@ struct VectorBatch {
 };
 using VectorBatch64 = VectorBatch<double>;
 using VectorBatch32 = VectorBatch<float>;
+
+// ------------------------------------------------------- solution_io.hpp:12-84
+inline void write_solution(const VectorBatch64& u, const std::string& path) {
+  detail::check(ts_tsvec_write(path.c_str(), u.data.data(), u.n_nodes, u.batch, 0));
+}
+inline VectorBatch64 read_solution(const std::string& path) {
+  int64_t nodes = 0;
+  int32_t batch = 0;
+  detail::check(ts_tsvec_info(path.c_str(), &nodes, &batch));
+  VectorBatch64 u(static_cast<int32_t>(nodes), batch);
+  detail::check(ts_tsvec_read(path.c_str(), u.data.data(), nodes, batch, 0));
+  return u;
+}
 
 template <typename T>
 struct BlockJacobi {  // block_jacobi.hpp:15-39 (host copy of the inverse blocks)
