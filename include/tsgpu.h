@@ -160,8 +160,14 @@ ts_status ts_ebe_info(const ts_ebe* op, int32_t* n_nodes, int32_t* n_elements, i
                       int32_t* prec);
 /* EbeOperator::apply (ebe_operator.hpp:90-134) on device pointers. */
 ts_status ts_ebe_apply(const ts_ebe* op, const void* u, void* f, int32_t batch, void* stream);
-/* same, host pointers (H2D + apply + D2H inside) */
+/* same, host pointers (H2D + apply + D2H inside). With pinned u and f the
+ * transfers overlap the sweep: u rows go up ahead of the first chunk of
+ * elements that reads them, finished f rows come back while later chunks
+ * sweep (PCIe full duplex); pageable buffers copy, apply, copy. */
 ts_status ts_ebe_apply_host(const ts_ebe* op, const void* u, void* f, int32_t batch);
+/* chunks of the host-buffer streaming schedule (0 = copy-apply-copy; the
+ * schedule is built by the first pinned-host apply) */
+ts_status ts_ebe_host_stream_chunks(const ts_ebe* op, int32_t* chunks);
 /* extract_block_jacobi(EbeOperator) (ebe_operator.hpp:288-313): inverse 3x3
  * node blocks in the operator precision, written to a HOST array
  * [n_nodes][9] of prec-sized scalars. */

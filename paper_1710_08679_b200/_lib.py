@@ -94,6 +94,7 @@ _sig = {
     "ts_ebe_apply": (C.c_int, [vp, vp, vp, i32, vp]),
     "ts_ebe_apply_host": (C.c_int, [vp, vp, vp, i32]),
     "ts_ebe_block_jacobi_host": (C.c_int, [vp, vp]),
+    "ts_ebe_host_stream_chunks": (C.c_int, [vp, vp]),
     "ts_ebe_set_timing": (C.c_int, [vp, i32]),
     "ts_ebe_last_kernel_ms": (C.c_int, [vp, vp]),
     "ts_ebe_launches_per_apply": (C.c_int, [vp, vp]),

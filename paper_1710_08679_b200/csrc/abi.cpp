@@ -274,13 +274,15 @@ ts_status ts_ebe_apply_host(const ts_ebe* op, const void* u, void* f, int32_t ba
   TS_API_BEGIN
   TS_REQUIRE(op && u && f, "ebe apply: null argument");
   TS_REQUIRE(batch >= 1, "ebe apply: batch must be >= 1");
-  const size_t bytes = 3 * static_cast<size_t>(op->n_nodes) * batch * (op->prec / 8);
+  tsg::ebe_apply_host(*op, u, f, batch);
+  TS_API_END
+}
+
+ts_status ts_ebe_host_stream_chunks(const ts_ebe* op, int32_t* chunks) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && chunks, "ebe: null argument");
   std::lock_guard<std::mutex> lock(op->host_mu);
-  op->stage_u.ensure(bytes);
-  op->stage_f.ensure(bytes);
-  TS_CUDA(cudaMemcpy(op->stage_u.get(), u, bytes, cudaMemcpyHostToDevice));
-  tsg::ebe_apply(*op, op->stage_u.get(), op->stage_f.get(), batch, nullptr);
-  TS_CUDA(cudaMemcpy(f, op->stage_f.get(), bytes, cudaMemcpyDeviceToHost));
+  *chunks = op->stream && op->stream->usable ? op->stream->chunks : 0;
   TS_API_END
 }
 

@@ -658,6 +658,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   op->conn_stride = order == 1 ? 4 : 12;
   op->n_nodes = order == 1 ? m.vertex_count : m.n_nodes();
   op->n_elems = m.n_elems();
+  op->n_vertices = m.vertex_count;
   if (op->n_nodes >= (1 << 28)) validation("ebe: more than 2^28 nodes per device is not supported");
   op->has_mask = dof_mask != nullptr;
   const int npe = op->npe, cs = op->conn_stride;
@@ -757,14 +758,26 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     double ext = 0.0;
     for (int c = 0; c < 3; ++c) ext = std::max(ext, hi[c] - lo[c]);
     const double scale = ext > 0.0 ? double((1 << 20) - 1) / ext : 0.0;
-    // (group, Morton key, id): a partitioned operator keeps its boundary elements
-    // (group 0) ahead of the interior ones so the two sweep separately
-    std::vector<std::tuple<uint8_t, uint64_t, int32_t>> key(E);
+    // (group, slab, Morton key, id): a partitioned operator keeps its boundary
+    // elements (group 0) ahead of the interior ones so the two sweep separately;
+    // within a group, elements go in kSlabs slabs of their lowest vertex id, then
+    // Morton order. The slabs make node first/last use monotone in node id for
+    // meshes numbered along an axis (the box generator, most mesh tools), which
+    // lets the host-buffer apply stream u in and f out while it sweeps
+    // (ebe_stream.cu); inside a slab the Morton order keeps gathers L2-local.
+    constexpr int kSlabs = kEbeSlabs;
+    const int64_t vmax = std::max<int64_t>(1, m.vertex_count);
+    auto slab_of = [&](size_t e) {
+      int32_t lo = m.tets10[10 * e];
+      for (int a = 1; a < 4; ++a) lo = std::min(lo, m.tets10[10 * e + a]);
+      return static_cast<uint8_t>(std::min<int64_t>(kSlabs - 1, int64_t(lo) * kSlabs / vmax));
+    };
+    std::vector<std::tuple<uint8_t, uint8_t, uint64_t, int32_t>> key(E);
     if (reuse) {  // the level set's other operators share one element order
 #pragma omp parallel for schedule(static)
       for (size_t i = 0; i < E; ++i) {
         const int32_t e = (*element_order)[i];
-        key[i] = {elem_group ? elem_group[e] : uint8_t(0), 0, e};
+        key[i] = {elem_group ? elem_group[e] : uint8_t(0), 0, 0, e};
       }
     } else {
 #pragma omp parallel for schedule(static)
@@ -772,12 +785,12 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
         uint64_t k = 0;
         for (int c = 0; c < 3; ++c)
           k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
-        key[e] = {elem_group ? elem_group[e] : uint8_t(0), k, static_cast<int32_t>(e)};
+        key[e] = {elem_group ? elem_group[e] : uint8_t(0), slab_of(e), k, static_cast<int32_t>(e)};
       }
       __gnu_parallel::sort(key.begin(), key.end());
       if (element_order) {
         element_order->resize(E);
-        for (size_t i = 0; i < E; ++i) (*element_order)[i] = std::get<2>(key[i]);
+        for (size_t i = 0; i < E; ++i) (*element_order)[i] = std::get<3>(key[i]);
       }
     }
     op->group_split = 0;
@@ -789,7 +802,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     std::vector<unsigned char> coef2(coef.size());
 #pragma omp parallel for schedule(static)
     for (size_t i = 0; i < E; ++i) {
-      const size_t e = static_cast<size_t>(std::get<2>(key[i]));
+      const size_t e = static_cast<size_t>(std::get<3>(key[i]));
       std::memcpy(&conn2[i * cs], &conn[e * cs], cs * sizeof(int32_t));
       std::memcpy(&hconn2[i * npe], &op->host_conn[e * npe], npe * sizeof(int32_t));
       std::memcpy(&c642[i * 12], &op->coef64[e * 12], 12 * sizeof(double));

@@ -1,8 +1,10 @@
 // ebe.h — device-resident matrix-free EBE operator (EbeOperator<T>,
 // ebe_operator.hpp:29-226), shared by the solver translation units.
 #pragma once
+#include <array>
 #include <memory>
 #include <mutex>
+#include <vector>
 
 #include "ts_common.h"
 
@@ -22,11 +24,31 @@ struct EbeTilePlan {
 
 // Face-sharing element pairs for the pair sweep (ebe_pair.cu).
 struct EbePairPlan {
-  int32_t n_units = 0;           // pairs, then singles, per element group
+  int32_t n_units = 0;           // pairs and singles in element order, per element group
   int32_t group_split = 0;       // units [0, split) cover element group 0
   double paired_fraction = 0.0;  // elements that are in a pair
   tsg::DevBuf<int32_t> conn;     // [units][16 | 8]: A's slots, B's own slots (3*node), mask words
   tsg::DevBuf<unsigned char> coef;  // [units][24] of T: A and B coefficient records
+};
+
+// Elements sweep in slabs of their lowest vertex id (then Morton order), ebe.cu
+constexpr int kEbeSlabs = 32;
+
+// Host-buffer streaming schedule (ebe_stream.cu): the pair units cut into
+// chunks; node rows go up before the first chunk that reads them and come back
+// after the last chunk that writes them.
+struct EbeStreamPlan {
+  bool usable = false;
+  int chunks = 0;
+  std::vector<int32_t> unit_ptr;                 // [chunks + 1] pair-unit ranges
+  std::vector<int32_t> in_ptr, out_ptr;          // [chunks + 1] into in_runs / out_runs
+  std::vector<std::array<int32_t, 2>> in_runs;   // node ranges [a, b) uploaded before chunk k
+  std::vector<std::array<int32_t, 2>> out_runs;  // node ranges final after chunk k
+  std::vector<int32_t> mdof_ptr;                 // [chunks + 1] into mdofs
+  tsg::DevBuf<int32_t> mdofs;                    // constrained dofs by upload chunk
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done;
+  ~EbeStreamPlan();
 };
 
 struct ts_ebe {
@@ -35,6 +57,7 @@ struct ts_ebe {
   int prec = 32;   // 32 | 64 : the reference's T
   int32_t n_nodes = 0;
   int32_t n_elems = 0;
+  int32_t n_vertices = 0;  // mesh vertex count (the slab key's range)
   bool has_mask = false;
   int conn_stride = 12;                 // int32 per element (npe padded to 4)
   tsg::DevBuf<int32_t> conn;            // [E][conn_stride]: node | (dof-mask bits << 28)
@@ -51,7 +74,8 @@ struct ts_ebe {
   std::unique_ptr<EbePairPlan> pair;    // face-sharing pairs (kernel 7)
   int kernel = 6;  // 2 pipelined generic, 3 pipelined batch-specialised, 5 tiled, 6 = 7 = face pairs (default);
                    // each falls back to 3, then 2, for batch widths it does not cover
-  mutable std::mutex host_mu;            // guards the host-entry staging buffers
+  mutable std::mutex host_mu;            // guards the host-entry staging buffers (and `stream`)
+  mutable std::unique_ptr<EbeStreamPlan> stream;  // built at the first pinned-host apply
   mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -60,6 +84,12 @@ struct ts_ebe {
 };
 
 namespace tsg {
+// pair sweep over units [p0, p1) (no init); false if the pair kernel does not cover `batch`
+bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t p0,
+                          int32_t p1);
+// f = A u with HOST u, f: H2D of u, the sweep and D2H of f overlapped chunk by chunk when
+// the buffers are pinned and the operator has a streamable schedule, else copy-apply-copy
+void ebe_apply_host(const ts_ebe& op, const void* u, void* f, int32_t batch);
 // f = A u on device pointers (EbeOperator::apply, ebe_operator.hpp:90-134)
 void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s);
 // inverse nodal diagonal blocks, fp64 math, rounded to prec (ebe_operator.hpp:288-313);

@@ -297,6 +297,12 @@ bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cud
   if (!op.pair) return false;
   const int32_t p0 = part == 1 ? op.pair->group_split : 0;
   const int32_t p1 = part == 0 ? op.pair->group_split : op.pair->n_units;
+  return ebe_pair_apply_range(op, u, f, batch, s, p0, p1);
+}
+
+bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t p0,
+                          int32_t p1) {
+  if (!op.pair) return false;
   if (op.prec == 32) {
     const float* uu = static_cast<const float*>(u);
     float* ff = static_cast<float*>(f);
@@ -384,15 +390,16 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn
       mate_k[e] = static_cast<int8_t>(best);
     }
   }
-  // units in group order: pairs (led by the lower index), then singles
+  // units in element order (a pair sits at its lower element, singles in place),
+  // so consecutive unit ranges stay spatially compact (ebe_stream.cu chunks them)
   std::vector<int32_t> units;  // leader element; singles encoded as ~e
   int32_t split = 0;
   for (int g = 0; g < 2; ++g) {
     const int64_t lo = g == 0 ? 0 : op.group_split, hi = g == 0 ? op.group_split : E;
-    for (int64_t e = lo; e < hi; ++e)
+    for (int64_t e = lo; e < hi; ++e) {
       if (mate[e] > e) units.push_back(static_cast<int32_t>(e));
-    for (int64_t e = lo; e < hi; ++e)
-      if (mate[e] < 0) units.push_back(~static_cast<int32_t>(e));
+      else if (mate[e] < 0) units.push_back(~static_cast<int32_t>(e));
+    }
     if (g == 0) split = static_cast<int32_t>(units.size());
   }
   const int32_t U = static_cast<int32_t>(units.size());

@@ -428,6 +428,12 @@ class EbeOperator:
         _ck(lib.ts_ebe_apply_host(self._h, _p(u), _p(out), batch))
         return out
 
+    def host_stream_chunks(self) -> int:
+        """Chunks of the pinned-host streaming schedule (0 = copy-apply-copy)."""
+        n = C.c_int32()
+        _ck(lib.ts_ebe_host_stream_chunks(self._h, C.byref(n)))
+        return n.value
+
     def block_jacobi(self) -> np.ndarray:
         """extract_block_jacobi(EbeOperator) (ebe_operator.hpp:288-313): [n_nodes, 9]."""
         inv = np.zeros((self._n, 9), self.dtype_np)
