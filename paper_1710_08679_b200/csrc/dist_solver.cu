@@ -378,7 +378,7 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
     L->l1.halo.run<double>(d1.get(), 9, 3, nullptr, *comm, s);
     bj_invert(d0.get(), L->mask0.get(), L->n0, 32, L->m0.get(), s);
     bj_invert(d1.get(), L->mask1.get(), L->n1, 32, L->m1.get(), s);
-    for (ts_ebe* op : {L->l0.op.get(), L->l1.op.get(), L->outer.op.get()}) std::vector<double>().swap(op->coef64);
+    for (ts_ebe* op : {L->l0.op.get(), L->l1.op.get(), L->outer.op.get()}) HostVec<double>().swap(op->coef64);
   }
   TS_CUDA(cudaDeviceSynchronize());
   comm->barrier();
@@ -495,7 +495,7 @@ ts_dist_ebe* dist_ebe_create(const Mesh& m, int order, int32_t n_mat, const doub
   const int32_t nn = order == 1 ? P.n_local_vertices : P.n_local;
   const std::vector<uint8_t> mk(P.mask.begin(), P.mask.begin() + 3 * size_t(nn));
   D->d.op.reset(ebe_create(P.local, order, n_mat, lam, mu, mk.data(), prec, group.data()));
-  std::vector<double>().swap(D->d.op->coef64);
+  HostVec<double>().swap(D->d.op->coef64);
   D->mask.upload(mk);
   D->d.halo.build(order == 1 ? P.halo1 : P.halo0);
   D->d.mask = D->mask.get();

@@ -611,6 +611,7 @@ void ebe_diag_blocks(const ts_ebe& op, double* diag, cudaStream_t s) {
     validation("block jacobi: operator setup data released (level-set inner operators keep only device state)");
   DevBuf<double> c64;
   c64.upload(op.coef64, s);
+  setup_mark("bj: upload records");
   TS_CUDA(cudaMemsetAsync(diag, 0, 9 * static_cast<size_t>(op.n_nodes) * sizeof(double), s));
   if (op.n_elems > 0) {
     if (op.order == 2)
@@ -663,11 +664,6 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   op->has_mask = dof_mask != nullptr;
   const int npe = op->npe, cs = op->conn_stride;
   const size_t E = static_cast<size_t>(op->n_elems);
-  std::vector<int32_t> conn(E * cs, 0);
-  op->host_conn.resize(E * npe);
-  op->coef64.assign(E * 12, 0.0);
-  const size_t ts = prec == 32 ? 4 : 8;
-  std::vector<unsigned char> coef(E * 12 * ts, 0);
   if (dof_mask) op->host_mask.assign(dof_mask, dof_mask + 3 * static_cast<size_t>(op->n_nodes));
   auto rnd = [prec](double x) { return prec == 32 ? static_cast<double>(static_cast<float>(x)) : x; };
   for (size_t e = 0; e < E; ++e) {  // validation first (exceptions stay out of the parallel loop)
@@ -682,8 +678,82 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
                    " out of range");
     }
   }
+  setup_mark("ebe: validate");
+  // Element order: (group, slab, Morton key, id). A partitioned operator keeps
+  // its boundary elements (group 0) ahead of the interior ones so the two sweep
+  // separately; within a group, elements go in kSlabs slabs of their lowest
+  // vertex id, then Morton (Z-order) of centroids. The slabs make node first /
+  // last use monotone in node id for meshes numbered along an axis (the box
+  // generator, most mesh tools), which lets the host-buffer apply stream u in
+  // and f out while it sweeps (ebe_stream.cu); inside a slab the Morton order
+  // keeps gathers and scatters L2-local.
+  HostVec<int32_t> ord(E);
+  {
+    const bool reuse = element_order && element_order->size() == E;
+    if (reuse) {  // the level set's other operators share one element order
+      std::copy(element_order->begin(), element_order->end(), ord.begin());
+    } else {
+      HostVec<double> cen(3 * E);
 #pragma omp parallel for schedule(static)
-  for (size_t e = 0; e < E; ++e) {
+      for (size_t e = 0; e < E; ++e)
+        for (int c = 0; c < 3; ++c) {
+          double x = 0.0;
+          for (int a = 0; a < 4; ++a) x += m.coords[3 * static_cast<size_t>(m.tets10[10 * e + a]) + c];
+          cen[3 * e + c] = 0.25 * x;
+        }
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (size_t e = 0; e < E; ++e)
+        for (int c = 0; c < 3; ++c) {
+          lo[c] = std::min(lo[c], cen[3 * e + c]);
+          hi[c] = std::max(hi[c], cen[3 * e + c]);
+        }
+      auto spread = [](uint64_t v) {
+        v &= 0x1FFFFF;
+        v = (v | v << 32) & 0x1F00000000FFFFULL;
+        v = (v | v << 16) & 0x1F0000FF0000FFULL;
+        v = (v | v << 8) & 0x100F00F00F00F00FULL;
+        v = (v | v << 4) & 0x10C30C30C30C30C3ULL;
+        v = (v | v << 2) & 0x1249249249249249ULL;
+        return v;
+      };
+      double ext = 0.0;
+      for (int c = 0; c < 3; ++c) ext = std::max(ext, hi[c] - lo[c]);
+      const double scale = ext > 0.0 ? double((1 << 20) - 1) / ext : 0.0;
+      const int64_t vmax = std::max<int64_t>(1, m.vertex_count);
+      HostVec<std::tuple<uint8_t, uint8_t, uint64_t, int32_t>> key(E);
+#pragma omp parallel for schedule(static)
+      for (size_t e = 0; e < E; ++e) {
+        uint64_t k = 0;
+        for (int c = 0; c < 3; ++c) k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
+        int32_t vlo = m.tets10[10 * e];
+        for (int a = 1; a < 4; ++a) vlo = std::min(vlo, m.tets10[10 * e + a]);
+        const auto slab = static_cast<uint8_t>(std::min<int64_t>(kEbeSlabs - 1, int64_t(vlo) * kEbeSlabs / vmax));
+        key[e] = {elem_group ? elem_group[e] : uint8_t(0), slab, k, static_cast<int32_t>(e)};
+      }
+      __gnu_parallel::sort(key.begin(), key.end());
+#pragma omp parallel for schedule(static)
+      for (size_t i = 0; i < E; ++i) ord[i] = std::get<3>(key[i]);
+      if (element_order) element_order->assign(ord.begin(), ord.end());
+    }
+    op->group_split = 0;
+    if (elem_group) {
+      for (size_t i = 0; i < E; ++i)
+        if (elem_group[ord[i]] == 0) op->group_split = static_cast<int32_t>(i + 1);
+    } else {
+      op->group_split = static_cast<int32_t>(E);
+    }
+  }
+  setup_mark("ebe: element order");
+  // element records, written straight into sweep order (no zero fill: every
+  // slot, padding included, is written by the parallel loop that first touches it)
+  HostVec<int32_t> conn(E * cs);
+  op->host_conn.resize(E * npe);
+  op->coef64.resize(E * 12);
+  const size_t ts = prec == 32 ? 4 : 8;
+  HostVec<unsigned char> coef(E * 12 * ts);
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < E; ++i) {
+    const size_t e = static_cast<size_t>(ord[i]);
     const int32_t mid = m.material_id[e];
     const int32_t* t = m.tets10.data() + 10 * e;
     for (int a = 0; a < npe; ++a) {
@@ -692,9 +762,10 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
       if (dof_mask)
         for (int c = 0; c < 3; ++c)
           if (dof_mask[3 * static_cast<size_t>(node) + c]) word |= 1 << (28 + c);
-      conn[e * cs + a] = word;
-      op->host_conn[e * npe + a] = node;
+      conn[i * cs + a] = word;
+      op->host_conn[i * npe + a] = node;
     }
+    for (int a = npe; a < cs; ++a) conn[i * cs + a] = 0;
     // T-rounded vertices and Lame values (ebe_operator.hpp:54-62), geometry in fp64
     double v[4][3];
     for (int a = 0; a < 4; ++a)
@@ -705,7 +776,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
       for (int r = 0; r < 3; ++r) j[r][c] = v[c + 1][r] - v[0][r];
     det_inv3(j, inv, &det);
     const double vol = det / 6.0;
-    double* c64 = op->coef64.data() + 12 * e;
+    double* c64 = op->coef64.data() + 12 * i;
     for (int k = 0; k < 3; ++k)
       for (int d = 0; d < 3; ++d) c64[3 * k + d] = inv[k][d];  // b_{k+1} = row k of J^-1
     c64[9] = lam * vol;
@@ -720,99 +791,13 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     for (int q = 0; q < 12; ++q) {
       if (prec == 32) {
         const float x = static_cast<float>(rec[q]);
-        std::memcpy(coef.data() + (12 * e + q) * ts, &x, 4);
+        std::memcpy(coef.data() + (12 * i + q) * ts, &x, 4);
       } else {
-        std::memcpy(coef.data() + (12 * e + q) * ts, &rec[q], 8);
+        std::memcpy(coef.data() + (12 * i + q) * ts, &rec[q], 8);
       }
     }
   }
   setup_mark("ebe: element records");
-  // Morton (Z-order) element ordering of centroids: consecutive elements — and
-  // so each block's cluster — are spatially compact, which minimises the
-  // cluster node count (scatter traffic) and keeps gathers L2-local.
-  {
-    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    const bool reuse = element_order && element_order->size() == E;
-    std::vector<double> cen(reuse ? 0 : 3 * E);
-#pragma omp parallel for schedule(static) if (!reuse)
-    for (size_t e = 0; e < (reuse ? 0 : E); ++e)
-      for (int c = 0; c < 3; ++c) {
-        double x = 0.0;
-        for (int a = 0; a < 4; ++a) x += m.coords[3 * static_cast<size_t>(m.tets10[10 * e + a]) + c];
-        cen[3 * e + c] = 0.25 * x;
-      }
-    for (size_t e = 0; e < (reuse ? 0 : E); ++e)
-      for (int c = 0; c < 3; ++c) {
-        lo[c] = std::min(lo[c], cen[3 * e + c]);
-        hi[c] = std::max(hi[c], cen[3 * e + c]);
-      }
-    auto spread = [](uint64_t v) {
-      v &= 0x1FFFFF;
-      v = (v | v << 32) & 0x1F00000000FFFFULL;
-      v = (v | v << 16) & 0x1F0000FF0000FFULL;
-      v = (v | v << 8) & 0x100F00F00F00F00FULL;
-      v = (v | v << 4) & 0x10C30C30C30C30C3ULL;
-      v = (v | v << 2) & 0x1249249249249249ULL;
-      return v;
-    };
-    double ext = 0.0;
-    for (int c = 0; c < 3; ++c) ext = std::max(ext, hi[c] - lo[c]);
-    const double scale = ext > 0.0 ? double((1 << 20) - 1) / ext : 0.0;
-    // (group, slab, Morton key, id): a partitioned operator keeps its boundary
-    // elements (group 0) ahead of the interior ones so the two sweep separately;
-    // within a group, elements go in kSlabs slabs of their lowest vertex id, then
-    // Morton order. The slabs make node first/last use monotone in node id for
-    // meshes numbered along an axis (the box generator, most mesh tools), which
-    // lets the host-buffer apply stream u in and f out while it sweeps
-    // (ebe_stream.cu); inside a slab the Morton order keeps gathers L2-local.
-    constexpr int kSlabs = kEbeSlabs;
-    const int64_t vmax = std::max<int64_t>(1, m.vertex_count);
-    auto slab_of = [&](size_t e) {
-      int32_t lo = m.tets10[10 * e];
-      for (int a = 1; a < 4; ++a) lo = std::min(lo, m.tets10[10 * e + a]);
-      return static_cast<uint8_t>(std::min<int64_t>(kSlabs - 1, int64_t(lo) * kSlabs / vmax));
-    };
-    std::vector<std::tuple<uint8_t, uint8_t, uint64_t, int32_t>> key(E);
-    if (reuse) {  // the level set's other operators share one element order
-#pragma omp parallel for schedule(static)
-      for (size_t i = 0; i < E; ++i) {
-        const int32_t e = (*element_order)[i];
-        key[i] = {elem_group ? elem_group[e] : uint8_t(0), 0, 0, e};
-      }
-    } else {
-#pragma omp parallel for schedule(static)
-      for (size_t e = 0; e < E; ++e) {
-        uint64_t k = 0;
-        for (int c = 0; c < 3; ++c)
-          k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
-        key[e] = {elem_group ? elem_group[e] : uint8_t(0), slab_of(e), k, static_cast<int32_t>(e)};
-      }
-      __gnu_parallel::sort(key.begin(), key.end());
-      if (element_order) {
-        element_order->resize(E);
-        for (size_t i = 0; i < E; ++i) (*element_order)[i] = std::get<3>(key[i]);
-      }
-    }
-    op->group_split = 0;
-    for (size_t i = 0; i < E; ++i)
-      if (std::get<0>(key[i]) == 0) op->group_split = static_cast<int32_t>(i + 1);
-    std::vector<int32_t> conn2(conn.size());
-    std::vector<int32_t> hconn2(op->host_conn.size());
-    std::vector<double> c642(op->coef64.size());
-    std::vector<unsigned char> coef2(coef.size());
-#pragma omp parallel for schedule(static)
-    for (size_t i = 0; i < E; ++i) {
-      const size_t e = static_cast<size_t>(std::get<3>(key[i]));
-      std::memcpy(&conn2[i * cs], &conn[e * cs], cs * sizeof(int32_t));
-      std::memcpy(&hconn2[i * npe], &op->host_conn[e * npe], npe * sizeof(int32_t));
-      std::memcpy(&c642[i * 12], &op->coef64[e * 12], 12 * sizeof(double));
-      std::memcpy(&coef2[i * 12 * ts], &coef[e * 12 * ts], 12 * ts);
-    }
-    conn.swap(conn2);
-    op->host_conn.swap(hconn2);
-    op->coef64.swap(c642);
-    coef.swap(coef2);
-  }
   if (kernel_override >= 0) op->kernel = kernel_override;
   else if (const char* k = std::getenv("TSGPU_EBE_KERNEL"))
     op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5
@@ -820,9 +805,10 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   {
     // fast-kernel layout: 3*node per local node, then the dof-mask word (bit 3a+c)
     const int cs3 = order == 1 ? 8 : 12;
-    std::vector<int32_t> conn3(E * cs3, 0);
+    HostVec<int32_t> conn3(E * cs3);
 #pragma omp parallel for schedule(static)
     for (size_t e = 0; e < E; ++e) {
+      for (int a = npe + 1; a < cs3; ++a) conn3[e * cs3 + a] = 0;
       uint32_t mw = 0;
       for (int a = 0; a < npe; ++a) {
         const int32_t w = conn[e * cs + a];
@@ -834,7 +820,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     }
     op->conn3.upload(conn3);
   }
-  setup_mark("ebe: morton + conn3");
+  setup_mark("ebe: conn3");
   // the tiled sweep's chunk records serve kernel 5 only (in the default mode the pair sweep covers the
   // common batch widths and the element-parallel sweeps the rest)
   if (op->kernel == 5) build_tile_plan(*op, conn, cs);

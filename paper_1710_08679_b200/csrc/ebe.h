@@ -66,8 +66,8 @@ struct ts_ebe {
   tsg::DevBuf<unsigned char> mask;      // [3N] uint8 (empty if unconstrained)
   tsg::DevBuf<int32_t> masked_dofs;     // constrained dof indices (identity rows)
   int32_t n_masked_dofs = 0;
-  std::vector<double> coef64;           // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
-  std::vector<int32_t> host_conn;       // host [E][npe] (setup only)
+  tsg::HostVec<double> coef64;          // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
+  tsg::HostVec<int32_t> host_conn;      // host [E][npe] (setup only)
   std::vector<uint8_t> host_mask;       // host [3N]
   std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, kernel 5)
   int32_t group_split = 0;              // elements [0, split) = group 0 (partition boundary), rest group 1
@@ -103,11 +103,11 @@ void bj_invert(const double* diag_dev, const uint8_t* mask_dev, int32_t n, int p
 bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part = -1);
 // element-group sweep of a partitioned operator (part -1 all, 0 boundary, 1 interior)
 void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part, bool init);
-void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int conn_stride);
+void build_tile_plan(ts_ebe& op, const HostVec<int32_t>& conn_words, int conn_stride);
 // pair sweep (ebe_pair.cu); false when no instance covers this batch width
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
-void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn_words, int cs,
-                     const std::vector<double>& coef64, bool fp32);
+void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_words, int cs,
+                     const HostVec<double>& coef64, bool fp32);
 // elem_group (nullable, [E] in {0,1}): group-0 elements sweep separately (boundary first);
 // kernel_override >= 0 fixes the sweep kernel (and so which plans are built);
 // element_order (nullable): empty -> receives the Morton order, filled -> reused

@@ -319,8 +319,8 @@ bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batc
 // permuted connectivity words (3*node), mask bits and coefficient records.
 //   conn_words: Morton-ordered [E][cs] node | mask << 28; coef64: Morton-ordered
 //   [E][12] fp64 (b rows, lambda V, mu V, V); vrnd: T-rounded vertex coordinates.
-void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn_words, int cs,
-                     const std::vector<double>& coef64, bool fp32) {
+void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_words, int cs,
+                     const HostVec<double>& coef64, bool fp32) {
   const int npe = op.npe;
   const int NR = npe == 10 ? PairGeo<10>::NR : PairGeo<4>::NR;
   const int kPairWords = npe == 10 ? PairGeo<10>::WORDS : PairGeo<4>::WORDS;
@@ -335,19 +335,26 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn
   };
   // face adjacency through the vertex -> element incidence: the element across
   // face k (opposite local vertex k) is the other element containing its 3 vertices
+  // (parallel counting sort; the order inside a vertex's list does not matter:
+  // the element across a face is unique)
   int32_t nv = 0;
+#pragma omp parallel for schedule(static) reduction(max : nv)
   for (int64_t e = 0; e < E; ++e)
     for (int a = 0; a < 4; ++a) nv = std::max(nv, node(e, a) + 1);
-  std::vector<int32_t> vptr(size_t(nv) + 1, 0), velem(size_t(E) * 4);
+  std::vector<int32_t> vptr(size_t(nv) + 1, 0);
+  HostVec<int32_t> velem(size_t(E) * 4);
+#pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) ++vptr[node(e, a) + 1];
+    for (int a = 0; a < 4; ++a) __atomic_fetch_add(&vptr[node(e, a) + 1], 1, __ATOMIC_RELAXED);
   for (int32_t v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
   {
     std::vector<int32_t> cur(vptr.begin(), vptr.end() - 1);
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < E; ++e)
-      for (int a = 0; a < 4; ++a) velem[cur[node(e, a)]++] = static_cast<int32_t>(e);
+      for (int a = 0; a < 4; ++a)
+        velem[__atomic_fetch_add(&cur[node(e, a)], 1, __ATOMIC_RELAXED)] = static_cast<int32_t>(e);
   }
-  std::vector<std::array<int32_t, 4>> nbr(E);
+  HostVec<std::array<int32_t, 4>> nbr(E);
 #pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < E; ++e)
     for (int k = 0; k < 4; ++k) {
@@ -367,6 +374,7 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn
       }
       nbr[e][k] = found;
     }
+  setup_mark("pair: face adjacency");
   auto group_of = [&](int64_t e) { return e < op.group_split ? 0 : 1; };
   std::vector<int32_t> mate(E, -1);
   std::vector<int8_t> mate_k(E, -1);
@@ -402,10 +410,11 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn
     }
     if (g == 0) split = static_cast<int32_t>(units.size());
   }
+  setup_mark("pair: matching");
   const int32_t U = static_cast<int32_t>(units.size());
-  std::vector<int32_t> pc(size_t(U) * kPairWords, 0);
+  HostVec<int32_t> pc(size_t(U) * kPairWords);
   const size_t ts = fp32 ? 4 : 8;
-  std::vector<unsigned char> pcf(size_t(U) * 24 * ts, 0);
+  HostVec<unsigned char> pcf(size_t(U) * 24 * ts);
   auto rnd = [fp32](double x) { return fp32 ? static_cast<double>(static_cast<float>(x)) : x; };
   // coefficient record of element e with local vertex order perm (orientation from the original order)
   auto record = [&](int64_t e, const int perm[4], unsigned char* dst) -> bool {
@@ -490,12 +499,16 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const std::vector<int32_t>& conn
         w[s] = 3 * nd;
         ma |= mk << (3 * s);
       }
+      for (int s = npe; s < NR; ++s) w[s] = 0;  // no B
+      std::memset(cf + 12 * ts, 0, 12 * ts);
       bad = bad || !record(a, pa, cf);
     }
     w[NR] = static_cast<int32_t>(ma);
     w[NR + 1] = static_cast<int32_t>(mb);
+    for (int s = NR + 2; s < kPairWords; ++s) w[s] = 0;
   }
   if (bad) validation("pair plan: inconsistent face pairing or degenerate element");
+  setup_mark("pair: unit records");
   auto plan = std::make_unique<EbePairPlan>();
   plan->n_units = U;
   plan->group_split = split;

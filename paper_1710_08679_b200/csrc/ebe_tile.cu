@@ -402,7 +402,7 @@ bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cud
 }
 
 // Chunk records from the Morton-ordered connectivity words (node | mask << 28).
-void build_tile_plan(ts_ebe& op, const std::vector<int32_t>& conn_words, int conn_stride) {
+void build_tile_plan(ts_ebe& op, const HostVec<int32_t>& conn_words, int conn_stride) {
   const int npe = op.npe;
   const int64_t E = op.n_elems;
   auto plan = std::make_unique<EbeTilePlan>();

@@ -47,87 +47,134 @@ int32_t find_col(const BcsrD& a, int32_t r, int32_t c) {
 }  // namespace
 
 // assemble_bcsr(EbeOperator<double>(mesh, 1, ...)) (ebe_operator.hpp:230-284)
-// for the first-order vertex grid with the level-1 mask.
+// for the first-order vertex grid with the level-1 mask. With `blocks32`, the
+// same pass also assembles the fp32 operator's image (float-rounded vertices
+// and Lame values, as EbeOperator<float> stores them, ebe_operator.hpp:54-62;
+// summed in fp64, stored as float) on the same pattern.
 BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
-                    const std::vector<uint8_t>& mask1, bool round32) {
-  // round32: float-rounded vertices and Lame values, as the fp32 EbeOperator
-  // stores them (ebe_operator.hpp:54-62) — the assembled image of the level-1 operator
-  auto rnd = [round32](double x) { return round32 ? static_cast<double>(static_cast<float>(x)) : x; };
+                    const std::vector<uint8_t>& mask1, HostVec<float>* blocks32) {
+  auto r32 = [](double x) { return static_cast<double>(static_cast<float>(x)); };
   const int32_t n = m.vertex_count;
   const int64_t E = m.n_elems();
-  // node -> elements CSR
+  // node -> elements CSR (counting sort; element order within a row kept ascending)
   std::vector<int64_t> nptr(n + 1, 0);
   for (int64_t e = 0; e < E; ++e)
     for (int a = 0; a < 4; ++a) ++nptr[m.tets10[10 * e + a] + 1];
   for (int32_t i = 0; i < n; ++i) nptr[i + 1] += nptr[i];
-  std::vector<int32_t> nel(nptr[n]);
+  HostVec<int32_t> nel(nptr[n]);
   {
     std::vector<int64_t> cur(nptr.begin(), nptr.end() - 1);
     for (int64_t e = 0; e < E; ++e)
       for (int a = 0; a < 4; ++a) nel[cur[m.tets10[10 * e + a]]++] = static_cast<int32_t>(e);
   }
+  setup_mark("assemble: incidence");
   BcsrD A;
   A.n = n;
   A.row_ptr.assign(n + 1, 0);
-  // pattern: sorted unique vertex neighbours (incl. self)
-  std::vector<std::vector<int32_t>> rows(n);
-#pragma omp parallel for schedule(dynamic, 4096)
-  for (int32_t r = 0; r < n; ++r) {
-    auto& row = rows[r];
-    row.reserve(32);
-    for (int64_t k = nptr[r]; k < nptr[r + 1]; ++k)
-      for (int a = 0; a < 4; ++a) row.push_back(m.tets10[10 * int64_t(nel[k]) + a]);
-    std::sort(row.begin(), row.end());
-    row.erase(std::unique(row.begin(), row.end()), row.end());
+  // pattern: sorted unique vertex neighbours (incl. self), counted then filled in place
+#pragma omp parallel
+  {
+    std::vector<int32_t> row;
+#pragma omp for schedule(dynamic, 4096)
+    for (int32_t r = 0; r < n; ++r) {
+      row.clear();
+      for (int64_t k = nptr[r]; k < nptr[r + 1]; ++k)
+        for (int a = 0; a < 4; ++a) row.push_back(m.tets10[10 * int64_t(nel[k]) + a]);
+      std::sort(row.begin(), row.end());
+      A.row_ptr[r + 1] = static_cast<int32_t>(std::unique(row.begin(), row.end()) - row.begin());
+    }
   }
-  for (int32_t r = 0; r < n; ++r) A.row_ptr[r + 1] = A.row_ptr[r] + static_cast<int32_t>(rows[r].size());
+  for (int32_t r = 0; r < n; ++r) A.row_ptr[r + 1] += A.row_ptr[r];
   A.col_idx.resize(A.row_ptr[n]);
-  for (int32_t r = 0; r < n; ++r) std::copy(rows[r].begin(), rows[r].end(), A.col_idx.begin() + A.row_ptr[r]);
-  rows.clear();
-  rows.shrink_to_fit();
-  A.blocks.assign(static_cast<size_t>(A.row_ptr[n]) * 9, 0.0);
+#pragma omp parallel
+  {
+    std::vector<int32_t> row;
+#pragma omp for schedule(dynamic, 4096)
+    for (int32_t r = 0; r < n; ++r) {
+      row.clear();
+      for (int64_t k = nptr[r]; k < nptr[r + 1]; ++k)
+        for (int a = 0; a < 4; ++a) row.push_back(m.tets10[10 * int64_t(nel[k]) + a]);
+      std::sort(row.begin(), row.end());
+      std::unique(row.begin(), row.end());
+      std::copy(row.begin(), row.begin() + (A.row_ptr[r + 1] - A.row_ptr[r]), A.col_idx.begin() + A.row_ptr[r]);
+    }
+  }
+  setup_mark("assemble: pattern");
+  A.blocks.resize(static_cast<size_t>(A.row_ptr[n]) * 9);
+  if (blocks32) blocks32->resize(A.blocks.size());
   // values: row-owner accumulation (each row summed by one thread, element order)
-#pragma omp parallel for schedule(dynamic, 4096)
-  for (int32_t r = 0; r < n; ++r) {
-    for (int64_t k = nptr[r]; k < nptr[r + 1]; ++k) {
-      const int64_t e = nel[k];
-      const int32_t* t = m.tets10.data() + 10 * e;
-      double v[4][3];
-      for (int a = 0; a < 4; ++a)
-        for (int c = 0; c < 3; ++c) v[a][c] = rnd(m.coords[3 * size_t(t[a]) + c]);
-      double j[3][3], inv[3][3];
-      for (int c = 0; c < 3; ++c)
-        for (int q = 0; q < 3; ++q) j[q][c] = v[c + 1][q] - v[0][q];
-      if (!invert3(j, inv, 0.0)) continue;
-      const double det = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
-                         j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
-                         j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
-      const double vol = det / 6.0;
-      double g[4][3];
-      for (int d = 0; d < 3; ++d) {
-        g[1][d] = inv[0][d];
-        g[2][d] = inv[1][d];
-        g[3][d] = inv[2][d];
-        g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
+  struct Geo {
+    double g[4][3], wl, wm;
+    bool ok;
+  };
+  auto geometry = [&](const int32_t* t, int64_t e, bool round) {
+    Geo G{};
+    double v[4][3];
+    for (int a = 0; a < 4; ++a)
+      for (int c = 0; c < 3; ++c) {
+        const double x = m.coords[3 * size_t(t[a]) + c];
+        v[a][c] = round ? r32(x) : x;
       }
-      const double wl = vol * rnd(lam_e[e]), wm = vol * rnd(mu_e[e]);
-      int a = 0;
-      while (t[a] != r) ++a;
-      for (int b = 0; b < 4; ++b) {
-        const int32_t gb = t[b];
-        double* blk = A.blocks.data() + 9 * static_cast<size_t>(find_col(A, r, gb));
-        const double gdot = g[a][0] * g[b][0] + g[a][1] * g[b][1] + g[a][2] * g[b][2];
-        for (int i = 0; i < 3; ++i) {
-          if (mask1[3 * size_t(r) + i]) continue;
-          for (int jj = 0; jj < 3; ++jj) {
-            if (mask1[3 * size_t(gb) + jj]) continue;
-            blk[3 * i + jj] += wl * g[a][i] * g[b][jj] + wm * g[b][i] * g[a][jj] + (i == jj ? wm * gdot : 0.0);
-          }
-        }
+    double j[3][3], inv[3][3];
+    for (int c = 0; c < 3; ++c)
+      for (int q = 0; q < 3; ++q) j[q][c] = v[c + 1][q] - v[0][q];
+    G.ok = invert3(j, inv, 0.0);
+    if (!G.ok) return G;
+    const double det = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
+                       j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
+                       j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
+    const double vol = det / 6.0;
+    for (int d = 0; d < 3; ++d) {
+      G.g[1][d] = inv[0][d];
+      G.g[2][d] = inv[1][d];
+      G.g[3][d] = inv[2][d];
+      G.g[0][d] = -(G.g[1][d] + G.g[2][d] + G.g[3][d]);
+    }
+    G.wl = vol * (round ? r32(lam_e[e]) : lam_e[e]);
+    G.wm = vol * (round ? r32(mu_e[e]) : mu_e[e]);
+    return G;
+  };
+  auto add = [&](const Geo& G, int a, int b, int32_t r, int32_t gb, double* blk) {
+    const double gdot = G.g[a][0] * G.g[b][0] + G.g[a][1] * G.g[b][1] + G.g[a][2] * G.g[b][2];
+    for (int i = 0; i < 3; ++i) {
+      if (mask1[3 * size_t(r) + i]) continue;
+      for (int jj = 0; jj < 3; ++jj) {
+        if (mask1[3 * size_t(gb) + jj]) continue;
+        blk[3 * i + jj] += G.wl * G.g[a][i] * G.g[b][jj] + G.wm * G.g[b][i] * G.g[a][jj] + (i == jj ? G.wm * gdot : 0.0);
       }
     }
-    for (int i = 0; i < 3; ++i)
-      if (mask1[3 * size_t(r) + i]) A.blocks[9 * static_cast<size_t>(find_col(A, r, r)) + 4 * i] = 1.0;
+  };
+#pragma omp parallel
+  {
+    std::vector<double> acc32;
+#pragma omp for schedule(dynamic, 4096)
+    for (int32_t r = 0; r < n; ++r) {
+      const int32_t rb = A.row_ptr[r], len = A.row_ptr[r + 1] - rb;
+      std::fill(A.blocks.begin() + 9 * size_t(rb), A.blocks.begin() + 9 * size_t(rb + len), 0.0);
+      if (blocks32) acc32.assign(9 * size_t(len), 0.0);
+      for (int64_t k = nptr[r]; k < nptr[r + 1]; ++k) {
+        const int64_t e = nel[k];
+        const int32_t* t = m.tets10.data() + 10 * e;
+        const Geo G = geometry(t, e, false);
+        const Geo G32 = blocks32 ? geometry(t, e, true) : Geo{};
+        int a = 0;
+        while (t[a] != r) ++a;
+        for (int b = 0; b < 4; ++b) {
+          const int32_t gb = t[b];
+          const int32_t q = find_col(A, r, gb);
+          if (G.ok) add(G, a, b, r, gb, A.blocks.data() + 9 * static_cast<size_t>(q));
+          if (blocks32 && G32.ok) add(G32, a, b, r, gb, acc32.data() + 9 * static_cast<size_t>(q - rb));
+        }
+      }
+      const int32_t qd = find_col(A, r, r);
+      for (int i = 0; i < 3; ++i)
+        if (mask1[3 * size_t(r) + i]) {
+          A.blocks[9 * static_cast<size_t>(qd) + 4 * i] = 1.0;
+          if (blocks32) acc32[9 * static_cast<size_t>(qd - rb) + 4 * i] = 1.0;
+        }
+      if (blocks32)
+        for (size_t x = 0; x < 9 * size_t(len); ++x) (*blocks32)[9 * size_t(rb) + x] = static_cast<float>(acc32[x]);
+    }
   }
   return A;
 }

@@ -9,8 +9,9 @@ namespace tsg {
 // 3x3-block CSR with fp64 values (BlockCsrMatrix<double>, block_csr.hpp:16-70)
 struct BcsrD {
   int32_t n = 0;
-  std::vector<int32_t> row_ptr, col_idx;
-  std::vector<double> blocks;  // [nnzb][9]
+  std::vector<int32_t> row_ptr;
+  HostVec<int32_t> col_idx;
+  HostVec<double> blocks;  // [nnzb][9]
 };
 
 struct Aggregation {  // aggregation.hpp:13-17
@@ -18,8 +19,10 @@ struct Aggregation {  // aggregation.hpp:13-17
   int32_t n_aggregates = 0;
 };
 
+// K1 (fp64, the reference's assembly); blocks32 (optional) receives the fp32
+// operator's float-rounded image on the same pattern
 BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
-                    const std::vector<uint8_t>& mask1, bool round32 = false);
+                    const std::vector<uint8_t>& mask1, HostVec<float>* blocks32 = nullptr);
 Aggregation aggregate_p1(const BcsrD& a, int32_t target);
 BcsrD build_level2(const BcsrD& k1, const Aggregation& agg, const std::vector<uint8_t>& fine_mask);
 std::vector<uint8_t> coarse_mask(const Aggregation& agg, const std::vector<uint8_t>& fine_mask);

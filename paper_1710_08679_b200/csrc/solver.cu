@@ -219,16 +219,13 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   // K1 -> aggregation -> Galerkin level 2 (adaptive_cg.hpp:53-60)
   const std::vector<double> lam_e = lame_per_element(m, n_mat, lam), mu_e = lame_per_element(m, n_mat, mu);
   setup_mark("levels: P1");
-  const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1);
+  HostVec<float> k1f;  // the fp32 level-1 operator, float-rounded inputs, same pattern
+  const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1, lv->l1_assembled ? &k1f : nullptr);
   setup_mark("levels: K1 assembly");
   if (lv->l1_assembled) {
-    const BcsrD k1f = assemble_tet4(m, lam_e, mu_e, mask1, true);
-    std::vector<float> bl(k1f.blocks.size());
-#pragma omp parallel for schedule(static)
-    for (size_t q = 0; q < bl.size(); ++q) bl[q] = static_cast<float>(k1f.blocks[q]);
-    lv->l1_row_ptr.upload(k1f.row_ptr);
-    lv->l1_col_idx.upload(k1f.col_idx);
-    lv->l1_blocks.upload(bl);
+    lv->l1_row_ptr.upload(k1.row_ptr);
+    lv->l1_col_idx.upload(k1.col_idx);
+    lv->l1_blocks.upload(k1f);
     setup_mark("levels: K1 fp32 operator");
   }
   Aggregation agg = aggregate_p1(k1, cfg.aggregate_target);
@@ -240,7 +237,7 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   lv->h_m2 = bcsr_block_jacobi_f32(a2);
   lv->h_agg = agg.agg_of_node;
   lv->h_rp2 = a2.row_ptr;
-  lv->h_ci2 = a2.col_idx;
+  lv->h_ci2.assign(a2.col_idx.begin(), a2.col_idx.end());
   lv->h_bl2.resize(a2.blocks.size());
   for (size_t q = 0; q < a2.blocks.size(); ++q) lv->h_bl2[q] = static_cast<float>(a2.blocks[q]);
   {
@@ -267,7 +264,7 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   ebe_block_jacobi(*lv->l1, lv->m1.get(), nullptr);
   // host setup copies no longer needed by the operators
   for (ts_ebe* op : {lv->l0.get(), lv->l1.get()}) {  // outer keeps them for solve_pcge's block Jacobi
-    std::vector<double>().swap(op->coef64);
+    HostVec<double>().swap(op->coef64);
   }
   TS_CUDA(cudaDeviceSynchronize());
   setup_mark("levels: block Jacobi");

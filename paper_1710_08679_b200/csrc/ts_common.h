@@ -5,8 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -38,6 +41,30 @@ void set_last_error(const std::string& m);
 // Ensure a usable device exists; the product has no CPU fallback.
 void require_device();
 
+// Allocator whose value-initialising constructions default-initialise: a
+// HostVec<T>(n) of scalars is NOT zero-filled, so big setup arrays are first
+// touched (paged in) by the parallel loops that fill them, not by one thread.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using HostVec = std::vector<T, NoInitAlloc<T>>;
+
 // RAII device allocation.
 template <typename T>
 class DevBuf {
@@ -67,7 +94,8 @@ class DevBuf {
     ensure(n);
     if (n) TS_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
   }
-  void upload(const std::vector<T>& h, cudaStream_t s = 0) { upload(h.data(), h.size(), s); }
+  template <class A>
+  void upload(const std::vector<T, A>& h, cudaStream_t s = 0) { upload(h.data(), h.size(), s); }
   void release() {
     if (p_) cudaFree(p_);
     p_ = nullptr;
