@@ -126,15 +126,24 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         cpa(cbuf + (stage * GROUPS + grp) * 24 + q * TPC, pcoef + static_cast<size_t>(ee) * 24 + q * TPC, 16, 16);
       V* dst = ubuf + stage * NIN * NT + threadIdx.x;
       const unsigned ma = static_cast<unsigned>(nd[MW]), mb = static_cast<unsigned>(nd[MW + 1]);
-      const int nrows = (mb & unsigned(kHasB)) ? NR : NPE;
+      if (mb == unsigned(kHasB) && ma == 0u) {  // interior pair: no constrained dof, no per-dof predicates
 #pragma unroll
-      for (int a = 0; a < NR; ++a) {
-        if (a >= nrows) break;
-        const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
+        for (int a = 0; a < NR; ++a) {
+          const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const unsigned m = a < NPE ? (ma >> (3 * a + c)) & 1u : (mb >> (3 * (a - NPE) + c)) & 1u;
-          cpa(dst + (a * 3 + c) * NT, row + c * B, m ? 0 : int(sizeof(V)), sizeof(V));
+          for (int c = 0; c < 3; ++c) cpa(dst + (a * 3 + c) * NT, row + c * B, int(sizeof(V)), sizeof(V));
+        }
+      } else {
+        const int nrows = (mb & unsigned(kHasB)) ? NR : NPE;
+#pragma unroll
+        for (int a = 0; a < NR; ++a) {
+          if (a >= nrows) break;
+          const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const unsigned m = a < NPE ? (ma >> (3 * a + c)) & 1u : (mb >> (3 * (a - NPE) + c)) & 1u;
+            cpa(dst + (a * 3 + c) * NT, row + c * B, m ? 0 : int(sizeof(V)), sizeof(V));
+          }
         }
       }
     }
@@ -177,8 +186,13 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         for (int k = 0; k < Geo::NA_OWN; ++k) {
           const int a = Geo::a_own(k);
           T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
+          if (ma == 0u) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], (ma >> (3 * a + c)) & 1u);
+            for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(row + c * B), ff[a][c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], (ma >> (3 * a + c)) & 1u);
+          }
         }
 #pragma unroll
         for (int k = 0; k < Geo::NFACE; ++k)
@@ -205,14 +219,20 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         for (int k = 0; k < Geo::NFACE; ++k)
 #pragma unroll
           for (int c = 0; c < 3; ++c) ff[Geo::b_face(k)][c] = O::add(ff[Geo::b_face(k)][c], carry[k][c]);
+        const bool interior = ma == 0u && mb == unsigned(kHasB);
 #pragma unroll
         for (int a = 0; a < NPE; ++a) {
           const int r = Geo::b_row(a);
           T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[r])) * B + col;
+          if (interior) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const unsigned m = r < NPE ? (ma >> (3 * r + c)) & 1u : (mb >> (3 * (r - NPE) + c)) & 1u;
-            red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], m);
+            for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(row + c * B), ff[a][c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const unsigned m = r < NPE ? (ma >> (3 * r + c)) & 1u : (mb >> (3 * (r - NPE) + c)) & 1u;
+              red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], m);
+            }
           }
         }
       } else {
