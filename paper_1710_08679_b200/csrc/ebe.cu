@@ -646,6 +646,15 @@ void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s) {
   bj_invert(diag.get(), op.has_mask ? op.mask.get() : nullptr, op.n_nodes, op.prec, inv_dev, s);
 }
 
+int ebe_slab_count() {
+  static const int n = [] {
+    const char* e = std::getenv("TSGPU_EBE_SLABS");
+    const int v = e ? std::atoi(e) : kEbeSlabs;
+    return std::max(1, std::min(255, v));
+  }();
+  return n;
+}
+
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda, const double* mu,
                    const uint8_t* dof_mask, int prec, const uint8_t* elem_group, int kernel_override,
                    std::vector<int32_t>* element_order) {
@@ -660,6 +669,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   op->n_nodes = order == 1 ? m.vertex_count : m.n_nodes();
   op->n_elems = m.n_elems();
   op->n_vertices = m.vertex_count;
+  op->n_slabs = ebe_slab_count();
   if (op->n_nodes >= (1 << 28)) validation("ebe: more than 2^28 nodes per device is not supported");
   op->has_mask = dof_mask != nullptr;
   const int npe = op->npe, cs = op->conn_stride;
@@ -727,7 +737,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
         for (int c = 0; c < 3; ++c) k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
         int32_t vlo = m.tets10[10 * e];
         for (int a = 1; a < 4; ++a) vlo = std::min(vlo, m.tets10[10 * e + a]);
-        const auto slab = static_cast<uint8_t>(std::min<int64_t>(kEbeSlabs - 1, int64_t(vlo) * kEbeSlabs / vmax));
+        const auto slab = static_cast<uint8_t>(std::min<int64_t>(op->n_slabs - 1, int64_t(vlo) * op->n_slabs / vmax));
         key[e] = {elem_group ? elem_group[e] : uint8_t(0), slab, k, static_cast<int32_t>(e)};
       }
       __gnu_parallel::sort(key.begin(), key.end());

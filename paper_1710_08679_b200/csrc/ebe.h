@@ -31,8 +31,10 @@ struct EbePairPlan {
   tsg::DevBuf<unsigned char> coef;  // [units][24] of T: A and B coefficient records
 };
 
-// Elements sweep in slabs of their lowest vertex id (then Morton order), ebe.cu
-constexpr int kEbeSlabs = 32;
+// Elements sweep in slabs of their lowest vertex id (then Morton order), ebe.cu;
+// TSGPU_EBE_SLABS overrides (1 = plain Morton)
+constexpr int kEbeSlabs = 16;
+int ebe_slab_count();
 
 // Host-buffer streaming schedule (ebe_stream.cu): the pair units cut into
 // chunks; node rows go up before the first chunk that reads them and come back
@@ -58,6 +60,7 @@ struct ts_ebe {
   int32_t n_nodes = 0;
   int32_t n_elems = 0;
   int32_t n_vertices = 0;  // mesh vertex count (the slab key's range)
+  int n_slabs = kEbeSlabs; // element-order slabs (ebe_stream.cu chunks on them)
   bool has_mask = false;
   int conn_stride = 12;                 // int32 per element (npe padded to 4)
   tsg::DevBuf<int32_t> conn;            // [E][conn_stride]: node | (dof-mask bits << 28)
