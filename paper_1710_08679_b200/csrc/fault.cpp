@@ -251,33 +251,12 @@ std::vector<double> unit_slip_magnitudes(const FaultPatch& patch, const Mesh& ba
   return mag;
 }
 
-bool locate_point(const Mesh& m, const V3& p, int32_t* elem, double n10[10]) {
-  const double bary_tol = -1e-8;
-  const int32_t E = m.n_elems();
-  int32_t best = E;
-#pragma omp parallel for schedule(static) reduction(min : best)
-  for (int32_t e = 0; e < E; ++e) {
-    if (e >= best) continue;
-    const V3 v0 = coord(m, m.tets10[10 * size_t(e)]);
-    double jac[3][3], inv[3][3];
-    for (int c = 0; c < 3; ++c) {
-      const V3 ed = sub(coord(m, m.tets10[10 * size_t(e) + c + 1]), v0);
-      for (int r = 0; r < 3; ++r) jac[r][c] = ed[r];
-    }
-    if (!invert3(jac, inv)) continue;
-    const V3 d = sub(p, v0);
-    double xi[3];
-    for (int r = 0; r < 3; ++r) xi[r] = inv[r][0] * d[0] + inv[r][1] * d[1] + inv[r][2] * d[2];
-    const double l0 = 1.0 - xi[0] - xi[1] - xi[2];
-    if (xi[0] < bary_tol || xi[1] < bary_tol || xi[2] < bary_tol || l0 < bary_tol) continue;
-    best = std::min(best, e);
-  }
-  if (best == E) return false;
-  // tet10_shape_values (element_stiffness.hpp:56-61) at the point in the first containing element
-  const V3 v0 = coord(m, m.tets10[10 * size_t(best)]);
+// tet10_shape_values (element_stiffness.hpp:56-61) of element e at point p
+void tet10_shape_at(const Mesh& m, int32_t e, const V3& p, double n10[10]) {
+  const V3 v0 = coord(m, m.tets10[10 * size_t(e)]);
   double jac[3][3], inv[3][3];
   for (int c = 0; c < 3; ++c) {
-    const V3 ed = sub(coord(m, m.tets10[10 * size_t(best) + c + 1]), v0);
+    const V3 ed = sub(coord(m, m.tets10[10 * size_t(e) + c + 1]), v0);
     for (int r = 0; r < 3; ++r) jac[r][c] = ed[r];
   }
   invert3(jac, inv);
@@ -287,8 +266,6 @@ bool locate_point(const Mesh& m, const V3& p, int32_t* elem, double n10[10]) {
   const double l[4] = {1.0 - xi[0] - xi[1] - xi[2], xi[0], xi[1], xi[2]};
   for (int a = 0; a < 4; ++a) n10[a] = l[a] * (2.0 * l[a] - 1.0);
   for (int k = 0; k < 6; ++k) n10[4 + k] = 4.0 * l[kEdgeEnds[k][0]] * l[kEdgeEnds[k][1]];
-  *elem = best;
-  return true;
 }
 
 }  // namespace tsg

@@ -37,8 +37,8 @@ void split_nodes(const Mesh& m, const std::vector<std::array<int32_t, 3>>& tris,
 double bspline_bell(double s);
 std::vector<double> unit_slip_magnitudes(const FaultPatch& patch, const Mesh& base, const V3& center,
                                          double radius);
-// sample_displacement's point location (greens.hpp:50-76): first element containing the point,
-// its tet10 shape values and node ids; false when outside the mesh
-bool locate_point(const Mesh& m, const V3& p, int32_t* elem, double n10[10]);
+// sample_displacement (greens.hpp:50-76): tet10 shape values of element e at p. The first
+// containing element itself is found on the device (greens.cu locate_points).
+void tet10_shape_at(const Mesh& m, int32_t e, const V3& p, double n10[10]);
 
 }  // namespace tsg

@@ -5,6 +5,7 @@
 // split mesh for the whole batch), solve the batch (adaptive_cg.hpp:242-263),
 // sample every observation (greens.hpp:50-76: first containing element, tet10
 // shape values — located once, then a device gather for all columns).
+#include <climits>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -52,6 +53,55 @@ __global__ void k_sample(const double* __restrict__ u, const int32_t* __restrict
   bank[int64_t(r) * n_cols + col0 + j] = v;
 }
 
+// IEEE ops without contraction: the device scan reproduces the host arithmetic
+// of the reference's point location (greens.hpp:50-76, geometry.hpp:27-42) operation for operation
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+// sample_displacement's point location (greens.hpp:50-76): the FIRST element (lowest id)
+// containing each point, barycentric tolerance -1e-8. One thread per element tests every
+// point; best[p] = atomicMin over containing elements. tet4 = the vertex ids of each element.
+__global__ void k_locate(const double* __restrict__ xyz, const int32_t* __restrict__ tet4, int32_t E,
+                         const double* __restrict__ pts, int32_t n, int32_t* __restrict__ best) {
+  const int32_t e = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (e >= E) return;
+  double v[4][3];
+  for (int a = 0; a < 4; ++a) {
+    const int64_t id = __ldg(tet4 + 4 * int64_t(e) + a);
+    for (int c = 0; c < 3; ++c) v[a][c] = __ldg(xyz + 3 * id + c);
+  }
+  double m[3][3];
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < 3; ++r) m[r][c] = ds(v[c + 1][r], v[0][r]);
+  // invert3 (geometry.hpp:27-42), same operation order as the host
+  const double d = da(ds(dm(m[0][0], ds(dm(m[1][1], m[2][2]), dm(m[1][2], m[2][1]))),
+                         dm(m[0][1], ds(dm(m[1][0], m[2][2]), dm(m[1][2], m[2][0])))),
+                      dm(m[0][2], ds(dm(m[1][0], m[2][1]), dm(m[1][1], m[2][0]))));
+  if (d == 0.0) return;
+  const double id = __ddiv_rn(1.0, d);
+  double inv[3][3];
+  inv[0][0] = dm(ds(dm(m[1][1], m[2][2]), dm(m[1][2], m[2][1])), id);
+  inv[0][1] = dm(ds(dm(m[0][2], m[2][1]), dm(m[0][1], m[2][2])), id);
+  inv[0][2] = dm(ds(dm(m[0][1], m[1][2]), dm(m[0][2], m[1][1])), id);
+  inv[1][0] = dm(ds(dm(m[1][2], m[2][0]), dm(m[1][0], m[2][2])), id);
+  inv[1][1] = dm(ds(dm(m[0][0], m[2][2]), dm(m[0][2], m[2][0])), id);
+  inv[1][2] = dm(ds(dm(m[0][2], m[1][0]), dm(m[0][0], m[1][2])), id);
+  inv[2][0] = dm(ds(dm(m[1][0], m[2][1]), dm(m[1][1], m[2][0])), id);
+  inv[2][1] = dm(ds(dm(m[0][1], m[2][0]), dm(m[0][0], m[2][1])), id);
+  inv[2][2] = dm(ds(dm(m[0][0], m[1][1]), dm(m[0][1], m[1][0])), id);
+  constexpr double kTol = -1e-8;
+  for (int32_t q = 0; q < n; ++q) {
+    const double d0 = ds(__ldg(pts + 3 * q), v[0][0]), d1 = ds(__ldg(pts + 3 * q + 1), v[0][1]),
+                 d2 = ds(__ldg(pts + 3 * q + 2), v[0][2]);
+    double xi[3];
+    for (int r = 0; r < 3; ++r) xi[r] = da(da(dm(inv[r][0], d0), dm(inv[r][1], d1)), dm(inv[r][2], d2));
+    const double l0 = ds(ds(ds(1.0, xi[0]), xi[1]), xi[2]);
+    if (xi[0] < kTol || xi[1] < kTol || xi[2] < kTol || l0 < kTol) continue;
+    atomicMin(best + q, e);
+  }
+}
+
 }  // namespace
 }  // namespace tsg
 
@@ -63,6 +113,9 @@ struct ts_faulted {
   ts_levels* levels = nullptr;
   std::unique_ptr<ts_ebe> split_raw;  // unmasked fp64 tet10 on the split mesh
   tsg::DevBuf<int32_t> plus, minus, s1, s2;
+  tsg::DevBuf<double> loc_xyz;    // base vertex coordinates (device point location)
+  tsg::DevBuf<int32_t> loc_tet4;  // base element vertex ids
+  tsg::DevBuf<double> bf, bu0, bu;  // per-batch f, u0, u of the bank loop (kept across calls)
   ~ts_faulted() { tsg::levels_free(levels); }
 };
 
@@ -94,6 +147,33 @@ ts_faulted* faulted_create(const Mesh& m, int32_t n_mat, const double* lam, cons
   F->s2.upload(s2);
   TS_CUDA(cudaDeviceSynchronize());
   return F.release();
+}
+
+// first containing element of each point (-1 = outside), device scan over the base mesh
+std::vector<int32_t> locate_points(ts_faulted& F, int32_t n, const double* points) {
+  const Mesh& m = F.base;
+  const int32_t E = m.n_elems(), V = m.vertex_count;
+  if (F.loc_tet4.size() != 4 * size_t(E)) {
+    std::vector<double> xyz(m.coords.begin(), m.coords.begin() + 3 * size_t(V));
+    std::vector<int32_t> t4(4 * size_t(E));
+    for (int32_t e = 0; e < E; ++e)
+      for (int a = 0; a < 4; ++a) t4[4 * size_t(e) + a] = m.tets10[10 * size_t(e) + a];
+    F.loc_xyz.upload(xyz);
+    F.loc_tet4.upload(t4);
+  }
+  DevBuf<double> dp;
+  dp.upload(points, 3 * size_t(n));
+  DevBuf<int32_t> best(n);
+  std::vector<int32_t> h(n, INT32_MAX);
+  TS_CUDA(cudaMemcpy(best.get(), h.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (E > 0) {
+    k_locate<<<grid_for(E, 128), 128>>>(F.loc_xyz.get(), F.loc_tet4.get(), E, dp.get(), n, best.get());
+    TS_CUDA(cudaGetLastError());
+  }
+  TS_CUDA(cudaMemcpy(h.data(), best.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int32_t& x : h)
+    if (x == INT32_MAX) x = -1;
+  return h;
 }
 
 // delta (device [ns][3][W]) of W unit slips (slip_vectors, fault.hpp:347-361)
@@ -218,17 +298,20 @@ ts_status ts_greens_bank(ts_faulted* fm, int32_t n_slips, const double* centers,
     if (cfg->batch_size < 1) tsg::validation("greens: batch size must be >= 1");
     if (n_obs < 1) tsg::validation("greens: no observation components");
     const int32_t N = fm->base.n_nodes();
-    // locate every observation once (the reference re-scans per column; same element, same values)
+    // locate every observation once (the reference re-scans per column; same element, same
+    // values): first containing element by a device scan, tet10 shape values on the host
+    for (int32_t r = 0; r < n_obs; ++r)
+      if (axes[r] < 0 || axes[r] > 2) tsg::validation("greens: observation axis must be 0..2");
+    const std::vector<int32_t> elem = tsg::locate_points(*fm, n_obs, points);
     std::vector<int32_t> nodes(10 * size_t(n_obs)), ax(n_obs);
     std::vector<double> sh(10 * size_t(n_obs));
     for (int32_t r = 0; r < n_obs; ++r) {
-      if (axes[r] < 0 || axes[r] > 2) tsg::validation("greens: observation axis must be 0..2");
-      int32_t e = -1;
       const tsg::V3 p = {points[3 * r], points[3 * r + 1], points[3 * r + 2]};
-      if (!tsg::locate_point(fm->base, p, &e, sh.data() + 10 * r))
+      if (elem[r] < 0)
         tsg::validation("observation point (" + std::to_string(p[0]) + ", " + std::to_string(p[1]) + ", " +
                         std::to_string(p[2]) + ") lies outside the mesh");
-      for (int a = 0; a < 10; ++a) nodes[10 * r + a] = fm->base.tets10[10 * size_t(e) + a];
+      tsg::tet10_shape_at(fm->base, elem[r], p, sh.data() + 10 * r);
+      for (int a = 0; a < 10; ++a) nodes[10 * r + a] = fm->base.tets10[10 * size_t(elem[r]) + a];
       ax[r] = axes[r];
     }
     tsg::DevBuf<int32_t> dn, da;
@@ -237,7 +320,8 @@ ts_status ts_greens_bank(ts_faulted* fm, int32_t n_slips, const double* centers,
     da.upload(ax);
     ds.upload(sh);
     const int32_t B = cfg->batch_size;
-    tsg::DevBuf<double> f(3 * size_t(N) * B), u0(3 * size_t(N) * B), u(3 * size_t(N) * B);
+    tsg::DevBuf<double>&f = fm->bf, &u0 = fm->bu0, &u = fm->bu;
+    for (tsg::DevBuf<double>* b : {&f, &u0, &u}) b->ensure(3 * size_t(N) * B);
     int32_t calls = 0;
     int64_t outer = 0;
     for (int32_t lo = 0; lo < n_slips; lo += B) {  // greens_batch_plan (greens.hpp:102-110)

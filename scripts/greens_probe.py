@@ -1,0 +1,28 @@
+import os, sys, time
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
+import numpy as np, torch
+import bench
+import paper_1710_08679_b200 as ts
+from paper_1710_08679_b200.greens import DIP, STRIKE, FaultedModel, find_plane_fault_faces
+cells = (82, 123, 41)
+ext, div, ifs = bench.mesh_spec(cells)
+h = bench.CELL_KM * 1e3
+xm = (cells[0] // 2) * h
+mesh = ts.generate_box_mesh(ext, div, ifs)
+lo = (xm, 4 * h, 4 * h); hi = (xm, (cells[1] - 4) * h, (cells[2] - 8) * h)
+faces = find_plane_fault_faces(mesh, 0, xm, lo, hi)
+cfg = ts.SolverConfig(batch_size=16)
+t = time.perf_counter()
+fm = FaultedModel(mesh, [ts.material_from_wavespeeds(*x) for x in bench.TWO_LAYER], faces, cfg)
+print("setup", time.perf_counter() - t)
+ny, nz = 6, 4
+ys = np.linspace(lo[1] + 0.15 * (hi[1] - lo[1]), hi[1] - 0.15 * (hi[1] - lo[1]), ny)
+zs = np.linspace(lo[2] + 0.2 * (hi[2] - lo[2]), hi[2] - 0.2 * (hi[2] - lo[2]), nz)
+centers = np.array([[xm, y, z] for y in ys for z in zs for _ in (DIP, STRIKE)])
+dirs = np.array([d for _ in ys for _ in zs for d in (DIP, STRIKE)], np.int32)
+radii = np.full(len(dirs), 0.6 * (hi[1] - lo[1]) / ny)
+pts = np.array([[0.5 * ext[0], 0.5 * ext[1], ext[2]]]); axes = np.array([2], np.int32)
+for rep in range(2):
+    torch.cuda.synchronize(); t = time.perf_counter()
+    bank, calls, outer = fm.greens_bank(centers, dirs, radii, pts, axes, cfg)
+    print("sweep", rep, round(time.perf_counter() - t, 3), calls, outer, flush=True)
