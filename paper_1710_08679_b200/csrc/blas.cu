@@ -539,6 +539,8 @@ __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* 
 #pragma unroll
     for (int k = 0; k < W; ++k) acc[i][k] = ACC(0);
   const int32_t e1 = __ldg(row_ptr + r + 1);
+  // unrolled so the loads of several blocks (index -> u gathers) are in flight together
+#pragma unroll 4
   for (int32_t e = __ldg(row_ptr + r); e < e1; ++e) {
     const float* blk = blocks + 9 * int64_t(e);
     float m[9];
