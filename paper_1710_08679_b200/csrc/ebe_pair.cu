@@ -182,14 +182,19 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         V ff[NPE][3];
         if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
         else tet4_product<V>(uu, b, lp, mp, ff);
+        if (ma == 0u) {  // (branch hoisted out of the row loop: one divergence region, not one per row)
 #pragma unroll
-        for (int k = 0; k < Geo::NA_OWN; ++k) {
-          const int a = Geo::a_own(k);
-          T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
-          if (ma == 0u) {
+          for (int k = 0; k < Geo::NA_OWN; ++k) {
+            const int a = Geo::a_own(k);
+            T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
 #pragma unroll
             for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(row + c * B), ff[a][c]);
-          } else {
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < Geo::NA_OWN; ++k) {
+            const int a = Geo::a_own(k);
+            T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
 #pragma unroll
             for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], (ma >> (3 * a + c)) & 1u);
           }
@@ -219,15 +224,18 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         for (int k = 0; k < Geo::NFACE; ++k)
 #pragma unroll
           for (int c = 0; c < 3; ++c) ff[Geo::b_face(k)][c] = O::add(ff[Geo::b_face(k)][c], carry[k][c]);
-        const bool interior = ma == 0u && mb == unsigned(kHasB);
+        if (ma == 0u && mb == unsigned(kHasB)) {
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) {
-          const int r = Geo::b_row(a);
-          T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[r])) * B + col;
-          if (interior) {
+          for (int a = 0; a < NPE; ++a) {
+            T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[Geo::b_row(a)])) * B + col;
 #pragma unroll
             for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(row + c * B), ff[a][c]);
-          } else {
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < NPE; ++a) {
+            const int r = Geo::b_row(a);
+            T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[r])) * B + col;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               const unsigned m = r < NPE ? (ma >> (3 * r + c)) & 1u : (mb >> (3 * (r - NPE) + c)) & 1u;
