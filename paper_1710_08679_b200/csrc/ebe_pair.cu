@@ -134,10 +134,8 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
           for (int c = 0; c < 3; ++c) cpa(dst + (a * 3 + c) * NT, row + c * B, int(sizeof(V)), sizeof(V));
         }
       } else {
-        const int nrows = (mb & unsigned(kHasB)) ? NR : NPE;
 #pragma unroll
         for (int a = 0; a < NR; ++a) {
-          if (a >= nrows) break;
           const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
@@ -165,7 +163,6 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
       const int32_t* w = nbuf + (s * GROUPS + grp) * kPairWords;
       const V* src = ubuf + s * NIN * NT + threadIdx.x;
       const unsigned ma = static_cast<unsigned>(w[MW]), mb = static_cast<unsigned>(w[MW + 1]);
-      const bool hasB = (mb & unsigned(kHasB)) != 0;
       V carry[Geo::NFACE][3];  // A's face rows (= B's face rows)
       {
         V b[3][3];
@@ -204,7 +201,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 #pragma unroll
           for (int c = 0; c < 3; ++c) carry[k][c] = ff[Geo::a_face(k)][c];
       }
-      if (hasB) {
+      {  // B (a null B for unpaired A: zero record, own rows masked)
         const T* cfb = cf + 12;
         V b[3][3];
 #pragma unroll
@@ -242,14 +239,6 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
               red_p(reinterpret_cast<V*>(row + c * B), ff[a][c], m);
             }
           }
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < Geo::NFACE; ++k) {
-          const int a = Geo::a_face(k);
-          T* row = f + static_cast<size_t>(static_cast<uint32_t>(w[a])) * B + col;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(row + c * B), carry[k][c], (ma >> (3 * a + c)) & 1u);
         }
       }
     }
@@ -519,7 +508,6 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_wor
         const int as = npe == 10 ? PairGeo<10>::a_face(q) : PairGeo<4>::a_face(q);
         if (slot_node(b, pb, bs).first * 3 != w[as]) bad = true;
       }
-      mb |= uint32_t(kHasB);
       bad = bad || !record(a, pa, cf) || !record(b, pb, cf + 12 * ts);
     } else {
       for (int s = 0; s < npe; ++s) {
@@ -527,12 +515,15 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_wor
         w[s] = 3 * nd;
         ma |= mk << (3 * s);
       }
-      for (int s = npe; s < NR; ++s) w[s] = 0;  // no B
+      // no face neighbour: a pair with a NULL B (zero record, own rows fully masked -> no gather, no
+      // reduction), so every unit takes the same code path; its face rows reduce through B's
+      for (int s = npe; s < NR; ++s) w[s] = 0;
       std::memset(cf + 12 * ts, 0, 12 * ts);
+      mb = (1u << (3 * (NR - npe))) - 1u;
       bad = bad || !record(a, pa, cf);
     }
     w[NR] = static_cast<int32_t>(ma);
-    w[NR + 1] = static_cast<int32_t>(mb);
+    w[NR + 1] = static_cast<int32_t>(mb | uint32_t(kHasB));
     for (int s = NR + 2; s < kPairWords; ++s) w[s] = 0;
   }
   if (bad) validation("pair plan: inconsistent face pairing or degenerate element");

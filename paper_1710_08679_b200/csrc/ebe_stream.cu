@@ -74,9 +74,10 @@ std::unique_ptr<EbeStreamPlan> build_stream_plan(const ts_ebe& op) {
   for (int k = 0; k < K; ++k)
     for (int32_t i = P->unit_ptr[k]; i < P->unit_ptr[k + 1]; ++i) {
       const int32_t* w = pc.data() + size_t(i) * W;
-      const bool hasB = (static_cast<uint32_t>(w[NR + 1]) >> 31) != 0;
-      const int rows = hasB ? NR : npe;
-      for (int r = 0; r < rows; ++r) {
+      const uint32_t ma = static_cast<uint32_t>(w[NR]), mb = static_cast<uint32_t>(w[NR + 1]);
+      for (int r = 0; r < NR; ++r) {
+        const uint32_t bits = r < npe ? (ma >> (3 * r)) & 7u : (mb >> (3 * (r - npe))) & 7u;
+        if (bits == 7u) continue;  // row neither gathered nor reduced (e.g. a null B's own rows)
         const int32_t n = w[r] / 3;
         first[n] = std::min(first[n], k);
         last[n] = k;  // chunks are visited in order
