@@ -152,9 +152,10 @@ __global__ void __launch_bounds__(kRedThreads) k_dot2(const T* __restrict__ x0, 
   }
 }
 
-__global__ void __launch_bounds__(kFinThreads) k_sum_partials(const double* partial, int nd, int32_t B, double* out) {
+__global__ void __launch_bounds__(kFinThreads) k_sum_partials(const double* partial, int nd, int32_t B, int nblk,
+                                                              double* out) {
   __shared__ double tot[kFinThreads], scr[kFinThreads];
-  block_totals(partial, nd, B, kRedBlocks, tot, scr);
+  block_totals(partial, nd, B, nblk, tot, scr);
   const int t = threadIdx.x;
   if (t < nd * B) out[t] = tot[t];
 }
@@ -669,8 +670,8 @@ struct Partials {
   int nblk;
 };
 Partials finish_partials(Workspace& ws, int nd, int32_t B, cudaStream_t s) {
-  if (!ws.comm) return {ws.partial.get(), kRedBlocks};
-  k_sum_partials<<<1, kFinThreads, 0, s>>>(ws.partial.get(), nd, B, ws.summed.get());
+  if (!ws.comm) return {ws.partial.get(), ws.nblk};
+  k_sum_partials<<<1, kFinThreads, 0, s>>>(ws.partial.get(), nd, B, ws.nblk, ws.summed.get());
   TS_CUDA_LAUNCH();
   ws.comm->allreduce_sum(ws.summed.get(), size_t(nd) * B, s);
   return {ws.summed.get(), 1};
@@ -678,6 +679,14 @@ Partials finish_partials(Workspace& ws, int nd, int32_t B, cudaStream_t s) {
 
 void check_batch(int32_t B) {
   if (B < 1 || B > kRedThreads) validation("batch must be in [1, 256]");
+}
+
+// Reduction grid for `len` entries: up to kRedBlocks (8 per SM) for the big levels, fewer for small
+// vectors so the one-block finalize sums fewer partials. A function of len only: the block ranges,
+// and so the summation order, are the same every call.
+int red_grid(int64_t len) {
+  const int64_t g = len / (int64_t(kRedThreads) * 32);
+  return static_cast<int>(std::max<int64_t>(kRedMinBlocks, std::min<int64_t>(kRedBlocks, g)));
 }
 
 }  // namespace
@@ -699,10 +708,11 @@ void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int3
           Workspace& ws, cudaStream_t s) {
   check_batch(batch);
   ws.ensure(batch);
-  TS_WIDTH_DISPATCH(T, batch, (k_dot2<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch,
-                                                                          ws.partial.get(), ws.owned)));
+  ws.nblk = red_grid(ndof * batch);
+  TS_WIDTH_DISPATCH(T, batch, (k_dot2<T, W><<<ws.nblk, kRedThreads, 0, s>>>(x0, y0, x1, y1, ndof * batch, batch,
+                                                                       ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
-  k_sum_partials<<<1, kFinThreads, 0, s>>>(ws.partial.get(), x1 ? 2 : 1, batch, out);
+  k_sum_partials<<<1, kFinThreads, 0, s>>>(ws.partial.get(), x1 ? 2 : 1, batch, ws.nblk, out);
   TS_CUDA_LAUNCH();
   if (ws.comm) ws.comm->allreduce_sum(out, size_t(x1 ? 2 : 1) * batch, s);
 }
@@ -731,7 +741,8 @@ void pcg_direction(const T* inv, const T* e, T* p, int32_t n, int32_t B, bool fi
 template <typename T>
 void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                cudaStream_t s) {
-  TS_WIDTH_DISPATCH(T, B, (k_gamma<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B,
+  ws.nblk = red_grid(3 * int64_t(n) * B);
+  TS_WIDTH_DISPATCH(T, B, (k_gamma<T, W><<<ws.nblk, kRedThreads, 0, s>>>(p, q, 3 * int64_t(n) * B, B,
                                                                           ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 3, B, s);
@@ -743,7 +754,8 @@ void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& c
 template <typename T>
 void pcg_update(const T* inv, T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs,
                 Workspace& ws, cudaStream_t s) {
-  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(inv, e, u, p, q, n, B,
+  ws.nblk = red_grid(int64_t(n) * B);
+  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<ws.nblk, kRedThreads, 0, s>>>(inv, e, u, p, q, n, B,
                                                                            cs[ColScalars::ALPHA], ws.status.get(),
                                                                            ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
@@ -759,7 +771,8 @@ void pcg_update(const T* inv, T* e, T* u, const T* p, const T* q, int32_t n, int
 template <typename T>
 void pcg_init(const T* inv, const T* r, T* e, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
               cudaStream_t s) {
-  TS_WIDTH_DISPATCH(T, B, (k_init<T, W><<<kRedBlocks, kRedThreads, 0, s>>>(inv, r, e, n, B, ws.partial.get(),
+  ws.nblk = red_grid(int64_t(n) * B);
+  TS_WIDTH_DISPATCH(T, B, (k_init<T, W><<<ws.nblk, kRedThreads, 0, s>>>(inv, r, e, n, B, ws.partial.get(),
                                                                          ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 3, B, s);
@@ -791,7 +804,8 @@ INST(double)
 
 void cg_true_residual(const double* f, double* r, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
                       cudaStream_t s) {
-  TS_WIDTH_DISPATCH(double, B, (k_true_res<W><<<kRedBlocks, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B,
+  ws.nblk = red_grid(3 * int64_t(n) * B);
+  TS_WIDTH_DISPATCH(double, B, (k_true_res<W><<<ws.nblk, kRedThreads, 0, s>>>(f, r, 3 * int64_t(n) * B, B,
                                                                                ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);
@@ -803,7 +817,8 @@ void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_
                   const ColScalars& cs, Workspace& ws, cudaStream_t s) {
   const int64_t len = 3 * int64_t(n) * B;
   if (!first) {
-    TS_WIDTH_DISPATCH(double, B, (k_dot2<double, W><<<kRedBlocks, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B,
+    ws.nblk = red_grid(len);
+    TS_WIDTH_DISPATCH(double, B, (k_dot2<double, W><<<ws.nblk, kRedThreads, 0, s>>>(z, q, nullptr, nullptr, len, B,
                                                                                      ws.partial.get(), ws.owned)));
     TS_CUDA_LAUNCH();
     const Partials pp = finish_partials(ws, 1, B, s);
@@ -816,7 +831,8 @@ void cg_direction(const double* z, const double* q, double* p, int32_t n, int32_
 
 void cg_alpha(const double* z, const double* r, const double* p, const double* q, int32_t n, int32_t B,
               const ColScalars& cs, Workspace& ws, cudaStream_t s) {
-  TS_WIDTH_DISPATCH(double, B, (k_dot2<double, W><<<kRedBlocks, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B,
+  ws.nblk = red_grid(3 * int64_t(n) * B);
+  TS_WIDTH_DISPATCH(double, B, (k_dot2<double, W><<<ws.nblk, kRedThreads, 0, s>>>(z, r, p, q, 3 * int64_t(n) * B, B,
                                                                                    ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 2, B, s);
@@ -827,7 +843,8 @@ void cg_alpha(const double* z, const double* r, const double* p, const double* q
 
 void cg_update(double* r, double* u, const double* p, const double* q, int32_t n, int32_t B, const ColScalars& cs,
                Workspace& ws, cudaStream_t s) {
-  TS_WIDTH_DISPATCH(double, B, (k_cg_update<W><<<kRedBlocks, kRedThreads, 0, s>>>(r, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
+  ws.nblk = red_grid(3 * int64_t(n) * B);
+  TS_WIDTH_DISPATCH(double, B, (k_cg_update<W><<<ws.nblk, kRedThreads, 0, s>>>(r, u, p, q, 3 * int64_t(n) * B, B, cs[ColScalars::ALPHA],
                                                  ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
   const Partials pp = finish_partials(ws, 1, B, s);

@@ -7,7 +7,8 @@
 namespace tsg {
 
 // fixed reduction geometry: deterministic per-column fp64 sums
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedBlocks = 1184;   // reduction grid cap: 8 x 148 SMs (big levels)
+constexpr int kRedMinBlocks = 148; // floor: one block per SM (small levels; fewer partials to finalize)
 constexpr int kRedThreads = 256;
 
 // Per-column solver scalars living on the device (one array of `batch` each).
@@ -46,6 +47,7 @@ struct Workspace {
   // (M^-1 e, e) partials left by the last pcg_init / pcg_update (slot nd-1), consumed by pcg_rho
   const double* last_p = nullptr;
   int last_nblk = 0, last_nd = 0;
+  int nblk = kRedBlocks;  // grid of the last reduction launch (red_grid)
   void ensure(int32_t batch);
   ~Workspace();
 };
