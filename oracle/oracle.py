@@ -191,6 +191,11 @@ class Oracle:
         self._f("solve_pcge").argtypes = [vp, vp, vp, vp, C.c_int32, C.c_double, C.c_int32, vp]
         self._f("rng_sym").argtypes = [C.c_uint64, C.c_int64, vp]
         if kind == "reference":
+            # every pointer argument needs its argtypes: an undeclared handle would be passed as a 32-bit int
+            L.ref_fault_plane_faces.argtypes = [vp, C.c_int32, C.c_double, vp, vp, vp, vp]
+            L.ref_slip_to_rhs.argtypes = [vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]
+            L.ref_greens_bank.argtypes = [vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_int32, vp, vp,
+                                          vp, vp, vp, vp]
             L.ref_time_ebe_apply.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, C.c_int32, C.c_int32,
                                              C.c_int32, C.c_int32, C.c_int32, C.c_uint64, vp, vp]
             L.ref_hw_threads.restype = C.c_int
