@@ -116,6 +116,7 @@ struct ts_faulted {
   tsg::DevBuf<double> loc_xyz;    // base vertex coordinates (device point location)
   tsg::DevBuf<int32_t> loc_tet4;  // base element vertex ids
   tsg::DevBuf<double> bf, bu0, bu;  // per-batch f, u0, u of the bank loop (kept across calls)
+  tsg::DevBuf<double> sg, sw;       // split-mesh work vectors of slip_to_rhs (kept across calls)
   ~ts_faulted() { tsg::levels_free(levels); }
 };
 
@@ -198,9 +199,12 @@ void slips_to_rhs(ts_faulted& F, int32_t W, const double* centers, const int32_t
                   cudaStream_t s) {
   const int32_t ns = static_cast<int32_t>(F.patch.split_nodes.size());
   const int32_t NS = F.split.n_nodes(), N = F.base.n_nodes();
-  DevBuf<double> d, g(3 * size_t(NS) * W), w(3 * size_t(NS) * W);
+  DevBuf<double> d;
+  DevBuf<double>&g = F.sg, &w = F.sw;  // split-mesh slip jumps / products, kept across calls
+  g.ensure(3 * size_t(NS) * W);
+  w.ensure(3 * size_t(NS) * W);
   slip_deltas(F, W, centers, dirs, radii, d);
-  TS_CUDA(cudaMemsetAsync(g.get(), 0, g.size() * sizeof(double), s));
+  TS_CUDA(cudaMemsetAsync(g.get(), 0, 3 * size_t(NS) * W * sizeof(double), s));
   k_slip_jump<<<grid_for(int64_t(ns) * 3 * W, 256), 256, 0, s>>>(F.plus.get(), F.minus.get(), ns, W, d.get(), g.get());
   TS_CUDA_LAUNCH();
   ebe_apply(*F.split_raw, g.get(), w.get(), W, s);

@@ -21,8 +21,15 @@ zs = np.linspace(lo[2] + 0.2 * (hi[2] - lo[2]), hi[2] - 0.2 * (hi[2] - lo[2]), n
 centers = np.array([[xm, y, z] for y in ys for z in zs for _ in (DIP, STRIKE)])
 dirs = np.array([d for _ in ys for _ in zs for d in (DIP, STRIKE)], np.int32)
 radii = np.full(len(dirs), 0.6 * (hi[1] - lo[1]) / ny)
-pts = np.array([[0.5 * ext[0], 0.5 * ext[1], ext[2]]]); axes = np.array([2], np.int32)
-for rep in range(2):
-    torch.cuda.synchronize(); t = time.perf_counter()
-    bank, calls, outer = fm.greens_bank(centers, dirs, radii, pts, axes, cfg)
-    print("sweep", rep, round(time.perf_counter() - t, 3), calls, outer, flush=True)
+gx, gy = np.meshgrid(np.linspace(0.1, 0.9, 10) * ext[0], np.linspace(0.1, 0.9, 10) * ext[1])
+pts100 = np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, ext[2])], 1); axes100 = (np.arange(100) % 3).astype(np.int32)
+pts1 = pts100[:1]; axes1 = axes100[:1]
+for label, pts, axes, sampler in (("1pt", pts1, axes1, False), ("100pt", pts100, axes100, False), ("100pt+clk", pts100, axes100, True)):
+    for rep in range(2):
+        ctx = bench.ClockSampler(0) if sampler else None
+        if ctx: ctx.__enter__()
+        torch.cuda.synchronize(); t = time.perf_counter()
+        bank, calls, outer = fm.greens_bank(centers, dirs, radii, pts, axes, cfg)
+        dt = time.perf_counter() - t
+        if ctx: ctx.__exit__(None, None, None)
+        print("sweep", label, rep, round(dt, 3), calls, outer, flush=True)

@@ -192,17 +192,20 @@ def test_ebe_many_chunks_per_block(checker, monkeypatch, kernel, prec, batch, or
     assert np.array_equal(got[mask == 1], u[mask == 1])
 
 
+@pytest.mark.parametrize("order", [2, 1])
 @pytest.mark.parametrize("prec", [32, 64])
 @pytest.mark.parametrize("batch", [1, 4, 16, 3])
-def test_host_apply_streams_and_matches_device(prec, batch):
+def test_host_apply_streams_and_matches_device(order, prec, batch):
     """ts_ebe_apply_host with pinned buffers overlaps H2D / sweep / D2H chunk by
     chunk (ebe_stream.cu): same f as the device apply, every row copied back;
     batch 3 (no pair kernel) and pageable buffers take copy-apply-copy."""
-    mesh = ts.generate_box_mesh((4000.0, 4000.0, 2000.0), (40, 40, 20), (1200.0,))
-    op = ts.EbeOperator(mesh, 2, mats(TWO_LAYER), mesh.dirichlet_mask(), prec=prec)
+    cells = (40, 40, 20) if order == 2 else (60, 60, 30)
+    mesh = ts.generate_box_mesh((4000.0, 4000.0, 2000.0), cells, (1200.0,))
+    nn = mesh.node_count() if order == 2 else mesh.vertex_count
+    op = ts.EbeOperator(mesh, order, mats(TWO_LAYER), mesh.dirichlet_mask()[: 3 * nn], prec=prec)
     dt = torch.float32 if prec == 32 else torch.float64
     g = torch.Generator(device="cuda").manual_seed(7)
-    u = torch.rand(3 * mesh.node_count(), batch, device="cuda", dtype=dt, generator=g) * 2 - 1
+    u = torch.rand(3 * nn, batch, device="cuda", dtype=dt, generator=g) * 2 - 1
     f_dev = op.apply(u)
     uh = torch.empty(u.shape, dtype=dt, pin_memory=True)
     uh.copy_(u.cpu())
@@ -213,7 +216,7 @@ def test_host_apply_streams_and_matches_device(prec, batch):
     assert torch.isfinite(got).all()
     rel = float((got.double() - f_dev.double()).norm() / f_dev.double().norm())
     assert rel <= (1e-6 if prec == 32 else 1e-14)
-    mask = torch.from_numpy(mesh.dirichlet_mask().astype(bool)).cuda()
+    mask = torch.from_numpy(mesh.dirichlet_mask()[: 3 * nn].astype(bool)).cuda()
     assert torch.equal(got[mask], u[mask])  # identity rows exact
     # pageable buffers: copy-apply-copy, same answer
     fp = op.apply(u.cpu().numpy())
