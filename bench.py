@@ -308,6 +308,20 @@ def solve_leg(args, ts, torch, world, rank, local):
     return out
 
 
+class stdout_to_stderr:
+    """Route the process's C-level stdout (fd 1) to stderr for the block."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 # -------------------------------------------------- N > 1: partitioned matvec
 def main_partitioned(args, world, rank, local):
     """N GPUs: ONE mesh of N configs[1] slabs (82 x 123N x 41 cells) split by
@@ -322,13 +336,30 @@ def main_partitioned(args, world, rank, local):
     import paper_1710_08679_b200 as ts
     from paper_1710_08679_b200.dist import Comm, DistEbeOperator, partition_rcb
 
+    # pre-flight of our own NCCL communicator (all ranks agree through torch.distributed before any
+    # partitioned work): on failure every rank falls back to independent replicas
+    err = ""
+    try:
+        with stdout_to_stderr():  # NCCL prints its version banner on stdout; the JSON line must be alone there
+            comm = Comm.nccl_from_torch(local)
+        probe = comm.allreduce_sum(torch.ones(4, dtype=torch.float64, device="cuda"))
+        torch.cuda.synchronize()
+        if not bool((probe == world).all()):
+            err = f"all-reduce self-test returned {probe.tolist()}"
+    except Exception as exc:  # noqa: BLE001
+        err = f"{type(exc).__name__}: {exc}"
+    bad = torch.tensor([1.0 if err else 0.0], device="cuda")
+    dist.all_reduce(bad)
+    if bad.item() > 0:
+        log(f"[rank {rank}] partitioned path unavailable ({err or 'another rank failed'}); running replicas")
+        return f"partitioned path unavailable: {err or 'another rank failed'}"
+
     cells = (args.cells[0], args.cells[1] * world, args.cells[2])
     ext, div, ifs = mesh_spec(cells)
     t0 = time.time()
     mesh = ts.generate_box_mesh(ext, div, ifs)
     mats = [ts.material_from_wavespeeds(*t) for t in TWO_LAYER]
     part = partition_rcb(mesh, world)
-    comm = Comm.nccl_from_torch(local)
     op = DistEbeOperator(mesh, 2, mats, part, comm, prec=args.prec)
     del mesh
     E, N = op.n_elements, op.n_local
@@ -517,9 +548,13 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
         if not args.replicas:
-            return main_partitioned(args, world, rank, local)
+            fallback = main_partitioned(args, world, rank, local)
+            if fallback is None:
+                return None
+            args.partitioned_fallback = fallback
 
     cells = tuple(args.cells)
     ext, div, ifs = mesh_spec(cells)
@@ -677,6 +712,8 @@ def main():
             "solve": solve,
             "greens": greens,
         }
+        if getattr(args, "partitioned_fallback", None):
+            out["partitioned_fallback"] = args.partitioned_fallback
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -239,6 +239,9 @@ void ts_thread_world_destroy(ts_thread_world* w);
 ts_status ts_comm_create_thread(ts_thread_world* w, int32_t rank, int32_t device, ts_comm** out);
 void ts_comm_destroy(ts_comm* c);
 ts_status ts_comm_info(const ts_comm* c, int32_t* rank, int32_t* size, int32_t* device);
+/* in-place sum over the ranks of a DEVICE fp64 array (the dot-product all-reduce
+ * of the partitioned solve); enqueued on `stream` */
+ts_status ts_comm_allreduce_sum(const ts_comm* c, double* data, int64_t n, void* stream);
 
 /* recursive coordinate bisection of element centroids: part[E] in [0, nparts) */
 ts_status ts_partition_rcb(const ts_mesh* mesh, int32_t nparts, int32_t* part);

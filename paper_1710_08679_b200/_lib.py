@@ -115,6 +115,7 @@ _sig = {
     "ts_comm_create_thread": (C.c_int, [vp, i32, i32, vp]),
     "ts_comm_destroy": (None, [vp]),
     "ts_comm_info": (C.c_int, [vp, vp, vp, vp]),
+    "ts_comm_allreduce_sum": (C.c_int, [vp, vp, C.c_int64, vp]),
     "ts_partition_rcb": (C.c_int, [vp, i32, vp]),
     "ts_dist_plan_sizes": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "ts_dist_plan_export": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),

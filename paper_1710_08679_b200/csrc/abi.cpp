@@ -383,6 +383,13 @@ ts_status ts_comm_info(const ts_comm* c, int32_t* rank, int32_t* size, int32_t* 
   TS_API_END
 }
 
+ts_status ts_comm_allreduce_sum(const ts_comm* c, double* data, int64_t n, void* stream) {
+  TS_API_BEGIN
+  TS_REQUIRE(c && (data || n == 0) && n >= 0, "comm allreduce: bad argument");
+  if (n > 0) c->c->allreduce_sum(data, static_cast<size_t>(n), static_cast<cudaStream_t>(stream));
+  TS_API_END
+}
+
 ts_status ts_partition_rcb(const ts_mesh* mesh, int32_t nparts, int32_t* part) {
   TS_API_BEGIN
   TS_REQUIRE(mesh && part, "partition: null argument");

@@ -55,6 +55,16 @@ class Comm:
         _ck(lib.ts_comm_create_thread(world._h, int(rank), int(device), C.byref(h)))
         return cls(h, keep=world)
 
+    def allreduce_sum(self, t):
+        """In-place sum over the ranks of a CUDA float64 tensor (on the current stream)."""
+        import torch
+
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError("allreduce_sum: expected a contiguous CUDA float64 tensor")
+        _ck(lib.ts_comm_allreduce_sum(self._h, C.c_void_p(t.data_ptr()), t.numel(),
+                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return t
+
     @staticmethod
     def nccl_available() -> tuple[bool, str]:
         buf = C.create_string_buffer(256)
