@@ -171,3 +171,25 @@ def test_nccl_single_rank_solve_matches_single_device():
     u, rep = dl.solve(f, np.zeros_like(f), cfg)
     assert rep.outer_iterations == rep1.outer_iterations
     assert rel(u, u1) <= 1e-9
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_comm_allreduce_sum(P):
+    """ts_comm_allreduce_sum (the partitioned solve's dot-product all-reduce) over in-process ranks,
+    and over a one-rank NCCL communicator."""
+    def fn(rank, comm):
+        t = torch.arange(5, dtype=torch.float64, device="cuda") * (rank + 1)
+        comm.allreduce_sum(t)
+        torch.cuda.synchronize()
+        return t.cpu().numpy()
+
+    out = run_ranks(P, fn)
+    want = np.arange(5, dtype=np.float64) * sum(range(1, P + 1))
+    for o in out:
+        assert np.array_equal(o, want)
+    ok, _ = Comm.nccl_available()
+    if ok and P == 1:
+        comm = Comm.nccl(1, 0, Comm.nccl_id(), 0)
+        t = torch.full((7,), 2.5, dtype=torch.float64, device="cuda")
+        comm.allreduce_sum(t)
+        assert torch.equal(t.cpu(), torch.full((7,), 2.5, dtype=torch.float64))
