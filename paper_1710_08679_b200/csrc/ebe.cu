@@ -19,6 +19,7 @@
 //  * f starts as the masked identity (ebe_operator.hpp:96-110) and element
 //    contributions land through fire-and-forget vector REDs in L2.
 #include <algorithm>
+#include <climits>
 #include <parallel/algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -657,7 +658,7 @@ int ebe_slab_count() {
 
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda, const double* mu,
                    const uint8_t* dof_mask, int prec, const uint8_t* elem_group, int kernel_override,
-                   std::vector<int32_t>* element_order) {
+                   std::vector<int32_t>* element_order, PairTopology* pair_topology) {
   if (order != 1 && order != 2) validation("ebe: order must be 1 or 2");
   if (prec != 32 && prec != 64) validation("ebe: precision must be 32 or 64");
   require_device();
@@ -676,7 +677,21 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   const size_t E = static_cast<size_t>(op->n_elems);
   if (dof_mask) op->host_mask.assign(dof_mask, dof_mask + 3 * static_cast<size_t>(op->n_nodes));
   auto rnd = [prec](double x) { return prec == 32 ? static_cast<double>(static_cast<float>(x)) : x; };
-  for (size_t e = 0; e < E; ++e) {  // validation first (exceptions stay out of the parallel loop)
+  // validation first (exceptions stay out of the parallel loops): find the first bad element in
+  // parallel, then report it exactly as a sequential scan would
+  int64_t first_bad = INT64_MAX;
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
+  for (int64_t e = 0; e < int64_t(E); ++e) {
+    const int32_t mid = m.material_id[e];
+    bool bad = mid < 0 || mid >= n_mat;
+    for (int a = 0; a < npe; ++a) {
+      const int32_t node = m.tets10[10 * e + a];
+      bad |= node < 0 || node >= op->n_nodes;
+    }
+    if (bad) first_bad = std::min(first_bad, e);
+  }
+  if (first_bad != INT64_MAX) {
+    const size_t e = static_cast<size_t>(first_bad);
     const int32_t mid = m.material_id[e];
     if (mid < 0 || mid >= n_mat)
       validation("ebe: element " + std::to_string(e) + " references material " + std::to_string(mid) +
@@ -835,7 +850,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   // common batch widths and the element-parallel sweeps the rest)
   if (op->kernel == 5) build_tile_plan(*op, conn, cs);
   setup_mark("ebe: tile plan");
-  if (op->kernel == 7 || op->kernel == 6) build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32);
+  if (op->kernel == 7 || op->kernel == 6) build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32, pair_topology);
   setup_mark("ebe: pair plan");
   op->conn.upload(conn);
   op->coef.upload(coef);

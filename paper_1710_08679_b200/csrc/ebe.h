@@ -109,12 +109,23 @@ void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cud
 void build_tile_plan(ts_ebe& op, const HostVec<int32_t>& conn_words, int conn_stride);
 // pair sweep (ebe_pair.cu); false when no instance covers this batch width
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
+// face-pair topology of an element order (greedy matching result), shareable between the
+// level set's tet10 operators, which use the same mesh and element order
+struct PairTopology {
+  int64_t n_elems = -1;
+  int32_t group_split = -1;
+  std::vector<int32_t> mate;
+  std::vector<int8_t> mate_k;
+  std::vector<int32_t> units;
+  int32_t split = 0;
+};
 void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_words, int cs,
-                     const HostVec<double>& coef64, bool fp32);
+                     const HostVec<double>& coef64, bool fp32, PairTopology* topo = nullptr);
 // elem_group (nullable, [E] in {0,1}): group-0 elements sweep separately (boundary first);
 // kernel_override >= 0 fixes the sweep kernel (and so which plans are built);
 // element_order (nullable): empty -> receives the Morton order, filled -> reused
 ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda,
                    const double* mu, const uint8_t* dof_mask, int prec, const uint8_t* elem_group = nullptr,
-                   int kernel_override = -1, std::vector<int32_t>* element_order = nullptr);
+                   int kernel_override = -1, std::vector<int32_t>* element_order = nullptr,
+                   PairTopology* pair_topology = nullptr);
 }  // namespace tsg

@@ -337,7 +337,7 @@ bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batc
 //   conn_words: Morton-ordered [E][cs] node | mask << 28; coef64: Morton-ordered
 //   [E][12] fp64 (b rows, lambda V, mu V, V); vrnd: T-rounded vertex coordinates.
 void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_words, int cs,
-                     const HostVec<double>& coef64, bool fp32) {
+                     const HostVec<double>& coef64, bool fp32, PairTopology* topo) {
   const int npe = op.npe;
   const int NR = npe == 10 ? PairGeo<10>::NR : PairGeo<4>::NR;
   const int kPairWords = npe == 10 ? PairGeo<10>::WORDS : PairGeo<4>::WORDS;
@@ -350,82 +350,101 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_wor
       if ((ev[k][0] == p && ev[k][1] == q) || (ev[k][0] == q && ev[k][1] == p)) return 4 + k;
     return -1;
   };
-  // face adjacency through the vertex -> element incidence: the element across
-  // face k (opposite local vertex k) is the other element containing its 3 vertices
-  // (parallel counting sort; the order inside a vertex's list does not matter:
-  // the element across a face is unique)
-  int32_t nv = 0;
-#pragma omp parallel for schedule(static) reduction(max : nv)
-  for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) nv = std::max(nv, node(e, a) + 1);
-  std::vector<int32_t> vptr(size_t(nv) + 1, 0);
-  HostVec<int32_t> velem(size_t(E) * 4);
-#pragma omp parallel for schedule(static)
-  for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) __atomic_fetch_add(&vptr[node(e, a) + 1], 1, __ATOMIC_RELAXED);
-  for (int32_t v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
-  {
-    std::vector<int32_t> cur(vptr.begin(), vptr.end() - 1);
-#pragma omp parallel for schedule(static)
-    for (int64_t e = 0; e < E; ++e)
-      for (int a = 0; a < 4; ++a)
-        velem[__atomic_fetch_add(&cur[node(e, a)], 1, __ATOMIC_RELAXED)] = static_cast<int32_t>(e);
-  }
-  HostVec<std::array<int32_t, 4>> nbr(E);
-#pragma omp parallel for schedule(static)
-  for (int64_t e = 0; e < E; ++e)
-    for (int k = 0; k < 4; ++k) {
-      int32_t f3[3], n = 0;
-      for (int a = 0; a < 4; ++a)
-        if (a != k) f3[n++] = node(e, a);
-      int32_t found = -1;
-      for (int32_t p = vptr[f3[0]]; p < vptr[f3[0] + 1] && found < 0; ++p) {
-        const int32_t j = velem[p];
-        if (j == e) continue;
-        int hits = 0;
-        for (int a = 0; a < 4; ++a) {
-          const int32_t x = node(j, a);
-          hits += (x == f3[1]) + (x == f3[2]);
-        }
-        if (hits == 2) found = j;
-      }
-      nbr[e][k] = found;
-    }
-  setup_mark("pair: face adjacency");
-  auto group_of = [&](int64_t e) { return e < op.group_split ? 0 : 1; };
-  std::vector<int32_t> mate(E, -1);
-  std::vector<int8_t> mate_k(E, -1);
-  for (int64_t e = 0; e < E; ++e) {
-    if (mate[e] >= 0) continue;
-    int best = -1;
-    int64_t bd = 0;
-    for (int k = 0; k < 4; ++k) {
-      const int32_t j = nbr[e][k];
-      if (j < 0 || j == e || mate[j] >= 0 || group_of(j) != group_of(e)) continue;
-      const int64_t d = std::llabs(int64_t(j) - e);
-      if (best < 0 || d < bd) {
-        best = k;
-        bd = d;
-      }
-    }
-    if (best >= 0) {
-      const int32_t j = nbr[e][best];
-      mate[e] = j;
-      mate[j] = static_cast<int32_t>(e);
-      mate_k[e] = static_cast<int8_t>(best);
-    }
-  }
-  // units in element order (a pair sits at its lower element, singles in place),
-  // so consecutive unit ranges stay spatially compact (ebe_stream.cu chunks them)
+  std::vector<int32_t> mate;
+  std::vector<int8_t> mate_k;
   std::vector<int32_t> units;  // leader element; singles encoded as ~e
   int32_t split = 0;
-  for (int g = 0; g < 2; ++g) {
-    const int64_t lo = g == 0 ? 0 : op.group_split, hi = g == 0 ? op.group_split : E;
-    for (int64_t e = lo; e < hi; ++e) {
-      if (mate[e] > e) units.push_back(static_cast<int32_t>(e));
-      else if (mate[e] < 0) units.push_back(~static_cast<int32_t>(e));
+  if (topo && topo->n_elems == E && topo->group_split == op.group_split && !topo->units.empty()) {
+    // the level set's other tet10 operator: same mesh, same element order -> same pairs
+    mate = topo->mate;
+    mate_k = topo->mate_k;
+    units = topo->units;
+    split = topo->split;
+  } else {
+    // face adjacency through the vertex -> element incidence: the element across
+    // face k (opposite local vertex k) is the other element containing its 3 vertices
+    // (parallel counting sort; the order inside a vertex's list does not matter:
+    // the element across a face is unique)
+    int32_t nv = 0;
+#pragma omp parallel for schedule(static) reduction(max : nv)
+    for (int64_t e = 0; e < E; ++e)
+      for (int a = 0; a < 4; ++a) nv = std::max(nv, node(e, a) + 1);
+    std::vector<int32_t> vptr(size_t(nv) + 1, 0);
+    HostVec<int32_t> velem(size_t(E) * 4);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e)
+      for (int a = 0; a < 4; ++a) __atomic_fetch_add(&vptr[node(e, a) + 1], 1, __ATOMIC_RELAXED);
+    for (int32_t v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
+    {
+      std::vector<int32_t> cur(vptr.begin(), vptr.end() - 1);
+#pragma omp parallel for schedule(static)
+      for (int64_t e = 0; e < E; ++e)
+        for (int a = 0; a < 4; ++a)
+          velem[__atomic_fetch_add(&cur[node(e, a)], 1, __ATOMIC_RELAXED)] = static_cast<int32_t>(e);
     }
-    if (g == 0) split = static_cast<int32_t>(units.size());
+    HostVec<std::array<int32_t, 4>> nbr(E);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e)
+      for (int k = 0; k < 4; ++k) {
+        int32_t f3[3], n = 0;
+        for (int a = 0; a < 4; ++a)
+          if (a != k) f3[n++] = node(e, a);
+        int32_t found = -1;
+        for (int32_t p = vptr[f3[0]]; p < vptr[f3[0] + 1] && found < 0; ++p) {
+          const int32_t j = velem[p];
+          if (j == e) continue;
+          int hits = 0;
+          for (int a = 0; a < 4; ++a) {
+            const int32_t x = node(j, a);
+            hits += (x == f3[1]) + (x == f3[2]);
+          }
+          if (hits == 2) found = j;
+        }
+        nbr[e][k] = found;
+      }
+    setup_mark("pair: face adjacency");
+    auto group_of = [&](int64_t e) { return e < op.group_split ? 0 : 1; };
+    mate.assign(E, -1);
+    mate_k.assign(E, -1);
+    for (int64_t e = 0; e < E; ++e) {
+      if (mate[e] >= 0) continue;
+      int best = -1;
+      int64_t bd = 0;
+      for (int k = 0; k < 4; ++k) {
+        const int32_t j = nbr[e][k];
+        if (j < 0 || j == e || mate[j] >= 0 || group_of(j) != group_of(e)) continue;
+        const int64_t d = std::llabs(int64_t(j) - e);
+        if (best < 0 || d < bd) {
+          best = k;
+          bd = d;
+        }
+      }
+      if (best >= 0) {
+        const int32_t j = nbr[e][best];
+        mate[e] = j;
+        mate[j] = static_cast<int32_t>(e);
+        mate_k[e] = static_cast<int8_t>(best);
+      }
+    }
+    // units in element order (a pair sits at its lower element, singles in place),
+    // so consecutive unit ranges stay spatially compact (ebe_stream.cu chunks them)
+    for (int g = 0; g < 2; ++g) {
+      const int64_t lo = g == 0 ? 0 : op.group_split, hi = g == 0 ? op.group_split : E;
+      for (int64_t e = lo; e < hi; ++e) {
+        if (mate[e] > e) units.push_back(static_cast<int32_t>(e));
+        else if (mate[e] < 0) units.push_back(~static_cast<int32_t>(e));
+      }
+      if (g == 0) split = static_cast<int32_t>(units.size());
+    }
+
+    if (topo) {
+      topo->n_elems = E;
+      topo->group_split = op.group_split;
+      topo->mate = mate;
+      topo->mate_k = mate_k;
+      topo->units = units;
+      topo->split = split;
+    }
   }
   setup_mark("pair: matching");
   const int32_t U = static_cast<int32_t>(units.size());

@@ -56,16 +56,22 @@ BcsrD assemble_tet4(const Mesh& m, const std::vector<double>& lam_e, const std::
   auto r32 = [](double x) { return static_cast<double>(static_cast<float>(x)); };
   const int32_t n = m.vertex_count;
   const int64_t E = m.n_elems();
-  // node -> elements CSR (counting sort; element order within a row kept ascending)
+  // node -> elements CSR: parallel counting sort, then each row's list sorted, so rows keep the
+  // ascending element order the reference's assembly sums in
   std::vector<int64_t> nptr(n + 1, 0);
+#pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) ++nptr[m.tets10[10 * e + a] + 1];
+    for (int a = 0; a < 4; ++a) __atomic_fetch_add(&nptr[m.tets10[10 * e + a] + 1], int64_t(1), __ATOMIC_RELAXED);
   for (int32_t i = 0; i < n; ++i) nptr[i + 1] += nptr[i];
   HostVec<int32_t> nel(nptr[n]);
   {
     std::vector<int64_t> cur(nptr.begin(), nptr.end() - 1);
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < E; ++e)
-      for (int a = 0; a < 4; ++a) nel[cur[m.tets10[10 * e + a]]++] = static_cast<int32_t>(e);
+      for (int a = 0; a < 4; ++a)
+        nel[__atomic_fetch_add(&cur[m.tets10[10 * e + a]], int64_t(1), __ATOMIC_RELAXED)] = static_cast<int32_t>(e);
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int32_t r = 0; r < n; ++r) std::sort(nel.begin() + nptr[r], nel.begin() + nptr[r + 1]);
   }
   setup_mark("assemble: incidence");
   BcsrD A;

@@ -8,6 +8,7 @@
 // kernels and reads one 24-byte status record per iteration (the reference's
 // convergence test is a host-side max over columns, pcg.hpp:71,116-117).
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <chrono>
 #include <cmath>
@@ -176,9 +177,10 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
     lv->l1_assembled = !(e && std::string(e) == "ebe");
   }
   std::vector<int32_t> eorder;  // one Morton element order for the three operators
-  lv->outer.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 64, nullptr, -1, &eorder));
+  PairTopology pairs;              // and one face-pair matching for the two tet10 operators
+  lv->outer.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 64, nullptr, -1, &eorder, &pairs));
   setup_mark("levels: outer operator");
-  lv->l0.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 32, nullptr, -1, &eorder));
+  lv->l0.reset(ebe_create(m, 2, n_mat, lam, mu, mask0.data(), 32, nullptr, -1, &eorder, &pairs));
   // with the assembled level 1 the tet4 EBE operator only serves the API and its
   // block-Jacobi diagonal: no sweep plans
   lv->l1.reset(ebe_create(m, 1, n_mat, lam, mu, mask1.data(), 32, nullptr, lv->l1_assembled ? 3 : -1, &eorder));
@@ -187,16 +189,30 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   {
     static constexpr int ee[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
     std::vector<int32_t> ends(2 * size_t(N - V), -1);
+    // parallel fill (an edge shared by several elements is written with the same endpoints by each);
+    // the first bad element, if any, is then reported as the sequential scan would
+    int32_t first_bad = INT32_MAX;
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
     for (int32_t e = 0; e < m.n_elems(); ++e) {
       const int32_t* t = m.tets10.data() + 10 * size_t(e);
       for (int q = 0; q < 6; ++q) {
         int32_t a = t[ee[q][0]], b = t[ee[q][1]];
         if (a > b) std::swap(a, b);
         const int32_t mid = t[4 + q];
+        if (mid < V || a >= V || b >= V) {
+          first_bad = std::min(first_bad, e);
+          break;
+        }
+        __atomic_store_n(&ends[2 * size_t(mid - V)], a, __ATOMIC_RELAXED);
+        __atomic_store_n(&ends[2 * size_t(mid - V) + 1], b, __ATOMIC_RELAXED);
+      }
+    }
+    if (first_bad != INT32_MAX) {
+      const int32_t* t = m.tets10.data() + 10 * size_t(first_bad);
+      for (int q = 0; q < 6; ++q) {
+        const int32_t a = t[ee[q][0]], b = t[ee[q][1]], mid = t[4 + q];
         if (mid < V) validation("geometric prolongation: edge node " + std::to_string(mid) + " is a vertex id");
         if (a >= V || b >= V) validation("geometric prolongation: edge endpoints must be vertices");
-        ends[2 * size_t(mid - V)] = a;
-        ends[2 * size_t(mid - V) + 1] = b;
       }
     }
     std::vector<int32_t> tptr(V + 1, 0);
