@@ -28,6 +28,11 @@ namespace {
 
 constexpr int kHasB = 1 << 31;
 
+template <typename V>
+struct __align__(2 * sizeof(V)) V2P {
+  V a, b;
+};
+
 // Slot geometry of a pair, per element order. A's shared face is its vertices
 // (1,2,3) (+ edges 5, 9, 8 for tet10); B's is (0,1,2) (+ edges 4, 5, 6).
 template <int NPE> struct PairGeo;
@@ -83,7 +88,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
   using O = LaneOps<V>;
   using Geo = PairGeo<NPE>;
   constexpr int CPT = O::kCols;
-  constexpr int NR = Geo::NR, NIN = NR * 3;  // gathered node rows / dofs per pair
+  constexpr int NR = Geo::NR, NIN = (NR * 3 + 1) & ~1;  // gathered node rows / dofs per pair (even: pair slots)
   constexpr int kPairWords = Geo::WORDS;
   constexpr int MW = NR;                     // index of A's mask word (B's own follows)
   constexpr int NT = 128;
@@ -93,13 +98,19 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
   constexpr int TPC = 16 / sizeof(T);
   constexpr int CHUNKS = 24 / TPC;  // two 12-scalar coefficient records
   extern __shared__ __align__(16) unsigned char smem[];
-  V* ubuf = reinterpret_cast<V*>(smem);                                    // [2][NIN][NT]
+  V* ubuf = reinterpret_cast<V*>(smem);  // [2][NIN/2][NT][2]: dofs 2k, 2k+1 of a thread side by side
   T* cbuf = reinterpret_cast<T*>(smem + 2 * NIN * NT * sizeof(V));          // [2][GROUPS][24]
   int32_t* nbuf = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(cbuf) +
                                              2 * GROUPS * 24 * sizeof(T));  // [2][GROUPS][16]
   const int grp = threadIdx.x / TPE;
   const int lane = threadIdx.x % TPE;
   const int G = gridDim.x * GROUPS;
+  // a thread's dof q lives at pair q/2, element q%2: one 2*sizeof(V) shared load serves two dofs
+  auto slot = [](int q) { return (q >> 1) * 2 * NT + (q & 1); };
+  auto dof = [](const V* base, int q) {
+    const V2P<V> pr = *reinterpret_cast<const V2P<V>*>(base + (q >> 1) * 2 * NT);
+    return (q & 1) ? pr.b : pr.a;
+  };
   const int col = lane * CPT;
   int e = p_begin + blockIdx.x * GROUPS + grp;
 
@@ -124,14 +135,14 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
       }
       for (int q = lane; q < CHUNKS; q += TPE)
         cpa(cbuf + (stage * GROUPS + grp) * 24 + q * TPC, pcoef + static_cast<size_t>(ee) * 24 + q * TPC, 16, 16);
-      V* dst = ubuf + stage * NIN * NT + threadIdx.x;
+      V* dst = ubuf + stage * NIN * NT + 2 * threadIdx.x;
       const unsigned ma = static_cast<unsigned>(nd[MW]), mb = static_cast<unsigned>(nd[MW + 1]);
       if (mb == unsigned(kHasB) && ma == 0u) {  // interior pair: no constrained dof, no per-dof predicates
 #pragma unroll
         for (int a = 0; a < NR; ++a) {
           const T* row = u + static_cast<size_t>(static_cast<uint32_t>(nd[a])) * B + col;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) cpa(dst + (a * 3 + c) * NT, row + c * B, int(sizeof(V)), sizeof(V));
+          for (int c = 0; c < 3; ++c) cpa(dst + slot(a * 3 + c), row + c * B, int(sizeof(V)), sizeof(V));
         }
       } else {
 #pragma unroll
@@ -140,7 +151,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const unsigned m = a < NPE ? (ma >> (3 * a + c)) & 1u : (mb >> (3 * (a - NPE) + c)) & 1u;
-            cpa(dst + (a * 3 + c) * NT, row + c * B, m ? 0 : int(sizeof(V)), sizeof(V));
+            cpa(dst + slot(a * 3 + c), row + c * B, m ? 0 : int(sizeof(V)), sizeof(V));
           }
         }
       }
@@ -161,7 +172,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
     if (e < p_end) {
       const T* cf = cbuf + (s * GROUPS + grp) * 24;
       const int32_t* w = nbuf + (s * GROUPS + grp) * kPairWords;
-      const V* src = ubuf + s * NIN * NT + threadIdx.x;
+      const V* src = ubuf + s * NIN * NT + 2 * threadIdx.x;
       const unsigned ma = static_cast<unsigned>(w[MW]), mb = static_cast<unsigned>(w[MW + 1]);
       V carry[Geo::NFACE][3];  // A's face rows (= B's face rows)
       {
@@ -175,7 +186,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 #pragma unroll
         for (int a = 0; a < NPE; ++a)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) uu[a][c] = src[(a * 3 + c) * NT];
+          for (int c = 0; c < 3; ++c) uu[a][c] = dof(src, a * 3 + c);
         V ff[NPE][3];
         if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
         else tet4_product<V>(uu, b, lp, mp, ff);
@@ -213,7 +224,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 #pragma unroll
         for (int a = 0; a < NPE; ++a)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) uu[a][c] = src[(Geo::b_row(a) * 3 + c) * NT];
+          for (int c = 0; c < 3; ++c) uu[a][c] = dof(src, Geo::b_row(a) * 3 + c);
         V ff[NPE][3];
         if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
         else tet4_product<V>(uu, b, lp, mp, ff);
@@ -258,7 +269,7 @@ bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p
   } else {
     using Geo = PairGeo<NPE>;
     constexpr int NT = 128, GROUPS = NT / TPE;
-    const size_t smem = 2 * (size_t(Geo::NR) * 3 * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
+    const size_t smem = 2 * (size_t((Geo::NR * 3 + 1) & ~1) * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
                              size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
     auto kern = k_ebe_pair<T, V, NPE, B>;
     static int per_sm = 0, sms = 0;
