@@ -33,6 +33,22 @@ struct __align__(2 * sizeof(V)) V2P {
   V a, b;
 };
 
+// an element's 12-scalar coefficient record from shared memory in 16-byte loads
+__device__ __forceinline__ void load_rec(const float* p, float (&c)[12]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float4 v = reinterpret_cast<const float4*>(p)[i];
+    c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
+  }
+}
+__device__ __forceinline__ void load_rec(const double* p, double (&c)[12]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double2 v = reinterpret_cast<const double2*>(p)[i];
+    c[2 * i] = v.x; c[2 * i + 1] = v.y;
+  }
+}
+
 // Slot geometry of a pair, per element order. A's shared face is its vertices
 // (1,2,3) (+ edges 5, 9, 8 for tet10); B's is (0,1,2) (+ edges 4, 5, 6).
 template <int NPE> struct PairGeo;
@@ -176,12 +192,14 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
       const unsigned ma = static_cast<unsigned>(w[MW]), mb = static_cast<unsigned>(w[MW + 1]);
       V carry[Geo::NFACE][3];  // A's face rows (= B's face rows)
       {
+        T rec[12];
+        load_rec(cf, rec);
         V b[3][3];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cf[3 * k + d]);
-        const V lp = O::splat(cf[9]), mp = O::splat(cf[10]);
+          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
+        const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
         V uu[NPE][3];
 #pragma unroll
         for (int a = 0; a < NPE; ++a)
@@ -213,13 +231,14 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
           for (int c = 0; c < 3; ++c) carry[k][c] = ff[Geo::a_face(k)][c];
       }
       {  // B (a null B for unpaired A: zero record, own rows masked)
-        const T* cfb = cf + 12;
+        T rec[12];
+        load_rec(cf + 12, rec);
         V b[3][3];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(cfb[3 * k + d]);
-        const V lp = O::splat(cfb[9]), mp = O::splat(cfb[10]);
+          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
+        const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
         V uu[NPE][3];
 #pragma unroll
         for (int a = 0; a < NPE; ++a)
