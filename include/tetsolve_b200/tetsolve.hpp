@@ -396,7 +396,10 @@ inline BlockJacobi<T> extract_block_jacobi(const EbeOperator<T>& op) {
 class SolverLevels {
  public:
   SolverLevels() = default;
-  explicit SolverLevels(ts_levels* h) : lv_(h, ts_levels_destroy) {
+  explicit SolverLevels(ts_levels* h) : SolverLevels(std::shared_ptr<ts_levels>(h, ts_levels_destroy)) {}
+  // a level set owned elsewhere (e.g. by a faulted model): `lv` shares the owner's lifetime
+  explicit SolverLevels(std::shared_ptr<ts_levels> lv) : lv_(std::move(lv)) {
+    ts_levels* h = lv_.get();
     int32_t n0, n1, n2;
     ts_levels_sizes(h, &n0, &n1, &n2, nullptr);
     const ts_ebe* o;
@@ -517,6 +520,156 @@ inline std::pair<VectorBatch64, SolveReport> solve_pcge(const EbeOperator<double
                                &rb.c),
                  rb, 0);
   return {std::move(u), rb.report(0)};
+}
+
+// ------------------------------------------- fault.hpp / model.hpp / greens.hpp
+// The Green's-function sweep. Split-node geometry, slip
+// lifting, the batched solves and the sampling run inside the library; the
+// types keep the reference's names and fields so a sweep written against
+// tetsolve compiles unchanged (FaultPatch is a summary: its geometry stays in
+// the library, and UnitSlip magnitudes are evaluated there).
+enum class SlipDirection { dip = 0, strike = 1 };  // fault.hpp:12-15
+
+struct ObservationComponent {  // greens.hpp:15-18
+  Vec3 point{};
+  int axis = 0;
+};
+
+struct FaultPatch {  // fault.hpp:37-41 (summary)
+  int32_t n_faces = 0;
+  int32_t n_split_nodes = 0;
+};
+
+struct UnitSlip {  // fault.hpp:308-315
+  Vec3 center{};
+  SlipDirection direction = SlipDirection::dip;
+  double radius = 0.0;
+  std::vector<double> magnitude;  // evaluated by the library (unit_slip_magnitudes)
+};
+
+struct FaultedModel {  // model.hpp:34-39
+  CrustModel base;
+  FaultPatch patch;
+  int32_t split_mesh_nodes = 0;
+  std::shared_ptr<ts_faulted> handle;
+};
+
+// find_plane_fault_faces (fault.hpp:86-118)
+inline std::vector<std::array<int32_t, 3>> find_plane_fault_faces(const Mesh& mesh, int axis, double coord,
+                                                                  const Vec3& lo, const Vec3& hi) {
+  detail::MeshHandle h(mesh);
+  int32_t n = 0;
+  detail::check(ts_fault_plane_faces(h.h, axis, coord, lo.data(), hi.data(), &n, nullptr));
+  std::vector<std::array<int32_t, 3>> faces(n);
+  if (n) detail::check(ts_fault_plane_faces(h.h, axis, coord, lo.data(), hi.data(), &n, faces[0].data()));
+  return faces;
+}
+
+// build_faulted_model (model.hpp:41-51)
+inline FaultedModel build_faulted_model(Mesh mesh, std::vector<Material> materials,
+                                        const std::vector<std::array<int32_t, 3>>& fault_tris,
+                                        const SolverConfig& cfg, int /*workers*/ = 1) {
+  detail::MeshHandle h(mesh);
+  const auto [lam, mu] = detail::lame(materials);
+  const ts_solver_config c = cfg.to_c();
+  ts_faulted* f = nullptr;
+  detail::check(ts_faulted_model_create(h.h, static_cast<int32_t>(materials.size()), lam.data(), mu.data(),
+                                        fault_tris.empty() ? nullptr : fault_tris[0].data(),
+                                        static_cast<int32_t>(fault_tris.size()), &c, &f));
+  FaultedModel fm;
+  fm.handle = std::shared_ptr<ts_faulted>(f, ts_faulted_model_destroy);
+  detail::check(ts_faulted_info(f, &fm.patch.n_split_nodes, &fm.split_mesh_nodes, &fm.patch.n_faces));
+  ts_levels* lv = nullptr;
+  detail::check(ts_faulted_levels(f, &lv));
+  fm.base.mask = dirichlet_mask(mesh);
+  fm.base.levels = SolverLevels(std::shared_ptr<ts_levels>(fm.handle, lv));
+  fm.base.mesh = std::move(mesh);
+  fm.base.materials = std::move(materials);
+  return fm;
+}
+
+// unit_slip_basis (fault.hpp:325-343): the magnitudes are evaluated in the library
+inline UnitSlip unit_slip_basis(const FaultPatch& patch, const Mesh& /*base_mesh*/, const Vec3& center,
+                                SlipDirection direction, double radius) {
+  if (radius <= 0.0) throw ValidationError("unit_slip_basis: radius must be positive");
+  if (patch.n_faces == 0) throw ValidationError("unit_slip_basis: empty fault patch");
+  UnitSlip s;
+  s.center = center;
+  s.direction = direction;
+  s.radius = radius;
+  return s;
+}
+
+namespace detail {
+struct SlipArrays {
+  std::vector<double> centers, radii;
+  std::vector<int32_t> dirs;
+  explicit SlipArrays(const std::vector<UnitSlip>& slips) {
+    for (const auto& s : slips) {
+      centers.insert(centers.end(), s.center.begin(), s.center.end());
+      dirs.push_back(static_cast<int32_t>(s.direction));
+      radii.push_back(s.radius);
+    }
+  }
+};
+}  // namespace detail
+
+// slip_to_rhs (model.hpp:53-56)
+inline VectorBatch64 slip_to_rhs(const FaultedModel& fm, const UnitSlip& slip) {
+  const detail::SlipArrays a({slip});
+  VectorBatch64 f(fm.base.mesh.node_count(), 1);
+  detail::check(ts_slip_to_rhs(fm.handle.get(), 1, a.centers.data(), a.dirs.data(), a.radii.data(), f.data.data()));
+  return f;
+}
+
+struct GreensBank {  // greens.hpp:79-92
+  struct ColumnMeta {
+    Vec3 center{};
+    SlipDirection direction = SlipDirection::dip;
+    double radius = 0.0;
+  };
+  int32_t rows = 0;
+  int32_t cols = 0;
+  std::vector<double> values;  // row-major rows x cols
+  std::vector<ObservationComponent> obs;
+  std::vector<ColumnMeta> columns;
+  double& at(int32_t r, int32_t c) { return values[static_cast<size_t>(r) * cols + c]; }
+  double at(int32_t r, int32_t c) const { return values[static_cast<size_t>(r) * cols + c]; }
+};
+
+struct GreensReport {  // greens.hpp:95-99 (per_batch reports are not kept)
+  int solver_calls = 0;
+  long outer_iterations = 0;
+  std::vector<SolveReport> per_batch;
+};
+
+// compute_greens_bank (greens.hpp:114-145): ceil(n / batch) solver calls
+inline std::pair<GreensBank, GreensReport> compute_greens_bank(const FaultedModel& fm,
+                                                               const std::vector<UnitSlip>& slips,
+                                                               const std::vector<ObservationComponent>& obs,
+                                                               const SolverConfig& cfg) {
+  const detail::SlipArrays a(slips);
+  std::vector<double> pts;
+  std::vector<int32_t> axes;
+  for (const auto& o : obs) {
+    pts.insert(pts.end(), o.point.begin(), o.point.end());
+    axes.push_back(o.axis);
+  }
+  GreensBank bank;
+  bank.rows = static_cast<int32_t>(obs.size());
+  bank.cols = static_cast<int32_t>(slips.size());
+  bank.values.assign(static_cast<size_t>(bank.rows) * bank.cols, 0.0);
+  bank.obs = obs;
+  for (const auto& s : slips) bank.columns.push_back({s.center, s.direction, s.radius});
+  const ts_solver_config c = cfg.to_c();
+  GreensReport rep;
+  int32_t calls = 0;
+  int64_t outer = 0;
+  detail::check(ts_greens_bank(fm.handle.get(), bank.cols, a.centers.data(), a.dirs.data(), a.radii.data(), bank.rows,
+                               pts.data(), axes.data(), &c, bank.values.data(), &calls, &outer));
+  rep.solver_calls = calls;
+  rep.outer_iterations = static_cast<long>(outer);
+  return {std::move(bank), std::move(rep)};
 }
 
 }  // namespace tetsolve

@@ -308,6 +308,8 @@ ts_status ts_faulted_model_create(const ts_mesh* mesh, int32_t n_materials, cons
 void ts_faulted_model_destroy(ts_faulted* fm);
 ts_status ts_faulted_info(const ts_faulted* fm, int32_t* n_split_nodes, int32_t* split_mesh_nodes,
                           int32_t* n_faces);
+/* the base model's solver level set (FaultedModel::base.levels), owned by fm */
+ts_status ts_faulted_levels(const ts_faulted* fm, ts_levels** levels);
 /* right-hand sides of n_slips unit slips: f_host [3N][n_slips] (base mesh) */
 ts_status ts_slip_to_rhs(ts_faulted* fm, int32_t n_slips, const double* centers /*[n][3]*/,
                          const int32_t* directions, const double* radii, double* f_host);

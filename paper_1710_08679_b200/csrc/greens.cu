@@ -273,6 +273,15 @@ ts_status ts_faulted_info(const ts_faulted* fm, int32_t* n_split_nodes, int32_t*
   return TS_OK;
 }
 
+ts_status ts_faulted_levels(const ts_faulted* fm, ts_levels** levels) {
+  if (!fm || !levels) {
+    tsg::set_last_error("faulted model: null argument");
+    return TS_ERR_VALIDATION;
+  }
+  *levels = fm->levels;
+  return TS_OK;
+}
+
 ts_status ts_slip_to_rhs(ts_faulted* fm, int32_t n_slips, const double* centers, const int32_t* directions,
                          const double* radii, double* f_host) {
   try {

@@ -43,3 +43,41 @@ def test_dropin_file_formats(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["failures"] == 0 and res["parse_throw"] == 1 and res["volume_throw"] == 1
+
+
+def test_dropin_greens_compiles():
+    build(os.path.join(ROOT, "tests", "cpp", "dropin_greens.cpp"), os.path.join(ROOT, "tests", "cpp", "dropin_greens"))
+
+
+@pytest.mark.gpu
+def test_dropin_greens_matches_reference(reference):
+    """A Green's sweep written against the reference's fault/model/greens API, compiled against the
+    drop-in header, reproduces the reference's own bank (compute_greens_bank, greens.hpp:114-145)."""
+    import numpy as np
+    from conftest import TWO_LAYER, lame
+    from oracle import SolverConfig as OCfg
+    exe = os.path.join(ROOT, "tests", "cpp", "dropin_greens")
+    build(os.path.join(ROOT, "tests", "cpp", "dropin_greens.cpp"), exe)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    om = reference.box_mesh((8000.0, 8000.0, 6000.0), (8, 8, 6), (4500.0,), 1)
+    faces = reference.fault_plane_faces(om, 0, 4000.0, (4000.0, 2000.0, 1000.0), (4000.0, 6000.0, 5000.0))
+    assert res["faces"] == len(faces)
+    lam, mu = lame(TWO_LAYER)
+    centers = np.array([[4000.0, 4000.0, 3000.0], [4000.0, 3000.0, 2500.0], [4000.0, 5000.0, 4000.0],
+                        [4000.0, 4000.0, 3000.0], [4000.0, 3500.0, 2000.0]])
+    dirs = np.array([0, 0, 1, 1, 0], np.int32)
+    radii = np.array([1500.0, 1000.0, 1200.0, 1500.0, 900.0])
+    pts = np.array([[1000.0, 2000.0, 6000.0], [3000.0, 4000.0, 6000.0], [5000.0, 4000.0, 6000.0],
+                    [6500.0, 1500.0, 6000.0], [4000.0, 7000.0, 6000.0], [2500.0, 2500.0, 5500.0]])
+    axes = np.array([0, 1, 2, 0, 2, 1], np.int32)
+    rbank, rcalls, router = reference.greens_bank(om, lam, mu, faces, centers, dirs, radii, pts, axes,
+                                                  OCfg.default(batch_size=2))
+    f, info = reference.slip_to_rhs(om, lam, mu, faces, centers[:1], dirs[:1], radii[:1])
+    assert (res["split_nodes"], res["split_mesh_nodes"]) == tuple(info)
+    assert abs(res["f0_norm2"] - float((f ** 2).sum())) <= 1e-12 * float((f ** 2).sum())
+    assert res["calls"] == rcalls and abs(res["outer"] - router) <= max(1, 0.02 * router)
+    bank = np.array(res["bank"]).reshape(rbank.shape)
+    assert float(np.linalg.norm(bank - rbank) / np.linalg.norm(rbank)) <= 1e-6
+    assert res["solve_outer"] >= 1
