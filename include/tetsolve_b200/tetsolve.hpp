@@ -672,4 +672,57 @@ inline std::pair<GreensBank, GreensReport> compute_greens_bank(const FaultedMode
   return {std::move(bank), std::move(rep)};
 }
 
+// Green's-sweep files (fault.hpp:44-84,414-419; greens.hpp:20-44,147-222): the reference's bytes
+inline void write_fault_faces(const std::vector<std::array<int32_t, 3>>& faces, const std::string& path) {
+  detail::check(ts_fault_faces_write(path.c_str(), faces.empty() ? nullptr : faces[0].data(),
+                                     static_cast<int32_t>(faces.size())));
+}
+inline std::vector<std::array<int32_t, 3>> read_fault_faces(const std::string& path) {
+  int32_t n = 0;
+  detail::check(ts_fault_faces_read(path.c_str(), &n, nullptr));
+  std::vector<std::array<int32_t, 3>> f(n);
+  detail::check(ts_fault_faces_read(path.c_str(), &n, f.empty() ? nullptr : f[0].data()));
+  return f;
+}
+inline std::vector<ObservationComponent> read_observations(const std::string& path) {
+  int32_t n = 0;
+  detail::check(ts_observations_read(path.c_str(), &n, nullptr, nullptr));
+  std::vector<double> p(3 * size_t(n));
+  std::vector<int32_t> ax(n);
+  detail::check(ts_observations_read(path.c_str(), &n, p.data(), ax.data()));
+  std::vector<ObservationComponent> out(n);
+  for (int32_t i = 0; i < n; ++i) out[i] = {{p[3 * i], p[3 * i + 1], p[3 * i + 2]}, ax[i]};
+  return out;
+}
+inline void write_greens_bank(const GreensBank& bank, const std::string& path) {
+  std::vector<double> pts, centers, radii;
+  std::vector<int32_t> axes, dirs;
+  for (const auto& o : bank.obs) {
+    pts.insert(pts.end(), o.point.begin(), o.point.end());
+    axes.push_back(o.axis);
+  }
+  for (const auto& c : bank.columns) {
+    centers.insert(centers.end(), c.center.begin(), c.center.end());
+    dirs.push_back(static_cast<int32_t>(c.direction));
+    radii.push_back(c.radius);
+  }
+  detail::check(ts_greens_bank_write(path.c_str(), bank.rows, bank.cols, pts.data(), axes.data(), centers.data(),
+                                     dirs.data(), radii.data(), bank.values.data()));
+}
+inline GreensBank read_greens_bank(const std::string& path) {
+  GreensBank b;
+  detail::check(ts_greens_bank_read(path.c_str(), &b.rows, &b.cols, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                    nullptr));
+  std::vector<double> pts(3 * size_t(b.rows)), centers(3 * size_t(b.cols)), radii(b.cols);
+  std::vector<int32_t> axes(b.rows), dirs(b.cols);
+  b.values.resize(size_t(b.rows) * b.cols);
+  detail::check(ts_greens_bank_read(path.c_str(), &b.rows, &b.cols, pts.data(), axes.data(), centers.data(),
+                                    dirs.data(), radii.data(), b.values.data()));
+  for (int32_t r = 0; r < b.rows; ++r) b.obs.push_back({{pts[3 * r], pts[3 * r + 1], pts[3 * r + 2]}, axes[r]});
+  for (int32_t c = 0; c < b.cols; ++c)
+    b.columns.push_back({{centers[3 * c], centers[3 * c + 1], centers[3 * c + 2]},
+                         dirs[c] == 0 ? SlipDirection::dip : SlipDirection::strike, radii[c]});
+  return b;
+}
+
 }  // namespace tetsolve

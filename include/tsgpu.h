@@ -138,6 +138,20 @@ ts_status ts_tsvec_info(const char* path, int64_t* nodes, int32_t* batch);
 /* payload into u (sized by the caller from ts_tsvec_info; mismatch = TS_ERR_VALIDATION) */
 ts_status ts_tsvec_read(const char* path, double* u, int64_t nodes, int32_t batch, int32_t on_device);
 
+/* Green's-sweep files. TSFAULT 1 fault faces (write_fault_faces / read_fault_faces,
+ * fault.hpp:44-84,414-419); observation lists "x y z axis" (read_observations,
+ * greens.hpp:20-44); TSGREENS 1 banks (write_greens_bank / read_greens_bank,
+ * greens.hpp:147-222). Readers: call with NULL outputs to get the sizes, then
+ * with arrays at least that large; TS_ERR_PARSE as the reference's ParseError. */
+ts_status ts_fault_faces_write(const char* path, const int32_t* faces, int32_t n);
+ts_status ts_fault_faces_read(const char* path, int32_t* n, int32_t* faces);
+ts_status ts_observations_read(const char* path, int32_t* n, double* points, int32_t* axes);
+ts_status ts_greens_bank_write(const char* path, int32_t rows, int32_t cols, const double* obs_points,
+                               const int32_t* obs_axes, const double* centers, const int32_t* directions,
+                               const double* radii, const double* values);
+ts_status ts_greens_bank_read(const char* path, int32_t* rows, int32_t* cols, double* obs_points, int32_t* obs_axes,
+                              double* centers, int32_t* directions, double* radii, double* values);
+
 /* material_from_wavespeeds (material.hpp:22-34) */
 ts_status ts_material_from_wavespeeds(double vp, double vs, double rho, double* lambda,
                                       double* mu);

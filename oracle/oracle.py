@@ -438,7 +438,52 @@ class Oracle:
         L.ref_read_dirichlet.argtypes = [vp, cp]
         L.ref_write_solution.argtypes = [cp, vp, C.c_int32, C.c_int32]
         L.ref_read_solution.argtypes = [cp, vp, vp, vp]
+        L.ref_write_fault_faces.argtypes = [cp, vp, C.c_int32]
+        L.ref_read_fault_faces.argtypes = [cp, vp, vp]
+        L.ref_read_observations.argtypes = [cp, vp, vp, vp]
+        L.ref_write_greens_bank.argtypes = [cp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp]
+        L.ref_read_greens_bank.argtypes = [cp, vp, vp, vp, vp, vp, vp, vp, vp]
         return L
+
+    def write_fault_faces(self, path, faces) -> None:
+        L = self._io()
+        f = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+        self._check(L.ref_write_fault_faces(os.fsencode(path), _p(f), f.shape[0]))
+
+    def read_fault_faces(self, path) -> np.ndarray:
+        L = self._io()
+        n = C.c_int32()
+        self._check(L.ref_read_fault_faces(os.fsencode(path), C.byref(n), None))
+        out = np.zeros((n.value, 3), np.int32)
+        self._check(L.ref_read_fault_faces(os.fsencode(path), C.byref(n), _p(out)))
+        return out
+
+    def read_observations(self, path):
+        L = self._io()
+        n = C.c_int32()
+        self._check(L.ref_read_observations(os.fsencode(path), C.byref(n), None, None))
+        pts, ax = np.zeros((n.value, 3)), np.zeros(n.value, np.int32)
+        self._check(L.ref_read_observations(os.fsencode(path), C.byref(n), _p(pts), _p(ax)))
+        return pts, ax
+
+    def write_greens_bank(self, path, bank, pts, axes, centers, dirs, radii) -> None:
+        L = self._io()
+        b = np.ascontiguousarray(bank, np.float64)
+        arr = [np.ascontiguousarray(x, t) for x, t in ((pts, np.float64), (axes, np.int32), (centers, np.float64),
+                                                         (dirs, np.int32), (radii, np.float64))]
+        self._check(L.ref_write_greens_bank(os.fsencode(path), b.shape[0], b.shape[1], *[_p(x) for x in arr], _p(b)))
+
+    def read_greens_bank(self, path) -> dict:
+        L = self._io()
+        rows, cols = C.c_int32(), C.c_int32()
+        self._check(L.ref_read_greens_bank(os.fsencode(path), C.byref(rows), C.byref(cols), *([None] * 6)))
+        R, K = rows.value, cols.value
+        out = dict(values=np.zeros((R, K)), obs_points=np.zeros((R, 3)), obs_axes=np.zeros(R, np.int32),
+                   centers=np.zeros((K, 3)), directions=np.zeros(K, np.int32), radii=np.zeros(K))
+        self._check(L.ref_read_greens_bank(os.fsencode(path), C.byref(rows), C.byref(cols), _p(out["obs_points"]),
+                                           _p(out["obs_axes"]), _p(out["centers"]), _p(out["directions"]),
+                                           _p(out["radii"]), _p(out["values"])))
+        return out
 
     def write_mesh(self, m: MeshArrays, path) -> None:
         L = self._io()

@@ -616,4 +616,72 @@ int ref_read_solution(const char* path, int32_t* nodes, int32_t* batch, double* 
   REF_CATCH
 }
 
+// write_fault_faces / read_fault_faces (fault.hpp), read_observations / write_greens_bank /
+// read_greens_bank (greens.hpp)
+int ref_write_fault_faces(const char* path, const int32_t* faces, int32_t n) {
+  REF_TRY
+  std::vector<std::array<int32_t, 3>> f(n);
+  for (int32_t i = 0; i < n; ++i) f[i] = {faces[3 * i], faces[3 * i + 1], faces[3 * i + 2]};
+  write_fault_faces(f, path);
+  REF_CATCH
+}
+
+int ref_read_fault_faces(const char* path, int32_t* n, int32_t* faces) {
+  REF_TRY
+  const auto f = read_fault_faces(path);
+  *n = static_cast<int32_t>(f.size());
+  if (faces)
+    for (size_t i = 0; i < f.size(); ++i)
+      for (int k = 0; k < 3; ++k) faces[3 * i + k] = f[i][k];
+  REF_CATCH
+}
+
+int ref_read_observations(const char* path, int32_t* n, double* points, int32_t* axes) {
+  REF_TRY
+  const auto o = read_observations(path);
+  *n = static_cast<int32_t>(o.size());
+  for (size_t i = 0; i < o.size(); ++i) {
+    if (points)
+      for (int c = 0; c < 3; ++c) points[3 * i + c] = o[i].point[c];
+    if (axes) axes[i] = o[i].axis;
+  }
+  REF_CATCH
+}
+
+int ref_write_greens_bank(const char* path, int32_t rows, int32_t cols, const double* pts, const int32_t* axes,
+                          const double* centers, const int32_t* dirs, const double* radii, const double* values) {
+  REF_TRY
+  GreensBank b;
+  b.rows = rows;
+  b.cols = cols;
+  b.values.assign(values, values + size_t(rows) * cols);
+  for (int32_t r = 0; r < rows; ++r) b.obs.push_back({{pts[3 * r], pts[3 * r + 1], pts[3 * r + 2]}, axes[r]});
+  for (int32_t c = 0; c < cols; ++c)
+    b.columns.push_back({{centers[3 * c], centers[3 * c + 1], centers[3 * c + 2]},
+                         dirs[c] == 0 ? SlipDirection::dip : SlipDirection::strike, radii[c]});
+  write_greens_bank(b, path);
+  REF_CATCH
+}
+
+int ref_read_greens_bank(const char* path, int32_t* rows, int32_t* cols, double* pts, int32_t* axes, double* centers,
+                         int32_t* dirs, double* radii, double* values) {
+  REF_TRY
+  const GreensBank b = read_greens_bank(path);
+  *rows = b.rows;
+  *cols = b.cols;
+  if (values) std::copy(b.values.begin(), b.values.end(), values);
+  for (int32_t r = 0; r < b.rows; ++r) {
+    if (pts)
+      for (int c = 0; c < 3; ++c) pts[3 * r + c] = b.obs[r].point[c];
+    if (axes) axes[r] = b.obs[r].axis;
+  }
+  for (int32_t c = 0; c < b.cols; ++c) {
+    if (centers)
+      for (int k = 0; k < 3; ++k) centers[3 * c + k] = b.columns[c].center[k];
+    if (dirs) dirs[c] = b.columns[c].direction == SlipDirection::dip ? 0 : 1;
+    if (radii) radii[c] = b.columns[c].radius;
+  }
+  REF_CATCH
+}
+
 }  // extern "C"

@@ -87,6 +87,11 @@ _sig = {
     "ts_tsvec_write": (C.c_int, [C.c_char_p, vp, C.c_int64, i32, i32]),
     "ts_tsvec_info": (C.c_int, [C.c_char_p, vp, vp]),
     "ts_tsvec_read": (C.c_int, [C.c_char_p, vp, C.c_int64, i32, i32]),
+    "ts_fault_faces_write": (C.c_int, [C.c_char_p, vp, i32]),
+    "ts_fault_faces_read": (C.c_int, [C.c_char_p, vp, vp]),
+    "ts_observations_read": (C.c_int, [C.c_char_p, vp, vp, vp]),
+    "ts_greens_bank_write": (C.c_int, [C.c_char_p, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "ts_greens_bank_read": (C.c_int, [C.c_char_p, vp, vp, vp, vp, vp, vp, vp, vp]),
     "ts_material_from_wavespeeds": (C.c_int, [C.c_double, C.c_double, C.c_double, vp, vp]),
     "ts_ebe_create": (C.c_int, [vp, i32, i32, vp, vp, vp, i32, vp]),
     "ts_ebe_destroy": (None, [vp]),

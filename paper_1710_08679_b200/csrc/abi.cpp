@@ -1,5 +1,6 @@
 // abi.cpp — extern "C" boundary of libtsgpu.so (include/tsgpu.h): argument
 // validation, exception -> ts_status translation, host-buffer conveniences.
+#include <array>
 #include <cstring>
 #include <memory>
 
@@ -193,6 +194,88 @@ ts_status ts_tsvec_read(const char* path, double* u, int64_t nodes, int32_t batc
   TS_API_BEGIN
   TS_REQUIRE(path && (u || nodes == 0), "solution io: null argument");
   tsg::read_tsvec(path, u, nodes, batch, on_device != 0);
+  TS_API_END
+}
+
+// ------------------------------------------------------------ Green's-sweep files
+ts_status ts_fault_faces_write(const char* path, const int32_t* faces, int32_t n) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && n >= 0 && (faces || n == 0), "fault file: bad argument");
+  std::vector<std::array<int32_t, 3>> f(static_cast<size_t>(n));
+  if (n) std::memcpy(f.data(), faces, sizeof(int32_t) * 3 * size_t(n));
+  tsg::write_fault_faces(f, path);
+  TS_API_END
+}
+
+ts_status ts_fault_faces_read(const char* path, int32_t* n, int32_t* faces) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && n, "fault file: null argument");
+  const auto f = tsg::read_fault_faces(path);
+  if (faces) {
+    TS_REQUIRE(*n >= static_cast<int32_t>(f.size()), "fault file: output too small");
+    std::memcpy(faces, f.data(), sizeof(int32_t) * 3 * f.size());
+  }
+  *n = static_cast<int32_t>(f.size());
+  TS_API_END
+}
+
+ts_status ts_observations_read(const char* path, int32_t* n, double* points, int32_t* axes) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && n, "observations: null argument");
+  const auto o = tsg::read_observations(path);
+  if (points || axes) {
+    TS_REQUIRE(*n >= static_cast<int32_t>(o.size()), "observations: output too small");
+    for (size_t i = 0; i < o.size(); ++i) {
+      if (points)
+        for (int c = 0; c < 3; ++c) points[3 * i + c] = o[i].p[c];
+      if (axes) axes[i] = o[i].axis;
+    }
+  }
+  *n = static_cast<int32_t>(o.size());
+  TS_API_END
+}
+
+ts_status ts_greens_bank_write(const char* path, int32_t rows, int32_t cols, const double* obs_points,
+                               const int32_t* obs_axes, const double* centers, const int32_t* directions,
+                               const double* radii, const double* values) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && rows >= 1 && cols >= 1 && obs_points && obs_axes && centers && directions && radii && values,
+             "greens bank: bad argument");
+  tsg::GreensBankData g;
+  g.rows = rows;
+  g.cols = cols;
+  for (int32_t r = 0; r < rows; ++r) {
+    tsg::Observation o;
+    for (int c = 0; c < 3; ++c) o.p[c] = obs_points[3 * r + c];
+    o.axis = obs_axes[r];
+    g.obs.push_back(o);
+  }
+  g.centers.assign(centers, centers + 3 * size_t(cols));
+  g.dirs.assign(directions, directions + cols);
+  g.radii.assign(radii, radii + cols);
+  g.values.assign(values, values + size_t(rows) * cols);
+  tsg::write_greens_bank(g, path);
+  TS_API_END
+}
+
+ts_status ts_greens_bank_read(const char* path, int32_t* rows, int32_t* cols, double* obs_points, int32_t* obs_axes,
+                              double* centers, int32_t* directions, double* radii, double* values) {
+  TS_API_BEGIN
+  TS_REQUIRE(path && rows && cols, "greens bank: null argument");
+  const tsg::GreensBankData g = tsg::read_greens_bank(path);
+  const bool fill = obs_points || obs_axes || centers || directions || radii || values;
+  if (fill) TS_REQUIRE(*rows >= g.rows && *cols >= g.cols, "greens bank: output too small");
+  *rows = g.rows;
+  *cols = g.cols;
+  for (int32_t r = 0; fill && r < g.rows; ++r) {
+    if (obs_points)
+      for (int c = 0; c < 3; ++c) obs_points[3 * r + c] = g.obs[r].p[c];
+    if (obs_axes) obs_axes[r] = g.obs[r].axis;
+  }
+  if (centers) std::copy(g.centers.begin(), g.centers.end(), centers);
+  if (directions) std::copy(g.dirs.begin(), g.dirs.end(), directions);
+  if (radii) std::copy(g.radii.begin(), g.radii.end(), radii);
+  if (values) std::copy(g.values.begin(), g.values.end(), values);
   TS_API_END
 }
 

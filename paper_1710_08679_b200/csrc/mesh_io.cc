@@ -773,4 +773,187 @@ void read_tsvec(const std::string& path, double* u, int64_t nodes, int64_t batch
   TS_CUDA(cudaStreamSynchronize(st.s));
 }
 
+// ------------------------------------------------------------ Green's-sweep files
+// TSFAULT 1 (fault.hpp:44-84, 414-419), observation lists (greens.hpp:20-44) and
+// TSGREENS 1 banks (greens.hpp:147-222): same bytes on write, same accept /
+// reject (ParseError line and message) on read.
+namespace {
+std::string g17(double x) {
+  char b[40];
+  return std::string(b, put_g17(b, x));
+}
+// whole-file line reader for the small Green's files (std::getline semantics)
+struct Lines {
+  std::vector<char> buf;
+  std::vector<std::pair<const char*, const char*>> lines;
+  Lines(const std::string& path, const char* what, bool binary_tail = false) {
+    (void)binary_tail;
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) validation(std::string("cannot open ") + what + ": " + path);
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    buf.resize(size_t(std::max(0L, n)));
+    const size_t got = n > 0 ? std::fread(buf.data(), 1, size_t(n), f) : 0;
+    std::fclose(f);
+    buf.resize(got);
+    const char* p = buf.data();
+    const char* e = p + buf.size();
+    while (p < e) {
+      const char* nl = static_cast<const char*>(std::memchr(p, '\n', e - p));
+      lines.push_back({p, nl ? nl : e});
+      p = nl ? nl + 1 : e;
+    }
+  }
+};
+}  // namespace
+
+void write_fault_faces(const std::vector<std::array<int32_t, 3>>& faces, const std::string& path) {
+  AtomicFile out(path);
+  std::string s = "TSFAULT 1\nfaces " + std::to_string(faces.size()) + "\n";
+  char b[48];
+  for (const auto& f : faces) {
+    char* o = put_int(b, f[0]);
+    *o++ = ' ';
+    o = put_int(o, f[1]);
+    *o++ = ' ';
+    o = put_int(o, f[2]);
+    *o++ = '\n';
+    s.append(b, o);
+  }
+  out.write(s);
+  out.commit();
+}
+
+std::vector<std::array<int32_t, 3>> read_fault_faces(const std::string& path) {
+  Lines L(path, "fault file");
+  size_t li = 0;
+  auto next = [&]() {
+    if (li >= L.lines.size()) parse_error(path, long(li) + 1, "unexpected end of file");
+    const auto [a, b] = L.lines[li++];
+    return Cur{a, b};
+  };
+  {
+    Cur c = next();
+    std::string magic;
+    int32_t ver = 0;
+    get_word(c, magic) && get_i32(c, ver);
+    if (magic != "TSFAULT" || ver != 1) parse_error(path, long(li), "expected 'TSFAULT 1'");
+  }
+  int64_t n = -1;
+  {
+    Cur c = next();
+    std::string k;
+    const bool ok = get_word(c, k) && get_i64(c, n);
+    if (k != "faces" || !ok || n < 1) parse_error(path, long(li), "expected 'faces F'");
+  }
+  std::vector<std::array<int32_t, 3>> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    Cur c = next();
+    if (!(get_i32(c, out[i][0]) && get_i32(c, out[i][1]) && get_i32(c, out[i][2])))
+      parse_error(path, long(li), "expected 3 vertex ids");
+  }
+  return out;
+}
+
+std::vector<Observation> read_observations(const std::string& path) {
+  Lines L(path, "observations file");
+  std::vector<Observation> out;
+  for (size_t li = 0; li < L.lines.size(); ++li) {
+    const char* a = L.lines[li].first;
+    const char* b = L.lines[li].second;
+    const char* hash = static_cast<const char*>(std::memchr(a, '#', b - a));
+    Cur c{a, hash ? hash : b};
+    Observation o;
+    if (!get_f64(c, o.p[0])) continue;  // blank, comment or non-numeric lines are skipped
+    std::string ax;
+    if (!(get_f64(c, o.p[1]) && get_f64(c, o.p[2]) && get_word(c, ax)))
+      parse_error(path, long(li) + 1, "expected 'x y z axis'");
+    if (ax == "x" || ax == "0") o.axis = 0;
+    else if (ax == "y" || ax == "1") o.axis = 1;
+    else if (ax == "z" || ax == "2") o.axis = 2;
+    else parse_error(path, long(li) + 1, "axis must be one of x, y, z or 0..2");
+    out.push_back(o);
+  }
+  if (out.empty()) validation(path + ": no observation components");
+  return out;
+}
+
+void write_greens_bank(const GreensBankData& g, const std::string& path) {
+  AtomicFile out(path);
+  std::string s = "TSGREENS 1\nrows " + std::to_string(g.rows) + " cols " + std::to_string(g.cols) + "\n";
+  for (int32_t r = 0; r < g.rows; ++r)
+    s += "obs " + g17(g.obs[r].p[0]) + ' ' + g17(g.obs[r].p[1]) + ' ' + g17(g.obs[r].p[2]) + ' ' +
+         std::to_string(g.obs[r].axis) + "\n";
+  for (int32_t c = 0; c < g.cols; ++c)
+    s += "col " + g17(g.centers[3 * size_t(c)]) + ' ' + g17(g.centers[3 * size_t(c) + 1]) + ' ' +
+         g17(g.centers[3 * size_t(c) + 2]) + ' ' + (g.dirs[c] == 0 ? "dip" : "strike") + ' ' + g17(g.radii[c]) + "\n";
+  s += "DATA\n";
+  out.write(s);
+  out.write(g.values.data(), g.values.size() * sizeof(double));
+  out.commit();
+}
+
+GreensBankData read_greens_bank(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) validation("cannot open greens bank: " + path);
+  struct Closer {
+    FILE* f;
+    ~Closer() { std::fclose(f); }
+  } closer{f};
+  GreensBankData g;
+  std::string line;
+  long lineno = 0;
+  auto next = [&]() {
+    if (!header_line(f, line)) parse_error(path, lineno + 1, "unexpected end of file");
+    ++lineno;
+    return Cur{line.data(), line.data() + line.size()};
+  };
+  {
+    Cur c = next();
+    std::string magic;
+    int32_t ver = 0;
+    get_word(c, magic) && get_i32(c, ver);
+    if (magic != "TSGREENS" || ver != 1) parse_error(path, lineno, "expected 'TSGREENS 1'");
+  }
+  {
+    Cur c = next();
+    std::string k1, k2;
+    const bool ok = get_word(c, k1) && get_i32(c, g.rows) && get_word(c, k2) && get_i32(c, g.cols);
+    if (k1 != "rows" || k2 != "cols" || !ok || g.rows < 1 || g.cols < 1)
+      parse_error(path, lineno, "expected 'rows M cols N'");
+  }
+  for (int32_t r = 0; r < g.rows; ++r) {
+    Cur c = next();
+    std::string tag;
+    Observation o;
+    const bool ok = get_word(c, tag) && get_f64(c, o.p[0]) && get_f64(c, o.p[1]) && get_f64(c, o.p[2]) &&
+                    get_i32(c, o.axis);
+    if (tag != "obs" || !ok) parse_error(path, lineno, "expected 'obs x y z axis'");
+    g.obs.push_back(o);
+  }
+  for (int32_t col = 0; col < g.cols; ++col) {
+    Cur c = next();
+    std::string tag, dir;
+    double x[3], rad = 0.0;
+    const bool ok = get_word(c, tag) && get_f64(c, x[0]) && get_f64(c, x[1]) && get_f64(c, x[2]) &&
+                    get_word(c, dir) && get_f64(c, rad);
+    if (tag != "col" || !ok || (dir != "dip" && dir != "strike"))
+      parse_error(path, lineno, "expected 'col x y z dip|strike radius'");
+    g.centers.insert(g.centers.end(), x, x + 3);
+    g.dirs.push_back(dir == "dip" ? 0 : 1);
+    g.radii.push_back(rad);
+  }
+  {
+    Cur c = next();
+    std::string tag;
+    get_word(c, tag);
+    if (tag != "DATA") parse_error(path, lineno, "expected 'DATA'");
+  }
+  g.values.resize(size_t(g.rows) * g.cols);
+  const size_t bytes = g.values.size() * sizeof(double);
+  if (std::fread(g.values.data(), 1, bytes, f) != bytes) parse_error(path, lineno + 1, "truncated binary matrix payload");
+  return g;
+}
+
 }  // namespace tsg

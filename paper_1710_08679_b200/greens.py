@@ -69,3 +69,59 @@ class FaultedModel:
             lib.ts_faulted_model_destroy(self._h)
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ files
+def _path(p) -> bytes:
+    import os
+
+    return os.fsencode(p)
+
+
+def write_fault_faces(faces, path) -> None:
+    """write_fault_faces (fault.hpp:414-419): TSFAULT 1, one "v0 v1 v2" line per face."""
+    f = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+    _ck(lib.ts_fault_faces_write(_path(path), _p(f), f.shape[0]))
+
+
+def read_fault_faces(path) -> np.ndarray:
+    """read_fault_faces (fault.hpp:47-78) -> (F, 3) int32."""
+    n = C.c_int32(0)
+    _ck(lib.ts_fault_faces_read(_path(path), C.byref(n), None))
+    out = np.zeros((n.value, 3), np.int32)
+    _ck(lib.ts_fault_faces_read(_path(path), C.byref(n), _p(out)))
+    return out
+
+
+def read_observations(path):
+    """read_observations (greens.hpp:20-44) -> (points (R, 3), axes (R,))."""
+    n = C.c_int32(0)
+    _ck(lib.ts_observations_read(_path(path), C.byref(n), None, None))
+    pts = np.zeros((n.value, 3), np.float64)
+    ax = np.zeros(n.value, np.int32)
+    _ck(lib.ts_observations_read(_path(path), C.byref(n), _p(pts), _p(ax)))
+    return pts, ax
+
+
+def write_greens_bank(path, bank, obs_points, obs_axes, centers, directions, radii) -> None:
+    """write_greens_bank (greens.hpp:147-165): TSGREENS 1 text header + row-major fp64 matrix."""
+    b = np.ascontiguousarray(bank, np.float64)
+    rows, cols = b.shape
+    pts = np.ascontiguousarray(obs_points, np.float64).reshape(rows, 3)
+    ax = np.ascontiguousarray(obs_axes, np.int32).reshape(rows)
+    c = np.ascontiguousarray(centers, np.float64).reshape(cols, 3)
+    d = np.ascontiguousarray(directions, np.int32).reshape(cols)
+    r = np.ascontiguousarray(radii, np.float64).reshape(cols)
+    _ck(lib.ts_greens_bank_write(_path(path), rows, cols, _p(pts), _p(ax), _p(c), _p(d), _p(r), _p(b)))
+
+
+def read_greens_bank(path) -> dict:
+    """read_greens_bank (greens.hpp:167-222) -> dict(values, obs_points, obs_axes, centers, directions, radii)."""
+    rows, cols = C.c_int32(0), C.c_int32(0)
+    _ck(lib.ts_greens_bank_read(_path(path), C.byref(rows), C.byref(cols), None, None, None, None, None, None))
+    R, K = rows.value, cols.value
+    out = dict(values=np.zeros((R, K)), obs_points=np.zeros((R, 3)), obs_axes=np.zeros(R, np.int32),
+               centers=np.zeros((K, 3)), directions=np.zeros(K, np.int32), radii=np.zeros(K))
+    _ck(lib.ts_greens_bank_read(_path(path), C.byref(rows), C.byref(cols), _p(out["obs_points"]), _p(out["obs_axes"]),
+                                _p(out["centers"]), _p(out["directions"]), _p(out["radii"]), _p(out["values"])))
+    return out

@@ -33,6 +33,13 @@ int main() {
   std::vector<ObservationComponent> obs;
   for (int r = 0; r < 6; ++r) obs.push_back({pts[r], axes[r]});
   const auto [bank, rep] = compute_greens_bank(fm, slips, obs, cfg);
+  // the reference's file formats round-trip the sweep's inputs and outputs
+  write_fault_faces(faces, "dropin_greens.tsfault");
+  write_greens_bank(bank, "dropin_greens.tsgreens");
+  const bool files_ok = read_fault_faces("dropin_greens.tsfault") == faces &&
+                        read_greens_bank("dropin_greens.tsgreens").values == bank.values;
+  std::remove("dropin_greens.tsfault");
+  std::remove("dropin_greens.tsgreens");
   const VectorBatch64 f0 = slip_to_rhs(fm, slips[0]);
   double f0n = 0.0;
   for (double x : f0.data) f0n += x * x;
@@ -42,9 +49,9 @@ int main() {
   c1.batch_size = 1;
   const auto sol = solve(fm.base.levels, f0, u0, c1);
   std::printf("{\"faces\": %zu, \"split_nodes\": %d, \"split_mesh_nodes\": %d, \"calls\": %d, \"outer\": %ld, "
-              "\"f0_norm2\": %.17g, \"solve_outer\": %d, \"bank\": [",
+              "\"f0_norm2\": %.17g, \"solve_outer\": %d, \"files_ok\": %d, \"bank\": [",
               faces.size(), fm.patch.n_split_nodes, fm.split_mesh_nodes, rep.solver_calls, rep.outer_iterations, f0n,
-              sol.second.outer_iterations);
+              sol.second.outer_iterations, files_ok ? 1 : 0);
   for (size_t i = 0; i < bank.values.size(); ++i) std::printf("%s%.17g", i ? ", " : "", bank.values[i]);
   std::printf("]}\n");
   return 0;

@@ -50,7 +50,7 @@ def test_dropin_greens_compiles():
 
 
 @pytest.mark.gpu
-def test_dropin_greens_matches_reference(reference):
+def test_dropin_greens_matches_reference(reference, tmp_path):
     """A Green's sweep written against the reference's fault/model/greens API, compiled against the
     drop-in header, reproduces the reference's own bank (compute_greens_bank, greens.hpp:114-145)."""
     import numpy as np
@@ -58,9 +58,10 @@ def test_dropin_greens_matches_reference(reference):
     from oracle import SolverConfig as OCfg
     exe = os.path.join(ROOT, "tests", "cpp", "dropin_greens")
     build(os.path.join(ROOT, "tests", "cpp", "dropin_greens.cpp"), exe)
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300, cwd=tmp_path)
     assert out.returncode == 0, out.stdout + out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["files_ok"] == 1
     om = reference.box_mesh((8000.0, 8000.0, 6000.0), (8, 8, 6), (4500.0,), 1)
     faces = reference.fault_plane_faces(om, 0, 4000.0, (4000.0, 2000.0, 1000.0), (4000.0, 6000.0, 5000.0))
     assert res["faces"] == len(faces)

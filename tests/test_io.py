@@ -320,3 +320,90 @@ def test_unstructured_mesh_files(reference, tmp_path):
     same_arrays(back, a)
     ts.write_mesh_binary(back, tmp_path / "u.tsbmesh")
     same_arrays(ts.read_mesh_binary(tmp_path / "u.tsbmesh"), a)
+
+
+# ---------------------------------------------------------------- Green's-sweep files
+from paper_1710_08679_b200 import greens as G  # noqa: E402
+
+
+def same_bank(a, b):
+    for k in ("values", "obs_points", "centers", "radii"):
+        assert np.array_equal(np.asarray(a[k]).view(np.uint64), np.asarray(b[k]).view(np.uint64)), k
+    for k in ("obs_axes", "directions"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_fault_faces_files(reference, tmp_path):
+    rng = np.random.default_rng(4)
+    faces = rng.integers(0, 10**6, (37, 3)).astype(np.int32)
+    G.write_fault_faces(faces, tmp_path / "a.tsfault")
+    reference.write_fault_faces(tmp_path / "b.tsfault", faces)
+    assert read_bytes(tmp_path / "a.tsfault") == read_bytes(tmp_path / "b.tsfault")
+    assert np.array_equal(G.read_fault_faces(tmp_path / "b.tsfault"), faces)
+    p = tmp_path / "x.tsfault"
+    good = read_bytes(tmp_path / "a.tsfault").decode().splitlines(keepends=True)
+    for text in ("", "TSFAULT 2\nfaces 1\n1 2 3\n", "TSFAULT 1\nfaces 0\n", "TSFAULT 1\nfaces 2\n1 2 3\n",
+                 "TSFAULT 1\nfaces 1\n1 2\n", "TSFAULT 1\nfacez 1\n1 2 3\n", "".join(good[:5]),
+                 "TSFAULT 1\nfaces 1\n1 2 3 4 extra\n"):
+        p.write_text(text)
+        try:
+            want = reference.read_fault_faces(p)
+        except Exception as e:
+            with pytest.raises(ts.ValidationError) as ours:
+                G.read_fault_faces(p)
+            assert str(ours.value) == str(e)
+            continue
+        assert np.array_equal(G.read_fault_faces(p), want)
+
+
+def test_observations_file(reference, tmp_path):
+    p = tmp_path / "obs.txt"
+    cases = [
+        "# surface stations\n1000 2000 6000 x\n3000.5 4000 6000 y  # trailing\n\n5e3 4e3 6e3 2\n",
+        "abc\n1 2 3 0\n",                  # non-numeric line skipped
+        "1 2 3 w\n",                      # bad axis
+        "1 2\n",                          # short line
+        "# nothing\n\n",                  # empty -> ValidationError
+        "1 2 3 z\n4 5 6 1",               # no final newline
+    ]
+    for text in cases:
+        p.write_text(text)
+        try:
+            want = reference.read_observations(p)
+        except Exception as e:
+            with pytest.raises(ts.ValidationError) as ours:
+                G.read_observations(p)
+            assert str(ours.value) == str(e)
+            continue
+        got = G.read_observations(p)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_greens_bank_files(reference, tmp_path):
+    rng = np.random.default_rng(8)
+    R, K = 7, 5
+    bank = rng.standard_normal((R, K)) * 1e-3
+    pts = rng.uniform(0, 8000, (R, 3))
+    axes = rng.integers(0, 3, R).astype(np.int32)
+    centers = rng.uniform(0, 8000, (K, 3))
+    dirs = rng.integers(0, 2, K).astype(np.int32)
+    radii = rng.uniform(500, 2000, K)
+    G.write_greens_bank(tmp_path / "a.tsgreens", bank, pts, axes, centers, dirs, radii)
+    reference.write_greens_bank(tmp_path / "b.tsgreens", bank, pts, axes, centers, dirs, radii)
+    assert read_bytes(tmp_path / "a.tsgreens") == read_bytes(tmp_path / "b.tsgreens")
+    same_bank(G.read_greens_bank(tmp_path / "b.tsgreens"), reference.read_greens_bank(tmp_path / "a.tsgreens"))
+    good = read_bytes(tmp_path / "a.tsgreens")
+    head, payload = good.split(b"DATA\n", 1)
+    p = tmp_path / "x.tsgreens"
+    for v in (head + b"DATA\n" + payload[:-8], head.replace(b"TSGREENS 1", b"TSGREENS 0") + b"DATA\n" + payload,
+              head.replace(b"rows 7", b"rows 0") + b"DATA\n" + payload, head.replace(b" dip ", b" dup ", 1)
+              + b"DATA\n" + payload, head.replace(b"obs ", b"ob ", 1) + b"DATA\n" + payload, head, b""):
+        p.write_bytes(v)
+        try:
+            want = reference.read_greens_bank(p)
+        except Exception as e:
+            with pytest.raises(ts.ValidationError) as ours:
+                G.read_greens_bank(p)
+            assert str(ours.value) == str(e)
+            continue
+        same_bank(G.read_greens_bank(p), want)
