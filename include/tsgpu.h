@@ -322,6 +322,13 @@ ts_status ts_faulted_model_create(const ts_mesh* mesh, int32_t n_materials, cons
 void ts_faulted_model_destroy(ts_faulted* fm);
 ts_status ts_faulted_info(const ts_faulted* fm, int32_t* n_split_nodes, int32_t* split_mesh_nodes,
                           int32_t* n_faces);
+/* reconstruct_split_solution (fault.hpp:392-411) for n_slips unit slips: u_base_host
+ * [3N][n_slips] (base mesh) -> u_split_host [3 NS][n_slips] (split mesh, NS from
+ * ts_faulted_info): every split copy takes its base node's value, plus copies then
+ * add half the slip jump and minus copies subtract it */
+ts_status ts_reconstruct_split_solution(ts_faulted* fm, int32_t n_slips, const double* centers,
+                                        const int32_t* directions, const double* radii, const double* u_base_host,
+                                        double* u_split_host);
 /* the base model's solver level set (FaultedModel::base.levels), owned by fm */
 ts_status ts_faulted_levels(const ts_faulted* fm, ts_levels** levels);
 /* right-hand sides of n_slips unit slips: f_host [3N][n_slips] (base mesh) */

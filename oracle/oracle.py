@@ -405,6 +405,24 @@ class Oracle:
             self._f("mesh_destroy")(h)
         return f, info
 
+    def reconstruct_split(self, m: MeshArrays, lam, mu, faces, centers, dirs, radii, u_base, n_split_mesh_nodes):
+        assert self.kind == "reference"
+        arrs = [np.ascontiguousarray(x, t) for x, t in ((lam, np.float64), (mu, np.float64), (faces, np.int32),
+                                                          (centers, np.float64), (dirs, np.int32), (radii, np.float64),
+                                                          (u_base, np.float64))]
+        lam_, mu_, faces_, centers_, dirs_, radii_, ub = arrs
+        out = np.zeros((3 * n_split_mesh_nodes, len(dirs_)), np.float64)
+        h = self._mesh(m)
+        try:
+            vp = C.c_void_p
+            self.lib.ref_reconstruct_split.argtypes = [vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]
+            self._check(self.lib.ref_reconstruct_split(h, len(lam_), _p(lam_), _p(mu_), _p(faces_), len(faces_),
+                                                       len(dirs_), _p(centers_), _p(dirs_), _p(radii_), _p(ub),
+                                                       _p(out)))
+        finally:
+            self._f("mesh_destroy")(h)
+        return out
+
     def greens_bank(self, m: MeshArrays, lam, mu, faces, centers, dirs, radii, points, axes, cfg: SolverConfig):
         assert self.kind == "reference"
         lam = np.ascontiguousarray(lam, np.float64)

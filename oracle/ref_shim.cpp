@@ -684,4 +684,22 @@ int ref_read_greens_bank(const char* path, int32_t* rows, int32_t* cols, double*
   REF_CATCH
 }
 
+// reconstruct_split_solution (fault.hpp:392-411) of each slip's column of u_base
+int ref_reconstruct_split(const void* mh, int32_t n_mat, const double* lam, const double* mu, const int32_t* faces,
+                          int32_t n_faces, int32_t n_slips, const double* centers, const int32_t* dirs,
+                          const double* radii, const double* u_base, double* u_split) {
+  REF_TRY
+  const FaultedModel fm = build_faulted_model(*static_cast<const Mesh*>(mh), mats_of(n_mat, lam, mu),
+                                              tris_of(faces, n_faces), SolverConfig{});
+  const auto slips = slips_of(fm, n_slips, centers, dirs, radii);
+  const int32_t N = fm.base.mesh.node_count(), NS = fm.split_mesh.node_count();
+  for (int32_t j = 0; j < n_slips; ++j) {
+    VectorBatch64 ub(N, 1);
+    for (int64_t d = 0; d < 3 * int64_t(N); ++d) ub.at(d, 0) = u_base[d * n_slips + j];
+    const VectorBatch64 us = reconstruct_split_solution(fm.patch, slip_vectors(fm.patch, slips[j]), ub, NS);
+    for (int64_t d = 0; d < 3 * int64_t(NS); ++d) u_split[d * n_slips + j] = us.at(d, 0);
+  }
+  REF_CATCH
+}
+
 }  // extern "C"

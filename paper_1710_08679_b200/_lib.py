@@ -142,6 +142,7 @@ _sig = {
     "ts_faulted_model_destroy": (None, [vp]),
     "ts_faulted_info": (C.c_int, [vp, vp, vp, vp]),
     "ts_faulted_levels": (C.c_int, [vp, vp]),
+    "ts_reconstruct_split_solution": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "ts_slip_to_rhs": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     "ts_greens_bank": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]),
 }

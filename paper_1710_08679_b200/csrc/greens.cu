@@ -53,6 +53,25 @@ __global__ void k_sample(const double* __restrict__ u, const int32_t* __restrict
   bank[int64_t(r) * n_cols + col0 + j] = v;
 }
 
+// reconstruct_split_solution (fault.hpp:392-411): u_split[s] = u_base[to_base[s]] ...
+__global__ void k_split_gather(const double* __restrict__ ub, const int32_t* __restrict__ to_base, int32_t ns_nodes,
+                               int32_t W, double* __restrict__ us) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(ns_nodes) * 3 * W) return;
+  const int64_t s = i / (3 * W), rem = i - s * 3 * W;
+  us[i] = ub[3 * int64_t(__ldg(to_base + s)) * W + rem];
+}
+// ... then plus copies += delta/2, minus copies -= delta/2 (in that order, as the reference)
+__global__ void k_split_jump(const int32_t* __restrict__ plus, const int32_t* __restrict__ minus, int32_t ns, int32_t W,
+                             const double* __restrict__ d, double* __restrict__ us) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(ns) * 3 * W) return;
+  const int64_t k = i / (3 * W), rem = i - k * 3 * W;
+  const double h = 0.5 * d[i];
+  us[3 * int64_t(plus[k]) * W + rem] += h;
+  us[3 * int64_t(minus[k]) * W + rem] -= h;
+}
+
 // IEEE ops without contraction: the device scan reproduces the host arithmetic
 // of the reference's point location (greens.hpp:50-76, geometry.hpp:27-42) operation for operation
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
@@ -117,6 +136,7 @@ struct ts_faulted {
   tsg::DevBuf<int32_t> loc_tet4;  // base element vertex ids
   tsg::DevBuf<double> bf, bu0, bu;  // per-batch f, u0, u of the bank loop (kept across calls)
   tsg::DevBuf<double> sg, sw;       // split-mesh work vectors of slip_to_rhs (kept across calls)
+  tsg::DevBuf<int32_t> to_base;     // split node -> base node (reconstruct_split_solution)
   ~ts_faulted() { tsg::levels_free(levels); }
 };
 
@@ -279,6 +299,36 @@ ts_status ts_faulted_levels(const ts_faulted* fm, ts_levels** levels) {
     return TS_ERR_VALIDATION;
   }
   *levels = fm->levels;
+  return TS_OK;
+}
+
+ts_status ts_reconstruct_split_solution(ts_faulted* fm, int32_t n_slips, const double* centers,
+                                        const int32_t* directions, const double* radii, const double* u_base_host,
+                                        double* u_split_host) {
+  try {
+    if (!fm || !centers || !directions || !radii || !u_base_host || !u_split_host)
+      tsg::validation("reconstruct_split_solution: null argument");
+    if (n_slips < 1) tsg::validation("reconstruct_split_solution: need at least one slip");
+    const int32_t N = fm->base.n_nodes(), NS = fm->split.n_nodes();
+    const int32_t ns = static_cast<int32_t>(fm->patch.split_nodes.size());
+    if (fm->to_base.size() != size_t(NS)) fm->to_base.upload(fm->patch.to_base);
+    tsg::DevBuf<double> ub, us(3 * size_t(NS) * n_slips), d;
+    ub.upload(u_base_host, 3 * size_t(N) * n_slips);
+    tsg::slip_deltas(*fm, n_slips, centers, directions, radii, d);
+    tsg::k_split_gather<<<tsg::grid_for(int64_t(NS) * 3 * n_slips, 256), 256>>>(ub.get(), fm->to_base.get(), NS,
+                                                                               n_slips, us.get());
+    TS_CUDA(cudaGetLastError());
+    tsg::k_split_jump<<<tsg::grid_for(int64_t(ns) * 3 * n_slips, 256), 256>>>(fm->plus.get(), fm->minus.get(), ns,
+                                                                            n_slips, d.get(), us.get());
+    TS_CUDA(cudaGetLastError());
+    TS_CUDA(cudaMemcpy(u_split_host, us.get(), us.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  } catch (const tsg::Error& e) {
+    tsg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    tsg::set_last_error(e.what());
+    return TS_ERR_VALIDATION;
+  }
   return TS_OK;
 }
 

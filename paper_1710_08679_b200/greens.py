@@ -8,7 +8,7 @@ import ctypes as C
 import numpy as np
 
 from ._lib import lib
-from .tetsolve import Mesh, SolverConfig, _ck, _lame, _p
+from .tetsolve import Mesh, SolverConfig, SolverLevels, _ck, _lame, _p
 
 DIP, STRIKE = 0, 1  # SlipDirection (fault.hpp:304)
 
@@ -39,6 +39,9 @@ class FaultedModel:
         ns, nsm, nf = C.c_int32(), C.c_int32(), C.c_int32()
         _ck(lib.ts_faulted_info(self._h, C.byref(ns), C.byref(nsm), C.byref(nf)))
         self.n_split_nodes, self.split_mesh_nodes, self.n_faces = ns.value, nsm.value, nf.value
+        lv = C.c_void_p()
+        _ck(lib.ts_faulted_levels(self._h, C.byref(lv)))
+        self.levels = SolverLevels(lv, mesh, owner=self)  # FaultedModel::base.levels
 
     def slip_to_rhs(self, centers, directions, radii) -> np.ndarray:
         """slip_to_rhs (fault.hpp:363-388) of each unit slip: [3N, n_slips]."""
@@ -48,6 +51,18 @@ class FaultedModel:
         f = np.zeros((3 * self.mesh.node_count(), len(directions)), np.float64)
         _ck(lib.ts_slip_to_rhs(self._h, len(directions), _p(centers), _p(directions), _p(radii), _p(f)))
         return f
+
+    def reconstruct_split_solution(self, centers, directions, radii, u_base) -> np.ndarray:
+        """reconstruct_split_solution (fault.hpp:392-411): base-mesh solutions [3N, n] of the n unit
+        slips -> split-mesh displacements [3 NS, n] with the prescribed jumps."""
+        centers = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        directions = np.ascontiguousarray(directions, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        ub = np.ascontiguousarray(u_base, np.float64).reshape(3 * self.mesh.node_count(), len(directions))
+        out = np.zeros((3 * self.split_mesh_nodes, len(directions)), np.float64)
+        _ck(lib.ts_reconstruct_split_solution(self._h, len(directions), _p(centers), _p(directions), _p(radii),
+                                              _p(ub), _p(out)))
+        return out
 
     def greens_bank(self, centers, directions, radii, points, axes, cfg: SolverConfig | None = None):
         """compute_greens_bank (greens.hpp:114-145): (bank [n_obs, n_slips], solver_calls, outer_iterations)."""

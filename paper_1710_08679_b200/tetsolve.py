@@ -461,9 +461,10 @@ class SolverLevels:
     """SolverLevels (adaptive_cg.hpp:27-37) built on the device by
     build_solver_levels (adaptive_cg.hpp:39-67)."""
 
-    def __init__(self, handle, mesh: Mesh):
+    def __init__(self, handle, mesh: Mesh, owner=None):
         self._h = handle
         self.mesh = mesh
+        self._owner = owner  # set: a level set owned by another object (e.g. a faulted model), not destroyed here
         n0, n1, n2, nz = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
         _ck(lib.ts_levels_sizes(self._h, C.byref(n0), C.byref(n1), C.byref(n2), C.byref(nz)))
         self.n0, self.n1, self.n2, self.nnzb2 = n0.value, n1.value, n2.value, nz.value
@@ -494,6 +495,8 @@ class SolverLevels:
         return dict(agg=agg, row_ptr2=rp, col_idx2=ci, blocks2=bl, mask2=mk, m2=m2)
 
     def __del__(self):
+        if self._owner is not None:
+            return
         try:
             # borrowed operators must not outlive the level set
             for op in (self.outer, self.level0, self.level1):

@@ -83,3 +83,19 @@ def test_validation_errors(setup):
         fm.greens_bank(CENTERS[:1], DIRS[:1], RADII[:1], [[1e6, 0.0, 0.0]], [0])  # observation outside
     with pytest.raises(ts.ValidationError):
         find_plane_fault_faces(mesh, 0, 4500.0, (4500.0, 0.0, 0.0), (4500.0, 8000.0, 6000.0))  # not a mesh plane
+
+
+def test_reconstruct_split_solution(setup, reference):
+    """reconstruct_split_solution (fault.hpp:392-411; test_fault.cpp:360-376): the split-mesh
+    displacement carries the prescribed jump exactly; on the same base solution it equals the
+    reference's reconstruction bit for bit."""
+    mesh, om, faces, _ = setup
+    lam, mu = lame(TWO_LAYER)
+    cfg = ts.SolverConfig(batch_size=4)
+    fm = FaultedModel(mesh, mats(), faces, cfg)
+    f = fm.slip_to_rhs(CENTERS, DIRS, RADII)
+    u, _ = ts.solve(fm.levels, f, np.zeros_like(f), ts.SolverConfig(batch_size=len(DIRS)))
+    us = fm.reconstruct_split_solution(CENTERS, DIRS, RADII, u)
+    want = reference.reconstruct_split(om, lam, mu, faces, CENTERS, DIRS, RADII, u, fm.split_mesh_nodes)
+    assert np.array_equal(us.view(np.uint64), want.view(np.uint64))
+    assert np.abs(us).max() > 0
