@@ -99,3 +99,46 @@ def test_reconstruct_split_solution(setup, reference):
     want = reference.reconstruct_split(om, lam, mu, faces, CENTERS, DIRS, RADII, u, fm.split_mesh_nodes)
     assert np.array_equal(us.view(np.uint64), want.view(np.uint64))
     assert np.abs(us).max() > 0
+
+
+def test_fault_rejections_match_reference(setup, reference):
+    """test_fault.cpp:119-143: a fault touching a Dirichlet boundary, and a boundary triangle, are
+    rejected — by the reference and by the library (ValidationError)."""
+    mesh, om, _, _ = setup
+    lam, mu = lame(TWO_LAYER)
+    full = find_plane_fault_faces(mesh, 0, 4000.0, (4000.0, 0.0, 0.0), (4000.0, 8000.0, 6000.0))
+    t = np.asarray(om.tets10)[:, :4]
+    z = np.asarray(om.coords)[:, 2]
+    bottom = None
+    for tet in t:
+        for fv in ((1, 2, 3), (0, 3, 2), (0, 1, 3), (0, 2, 1)):
+            tri = tet[list(fv)]
+            if (z[tri] == 0.0).all():
+                bottom = np.array([tri], np.int32)
+                break
+        if bottom is not None:
+            break
+    for faces in (full, bottom):
+        with pytest.raises(Exception):
+            reference.slip_to_rhs(om, lam, mu, faces, CENTERS[:1], DIRS[:1], RADII[:1])
+        with pytest.raises(ts.ValidationError):
+            FaultedModel(mesh, mats(), faces)
+
+
+def test_sampling_at_a_node_returns_the_nodal_value(setup):
+    """test_fault.cpp 'sampling at a node returns the nodal value': an observation placed on a
+    surface vertex samples exactly that vertex's displacement."""
+    mesh, _, faces, _ = setup
+    cfg = ts.SolverConfig(batch_size=len(DIRS))
+    fm = FaultedModel(mesh, mats(), faces, cfg)
+    coords = np.asarray(mesh.coords)
+    top = np.flatnonzero((coords[:, 2] == 6000.0) & (np.arange(len(coords)) < mesh.vertex_count)
+                         & (coords[:, 0] > 0) & (coords[:, 0] < 8000.0) & (coords[:, 1] > 0) & (coords[:, 1] < 8000.0))
+    node = int(top[len(top) // 2])
+    bank, _, _ = fm.greens_bank(CENTERS, DIRS, RADII, coords[node:node + 1].repeat(3, 0), np.arange(3, dtype=np.int32),
+                                cfg)
+    f = fm.slip_to_rhs(CENTERS, DIRS, RADII)
+    u, _ = ts.solve(fm.levels, f, np.zeros_like(f), cfg)
+    want = u[3 * node:3 * node + 3]
+    # the two solves agree to solver tolerance (the EBE scatter order is not fixed), the sampling itself is exact
+    assert rel(bank, want) <= 1e-8
