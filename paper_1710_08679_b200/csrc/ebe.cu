@@ -752,7 +752,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
         for (int c = 0; c < 3; ++c) k |= spread(static_cast<uint64_t>((cen[3 * e + c] - lo[c]) * scale)) << c;
         int32_t vlo = m.tets10[10 * e];
         for (int a = 1; a < 4; ++a) vlo = std::min(vlo, m.tets10[10 * e + a]);
-        const auto slab = static_cast<uint8_t>(std::min<int64_t>(op->n_slabs - 1, int64_t(vlo) * op->n_slabs / vmax));
+        const auto slab = static_cast<uint8_t>(ebe_slab_of(vlo, vmax, op->n_slabs));
         key[e] = {elem_group ? elem_group[e] : uint8_t(0), slab, k, static_cast<int32_t>(e)};
       }
       __gnu_parallel::sort(key.begin(), key.end());

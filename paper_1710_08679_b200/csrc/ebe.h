@@ -1,6 +1,7 @@
 // ebe.h — device-resident matrix-free EBE operator (EbeOperator<T>,
 // ebe_operator.hpp:29-226), shared by the solver translation units.
 #pragma once
+#include <algorithm>
 #include <array>
 #include <memory>
 #include <mutex>
@@ -35,6 +36,18 @@ struct EbePairPlan {
 // TSGPU_EBE_SLABS overrides (1 = plain Morton)
 constexpr int kEbeSlabs = 16;
 int ebe_slab_count();
+// Slab of an element whose lowest vertex id is v (of V vertices), S slabs. The first
+// and last slabs are half as thick as the others: they are the host-buffer
+// apply's pipeline fill (first upload) and drain (last download), ebe_stream.cu.
+inline int ebe_slab_of(int64_t v, int64_t V, int S) {
+  if (S <= 2) return static_cast<int>(std::min<int64_t>(S - 1, v * S / std::max<int64_t>(1, V)));
+  constexpr int64_t kMid = 2;             // width of a middle slab in end-slab units
+  const int64_t units = kMid * (S - 2) + 2;
+  const int64_t k = v * units / std::max<int64_t>(1, V);
+  if (k == 0) return 0;
+  if (k >= units - 1) return S - 1;
+  return static_cast<int>(1 + (k - 1) / kMid);
+}
 
 // Host-buffer streaming schedule (ebe_stream.cu): the pair units cut into
 // chunks; node rows go up before the first chunk that reads them and come back

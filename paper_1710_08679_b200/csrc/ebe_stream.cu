@@ -61,7 +61,7 @@ std::unique_ptr<EbeStreamPlan> build_stream_plan(const ts_ebe& op) {
   for (int32_t i = 0; i < U; ++i) {
     const int32_t* w = pc.data() + size_t(i) * W;
     const int32_t lo = std::min(std::min(w[0], w[1]), std::min(w[2], w[3])) / 3;
-    const int sl = static_cast<int>(std::min<int64_t>(op.n_slabs - 1, int64_t(lo) * op.n_slabs / V));
+    const int sl = ebe_slab_of(lo, V, op.n_slabs);
     if (sl < prev) return P;  // not slab-ordered (e.g. grouped partition operators)
     if (sl != prev && i > 0 && i - P->unit_ptr.back() >= kMinUnitsPerChunk) P->unit_ptr.push_back(i);
     prev = sl;
