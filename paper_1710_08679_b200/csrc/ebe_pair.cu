@@ -279,6 +279,24 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Units per launch. The persistent grid's lane groups stride through the units
+// without synchronising, so over thousands of strides they drift apart and the
+// front of concurrently swept elements spreads over the mesh, losing the L2
+// reuse of shared node rows. Splitting a long sweep into launches of a bounded
+// number of strides re-aligns the front (TSGPU_EBE_PAIR_STRIDES, 0 = one launch).
+// configs[3] on one device, fp32 r=8: 29.3 -> 24.6 ms (5300 strides); configs[1] stays one launch (`profiles/r01_pair_strides.txt`).
+constexpr int64_t kPairLaunchStrides = 1024;
+int64_t pair_launch_units(int64_t units_per_stride, int64_t units) {
+  static const int64_t strides = [] {
+    const char* e = std::getenv("TSGPU_EBE_PAIR_STRIDES");
+    return e ? std::max<int64_t>(0, std::atoll(e)) : kPairLaunchStrides;
+  }();
+  if (strides == 0) return std::max<int64_t>(units, 1);
+  // equal launches of at most `strides` strides each
+  const int64_t cap = strides * units_per_stride, n = (units + cap - 1) / cap;
+  return std::max<int64_t>((units + n - 1) / n, 1);
+}
+
 template <typename T, typename V, int NPE, int B>
 bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p0, int32_t p1) {
   constexpr int CPT = LaneOps<V>::kCols;
@@ -303,8 +321,13 @@ bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p
     if (p1 <= p0) return true;
     const int64_t need = (int64_t(p1 - p0) + GROUPS - 1) / GROUPS;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
-    kern<<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()), p0, p1, u, f);
-    TS_CUDA_LAUNCH();
+    const int64_t step = pair_launch_units(int64_t(grid) * GROUPS, int64_t(p1) - p0);
+    for (int64_t a = p0; a < p1; a += step) {
+      const int32_t b = static_cast<int32_t>(std::min<int64_t>(p1, a + step));
+      kern<<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()),
+                                  static_cast<int32_t>(a), b, u, f);
+      TS_CUDA_LAUNCH();
+    }
     return true;
   }
 }
