@@ -483,15 +483,8 @@ bool launch_fast_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t e
     const size_t smem = 2 * size_t(NPE) * 3 * NT * sizeof(V) + 2 * size_t(GROUPS) * 12 * sizeof(T) +
                         2 * size_t(GROUPS) * CS * sizeof(int32_t);
     auto kern = k_ebe_fast<T, V, NPE, CS, B>;
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
-      int dev = 0;
-      TS_CUDA(cudaGetDevice(&dev));
-      TS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-      per_sm = std::max(per_sm, 1);
-    }
+    const KernelFit fit = kernel_fit<k_ebe_fast<T, V, NPE, CS, B>>(NT, smem);
+    const int sms = fit.sms, per_sm = std::max(fit.per_sm, 1);
     if (e1 <= e0) return true;
     const int64_t need = (int64_t(e1 - e0) + GROUPS - 1) / GROUPS;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));

@@ -100,6 +100,36 @@ struct ts_ebe {
 };
 
 namespace tsg {
+// Launch facts of one persistent sweep kernel on the CURRENT device: SM count and
+// resident blocks per SM at `smem` bytes of dynamic shared memory. The shared-memory
+// opt-in is a per-device function attribute, so it is set (and the occupancy
+// queried) once per device and per larger size, under a lock (callers may run on
+// several host threads, e.g. the in-process ranks of the partitioned tests).
+struct KernelFit {
+  int sms = 0;
+  int per_sm = 0;
+};
+template <auto Kernel>
+KernelFit kernel_fit(int threads, size_t smem) {
+  constexpr int kMaxDevices = 64;
+  static std::mutex mu;
+  static KernelFit fit[kMaxDevices];
+  static size_t configured[kMaxDevices] = {};
+  int dev = 0;
+  TS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("kernel_fit: device ordinal out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (!fit[dev].sms || smem > configured[dev]) {
+    TS_CUDA(cudaDeviceGetAttribute(&fit[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+    if (smem > configured[dev]) {
+      TS_CUDA(cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      configured[dev] = smem;
+    }
+    TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit[dev].per_sm, Kernel, threads, configured[dev]));
+  }
+  return fit[dev];
+}
+
 // pair sweep over units [p0, p1) (no init); false if the pair kernel does not cover `batch`
 bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t p0,
                           int32_t p1);

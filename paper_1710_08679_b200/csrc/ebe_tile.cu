@@ -324,23 +324,9 @@ bool launch_tile_c(const ts_ebe& op, const EbeTilePlan& plan, const T* u, T* f, 
                       sizeof(int) * kChunk * NPE + 3 * size_t(plan.rec_max);
   if (smem > 227 * 1024) return false;
   auto kern = k_ebe_tile<T, V, NPE, B, kChunk, ROWRED>;
-  static int sms = 0;
-  static size_t configured = 0;
-  static int per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    TS_CUDA(cudaGetDevice(&dev));
-    TS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  if (smem > configured) {
-    TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-    per_sm = 0;
-  }
-  if (!per_sm) {
-    TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::NT, smem));
-    if (per_sm < 1) return false;
-  }
+  const KernelFit fit = kernel_fit<k_ebe_tile<T, V, NPE, B, kChunk, ROWRED>>(Cfg::NT, smem);
+  const int sms = fit.sms, per_sm = fit.per_sm;
+  if (per_sm < 1) return false;
   if (c1 <= c0) return true;
   const int grid = std::max(1, std::min(c1 - c0, sms * per_sm));
   kern<<<grid, Cfg::NT, smem, s>>>(reinterpret_cast<const uint4*>(plan.rec.get()), plan.rec_off.get(), c0,
