@@ -56,6 +56,18 @@ def main():
                              "alg_gb": round(alg / 1e9, 3), "apply_gb_s": round(alg / ms / 1e6, 1),
                              "kernel_gb_s": round(alg / float(np.mean(ks)) / 1e6, 1),
                              "vector_gb": round(3 * N * r * 4 / 1e9, 2)}
+        if r == 8:  # end to end through the host entry: pinned u in, pinned f out
+            uh = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+            uh.copy_(u)
+            fh = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+            op.apply(uh.numpy(), fh.numpy())
+            t = time.perf_counter()
+            for _ in range(3):
+                op.apply(uh.numpy(), fh.numpy())
+            ms_h = (time.perf_counter() - t) / 3 * 1e3
+            out[f"fp32_r{r}"]["e2e"] = {"ms": round(ms_h, 1), "gb_s": round(alg / ms_h / 1e6, 1),
+                                        "pcie_bytes": 2 * u.numel() * 4, "entry": "ts_ebe_apply_host"}
+            del uh, fh
         del u, f
         torch.cuda.empty_cache()
     print(json.dumps(out))

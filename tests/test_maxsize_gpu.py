@@ -9,6 +9,8 @@ Checks (north-star fp32 tolerance 1e-5):
   boundary, constrained and free rows, random interior nodes) the rows of K u equal the
   checker's product on the sub-mesh of the elements touching them — a row of K u depends
   only on those elements (ebe_operator.hpp:112-115);
+* the host entry (pinned host u and f: H2D, sweep and D2H overlapped slab by slab) gives the
+  device product (per case, to the rounding of the unordered scatter);
 * symmetry of the constrained operator, (v, K u) = (u, K v) per case, a size-independent
   property of the whole sweep.
 """
@@ -92,6 +94,21 @@ def test_configs3_mesh_on_one_device(checker):
     assert rel(got, want[rows_loc]) <= 1e-5
     assert np.array_equal(got[mask[rows_glb] == 1], u_loc[rows_loc][mask[rows_glb] == 1])
     assert mask[rows_glb].any() and not mask[rows_glb].all()
+
+    # ---- the host entry (streamed H2D / sweep / D2H) at this size -------------------
+    uh = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+    uh.copy_(u)
+    fh = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+    op.apply(uh.numpy(), fh.numpy())
+    del uh
+    fd = fh.cuda()
+    del fh
+    num = torch.zeros(R, dtype=torch.float64, device="cuda")
+    for i in range(0, f.shape[0], 1 << 27):
+        d = (fd[i:i + (1 << 27)] - f[i:i + (1 << 27)]).double()
+        num += (d * d).sum(0)
+    del fd
+    assert bool(torch.all(num.sqrt() <= 1e-6 * torch.from_numpy(np.sqrt(chunked_dot(f, f))).cuda()))
 
     # ---- symmetry: (v, K u) = (u, K v) per case ----------------------------------
     v = torch.rand(3 * N, R, device="cuda", generator=g) * 2 - 1
