@@ -207,10 +207,13 @@ __global__ void __launch_bounds__(kFinThreads) k_rho_final(const double* partial
 // q (optional): the next EBE product's starting value, the masked identity of
 // the new p (ebe_operator.hpp:96-110), written here so the product skips its own
 // initialisation pass (mask null: zeros).
+// u (optional): the previous iteration's u += (T)alpha p (pcg.hpp:112-113), applied
+// here, where the old p is read anyway, instead of in the update pass — the same
+// operation on the same values, one vector read fewer per iteration.
 template <typename T, int W>
 __global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, T* __restrict__ p, int32_t n,
                             int32_t B, int first, const double* __restrict__ beta, T* __restrict__ q,
-                            const uint8_t* __restrict__ mask) {
+                            const uint8_t* __restrict__ mask, T* __restrict__ u, const double* __restrict__ alpha) {
   const int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * W;
   if (it >= int64_t(n) * B) return;
   const int64_t node = it / B;
@@ -226,6 +229,13 @@ __global__ void k_direction(const T* __restrict__ inv, const T* __restrict__ e, 
       const Pack<T, W> pp = ld<T, W>(pv + i * B);
 #pragma unroll
       for (int k = 0; k < W; ++k) z[i].v[k] = z[i].v[k] + static_cast<T>(beta[b0 + k]) * pp.v[k];
+      if (u) {
+        T* uv = u + 3 * node * B + b0 + i * B;
+        Pack<T, W> x = ld<T, W>(uv);
+#pragma unroll
+        for (int k = 0; k < W; ++k) x.v[k] = x.v[k] + static_cast<T>(alpha[b0 + k]) * pp.v[k];
+        st<T, W>(uv, x);
+      }
     }
     st<T, W>(pv + i * B, z[i]);
     if (q) {
@@ -293,12 +303,12 @@ __global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* parti
   }
 }
 
-// e += (T)(-alpha) q ; u += (T)alpha p (axpy_columns, vector_batch.hpp:72-83);
-// partials ||e||^2 and — for the next iteration's beta — (M^-1 e, e)
-// (pcg.hpp:72-73,116), one pass over the node's 3 dofs x W cases.
+// e += (T)(-alpha) q (axpy_columns, vector_batch.hpp:72-83); partials ||e||^2 and
+// — for the next iteration's beta — (M^-1 e, e) (pcg.hpp:72-73,116), one pass over
+// the node's 3 dofs x W cases. u += (T)alpha p is deferred to the next direction
+// pass (or pcg_apply_pending when the loop ends).
 template <typename T, int W>
 __global__ void __launch_bounds__(kRedThreads) k_update(const T* __restrict__ inv, T* __restrict__ e,
-                                                        T* __restrict__ u, const T* __restrict__ p,
                                                         const T* __restrict__ q, int32_t n, int32_t B,
                                                         const double* __restrict__ alpha,
                                                         const PcgStatus* __restrict__ st_, double* partial,
@@ -313,17 +323,10 @@ __global__ void __launch_bounds__(kRedThreads) k_update(const T* __restrict__ in
     if (!skip) {
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const Pack<T, W> qv = ld<T, W>(q + base + i * B), pv = ld<T, W>(p + base + i * B);
-        Pack<T, W> uv = ld<T, W>(u + base + i * B);
+        const Pack<T, W> qv = ld<T, W>(q + base + i * B);
 #pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const T a = static_cast<T>(alpha[b0 + k]);
-          const T na = static_cast<T>(-alpha[b0 + k]);
-          ev[i].v[k] = ev[i].v[k] + na * qv.v[k];
-          uv.v[k] = uv.v[k] + a * pv.v[k];
-        }
+        for (int k = 0; k < W; ++k) ev[i].v[k] = ev[i].v[k] + static_cast<T>(-alpha[b0 + k]) * qv.v[k];
         st<T, W>(e + base + i * B, ev[i]);
-        st<T, W>(u + base + i * B, uv);
       }
     }
     if (!own) return;
@@ -337,6 +340,20 @@ __global__ void __launch_bounds__(kRedThreads) k_update(const T* __restrict__ in
         acc[1][k] += double(z[i].v[k]) * double(ev[i].v[k]);
       }
   });
+}
+
+// u += (T)alpha p: the last iteration's deferred update (see k_direction)
+template <typename T, int W>
+__global__ void k_apply_pending(T* __restrict__ u, const T* __restrict__ p, int32_t n, int32_t B,
+                                const double* __restrict__ alpha) {
+  const int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * W;
+  if (it >= 3 * int64_t(n) * B) return;
+  const int b0 = static_cast<int>(it % B);
+  Pack<T, W> x = ld<T, W>(u + it);
+  const Pack<T, W> pp = ld<T, W>(p + it);
+#pragma unroll
+  for (int k = 0; k < W; ++k) x.v[k] = x.v[k] + static_cast<T>(alpha[b0 + k]) * pp.v[k];
+  st<T, W>(u + it, x);
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_ratio_final(const double* partial, int nd, int nblk, int32_t B,
@@ -732,9 +749,18 @@ void pcg_rho(int32_t B, bool first, const ColScalars& cs, Workspace& ws, cudaStr
 
 template <typename T>
 void pcg_direction(const T* inv, const T* e, T* p, int32_t n, int32_t B, bool first, const ColScalars& cs,
-                   cudaStream_t s, T* q_init, const uint8_t* mask) {
+                   cudaStream_t s, T* q_init, const uint8_t* mask, T* u_pending) {
+  if (u_pending && first) validation("pcg_direction: no previous direction to apply");
   TS_WIDTH_DISPATCH(T, B, (k_direction<T, W><<<grid_for(int64_t(n) * B / W, 256), 256, 0, s>>>(
-                               inv, e, p, n, B, first ? 1 : 0, cs[ColScalars::BETA], q_init, mask)));
+                               inv, e, p, n, B, first ? 1 : 0, cs[ColScalars::BETA], q_init, mask, u_pending,
+                               cs[ColScalars::ALPHA])));
+  TS_CUDA_LAUNCH();
+}
+
+template <typename T>
+void pcg_apply_pending(T* u, const T* p, int32_t n, int32_t B, const ColScalars& cs, cudaStream_t s) {
+  TS_WIDTH_DISPATCH(T, B, (k_apply_pending<T, W><<<grid_for(3 * int64_t(n) * B / W, 256), 256, 0, s>>>(
+                               u, p, n, B, cs[ColScalars::ALPHA])));
   TS_CUDA_LAUNCH();
 }
 
@@ -752,10 +778,10 @@ void pcg_gamma(const T* p, const T* q, int32_t n, int32_t B, const ColScalars& c
 }
 
 template <typename T>
-void pcg_update(const T* inv, T* e, T* u, const T* p, const T* q, int32_t n, int32_t B, const ColScalars& cs,
-                Workspace& ws, cudaStream_t s) {
+void pcg_update(const T* inv, T* e, const T* q, int32_t n, int32_t B, const ColScalars& cs, Workspace& ws,
+                cudaStream_t s) {
   ws.nblk = red_grid(int64_t(n) * B);
-  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<ws.nblk, kRedThreads, 0, s>>>(inv, e, u, p, q, n, B,
+  TS_WIDTH_DISPATCH(T, B, (k_update<T, W><<<ws.nblk, kRedThreads, 0, s>>>(inv, e, q, n, B,
                                                                            cs[ColScalars::ALPHA], ws.status.get(),
                                                                            ws.partial.get(), ws.owned)));
   TS_CUDA_LAUNCH();
@@ -785,11 +811,12 @@ void pcg_init(const T* inv, const T* r, T* e, int32_t n, int32_t B, const ColSca
 
 #define INST(T)                                                                                              \
   template void pcg_direction<T>(const T*, const T*, T*, int32_t, int32_t, bool, const ColScalars&,         \
-                                 cudaStream_t, T*, const uint8_t*);                                          \
+                                 cudaStream_t, T*, const uint8_t*, T*);                                      \
+  template void pcg_apply_pending<T>(T*, const T*, int32_t, int32_t, const ColScalars&, cudaStream_t);       \
   template void pcg_gamma<T>(const T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,           \
                              cudaStream_t);                                                                  \
-  template void pcg_update<T>(const T*, T*, T*, const T*, const T*, int32_t, int32_t, const ColScalars&,     \
-                              Workspace&, cudaStream_t);                                                     \
+  template void pcg_update<T>(const T*, T*, const T*, int32_t, int32_t, const ColScalars&, Workspace&,       \
+                              cudaStream_t);                                                                 \
   template void pcg_init<T>(const T*, const T*, T*, int32_t, int32_t, const ColScalars&, Workspace&,         \
                             cudaStream_t);                                                                   \
   template void bj_apply<T>(const T*, const T*, T*, int32_t, int32_t, cudaStream_t);

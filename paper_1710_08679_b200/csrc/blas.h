@@ -63,19 +63,26 @@ void dot2(const T* x0, const T* y0, const T* x1, const T* y1, int64_t ndof, int3
 // beta = first ? 0 : (rho_b != 0 ? rho_a / rho_b : 0)
 void pcg_rho(int32_t batch, bool first, const ColScalars& cs, Workspace& ws, cudaStream_t s);
 // p = M^-1 e + beta p  (first: p = M^-1 e); q_init (optional): masked identity of the new p
-// (zeros where mask is null), the starting value of the following EBE product
+// (zeros where mask is null), the starting value of the following EBE product;
+// u_pending (optional, not on the first iteration): first u += alpha p with the OLD p
+// (the update pass defers it)
 template <typename T>
 void pcg_direction(const T* inv, const T* e, T* p, int32_t n_nodes, int32_t batch, bool first,
-                   const ColScalars& cs, cudaStream_t s, T* q_init = nullptr, const uint8_t* mask = nullptr);
+                   const ColScalars& cs, cudaStream_t s, T* q_init = nullptr, const uint8_t* mask = nullptr,
+                   T* u_pending = nullptr);
+// u += alpha p: the deferred update of the last iteration, when the loop ends after an update
+template <typename T>
+void pcg_apply_pending(T* u, const T* p, int32_t n_nodes, int32_t batch, const ColScalars& cs, cudaStream_t s);
 // gamma = (p,q), plus ||p||^2, ||q||^2; alpha + stagnation/breakdown flags
 template <typename T>
 void pcg_gamma(const T* p, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,
                cudaStream_t s);
-// unless stagnated/broken: e -= alpha q ; u += alpha p ; en2 = ||e||^2 ; ratio;
-// also the (M^-1 e, e) partials of the next iteration (pcg_rho)
+// unless stagnated/broken: e -= alpha q ; en2 = ||e||^2 ; ratio; also the (M^-1 e, e)
+// partials of the next iteration (pcg_rho). The matching u += alpha p is left pending
+// (pcg_direction's u_pending / pcg_apply_pending).
 template <typename T>
-void pcg_update(const T* inv, T* e, T* u, const T* p, const T* q, int32_t n_nodes, int32_t batch,
-                const ColScalars& cs, Workspace& ws, cudaStream_t s);
+void pcg_update(const T* inv, T* e, const T* q, int32_t n_nodes, int32_t batch, const ColScalars& cs,
+                Workspace& ws, cudaStream_t s);
 // e = r - Au (Au in e on entry); rn2 = ||r||^2, en2 = ||e||^2, ratio; (M^-1 e, e) partials
 template <typename T>
 void pcg_init(const T* inv, const T* r, T* e, int32_t n_nodes, int32_t batch, const ColScalars& cs, Workspace& ws,

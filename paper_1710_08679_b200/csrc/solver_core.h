@@ -45,23 +45,29 @@ InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t 
   const double tol2 = tol * tol;
   double ratio = read_status(ws, s).ratio;
   if (std::isnan(ratio)) fail(TS_ERR_NONFINITE, "inner_pcg: non-finite initial residual");
+  // u += alpha p of the last completed iteration, folded into the next direction pass
+  // (which reads the old p anyway) or applied once after the loop
+  bool pending = false;
   while (ratio > tol2 && st.iterations < max_iter) {
     const bool first = st.iterations == 0;
     pcg_rho(B, first, cs, ws, s);
-    pcg_direction<T>(inv, e, p, n, B, first, cs, s, fuse_init ? q : nullptr, op_mask);
+    pcg_direction<T>(inv, e, p, n, B, first, cs, s, fuse_init ? q : nullptr, op_mask, pending ? u : nullptr);
+    pending = false;
     A(p, q, !fuse_init);
     pcg_gamma<T>(p, q, n, B, cs, ws, s);
-    pcg_update<T>(inv, e, u, p, q, n, B, cs, ws, s);
+    pcg_update<T>(inv, e, q, n, B, cs, ws, s);
     const PcgStatus& ps = read_status(ws, s);
     if (ps.breakdown_col >= 0)
       fail(TS_ERR_BREAKDOWN, "inner_pcg: breakdown (p,Ap) <= 0 at iteration " + std::to_string(st.iterations + 1) +
                                  ", column " + std::to_string(ps.breakdown_col));
-    if (ps.stagnated) break;
+    if (ps.stagnated) break;  // the reference leaves u and e as they were (pcg.hpp:99-104)
+    pending = true;
     ++st.iterations;
     ratio = ps.ratio;
     if (std::isnan(ratio))
       fail(TS_ERR_NONFINITE, "inner_pcg: non-finite residual at iteration " + std::to_string(st.iterations));
   }
+  if (pending) pcg_apply_pending<T>(u, p, n, B, cs, s);
   st.converged = ratio <= tol2;
   return st;
 }
