@@ -17,7 +17,7 @@
 //   integrand, element_stiffness.hpp:35-51) also computes.
 //   tet4: constant strain, f_a = V sigma b_a.
 //
-// Cost per load case: ~500 flops (tet10) / ~85 flops (tet4), all FFMA2 /
+// Cost per load case: ~480 flops (tet10) / ~85 flops (tet4), all FFMA2 /
 // FADD2 / FMUL2 for fp32 pairs. Validated against the reference K_e to
 // 1.8e-15 relative (tests/test_element_formulation.py).
 //
@@ -68,17 +68,18 @@ template <class V>
 __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[3][3], V lp, V mp,
                                               V (&f)[10][3]) {
   using O = LaneOps<V>;
-  const V three = O::splat(3), four = O::splat(4), mfour = O::splat(-4);
+  const V three = O::splat(3), four = O::splat(4), mfour = O::splat(-4), mthree = O::splat(-3);
   const V mp2 = O::add(mp, mp);
   // edge nodes: 4=(0,1) 5=(1,2) 6=(2,0) 7=(0,3) 8=(1,3) 9=(2,3)
   V S[4][6];
   {
-    V E[3][3];  // vertex 0: E_0k = 4 u_0k - (3 u_0 + u_k)
+    V E[3][3];  // vertex 0: E_0k = 4 u_0k + (-3 u_0 - u_k)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      E[c][0] = O::sub(O::mul(four, u[4][c]), O::fma(three, u[0][c], u[1][c]));
-      E[c][1] = O::sub(O::mul(four, u[6][c]), O::fma(three, u[0][c], u[2][c]));
-      E[c][2] = O::sub(O::mul(four, u[7][c]), O::fma(three, u[0][c], u[3][c]));
+      const V m = O::mul(mthree, u[0][c]);
+      E[c][0] = O::fma(four, u[4][c], O::sub(m, u[1][c]));
+      E[c][1] = O::fma(four, u[6][c], O::sub(m, u[2][c]));
+      E[c][2] = O::fma(four, u[7][c], O::sub(m, u[3][c]));
     }
     V G[3][3];
     grad_from(E, b, G);
@@ -127,7 +128,13 @@ __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[
 #pragma unroll
   for (int q = 0; q < 6; ++q) Ssum[q] = O::add(O::add(S[0][q], S[1][q]), O::add(S[2][q], S[3][q]));
 
-  // j = 0: H_0k ; f0 = -3 T0 ; f4,f6,f7 = 4 H_0k ; f1,f2,f3 = -H_0k
+  // f = E^T H, H_jk = (S_j + sum_i S_i)(V/20) b_k, T_j = sum_k H_jk, accumulated per j:
+  //   f0 = -3 T0 + T1 + T2 + T3          f1 = -H01 + 3 H11 - H21 - H31
+  //   f2 = -H02 - H12 + 3 H22 - H32      f3 = -H03 - H13 - H23 + 3 H33
+  //   f4 = 4 (H01 - T1)  f6 = 4 (H02 - T2)  f7 = 4 (H03 - T3)
+  //   f5 = 4 (H12 + H21)  f8 = 4 (H13 + H31)  f9 = 4 (H23 + H32)
+  // The negated sums ride in FFMA2 operand signs (O::neg), so no separate negations.
+  V t0[3], s0[3];
   {
     V sh[6];
 #pragma unroll
@@ -138,17 +145,15 @@ __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[
     sym_mul(sh, b[2], h3);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
-      f[0][c] = O::mul(O::splat(-3), t);
+      t0[c] = O::add(O::add(h1[c], h2[c]), h3[c]);
       f[4][c] = O::mul(four, h1[c]);
       f[6][c] = O::mul(four, h2[c]);
       f[7][c] = O::mul(four, h3[c]);
-      f[1][c] = O::sub(O::zero(), h1[c]);
-      f[2][c] = O::sub(O::zero(), h2[c]);
-      f[3][c] = O::sub(O::zero(), h3[c]);
+      f[1][c] = h1[c];  // +H01 (negated below)
+      f[2][c] = h2[c];  // +H02 ...
+      f[3][c] = h3[c];  // +H03 ...
     }
   }
-  // j = 1: f0 += T1 ; f4 -= 4 T1 ; f1 += 3 H_11 ; f5 = 4 H_12 ; f2 -= H_12 ; f8 = 4 H_13 ; f3 -= H_13
   {
     V sh[6];
 #pragma unroll
@@ -160,16 +165,15 @@ __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
-      f[0][c] = O::add(f[0][c], t);
+      s0[c] = t;
       f[4][c] = O::fma(mfour, t, f[4][c]);
-      f[1][c] = O::fma(three, h1[c], f[1][c]);
+      f[1][c] = O::fma(three, h1[c], O::neg(f[1][c]));  // 3 H11 - H01
       f[5][c] = O::mul(four, h2[c]);
-      f[2][c] = O::sub(f[2][c], h2[c]);
+      f[2][c] = O::add(f[2][c], h2[c]);                 // H02 + H12
       f[8][c] = O::mul(four, h3[c]);
-      f[3][c] = O::sub(f[3][c], h3[c]);
+      f[3][c] = O::add(f[3][c], h3[c]);                 // H03 + H13
     }
   }
-  // j = 2: f0 += T2 ; f6 -= 4 T2 ; f5 += 4 H_21 ; f1 -= H_21 ; f2 += 3 H_22 ; f9 = 4 H_23 ; f3 -= H_23
   {
     V sh[6];
 #pragma unroll
@@ -181,16 +185,15 @@ __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
-      f[0][c] = O::add(f[0][c], t);
+      s0[c] = O::add(s0[c], t);
       f[6][c] = O::fma(mfour, t, f[6][c]);
       f[5][c] = O::fma(four, h1[c], f[5][c]);
       f[1][c] = O::sub(f[1][c], h1[c]);
-      f[2][c] = O::fma(three, h2[c], f[2][c]);
+      f[2][c] = O::fma(three, h2[c], O::neg(f[2][c]));  // 3 H22 - H02 - H12
       f[9][c] = O::mul(four, h3[c]);
-      f[3][c] = O::sub(f[3][c], h3[c]);
+      f[3][c] = O::add(f[3][c], h3[c]);                 // H03 + H13 + H23
     }
   }
-  // j = 3: f0 += T3 ; f7 -= 4 T3 ; f8 += 4 H_31 ; f1 -= H_31 ; f9 += 4 H_32 ; f2 -= H_32 ; f3 += 3 H_33
   {
     V sh[6];
 #pragma unroll
@@ -202,13 +205,13 @@ __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
-      f[0][c] = O::add(f[0][c], t);
+      f[0][c] = O::fma(mthree, t0[c], O::add(s0[c], t));
       f[7][c] = O::fma(mfour, t, f[7][c]);
       f[8][c] = O::fma(four, h1[c], f[8][c]);
       f[1][c] = O::sub(f[1][c], h1[c]);
       f[9][c] = O::fma(four, h2[c], f[9][c]);
       f[2][c] = O::sub(f[2][c], h2[c]);
-      f[3][c] = O::fma(three, h3[c], f[3][c]);
+      f[3][c] = O::fma(three, h3[c], O::neg(f[3][c]));  // 3 H33 - H03 - H13 - H23
     }
   }
 }

@@ -23,6 +23,8 @@ template <> struct LaneOps<float2> {
   }
   __device__ __forceinline__ static float2 mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
   __device__ __forceinline__ static float2 fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+  // only as an FFMA2 operand: the sign folds into the instruction (no extra op)
+  __device__ __forceinline__ static float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
   // c - a*b
   __device__ __forceinline__ static float2 fnma(float2 a, float2 b, float2 c) {
     return __ffma2_rn(make_float2(-a.x, -a.y), b, c);
@@ -38,6 +40,7 @@ template <> struct LaneOps<float> {
   __device__ __forceinline__ static float sub(float a, float b) { return a - b; }
   __device__ __forceinline__ static float mul(float a, float b) { return a * b; }
   __device__ __forceinline__ static float fma(float a, float b, float c) { return fmaf(a, b, c); }
+  __device__ __forceinline__ static float neg(float a) { return -a; }
   __device__ __forceinline__ static float fnma(float a, float b, float c) { return fmaf(-a, b, c); }
 };
 
@@ -50,6 +53,7 @@ template <> struct LaneOps<double> {
   __device__ __forceinline__ static double sub(double a, double b) { return a - b; }
   __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
   __device__ __forceinline__ static double fma(double a, double b, double c) { return ::fma(a, b, c); }
+  __device__ __forceinline__ static double neg(double a) { return -a; }
   __device__ __forceinline__ static double fnma(double a, double b, double c) { return ::fma(-a, b, c); }
 };
 
