@@ -222,3 +222,44 @@ def test_host_apply_streams_and_matches_device(order, prec, batch):
     fp = op.apply(u.cpu().numpy())
     assert float((torch.from_numpy(fp).cuda().double() - f_dev.double()).norm() / f_dev.double().norm()) <= (
         1e-6 if prec == 32 else 1e-14)
+
+
+_SPLIT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/oracle'); sys.path.insert(0, sys.argv[1] + '/tests')
+import paper_1710_08679_b200 as ts
+from conftest import TWO_LAYER, lame
+from oracle import Oracle, have_reference
+chk = Oracle('reference' if have_reference() else 'port')
+spec = ((4000.0, 3000.0, 2000.0), (40, 30, 20), (1000.0,), 1)
+mesh, om = ts.generate_box_mesh(*spec), chk.box_mesh(*spec)
+lam, mu = lame(TWO_LAYER)
+worst = 0.0
+for prec, order, batch in ((32, 2, 16), (32, 1, 4), (64, 2, 8), (32, 2, 1)):
+    nn = mesh.vertex_count if order == 1 else mesh.node_count()
+    mask = mesh.dirichlet_mask()[: 3 * nn]
+    op = ts.EbeOperator(mesh, order, [ts.material_from_wavespeeds(*t) for t in TWO_LAYER], mask, prec=prec)
+    dt = np.float32 if prec == 32 else np.float64
+    u = chk.rng_sym(5 + batch, 3 * nn * batch).reshape(3 * nn, batch).astype(dt)
+    want = chk.ebe_apply(om, order, lam, mu, mask, prec, u)
+    got = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    r = float(np.linalg.norm(got.astype(np.float64) - want) / np.linalg.norm(want))
+    worst = max(worst, r / (1e-5 if prec == 32 else 1e-12))
+print(worst)
+"""
+
+
+@pytest.mark.parametrize("strides", ["1", "3"])
+def test_pair_sweep_split_into_many_launches(strides):
+    """TSGPU_EBE_PAIR_STRIDES (read once per process, so in a child process): a sweep
+    split into launches of 1 or 3 grid strides each (up to ~30 launches here) gives
+    the reference's product, as the single-launch sweep does."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSGPU_EBE_PAIR_STRIDES=strides, TSGPU_EBE_KERNEL="pair")
+    out = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT, root], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1.0
