@@ -105,6 +105,8 @@ ts_status ts_mesh_sizes(const ts_mesh* m, int32_t* n_nodes, int32_t* vertex_coun
 /* any output pointer may be NULL */
 ts_status ts_mesh_export(const ts_mesh* m, double* coords, int32_t* tets10,
                          int32_t* material_id, int32_t* bc_node, int8_t* bc_axis);
+/* validate_mesh (mesh.hpp:75-113): TS_ERR_VALIDATION naming the first offending element */
+ts_status ts_mesh_validate(const ts_mesh* m);
 /* dirichlet_mask (mesh.hpp:150-154): 3*n_nodes bytes */
 ts_status ts_mesh_dirichlet_mask(const ts_mesh* m, uint8_t* mask);
 void ts_mesh_destroy(ts_mesh* m);
@@ -190,7 +192,99 @@ ts_status ts_ebe_block_jacobi_host(const ts_ebe* op, void* inv_blocks);
  * device time of the last apply's EBE kernel when timing is enabled. */
 ts_status ts_ebe_set_timing(ts_ebe* op, int32_t enable);
 ts_status ts_ebe_last_kernel_ms(const ts_ebe* op, float* ms);
-ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t* n);
+ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t batch, int32_t* n);
+/* deterministic mode (on != 0): the colored sweep (greedy element coloring, build_coloring
+ * ebe_operator.hpp:190-214, one launch per color, plain read-add-writes) — every node sums its
+ * elements in a fixed order, so results are bitwise reproducible and independent of the batch
+ * width (the reference's contract, test_ebe.cpp:254-317). Default off (atomic pair sweep). */
+ts_status ts_ebe_set_deterministic(ts_ebe* op, int32_t on);
+
+/* element_matrix (ebe_operator.hpp:78-87): K_e of caller element e in fp64 from the
+ * operator's (T-rounded) geometry, row-major [3 npe][3 npe], index 3 local_node + axis
+ * (element_stiffness.hpp:13-14). k is a HOST array. */
+ts_status ts_ebe_element_matrix(const ts_ebe* op, int32_t e, double* k);
+/* assemble_bcsr(EbeOperator<T>) (ebe_operator.hpp:230-284): identity rows at constrained
+ * dofs, constrained columns dropped, blocks summed in fp64 in ascending element order and
+ * rounded to T. Call with row_ptr = col_idx = blocks = NULL to get *nnzb, then with HOST
+ * arrays row_ptr [n_nodes + 1], col_idx [nnzb], blocks [nnzb][9] of the operator precision. */
+ts_status ts_ebe_assemble_bcsr(const ts_ebe* op, int64_t* nnzb, int32_t* row_ptr, int32_t* col_idx, void* blocks);
+
+/* ------------------------------------------------ standalone operators (block_csr.hpp,
+ * block_jacobi.hpp, prolongation.hpp, pcg.hpp). Created from HOST arrays, held on the
+ * device, immutable; *_apply take device pointers and a stream, *_host copy in/out. */
+
+/* BlockCsrMatrix<T> (block_csr.hpp:16-70): n_block_rows, row_ptr [n+1], col_idx [nnzb]
+ * (strictly increasing per row, block_csr.hpp:14), blocks [nnzb][9] of prec-sized scalars */
+typedef struct ts_bcsr ts_bcsr;
+ts_status ts_bcsr_create(int32_t n_block_rows, const int32_t* row_ptr, const int32_t* col_idx, const void* blocks,
+                         int32_t prec, ts_bcsr** out);
+void ts_bcsr_destroy(ts_bcsr* a);
+ts_status ts_bcsr_info(const ts_bcsr* a, int32_t* n_block_rows, int64_t* nnzb, int32_t* prec);
+/* BlockCsrMatrix::apply (block_csr.hpp:33-69): fp64 row accumulation in stored order, rounded to T */
+ts_status ts_bcsr_apply(const ts_bcsr* a, const void* u, void* f, int32_t batch, void* stream);
+ts_status ts_bcsr_apply_host(const ts_bcsr* a, const void* u, void* f, int32_t batch);
+/* extract_block_jacobi(BlockCsrMatrix) (block_jacobi.hpp:72-85) -> HOST [n][9] of prec scalars */
+ts_status ts_bcsr_block_jacobi_host(const ts_bcsr* a, void* inv_blocks);
+
+/* BlockJacobi<T> (block_jacobi.hpp:15-39): inverse 3x3 node blocks [n][9] */
+typedef struct ts_bj ts_bj;
+ts_status ts_bj_create(int32_t n_nodes, const void* inv_blocks, int32_t prec, ts_bj** out);
+void ts_bj_destroy(ts_bj* m);
+/* BlockJacobi::apply (block_jacobi.hpp:22-38): z = M^-1 r, fp64 math rounded to T */
+ts_status ts_bj_apply(const ts_bj* m, const void* r, void* z, int32_t batch, void* stream);
+ts_status ts_bj_apply_host(const ts_bj* m, const void* r, void* z, int32_t batch);
+
+/* Prolongation (prolongation.hpp:13-62): per fine node CSR row_ptr [n_fine+1], cols / weights;
+ * the same weights on every axis. apply: fine = P coarse; restrict: coarse = P^T fine, summed in
+ * ascending fine row (the reference's serial scatter order), both in T = prec. */
+typedef struct ts_prolong ts_prolong;
+ts_status ts_prolong_create(int32_t n_fine, int32_t n_coarse, const int32_t* row_ptr, const int32_t* cols,
+                            const double* weights, ts_prolong** out);
+void ts_prolong_destroy(ts_prolong* p);
+ts_status ts_prolong_apply(const ts_prolong* p, int32_t prec, const void* coarse, void* fine, int32_t batch,
+                           void* stream);
+ts_status ts_prolong_restrict(const ts_prolong* p, int32_t prec, const void* fine, void* coarse, int32_t batch,
+                              void* stream);
+/* host buffers: restrict_to_coarse = 0 -> apply (in = coarse), 1 -> restrict (in = fine) */
+ts_status ts_prolong_apply_host(const ts_prolong* p, int32_t prec, int32_t restrict_to_coarse, const void* in,
+                                void* out, int32_t batch);
+/* build_geometric_prolongation (prolongation.hpp:67-98) into HOST arrays row_ptr [N+1],
+ * cols / weights [V + 2 (N - V)] */
+ts_status ts_geometric_prolongation(const ts_mesh* mesh, int32_t* row_ptr, int32_t* cols, double* weights);
+
+/* inner_pcg (pcg.hpp:52-124) with the block-Jacobi preconditioner m: kind 0 = a ts_ebe,
+ * 1 = a ts_bcsr operator (same precision as m). u is the warm start and the result;
+ * iterations / converged are InnerStats (pcg.hpp:15-18). Breakdown -> TS_ERR_BREAKDOWN,
+ * non-finite residual -> TS_ERR_NONFINITE (SolverError). */
+ts_status ts_inner_pcg(int32_t kind, const void* op, const ts_bj* m, const void* r, void* u, int32_t n_nodes,
+                       int32_t batch, double tol, int32_t max_iter, int32_t* iterations, int32_t* converged,
+                       void* stream);
+ts_status ts_inner_pcg_host(int32_t kind, const void* op, const ts_bj* m, const void* r, void* u, int32_t n_nodes,
+                            int32_t batch, double tol, int32_t max_iter, int32_t* iterations, int32_t* converged);
+
+/* level-2 setup on HOST arrays (aggregation.hpp:23-170; the same sequential, order-exact code
+ * build_solver_levels runs). aggregate_p1: greedy BFS aggregation of the block graph of K1
+ * (row_ptr [n+1], col_idx) into agg_of_node [n], *n_aggregates, seeds [n] (first *n_aggregates
+ * used; may be NULL). build_level2: A2 = P^T K1 P of fp64 blocks [nnzb][9], constrained fine dofs
+ * (fine_mask [3n], NULL = none) dropped, empty coarse diagonals -> 1; call with NULL outputs for
+ * *nnzb2, then row_ptr2 [n_aggregates+1], col_idx2 [nnzb2], blocks2 [nnzb2][9]. */
+ts_status ts_aggregate_p1(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, int32_t target,
+                          int32_t* agg_of_node, int32_t* n_aggregates, int32_t* seeds);
+ts_status ts_build_level2(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, const double* blocks,
+                          const int32_t* agg_of_node, int32_t n_aggregates, const uint8_t* fine_mask, int64_t* nnzb2,
+                          int32_t* row_ptr2, int32_t* col_idx2, double* blocks2);
+
+/* per-column vector operations on HOST VectorBatch data (vector_batch.hpp:43-119), computed
+ * on the device: dot_columns (fp64 accumulation) -> out [batch]; axpy y += (T)alpha_b x;
+ * xpby p = z + (T)beta_b p; sub out = a - b (n scalars); zero_masked (mask [ndof]); cast_batch */
+ts_status ts_dot_columns_host(int32_t prec, int64_t ndof, int32_t batch, const void* x, const void* y, double* out);
+ts_status ts_axpy_columns_host(int32_t prec, int64_t ndof, int32_t batch, const double* alpha, const void* x,
+                               void* y);
+ts_status ts_xpby_columns_host(int32_t prec, int64_t ndof, int32_t batch, const void* z, const double* beta,
+                               void* p);
+ts_status ts_sub_columns_host(int32_t prec, int64_t n, const void* a, const void* b, void* out);
+ts_status ts_zero_masked_host(int32_t prec, int64_t ndof, int32_t batch, void* x, const uint8_t* mask);
+ts_status ts_cast_batch_host(int32_t from_prec, int32_t to_prec, int64_t n, const void* x, void* y);
 
 /* ------------------------------------------------------------ level set */
 
@@ -209,25 +303,39 @@ ts_status ts_levels_sizes(const ts_levels* lv, int32_t* n0, int32_t* n1, int32_t
  * blocks [nnzb2][9] float, mask2 [3*n2], m2 inverse blocks [n2][9] float */
 ts_status ts_levels_export(const ts_levels* lv, int32_t* agg_of_node, int32_t* row_ptr2,
                            int32_t* col_idx2, float* blocks2, uint8_t* mask2, float* m2_inv);
+/* the fine-level members of SolverLevels (adaptive_cg.hpp:27-36), any pointer may be NULL:
+ * m0 [n0][9], m1 [n1][9] float inverse blocks, mask0 [3 n0], mask1 [3 n1], and the
+ * aggregation's seed nodes [n2] (Aggregation::seeds, aggregation.hpp:13-17) */
+ts_status ts_levels_export_fine(const ts_levels* lv, float* m0_inv, float* m1_inv, uint8_t* mask0, uint8_t* mask1,
+                                int32_t* seeds);
 /* the operators inside the level set (borrowed, owned by lv) */
 ts_status ts_levels_operator(const ts_levels* lv, int32_t which /*0 outer,1 level0,2 level1*/,
                              const ts_ebe** op);
 
 /* the level operator the solve applies (device buffers): 0 outer fp64 tet10, 1 level-0
  * fp32 tet10, 2 level-1 fp32 tet4 — the assembled K1 (float-rounded inputs, fp32 sums)
- * unless TSGPU_L1=ebe; same product as EbeOperator<float> order 1 (ebe_operator.hpp:90) */
+ * unless TSGPU_L1=ebe; same product as EbeOperator<float> order 1 (ebe_operator.hpp:90) —
+ * 3 level-2 Galerkin BCSR (BlockCsrMatrix<float>::apply, block_csr.hpp:33-69) */
 ts_status ts_levels_apply(ts_levels* lv, int32_t which, const void* u, void* f, int32_t batch, void* stream);
+/* the preconditioner's inter-grid transfers as the solve runs them (fp32 device buffers), each
+ * followed by zero_masked on its output level (adaptive_cg.hpp:84-107): 0 u0 = P1 u1, 1 r1 = P1^T r0,
+ * 2 u1 = P2 u2, 3 r2 = P2^T r1 (Prolongation::apply / restrict_to_coarse, prolongation.hpp:25-61) */
+ts_status ts_levels_transfer(ts_levels* lv, int32_t which, const float* in, float* out, int32_t batch, void* stream);
 
-/* solve (adaptive_cg.hpp:242-263) with host buffers; u_out may alias u0. */
+/* solve (adaptive_cg.hpp:242-263) with host buffers; u_out may alias u0.
+ * n_nodes is the node count f, u0 and u_out were sized for: it must equal the
+ * level set's (TS_ERR_VALIDATION "solve: dimension mismatch" otherwise, the
+ * reference's shape check, ebe_operator.hpp:91-93), so no buffer is over-read
+ * or overrun. */
 ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_out,
-                   int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);
+                   int32_t n_nodes, int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);
 /* solve with device buffers on a stream */
 ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, double* u_out,
-                          int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep,
+                          int32_t n_nodes, int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep,
                           void* stream);
-/* solve_pcge (adaptive_cg.hpp:267-279), host buffers, 64-bit operator. */
+/* solve_pcge (adaptive_cg.hpp:267-279), host buffers, 64-bit operator; n_nodes as in ts_solve. */
 ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, double* u_out,
-                        int32_t batch, double tol, int32_t max_iter, ts_solve_report* rep);
+                        int32_t n_nodes, int32_t batch, double tol, int32_t max_iter, ts_solve_report* rep);
 
 /* ------------------------------------------------ partitioned (multi-GPU) solve
  *
@@ -282,9 +390,9 @@ ts_status ts_dist_levels_sizes(const ts_dist_levels* lv, int32_t* n_local, int32
 ts_status ts_dist_local_nodes(const ts_dist_levels* lv, int32_t* l2g);
 /* solve (adaptive_cg.hpp:242-263) on local vectors; host or device buffers */
 ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, double* u_out,
-                        int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);
+                        int32_t n_local, int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);
 ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double* u0, double* u_out,
-                               int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep,
+                               int32_t n_local, int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep,
                                void* stream);
 /* one partitioned EBE product (device buffers, local order) incl. the halo
  * exchange: which = 0 outer fp64 tet10, 1 level-0 fp32 tet10, 2 level-1 fp32 tet4 */

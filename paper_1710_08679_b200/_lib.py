@@ -102,16 +102,48 @@ _sig = {
     "ts_ebe_host_stream_chunks": (C.c_int, [vp, vp]),
     "ts_ebe_set_timing": (C.c_int, [vp, i32]),
     "ts_ebe_last_kernel_ms": (C.c_int, [vp, vp]),
-    "ts_ebe_launches_per_apply": (C.c_int, [vp, vp]),
+    "ts_ebe_launches_per_apply": (C.c_int, [vp, i32, vp]),
+    "ts_ebe_set_deterministic": (C.c_int, [vp, i32]),
     "ts_levels_create": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "ts_levels_destroy": (None, [vp]),
     "ts_levels_sizes": (C.c_int, [vp, vp, vp, vp, vp]),
     "ts_levels_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "ts_levels_operator": (C.c_int, [vp, i32, vp]),
     "ts_levels_apply": (C.c_int, [vp, i32, vp, vp, i32, vp]),
-    "ts_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
-    "ts_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
-    "ts_solve_pcge": (C.c_int, [vp, vp, vp, vp, i32, C.c_double, i32, vp]),
+    "ts_levels_transfer": (C.c_int, [vp, i32, vp, vp, i32, vp]),
+    "ts_levels_export_fine": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "ts_mesh_validate": (C.c_int, [vp]),
+    "ts_ebe_element_matrix": (C.c_int, [vp, i32, vp]),
+    "ts_ebe_assemble_bcsr": (C.c_int, [vp, vp, vp, vp, vp]),
+    "ts_bcsr_create": (C.c_int, [i32, vp, vp, vp, i32, vp]),
+    "ts_bcsr_destroy": (None, [vp]),
+    "ts_bcsr_info": (C.c_int, [vp, vp, vp, vp]),
+    "ts_bcsr_apply": (C.c_int, [vp, vp, vp, i32, vp]),
+    "ts_bcsr_apply_host": (C.c_int, [vp, vp, vp, i32]),
+    "ts_bcsr_block_jacobi_host": (C.c_int, [vp, vp]),
+    "ts_bj_create": (C.c_int, [i32, vp, i32, vp]),
+    "ts_bj_destroy": (None, [vp]),
+    "ts_bj_apply": (C.c_int, [vp, vp, vp, i32, vp]),
+    "ts_bj_apply_host": (C.c_int, [vp, vp, vp, i32]),
+    "ts_prolong_create": (C.c_int, [i32, i32, vp, vp, vp, vp]),
+    "ts_prolong_destroy": (None, [vp]),
+    "ts_prolong_apply": (C.c_int, [vp, i32, vp, vp, i32, vp]),
+    "ts_prolong_restrict": (C.c_int, [vp, i32, vp, vp, i32, vp]),
+    "ts_prolong_apply_host": (C.c_int, [vp, i32, i32, vp, vp, i32]),
+    "ts_geometric_prolongation": (C.c_int, [vp, vp, vp, vp]),
+    "ts_inner_pcg": (C.c_int, [i32, vp, vp, vp, vp, i32, i32, C.c_double, i32, vp, vp, vp]),
+    "ts_inner_pcg_host": (C.c_int, [i32, vp, vp, vp, vp, i32, i32, C.c_double, i32, vp, vp]),
+    "ts_aggregate_p1": (C.c_int, [i32, vp, vp, i32, vp, vp, vp]),
+    "ts_build_level2": (C.c_int, [i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp]),
+    "ts_dot_columns_host": (C.c_int, [i32, C.c_int64, i32, vp, vp, vp]),
+    "ts_axpy_columns_host": (C.c_int, [i32, C.c_int64, i32, vp, vp, vp]),
+    "ts_xpby_columns_host": (C.c_int, [i32, C.c_int64, i32, vp, vp, vp]),
+    "ts_sub_columns_host": (C.c_int, [i32, C.c_int64, vp, vp, vp]),
+    "ts_zero_masked_host": (C.c_int, [i32, C.c_int64, i32, vp, vp]),
+    "ts_cast_batch_host": (C.c_int, [i32, i32, C.c_int64, vp, vp]),
+    "ts_solve": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp]),
+    "ts_solve_device": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp, vp]),
+    "ts_solve_pcge": (C.c_int, [vp, vp, vp, vp, i32, i32, C.c_double, i32, vp]),
     "ts_comm_nccl_available": (C.c_int, [vp, i32]),
     "ts_comm_nccl_id": (C.c_int, [vp]),
     "ts_comm_create_nccl": (C.c_int, [i32, i32, vp, i32, vp]),
@@ -128,8 +160,8 @@ _sig = {
     "ts_dist_levels_destroy": (None, [vp]),
     "ts_dist_levels_sizes": (C.c_int, [vp, vp, vp, vp]),
     "ts_dist_local_nodes": (C.c_int, [vp, vp]),
-    "ts_dist_solve": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
-    "ts_dist_solve_device": (C.c_int, [vp, vp, vp, vp, i32, vp, vp, vp]),
+    "ts_dist_solve": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp]),
+    "ts_dist_solve_device": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp, vp]),
     "ts_dist_ebe_apply": (C.c_int, [vp, i32, vp, vp, i32, vp]),
     "ts_dist_ebe_create": (C.c_int, [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp]),
     "ts_dist_ebe_destroy": (None, [vp]),

@@ -125,6 +125,13 @@ ts_status ts_mesh_from_arrays(int32_t n_nodes, int32_t vertex_count, const doubl
   TS_API_END
 }
 
+ts_status ts_mesh_validate(const ts_mesh* m) {
+  TS_API_BEGIN
+  TS_REQUIRE(m, "mesh: null handle");
+  tsg::validate_mesh(m->m);
+  TS_API_END
+}
+
 // ------------------------------------------------------------ file formats
 ts_status ts_mesh_write_tsmesh(const ts_mesh* m, const char* path) {
   TS_API_BEGIN
@@ -399,10 +406,18 @@ ts_status ts_ebe_last_kernel_ms(const ts_ebe* op, float* ms) {
   TS_API_END
 }
 
-ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t* n) {
+ts_status ts_ebe_set_deterministic(ts_ebe* op, int32_t on) {
+  TS_API_BEGIN
+  TS_REQUIRE(op, "ebe: null handle");
+  tsg::ebe_set_deterministic(*op, on != 0);
+  TS_API_END
+}
+
+ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t batch, int32_t* n) {
   TS_API_BEGIN
   TS_REQUIRE(op && n, "ebe: null argument");
-  *n = 2;  // masked-identity init (or memset) + one element sweep per 32 cases
+  TS_REQUIRE(batch >= 1, "ebe: batch must be >= 1");
+  *n = tsg::ebe_launches_per_apply(*op, batch);
   TS_API_END
 }
 
@@ -541,18 +556,20 @@ ts_status ts_dist_local_nodes(const ts_dist_levels* lv, int32_t* l2g) {
   TS_API_END
 }
 
-ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
-                        const ts_solver_config* cfg, ts_solve_report* rep) {
+ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, double* u_out, int32_t n_local,
+                        int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep) {
   TS_API_BEGIN
   TS_REQUIRE(lv && f && u0 && u_out && cfg && rep, "solve: null argument");
+  TS_REQUIRE(size_t(n_local) == tsg::dist_local_nodes(*lv).size(), "solve: dimension mismatch");
   tsg::dist_solve_host(*lv, f, u0, u_out, batch, *cfg, *rep);
   TS_API_END
 }
 
-ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
-                               const ts_solver_config* cfg, ts_solve_report* rep, void* stream) {
+ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double* u0, double* u_out, int32_t n_local,
+                               int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep, void* stream) {
   TS_API_BEGIN
   TS_REQUIRE(lv && f && u0 && u_out && cfg && rep, "solve: null argument");
+  TS_REQUIRE(size_t(n_local) == tsg::dist_local_nodes(*lv).size(), "solve: dimension mismatch");
   tsg::dist_solve_device(*lv, f, u0, u_out, batch, *cfg, *rep, static_cast<cudaStream_t>(stream));
   TS_API_END
 }

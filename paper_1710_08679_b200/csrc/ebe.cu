@@ -540,11 +540,13 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
     return;
   }
   bool done = false;
+  if (op.deterministic) {  // order-fixed colored sweep (reference bitwise contract, test_ebe.cpp:254-317)
+    ebe_color_apply(op, u, f, batch, s, part);
+    done = true;
+  }
   // Default dispatch (6, measured: profiles/r01_ebe_tile.txt, r01_ebe_pair_ncu.txt): the face-pair sweep
-  // (ebe_pair.cu) for every batch width it covers (1, 2, 4, 8, 16), else the element-parallel sweep;
-  // the chunk-tiled sweep on request (5).
-  if (op.kernel == 7 || op.kernel == 6) done = ebe_pair_apply(op, u, f, batch, s, part);
-  if (!done && op.kernel == 5) done = ebe_tile_apply(op, u, f, batch, s, part);
+  // (ebe_pair.cu) for every batch width it covers (1, 2, 4, 8, 16), else the element-parallel sweep.
+  if (!done && (op.kernel == 7 || op.kernel == 6)) done = ebe_pair_apply(op, u, f, batch, s, part);
   if (!done && op.kernel >= 3)
     done = (op.order == 2)
                ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s, e0, e1)
@@ -591,6 +593,28 @@ void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStre
   if (u == f) validation("ebe apply: input and output must not alias");
   if (op.prec == 32) apply_t<float>(op, static_cast<const float*>(u), static_cast<float*>(f), batch, s, -1, true);
   else apply_t<double>(op, static_cast<const double*>(u), static_cast<double*>(f), batch, s, -1, true);
+}
+
+int ebe_launches_per_apply(const ts_ebe& op, int32_t batch) {
+  // masked-identity init: memset (copy engine) + identity-row kernel, or one masked-identity kernel
+  const int init = op.has_mask && op.n_masked_dofs > 0 ? 1 : 0;
+  if (op.deterministic) {
+    int n = 0;
+    for (size_t k = 0; k + 1 < op.color->color_ptr.size(); ++k) n += op.color->color_ptr[k + 1] > op.color->color_ptr[k];
+    return init + n;
+  }
+  if (op.kernel == 7 || op.kernel == 6) {
+    const int p = ebe_pair_launches(op, batch);
+    if (p >= 0) return init + p;
+  }
+  const int cpt = op.prec == 32 && batch % 2 == 0 ? 2 : 1;
+  const int nct = (batch + cpt - 1) / cpt;
+  const bool fast = op.kernel >= 3 && nct <= 16 &&
+                    (batch == 1 || batch == 2 || batch == 4 || batch == 8 || batch == 16 || batch == 20 || batch == 32);
+  const int groups = op.group_split > 0 && op.group_split < op.n_elems ? 2 : 1;
+  if (fast) return init + groups;
+  const int tpe = std::min(pow2ceil(nct), 16);
+  return init + groups * ((nct + tpe - 1) / tpe);
 }
 
 void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part, bool init) {
@@ -767,6 +791,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   HostVec<int32_t> conn(E * cs);
   op->host_conn.resize(E * npe);
   op->coef64.resize(E * 12);
+  op->elem_order.assign(ord.begin(), ord.end());
   const size_t ts = prec == 32 ? 4 : 8;
   HostVec<unsigned char> coef(E * 12 * ts);
 #pragma omp parallel for schedule(static)
@@ -818,8 +843,9 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   setup_mark("ebe: element records");
   if (kernel_override >= 0) op->kernel = kernel_override;
   else if (const char* k = std::getenv("TSGPU_EBE_KERNEL"))
-    op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "tile" ? 5
-               : std::string(k) == "pair" ? 7 : 6;
+    op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "pair" ? 7 : 6;
+  const char* kenv = std::getenv("TSGPU_EBE_KERNEL");
+  const bool colored = kernel_override < 0 && kenv && std::string(kenv) == "color";
   {
     // fast-kernel layout: 3*node per local node, then the dof-mask word (bit 3a+c)
     const int cs3 = order == 1 ? 8 : 12;
@@ -839,10 +865,6 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->conn3.upload(conn3);
   }
   setup_mark("ebe: conn3");
-  // the tiled sweep's chunk records serve kernel 5 only (in the default mode the pair sweep covers the
-  // common batch widths and the element-parallel sweeps the rest)
-  if (op->kernel == 5) build_tile_plan(*op, conn, cs);
-  setup_mark("ebe: tile plan");
   if (op->kernel == 7 || op->kernel == 6) build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32, pair_topology);
   setup_mark("ebe: pair plan");
   op->conn.upload(conn);
@@ -856,6 +878,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->masked_dofs.upload(md);
   }
   TS_CUDA(cudaDeviceSynchronize());
+  if (colored) ebe_set_deterministic(*op, true);
   return op.release();
 }
 

@@ -9,18 +9,15 @@
 
 #include "ts_common.h"
 
-// Chunk records for the tiled sweep (ebe_tile.cu): kChunk consecutive
-// elements per chunk; one 16-byte-aligned record per chunk holding its
-// distinct nodes, their incidence lists and the elements' local node slots.
-struct EbeTilePlan {
-  int chunk = 0;
-  int32_t n_chunks = 0;
-  int32_t group_chunk_split = 0;  // chunks [0, split) cover element group 0
-  int rec_max = 0;             // bytes of the largest record
-  int lmax = 0;                // most distinct nodes in a chunk (rounded up to 4)
-  double nodes_per_elem = 0.0; // chunk node rows moved per element
-  tsg::DevBuf<unsigned char> rec;
-  tsg::DevBuf<uint32_t> rec_off;  // [n_chunks + 1] in 16-byte units
+// Greedy first-fit element coloring over shared nodes (build_coloring,
+// ebe_operator.hpp:190-214), on sweep positions: no two elements of a color
+// share a node, so a color's contributions land with plain read-add-writes and
+// every node sums its elements in color order, independent of the batch width,
+// the launch geometry and the run (ebe_color.cu).
+struct EbeColorPlan {
+  int n_colors = 0;
+  std::vector<int32_t> color_ptr;  // [n_colors + 1] into elems
+  tsg::DevBuf<int32_t> elems;      // sweep positions, color-major, ascending within a color
 };
 
 // Face-sharing element pairs for the pair sweep (ebe_pair.cu).
@@ -63,6 +60,7 @@ struct EbeStreamPlan {
   tsg::DevBuf<int32_t> mdofs;                    // constrained dofs by upload chunk
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_done;
+  cudaEvent_t ev_entry = nullptr;  // recorded on the legacy stream at entry: the pipeline waits on it
   ~EbeStreamPlan();
 };
 
@@ -84,12 +82,15 @@ struct ts_ebe {
   int32_t n_masked_dofs = 0;
   tsg::HostVec<double> coef64;          // host [E][12]: b (9), lambda*V, mu*V, V  (setup only)
   tsg::HostVec<int32_t> host_conn;      // host [E][npe] (setup only)
+  tsg::HostVec<int32_t> elem_order;     // host [E]: caller's element id at each sweep position
   std::vector<uint8_t> host_mask;       // host [3N]
-  std::unique_ptr<EbeTilePlan> tile;    // chunk records (tiled sweep, kernel 5)
+  std::unique_ptr<EbeColorPlan> color;  // greedy element coloring (deterministic sweep)
+  bool deterministic = false;           // colored sweep: order-fixed sums, batch-independent bits
   int32_t group_split = 0;              // elements [0, split) = group 0 (partition boundary), rest group 1
   std::unique_ptr<EbePairPlan> pair;    // face-sharing pairs (kernel 7)
-  int kernel = 6;  // 2 pipelined generic, 3 pipelined batch-specialised, 5 tiled, 6 = 7 = face pairs (default);
-                   // each falls back to 3, then 2, for batch widths it does not cover
+  int kernel = 6;  // 2 pipelined generic, 3 pipelined batch-specialised, 6 = 7 = face pairs (default);
+                   // each falls back to 3, then 2, for batch widths it does not cover; `deterministic`
+                   // overrides all of them with the colored sweep
   mutable std::mutex host_mu;            // guards the host-entry staging buffers (and `stream`)
   mutable std::unique_ptr<EbeStreamPlan> stream;  // built at the first pinned-host apply
   mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
@@ -145,11 +146,15 @@ void ebe_block_jacobi(const ts_ebe& op, void* inv_dev, cudaStream_t s);
 // then invert_node_block per node (block_jacobi.hpp:45-66) rounded to prec
 void ebe_diag_blocks(const ts_ebe& op, double* diag_dev, cudaStream_t s);
 void bj_invert(const double* diag_dev, const uint8_t* mask_dev, int32_t n, int prec, void* inv_dev, cudaStream_t s);
-// tiled sweep (ebe_tile.cu); false when no instance covers this batch width
-bool ebe_tile_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part = -1);
+// colored deterministic sweep (ebe_color.cu) over element range part (-1 all, 0 boundary, 1 interior)
+void ebe_color_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
+// builds the coloring once (host, setup data); on = deterministic sweeps from now on
+void ebe_set_deterministic(ts_ebe& op, bool on);
 // element-group sweep of a partitioned operator (part -1 all, 0 boundary, 1 interior)
 void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part, bool init);
-void build_tile_plan(ts_ebe& op, const HostVec<int32_t>& conn_words, int conn_stride);
+// kernel launches of one device apply of `batch` cases (init + sweep); pair sweep alone: -1 = not covered
+int ebe_launches_per_apply(const ts_ebe& op, int32_t batch);
+int ebe_pair_launches(const ts_ebe& op, int32_t batch);
 // pair sweep (ebe_pair.cu); false when no instance covers this batch width
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
 // face-pair topology of an element order (greedy matching result), shareable between the

@@ -325,6 +325,38 @@ bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p
   }
 }
 
+// launches of one pair sweep over units [p0, p1) (the split of launch_pair_b); -1 = batch not covered
+template <typename T, typename V, int NPE, int B>
+int pair_launches_b(int32_t p0, int32_t p1) {
+  constexpr int CPT = LaneOps<V>::kCols;
+  constexpr int TPE = (B + CPT - 1) / CPT;
+  if constexpr (128 % TPE != 0 || TPE * CPT != B) {
+    return -1;
+  } else {
+    using Geo = PairGeo<NPE>;
+    constexpr int NT = 128, GROUPS = NT / TPE;
+    const size_t smem = 2 * (size_t((Geo::NR * 3 + 1) & ~1) * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
+                             size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
+    const KernelFit fit = kernel_fit<k_ebe_pair<T, V, NPE, B>>(NT, smem);
+    if (p1 <= p0) return 0;
+    const int64_t need = (int64_t(p1 - p0) + GROUPS - 1) / GROUPS;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(fit.sms) * std::max(fit.per_sm, 1))));
+    const int64_t step = pair_launch_units(int64_t(grid) * GROUPS, int64_t(p1) - p0);
+    return static_cast<int>((int64_t(p1) - p0 + step - 1) / step);
+  }
+}
+template <typename T, typename V, int NPE>
+int pair_launches_t(int32_t batch, int32_t p0, int32_t p1) {
+  switch (batch) {
+    case 1: return pair_launches_b<T, T, NPE, 1>(p0, p1);
+    case 2: return pair_launches_b<T, V, NPE, 2>(p0, p1);
+    case 4: return pair_launches_b<T, V, NPE, 4>(p0, p1);
+    case 8: return pair_launches_b<T, V, NPE, 8>(p0, p1);
+    case 16: return pair_launches_b<T, V, NPE, 16>(p0, p1);
+    default: return -1;
+  }
+}
+
 template <typename T, typename V, int NPE>
 bool launch_pair_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t p0, int32_t p1) {
   switch (batch) {
@@ -361,6 +393,18 @@ bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cud
   const int32_t p0 = part == 1 ? op.pair->group_split : 0;
   const int32_t p1 = part == 0 ? op.pair->group_split : op.pair->n_units;
   return ebe_pair_apply_range(op, u, f, batch, s, p0, p1);
+}
+
+int ebe_pair_launches(const ts_ebe& op, int32_t batch) {
+  if (!op.pair) return -1;
+  const int32_t n = op.pair->n_units, sp = op.pair->group_split;
+  auto count = [&](int32_t p0, int32_t p1) {
+    if (op.prec == 32)
+      return op.order == 2 ? pair_launches_t<float, float2, 10>(batch, p0, p1) : pair_launches_t<float, float2, 4>(batch, p0, p1);
+    return op.order == 2 ? pair_launches_t<double, double, 10>(batch, p0, p1) : pair_launches_t<double, double, 4>(batch, p0, p1);
+  };
+  const int a = count(0, sp), b = count(sp, n);
+  return a < 0 || b < 0 ? -1 : a + b;
 }
 
 bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t p0,

@@ -138,6 +138,7 @@ std::unique_ptr<EbeStreamPlan> build_stream_plan(const ts_ebe& op) {
   TS_CUDA(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
   TS_CUDA(cudaStreamCreateWithFlags(&P->s_comp, cudaStreamNonBlocking));
   TS_CUDA(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
+  TS_CUDA(cudaEventCreateWithFlags(&P->ev_entry, cudaEventDisableTiming));
   P->ev_in.resize(K);
   P->ev_done.resize(K);
   for (int k = 0; k < K; ++k) {
@@ -156,6 +157,12 @@ bool apply_streamed(const ts_ebe& op, const EbeStreamPlan& P, const T* uh, T* fh
   T* df = reinterpret_cast<T*>(op.stage_f.get());
   // probe: does the pair sweep cover this batch width? (an empty range launches nothing)
   if (!ebe_pair_apply_range(op, du, df, batch, P.s_comp, 0, 0)) return false;
+  // the pipeline's non-blocking streams start after work already queued on the legacy default
+  // stream (e.g. a producer of u or a pending reader of f), as the copy-apply-copy path would
+  TS_CUDA(cudaEventRecord(P.ev_entry, nullptr));
+  TS_CUDA(cudaStreamWaitEvent(P.s_in, P.ev_entry, 0));
+  TS_CUDA(cudaStreamWaitEvent(P.s_comp, P.ev_entry, 0));
+  TS_CUDA(cudaStreamWaitEvent(P.s_out, P.ev_entry, 0));
   TS_CUDA(cudaMemsetAsync(df, 0, row * op.n_nodes * sizeof(T), P.s_comp));
   for (int k = 0; k < P.chunks; ++k) {
     for (int32_t q = P.in_ptr[k]; q < P.in_ptr[k + 1]; ++q) {
@@ -192,7 +199,7 @@ void ebe_apply_host(const ts_ebe& op, const void* u, void* f, int32_t batch) {
   std::lock_guard<std::mutex> lock(op.host_mu);
   op.stage_u.ensure(bytes);
   op.stage_f.ensure(bytes);
-  if (op.kernel >= 6 && op.pair && is_pinned(u) && is_pinned(f)) {
+  if (op.kernel >= 6 && op.pair && !op.deterministic && is_pinned(u) && is_pinned(f)) {
     if (!op.stream) op.stream = build_stream_plan(op);
     if (op.stream->usable) {
       const bool done =
@@ -210,6 +217,7 @@ void ebe_apply_host(const ts_ebe& op, const void* u, void* f, int32_t batch) {
 }  // namespace tsg
 
 EbeStreamPlan::~EbeStreamPlan() {
+  if (ev_entry) cudaEventDestroy(ev_entry);
   for (cudaEvent_t e : ev_in) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_done) cudaEventDestroy(e);
   for (cudaStream_t s : {s_in, s_comp, s_out})

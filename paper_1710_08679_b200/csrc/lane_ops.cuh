@@ -31,17 +31,20 @@ template <> struct LaneOps<float2> {
   }
 };
 
+// Scalar lanes round exactly like one lane of the packed ops (explicit _rn
+// intrinsics: no FMA contraction of a separate mul + add), so a case's result
+// does not depend on whether the batch width selected packed or scalar lanes.
 template <> struct LaneOps<float> {
   using S = float;
   static constexpr int kCols = 1;
   __device__ __forceinline__ static float zero() { return 0.f; }
   __device__ __forceinline__ static float splat(float s) { return s; }
-  __device__ __forceinline__ static float add(float a, float b) { return a + b; }
-  __device__ __forceinline__ static float sub(float a, float b) { return a - b; }
-  __device__ __forceinline__ static float mul(float a, float b) { return a * b; }
-  __device__ __forceinline__ static float fma(float a, float b, float c) { return fmaf(a, b, c); }
+  __device__ __forceinline__ static float add(float a, float b) { return __fadd_rn(a, b); }
+  __device__ __forceinline__ static float sub(float a, float b) { return __fmaf_rn(b, -1.f, a); }
+  __device__ __forceinline__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+  __device__ __forceinline__ static float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
   __device__ __forceinline__ static float neg(float a) { return -a; }
-  __device__ __forceinline__ static float fnma(float a, float b, float c) { return fmaf(-a, b, c); }
+  __device__ __forceinline__ static float fnma(float a, float b, float c) { return __fmaf_rn(-a, b, c); }
 };
 
 template <> struct LaneOps<double> {
@@ -49,10 +52,10 @@ template <> struct LaneOps<double> {
   static constexpr int kCols = 1;
   __device__ __forceinline__ static double zero() { return 0.0; }
   __device__ __forceinline__ static double splat(double s) { return s; }
-  __device__ __forceinline__ static double add(double a, double b) { return a + b; }
-  __device__ __forceinline__ static double sub(double a, double b) { return a - b; }
-  __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
-  __device__ __forceinline__ static double fma(double a, double b, double c) { return ::fma(a, b, c); }
+  __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static double sub(double a, double b) { return __dsub_rn(a, b); }
+  __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ __forceinline__ static double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
   __device__ __forceinline__ static double neg(double a) { return -a; }
   __device__ __forceinline__ static double fnma(double a, double b, double c) { return ::fma(-a, b, c); }
 };

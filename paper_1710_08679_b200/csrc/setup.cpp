@@ -239,7 +239,10 @@ Aggregation aggregate_p1(const BcsrD& a, int32_t target) {
   }
   std::vector<int32_t> compact(nagg, -1);
   for (int32_t id = 0; id < nagg; ++id)
-    if (msize[id] > 0) compact[id] = agg.n_aggregates++;
+    if (msize[id] > 0) {
+      compact[id] = agg.n_aggregates++;
+      agg.seeds.push_back(first[id]);
+    }
   for (int32_t node = 0; node < n; ++node) agg.agg_of_node[node] = compact[agg.agg_of_node[node]];
   return agg;
 }

@@ -17,6 +17,7 @@ struct BcsrD {
 struct Aggregation {  // aggregation.hpp:13-17
   std::vector<int32_t> agg_of_node;
   int32_t n_aggregates = 0;
+  std::vector<int32_t> seeds;  // seed node of each aggregate, creation order
 };
 
 // K1 (fp64, the reference's assembly); blocks32 (optional) receives the fp32

@@ -47,7 +47,7 @@ struct ts_levels {
   DevBuf<int32_t> p1_ends, p1t_ptr, p1t_idx, agg, p2t_ptr, p2t_idx;
   DevBuf<float> m0, m1, m2;
   DevBuf<uint8_t> mask0, mask1, mask2;
-  std::vector<int32_t> h_agg, h_rp2, h_ci2;
+  std::vector<int32_t> h_agg, h_seeds, h_rp2, h_ci2;
   std::vector<float> h_bl2, h_m2;
   std::vector<uint8_t> h_mask2;
   double setup_s = 0.0;
@@ -252,6 +252,7 @@ ts_levels* levels_create(const Mesh& m, int32_t n_mat, const double* lam, const 
   lv->h_mask2 = coarse_mask(agg, mask1);
   lv->h_m2 = bcsr_block_jacobi_f32(a2);
   lv->h_agg = agg.agg_of_node;
+  lv->h_seeds = agg.seeds;
   lv->h_rp2 = a2.row_ptr;
   lv->h_ci2.assign(a2.col_idx.begin(), a2.col_idx.end());
   lv->h_bl2.resize(a2.blocks.size());
@@ -353,6 +354,18 @@ ts_status ts_levels_export(const ts_levels* lv, int32_t* agg, int32_t* row_ptr2,
   TS_API_END
 }
 
+ts_status ts_levels_export_fine(const ts_levels* lv, float* m0_inv, float* m1_inv, uint8_t* mask0, uint8_t* mask1,
+                                int32_t* seeds) {
+  TS_API_BEGIN
+  if (!lv) tsg::validation("levels: null handle");
+  if (m0_inv) TS_CUDA(cudaMemcpy(m0_inv, lv->m0.get(), 9 * size_t(lv->n0) * sizeof(float), cudaMemcpyDeviceToHost));
+  if (m1_inv) TS_CUDA(cudaMemcpy(m1_inv, lv->m1.get(), 9 * size_t(lv->n1) * sizeof(float), cudaMemcpyDeviceToHost));
+  if (mask0) TS_CUDA(cudaMemcpy(mask0, lv->mask0.get(), 3 * size_t(lv->n0), cudaMemcpyDeviceToHost));
+  if (mask1) TS_CUDA(cudaMemcpy(mask1, lv->mask1.get(), 3 * size_t(lv->n1), cudaMemcpyDeviceToHost));
+  if (seeds) std::memcpy(seeds, lv->h_seeds.data(), lv->h_seeds.size() * sizeof(int32_t));
+  TS_API_END
+}
+
 ts_status ts_levels_operator(const ts_levels* lv, int32_t which, const ts_ebe** op) {
   TS_API_BEGIN
   if (!lv || !op) tsg::validation("levels: null argument");
@@ -374,14 +387,37 @@ ts_status ts_levels_apply(ts_levels* lv, int32_t which, const void* u, void* f, 
     tsg::bcsr_rows_f32(lv->l1_row_ptr.get(), lv->l1_col_idx.get(), lv->l1_blocks.get(), lv->n1,
                        static_cast<const float*>(u), static_cast<float*>(f), batch, s);
   else if (which == 2) tsg::ebe_apply(*lv->l1, u, f, batch, s);
-  else tsg::validation("levels apply: operator index must be 0 (outer), 1 (level0) or 2 (level1)");
+  else if (which == 3)
+    tsg::bcsr_apply_f32(lv->l2_row_ptr.get(), lv->l2_col_idx.get(), lv->l2_blocks.get(), lv->n2,
+                        static_cast<const float*>(u), static_cast<float*>(f), batch, s);
+  else tsg::validation("levels apply: operator index must be 0 (outer), 1 (level0), 2 (level1) or 3 (level2)");
   TS_API_END
 }
 
-ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
-                          const ts_solver_config* cfg, ts_solve_report* rep, void* stream) {
+ts_status ts_levels_transfer(ts_levels* lv, int32_t which, const float* in, float* out, int32_t batch, void* stream) {
+  TS_API_BEGIN
+  if (!lv || !in || !out) tsg::validation("levels transfer: null argument");
+  if (batch < 1) tsg::validation("levels transfer: batch must be >= 1");
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (which) {
+    case 0: tsg::p1_apply(in, out, lv->p1_ends.get(), lv->n1, lv->n0, lv->mask0.get(), batch, s); break;
+    case 1:
+      tsg::p1_restrict(in, out, lv->p1t_ptr.get(), lv->p1t_idx.get(), lv->n1, lv->mask1.get(), batch, s);
+      break;
+    case 2: tsg::p2_apply(in, out, lv->agg.get(), lv->n1, lv->mask1.get(), batch, s); break;
+    case 3:
+      tsg::p2_restrict(in, out, lv->p2t_ptr.get(), lv->p2t_idx.get(), lv->n2, lv->mask2.get(), batch, s);
+      break;
+    default: tsg::validation("levels transfer: which must be 0 (P1), 1 (P1^T), 2 (P2) or 3 (P2^T)");
+  }
+  TS_API_END
+}
+
+ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, double* u_out, int32_t n_nodes,
+                          int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep, void* stream) {
   TS_API_BEGIN
   if (!lv || !f || !u0 || !u_out || !cfg) tsg::validation("solve: null argument");
+  if (n_nodes != lv->n0) tsg::validation("solve: dimension mismatch");
   ts_solve_report local{};
   ts_solve_report& r = rep ? *rep : local;
   std::lock_guard<std::mutex> lock(lv->mu);
@@ -389,10 +425,11 @@ ts_status ts_solve_device(ts_levels* lv, const double* f, const double* u0, doub
   TS_API_END
 }
 
-ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_out, int32_t batch,
+ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_out, int32_t n_nodes, int32_t batch,
                    const ts_solver_config* cfg, ts_solve_report* rep) {
   TS_API_BEGIN
   if (!lv || !f || !u0 || !u_out || !cfg) tsg::validation("solve: null argument");
+  if (n_nodes != lv->n0) tsg::validation("solve: dimension mismatch");
   if (batch < 1) tsg::validation("solve: batch must be >= 1");
   ts_solve_report local{};
   ts_solve_report& r = rep ? *rep : local;
@@ -416,10 +453,11 @@ ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_o
   TS_API_END
 }
 
-ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, double* u_out, int32_t batch, double tol,
-                        int32_t max_iter, ts_solve_report* rep) {
+ts_status ts_solve_pcge(const ts_ebe* k, const double* f, const double* u0, double* u_out, int32_t n_nodes,
+                        int32_t batch, double tol, int32_t max_iter, ts_solve_report* rep) {
   TS_API_BEGIN
   if (!k || !f || !u0 || !u_out) tsg::validation("solve_pcge: null argument");
+  if (n_nodes != k->n_nodes) tsg::validation("ebe apply: dimension mismatch");
   if (k->prec != 64 || k->order != 2) tsg::validation("solve_pcge: needs the 64-bit second-order operator");
   if (batch < 1 || batch > tsg::kRedThreads) tsg::validation("solve_pcge: batch must be in [1, 256]");
   ts_solve_report local{};

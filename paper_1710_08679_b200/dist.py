@@ -22,7 +22,8 @@ import ctypes as C
 import numpy as np
 
 from ._lib import lib
-from .tetsolve import Mesh, SolverConfig, _ck, _lame, _p, _ReportBuf, _is_torch, _stream
+from .tetsolve import (Mesh, SolverConfig, _ck, _device_vec, _host_vec, _is_torch, _lame, _p, _ReportBuf,
+                       _stream)
 
 
 class ThreadWorld:
@@ -163,16 +164,20 @@ class DistLevels:
         c = cfg.to_c()
         batch = int(f.shape[1])
         rb = _ReportBuf(batch, 0)
+        rows = 3 * self.n_local
         if _is_torch(f):
             import torch
+            f = _device_vec(f, rows, torch.float64, "solve")
+            u0 = _device_vec(u0, rows, torch.float64, "solve: initial guess", batch)
             u = torch.empty_like(f)
             rc = lib.ts_dist_solve_device(self._h, C.c_void_p(f.data_ptr()), C.c_void_p(u0.data_ptr()),
-                                          C.c_void_p(u.data_ptr()), batch, C.byref(c), C.byref(rb.c), _stream())
+                                          C.c_void_p(u.data_ptr()), self.n_local, batch, C.byref(c), C.byref(rb.c),
+                                          _stream())
         else:
-            f = np.ascontiguousarray(f, np.float64)
-            u0 = np.ascontiguousarray(u0, np.float64)
+            f = _host_vec(f, rows, np.float64, "solve")
+            u0 = _host_vec(u0, rows, np.float64, "solve: initial guess", batch)
             u = np.empty_like(f)
-            rc = lib.ts_dist_solve(self._h, _p(f), _p(u0), _p(u), batch, C.byref(c), C.byref(rb.c))
+            rc = lib.ts_dist_solve(self._h, _p(f), _p(u0), _p(u), self.n_local, batch, C.byref(c), C.byref(rb.c))
         rep = rb.report(0)
         _ck(rc, rep)
         return u, rep

@@ -80,6 +80,37 @@ def _p(a):
     return None if a is None else C.c_void_p(a.ctypes.data)
 
 
+def _device_vec(x, rows: int, dtype, what: str, batch: int | None = None):
+    """A (rows, batch) CUDA tensor of `dtype` on the current device, C-contiguous
+    (a strided view is copied). Anything else is the reference's ValidationError
+    (ebe_operator.hpp:91-93): nothing mismatched ever reaches a kernel."""
+    if not _is_torch(x) or not x.is_cuda or x.dtype != dtype or x.ndim != 2 or x.shape[0] != rows:
+        raise ValidationError(f"{what}: dimension mismatch")
+    if batch is not None and x.shape[1] != batch:
+        raise ValidationError(f"{what}: dimension mismatch")
+    if x.device.index != torch.cuda.current_device():
+        raise ValidationError(f"{what}: tensor is on another device")
+    return x if x.is_contiguous() else x.contiguous()
+
+
+def _host_vec(x, rows: int, dtype, what: str, batch: int | None = None):
+    """A (rows, batch) C-contiguous numpy array of `dtype` (converted copy if needed)."""
+    if _is_torch(x):
+        raise ValidationError(f"{what}: mixes host and device buffers")
+    x = np.ascontiguousarray(x, dtype)
+    if x.ndim != 2 or x.shape[0] != rows or (batch is not None and x.shape[1] != batch):
+        raise ValidationError(f"{what}: dimension mismatch")
+    return x
+
+
+def _host_out(f, like):
+    """`f` if it can receive the result in place (same shape/dtype, C-contiguous, writable), else a new array."""
+    if (f is not None and not _is_torch(f) and isinstance(f, np.ndarray) and f.shape == like.shape
+            and f.dtype == like.dtype and f.flags.c_contiguous and f.flags.writeable):
+        return f
+    return np.empty_like(like)
+
+
 # ------------------------------------------------------------------ config
 @dataclass
 class InnerLoopConfig:
@@ -410,23 +441,41 @@ class EbeOperator:
         return 4 if self._order == 1 else 10
 
     def apply(self, u, f=None):
-        """f = A u for all batch columns (ebe_operator.hpp:90-134)."""
+        """f = A u for all batch columns (ebe_operator.hpp:90-134). Like the
+        reference's apply, an `f` of the wrong shape is replaced (here: also a
+        wrong dtype, device or a non-contiguous one), never written through."""
         if u.ndim != 2 or u.shape[0] != 3 * self._n:
             raise ValidationError("ebe apply: dimension mismatch")
         batch = int(u.shape[1])
         if _is_torch(u):
             want = torch.float32 if self.prec == 32 else torch.float64
-            if u.dtype != want or not u.is_cuda:
-                raise ValidationError("ebe apply: input must be a CUDA tensor of the operator precision")
-            u = u.contiguous()
-            if f is None or f.shape != u.shape or f.dtype != u.dtype:
+            u = _device_vec(u, 3 * self._n, want, "ebe apply")
+            if not (_is_torch(f) and f.shape == u.shape and f.dtype == u.dtype and f.device == u.device
+                    and f.is_contiguous()):
                 f = torch.empty_like(u)
             _ck(lib.ts_ebe_apply(self._h, C.c_void_p(u.data_ptr()), C.c_void_p(f.data_ptr()), batch, _stream()))
             return f
-        u = np.ascontiguousarray(u, self.dtype_np)
-        out = np.empty_like(u) if f is None or f.shape != u.shape else f
+        u = _host_vec(u, 3 * self._n, self.dtype_np, "ebe apply")
+        out = _host_out(f, u)
         _ck(lib.ts_ebe_apply_host(self._h, _p(u), _p(out), batch))
         return out
+
+    def element_matrix(self, e: int) -> np.ndarray:
+        """element_matrix (ebe_operator.hpp:78-87): fp64 K_e [3 npe, 3 npe] of element e."""
+        n = 3 * self.nodes_per_element()
+        k = np.zeros((n, n), np.float64)
+        _ck(lib.ts_ebe_element_matrix(self._h, int(e), _p(k)))
+        return k
+
+    def set_deterministic(self, on: bool = True):
+        """Colored, order-fixed sweep (bitwise reproducible, batch-independent bits)."""
+        _ck(lib.ts_ebe_set_deterministic(self._h, 1 if on else 0))
+        return self
+
+    def launches_per_apply(self, batch: int) -> int:
+        n = C.c_int32()
+        _ck(lib.ts_ebe_launches_per_apply(self._h, int(batch), C.byref(n)))
+        return n.value
 
     def host_stream_chunks(self) -> int:
         """Chunks of the pinned-host streaming schedule (0 = copy-apply-copy)."""
@@ -457,6 +506,180 @@ class EbeOperator:
 
 
 # ------------------------------------------------------------------ solver
+def assemble_bcsr(op: EbeOperator) -> "BlockCsrMatrix":
+    """assemble_bcsr (ebe_operator.hpp:230-284): identity rows at constrained dofs, constrained
+    columns dropped, fp64 sums in element order rounded to the operator precision (device)."""
+    nnzb = C.c_int64()
+    _ck(lib.ts_ebe_assemble_bcsr(op._h, C.byref(nnzb), None, None, None))
+    rp = np.zeros(op.n_nodes() + 1, np.int32)
+    ci = np.zeros(nnzb.value, np.int32)
+    bl = np.zeros((nnzb.value, 9), op.dtype_np)
+    _ck(lib.ts_ebe_assemble_bcsr(op._h, C.byref(nnzb), _p(rp), _p(ci), _p(bl)))
+    return BlockCsrMatrix(op.n_nodes(), rp, ci, bl)
+
+
+class BlockCsrMatrix:
+    """BlockCsrMatrix<T> (block_csr.hpp:16-70): 3x3-block CSR held on the device; apply =
+    fp64 row accumulation in stored-block order rounded to T (bit-exact vs the reference)."""
+
+    def __init__(self, n_block_rows: int, row_ptr, col_idx, blocks):
+        self.n_block_rows = int(n_block_rows)
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        self.col_idx = np.ascontiguousarray(col_idx, np.int32)
+        bl = np.asarray(blocks)
+        self.prec = 32 if bl.dtype == np.float32 else 64
+        self.blocks = np.ascontiguousarray(bl, np.float32 if self.prec == 32 else np.float64).reshape(-1, 9)
+        self._h = C.c_void_p()
+        _ck(lib.ts_bcsr_create(self.n_block_rows, _p(self.row_ptr), _p(self.col_idx), _p(self.blocks), self.prec,
+                               C.byref(self._h)))
+
+    def apply(self, u, f=None):
+        rows = 3 * self.n_block_rows
+        if _is_torch(u):
+            u = _device_vec(u, rows, torch.float32 if self.prec == 32 else torch.float64, "bcsr apply")
+            f = torch.empty_like(u)
+            _ck(lib.ts_bcsr_apply(self._h, C.c_void_p(u.data_ptr()), C.c_void_p(f.data_ptr()), int(u.shape[1]),
+                                  _stream()))
+            return f
+        u = _host_vec(u, rows, np.float32 if self.prec == 32 else np.float64, "bcsr apply")
+        out = _host_out(f, u)
+        _ck(lib.ts_bcsr_apply_host(self._h, _p(u), _p(out), int(u.shape[1])))
+        return out
+
+    def block_jacobi(self) -> "BlockJacobi":
+        """extract_block_jacobi(BlockCsrMatrix) (block_jacobi.hpp:72-85)."""
+        inv = np.zeros((self.n_block_rows, 9), self.blocks.dtype)
+        _ck(lib.ts_bcsr_block_jacobi_host(self._h, _p(inv)))
+        return BlockJacobi(inv)
+
+    def __del__(self):
+        try:
+            lib.ts_bcsr_destroy(self._h)
+        except Exception:
+            pass
+
+
+class BlockJacobi:
+    """BlockJacobi<T> (block_jacobi.hpp:15-39): z = M^-1 r, fp64 math rounded to T (device)."""
+
+    def __init__(self, inv_blocks):
+        inv = np.asarray(inv_blocks)
+        self.prec = 32 if inv.dtype == np.float32 else 64
+        self.inv_blocks = np.ascontiguousarray(inv, np.float32 if self.prec == 32 else np.float64).reshape(-1, 9)
+        self._h = C.c_void_p()
+        _ck(lib.ts_bj_create(len(self.inv_blocks), _p(self.inv_blocks), self.prec, C.byref(self._h)))
+
+    def n_nodes(self) -> int:
+        return len(self.inv_blocks)
+
+    def apply(self, r, z=None):
+        rows = 3 * self.n_nodes()
+        if _is_torch(r):
+            r = _device_vec(r, rows, torch.float32 if self.prec == 32 else torch.float64, "block jacobi apply")
+            z = torch.empty_like(r)
+            _ck(lib.ts_bj_apply(self._h, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), int(r.shape[1]),
+                                _stream()))
+            return z
+        r = _host_vec(r, rows, np.float32 if self.prec == 32 else np.float64, "block jacobi apply")
+        out = _host_out(z, r)
+        _ck(lib.ts_bj_apply_host(self._h, _p(r), _p(out), int(r.shape[1])))
+        return out
+
+    def __del__(self):
+        try:
+            lib.ts_bj_destroy(self._h)
+        except Exception:
+            pass
+
+
+class Prolongation:
+    """Prolongation (prolongation.hpp:13-62): per-fine-node CSR, the same weights on every
+    axis; apply = P coarse, restrict_to_coarse = P^T fine (ascending fine rows), in T (device)."""
+
+    def __init__(self, n_fine: int, n_coarse: int, row_ptr, cols, weights):
+        self.n_fine_nodes, self.n_coarse_nodes = int(n_fine), int(n_coarse)
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        self.cols = np.ascontiguousarray(cols, np.int32)
+        self.weights = np.ascontiguousarray(weights, np.float64)
+        self._h = C.c_void_p()
+        _ck(lib.ts_prolong_create(self.n_fine_nodes, self.n_coarse_nodes, _p(self.row_ptr), _p(self.cols),
+                                  _p(self.weights), C.byref(self._h)))
+
+    def _run(self, x, restrict: bool):
+        n_in, n_out = (self.n_fine_nodes, self.n_coarse_nodes) if restrict else (self.n_coarse_nodes,
+                                                                                 self.n_fine_nodes)
+        what = "prolongation restrict: fine" if restrict else "prolongation apply: coarse"
+        if _is_torch(x):
+            if x.dtype not in (torch.float32, torch.float64):
+                raise ValidationError(f"{what} dimension mismatch")
+            x = _device_vec(x, 3 * n_in, x.dtype, what)
+            prec = 32 if x.dtype == torch.float32 else 64
+            y = torch.empty((3 * n_out, x.shape[1]), dtype=x.dtype, device=x.device)
+            fn = lib.ts_prolong_restrict if restrict else lib.ts_prolong_apply
+            _ck(fn(self._h, prec, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(x.shape[1]), _stream()))
+            return y
+        x = np.asarray(x)
+        dt = np.float32 if x.dtype == np.float32 else np.float64
+        x = _host_vec(x, 3 * n_in, dt, what)
+        y = np.empty((3 * n_out, x.shape[1]), dt)
+        _ck(lib.ts_prolong_apply_host(self._h, 32 if dt == np.float32 else 64, 1 if restrict else 0, _p(x), _p(y),
+                                      int(x.shape[1])))
+        return y
+
+    def apply(self, coarse):
+        return self._run(coarse, False)
+
+    def restrict_to_coarse(self, fine):
+        return self._run(fine, True)
+
+    def __del__(self):
+        try:
+            lib.ts_prolong_destroy(self._h)
+        except Exception:
+            pass
+
+
+def build_geometric_prolongation(mesh: Mesh) -> Prolongation:
+    """build_geometric_prolongation (prolongation.hpp:67-98)."""
+    n, v = mesh.node_count(), mesh.vertex_count
+    rp = np.zeros(n + 1, np.int32)
+    cols = np.zeros(v + 2 * (n - v), np.int32)
+    w = np.zeros(v + 2 * (n - v), np.float64)
+    _ck(lib.ts_geometric_prolongation(mesh._h, _p(rp), _p(cols), _p(w)))
+    return Prolongation(n, v, rp, cols, w)
+
+
+class InnerStats:
+    """InnerStats (pcg.hpp:15-18)."""
+
+    def __init__(self, iterations: int, converged: bool):
+        self.iterations, self.converged = iterations, converged
+
+
+def inner_pcg(a, m: BlockJacobi, r, u, tol: float, max_iter: int) -> InnerStats:
+    """inner_pcg (pcg.hpp:52-124) on an EbeOperator or a BlockCsrMatrix with the block-Jacobi
+    preconditioner m; u (warm start) is updated in place. CUDA tensors or numpy arrays."""
+    kind = 0 if isinstance(a, EbeOperator) else 1
+    n = a.n_nodes() if kind == 0 else a.n_block_rows
+    it, conv = C.c_int32(), C.c_int32()
+    if _is_torch(r):
+        dt = torch.float32 if a.prec == 32 else torch.float64
+        r = _device_vec(r, 3 * n, dt, "inner_pcg")
+        if not (_is_torch(u) and u.is_contiguous()):
+            raise ValidationError("inner_pcg: u must be a contiguous CUDA tensor (updated in place)")
+        _device_vec(u, 3 * n, dt, "inner_pcg", int(r.shape[1]))
+        _ck(lib.ts_inner_pcg(kind, a._h, m._h, C.c_void_p(r.data_ptr()), C.c_void_p(u.data_ptr()), n,
+                             int(r.shape[1]), float(tol), int(max_iter), C.byref(it), C.byref(conv), _stream()))
+    else:
+        dt = np.float32 if a.prec == 32 else np.float64
+        r = _host_vec(r, 3 * n, dt, "inner_pcg")
+        if not (isinstance(u, np.ndarray) and u.dtype == dt and u.flags.c_contiguous and u.shape == r.shape):
+            raise ValidationError("inner_pcg: u must be a contiguous array of r's shape and dtype (updated in place)")
+        _ck(lib.ts_inner_pcg_host(kind, a._h, m._h, _p(r), _p(u), n, int(r.shape[1]), float(tol), int(max_iter),
+                                  C.byref(it), C.byref(conv)))
+    return InnerStats(it.value, bool(conv.value))
+
+
 class SolverLevels:
     """SolverLevels (adaptive_cg.hpp:27-37) built on the device by
     build_solver_levels (adaptive_cg.hpp:39-67)."""
@@ -477,11 +700,28 @@ class SolverLevels:
 
     def apply(self, which: int, u, f=None):
         """The level operator the solve applies (CUDA tensors): 0 outer fp64, 1 level-0
-        fp32 tet10, 2 level-1 fp32 tet4 (assembled K1 unless TSGPU_L1=ebe)."""
-        f = torch.empty_like(u) if f is None else f
+        fp32 tet10, 2 level-1 fp32 tet4 (assembled K1 unless TSGPU_L1=ebe), 3 level-2 BCSR."""
+        if which not in (0, 1, 2, 3):
+            raise ValidationError("levels apply: operator index must be 0 (outer), 1 (level0), 2 (level1) or 3")
+        rows = 3 * (self.n1 if which == 2 else self.n2 if which == 3 else self.n0)
+        u = _device_vec(u, rows, torch.float64 if which == 0 else torch.float32, "levels apply")
+        if not (_is_torch(f) and f.shape == u.shape and f.dtype == u.dtype and f.device == u.device
+                and f.is_contiguous()):
+            f = torch.empty_like(u)
         _ck(lib.ts_levels_apply(self._h, int(which), C.c_void_p(u.data_ptr()), C.c_void_p(f.data_ptr()),
                                 int(u.shape[1]), _stream()))
         return f
+
+    def transfer(self, which: int, x):
+        """The solve's inter-grid transfers (fp32 CUDA tensors), each followed by zero_masked:
+        0 u0 = P1 u1, 1 r1 = P1^T r0, 2 u1 = P2 u2, 3 r2 = P2^T r1."""
+        n_in = {0: self.n1, 1: self.n0, 2: self.n2, 3: self.n1}[which]
+        n_out = {0: self.n0, 1: self.n1, 2: self.n1, 3: self.n2}[which]
+        x = _device_vec(x, 3 * n_in, torch.float32, "levels transfer")
+        y = torch.empty((3 * n_out, x.shape[1]), dtype=torch.float32, device=x.device)
+        _ck(lib.ts_levels_transfer(self._h, int(which), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                   int(x.shape[1]), _stream()))
+        return y
 
     def export(self) -> dict:
         """Setup introspection: aggregation, level-2 Galerkin matrix, masks, M2."""
@@ -540,19 +780,22 @@ def solve(levels: SolverLevels, f, u0, cfg: SolverConfig | None = None, history:
     pinned host array). Returns (u, SolveReport)."""
     cfg = cfg or SolverConfig()
     c = cfg.to_c()
+    if f.ndim != 2:
+        raise ValidationError("solve: dimension mismatch")
     batch = int(f.shape[1])
+    rows = 3 * levels.n0
     rb = _ReportBuf(batch, history if cfg.residual_history_stride > 0 else 0)
     if _is_torch(f):
+        f = _device_vec(f, rows, torch.float64, "solve")
+        u0 = _device_vec(u0, rows, torch.float64, "solve: initial guess", batch)
         u = torch.empty_like(f)
         rc = lib.ts_solve_device(levels._h, C.c_void_p(f.data_ptr()), C.c_void_p(u0.data_ptr()),
-                                 C.c_void_p(u.data_ptr()), batch, C.byref(c), C.byref(rb.c), _stream())
+                                 C.c_void_p(u.data_ptr()), levels.n0, batch, C.byref(c), C.byref(rb.c), _stream())
     else:
-        f = np.ascontiguousarray(f, np.float64)
-        u0 = np.ascontiguousarray(u0, np.float64)
-        if f.shape != u0.shape:
-            raise ValidationError("solve: initial guess shape mismatch")
-        u = out if out is not None and out.shape == f.shape and out.dtype == np.float64 else np.empty_like(f)
-        rc = lib.ts_solve(levels._h, _p(f), _p(u0), _p(u), batch, C.byref(c), C.byref(rb.c))
+        f = _host_vec(f, rows, np.float64, "solve")
+        u0 = _host_vec(u0, rows, np.float64, "solve: initial guess", batch)
+        u = _host_out(out, f)
+        rc = lib.ts_solve(levels._h, _p(f), _p(u0), _p(u), levels.n0, batch, C.byref(c), C.byref(rb.c))
     rep = rb.report(cfg.residual_history_stride)
     _ck(rc, rep)
     return u, rep
@@ -560,12 +803,14 @@ def solve(levels: SolverLevels, f, u0, cfg: SolverConfig | None = None, history:
 
 def solve_pcge(k: EbeOperator, f, u0, tol: float, max_iter: int):
     """solve_pcge (adaptive_cg.hpp:267-279): 64-bit CG + 3x3 block Jacobi."""
-    f = np.ascontiguousarray(f, np.float64)
-    u0 = np.ascontiguousarray(u0, np.float64)
+    if k.prec != 64:
+        raise ValidationError("solve_pcge: needs the 64-bit second-order operator")
+    f = _host_vec(f, 3 * k.n_nodes(), np.float64, "ebe apply")
     batch = int(f.shape[1])
+    u0 = _host_vec(u0, 3 * k.n_nodes(), np.float64, "ebe apply", batch)
     rb = _ReportBuf(batch, 0)
     u = np.empty_like(f)
-    rc = lib.ts_solve_pcge(k._h, _p(f), _p(u0), _p(u), batch, tol, max_iter, C.byref(rb.c))
+    rc = lib.ts_solve_pcge(k._h, _p(f), _p(u0), _p(u), k.n_nodes(), batch, tol, max_iter, C.byref(rb.c))
     rep = rb.report(0)
     _ck(rc, rep)
     return u, rep

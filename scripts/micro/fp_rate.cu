@@ -18,6 +18,9 @@ __global__ void kern(float* out, int iters, float s) {
       if (KIND == 3) a[i] = __fmul2_rn(a[i], b);
       if (KIND == 4) d[i] = fma(d[i], db, dc);
       if (KIND == 5) { a[i] = __ffma2_rn(a[i], b, c); x[i] = fmaf(x[i], xb, xc); }
+      if (KIND == 6) { a[i] = __ffma2_rn(a[i], b, c); d[i] = fma(d[i], db, dc); }
+      if (KIND == 7) { a[i] = __ffma2_rn(a[i], b, c); if (i & 1) d[i] = fma(d[i], db, dc); }
+      if (KIND == 8) { a[i] = __ffma2_rn(a[i], b, c); if ((i & 3) == 0) d[i] = fma(d[i], db, dc); }
     }
   }
   float acc = 0;
@@ -41,6 +44,6 @@ void run(const char* name, int per_iter) {
   cudaFree(out);
 }
 int main() {
-  run<0>("FFMA", 8); run<1>("FFMA2", 8); run<2>("FADD2", 8); run<3>("FMUL2", 8); run<4>("DFMA", 8); run<5>("FFMA2+FFMA", 16);
+  run<0>("FFMA", 8); run<1>("FFMA2", 8); run<2>("FADD2", 8); run<3>("FMUL2", 8); run<4>("DFMA", 8); run<5>("FFMA2+FFMA", 16); run<6>("FFMA2+DFMA", 16); run<7>("2FFMA2+DFMA", 12); run<8>("4FFMA2+DFMA", 10);
   return 0;
 }

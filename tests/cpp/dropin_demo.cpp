@@ -1,6 +1,6 @@
 // Drop-in demo: the reference's manufactured-solution test (test_solver.cpp:137-181)
 // written against tetsolve_b200/tetsolve.hpp instead of the reference headers.
-// Build: g++ -std=c++17 -Iinclude tests/cpp/dropin_demo.cpp -Lpaper_1710_08679_b200 -ltsgpu
+// Build: g++ -std=c++20 -Iinclude tests/cpp/dropin_demo.cpp -Lpaper_1710_08679_b200 -ltsgpu
 #include <cmath>
 #include <cstdio>
 

@@ -15,7 +15,7 @@ LIBDIR = os.path.join(ROOT, "paper_1710_08679_b200")
 
 
 def build(src=SRC, out=BIN):
-    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR, "-ltsgpu",
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR, "-ltsgpu",
                     f"-Wl,-rpath,{LIBDIR}", "-o", out], check=True)
 
 

@@ -41,8 +41,8 @@ CASES = [
 ]
 
 
-KERNELS = ["auto", "pipe", "fast", "tile", "pair"]  # TSGPU_EBE_KERNEL: default dispatch, generic and batch-specialised
-# element-parallel RED sweeps, chunk-tiled sweep, face-pair sweep
+KERNELS = ["auto", "pipe", "fast", "color", "pair"]  # TSGPU_EBE_KERNEL: default dispatch, generic and batch-specialised
+# element-parallel RED sweeps, deterministic colored sweep, face-pair sweep
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -175,7 +175,7 @@ def test_full_size_properties(batch):
 @pytest.mark.parametrize("order", [1, 2])
 def test_ebe_many_chunks_per_block(checker, monkeypatch, kernel, prec, batch, order):
     """A mesh with many more element chunks than resident blocks, so every
-    persistent block walks several chunks (pipelined tile / record prefetch)."""
+    persistent block walks several chunks (pipelined record prefetch)."""
     monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
     spec = ((6000.0, 5000.0, 4000.0), (24, 20, 16), (3000.0,), 1)
     mesh = ts.generate_box_mesh(*spec)
