@@ -378,9 +378,17 @@ ts_status ts_dist_plan_export(const ts_mesh* mesh, const uint8_t* dof_mask, cons
                               int32_t nranks, int32_t rank, int32_t* l2g, uint8_t* owned, int32_t* elems,
                               int32_t* nbr, int32_t* nbr_rows, int32_t* halo_rows);
 
+/* host-only: level 2 of build_solver_levels (adaptive_cg.hpp:53-65) from the global mesh —
+ * K1 assembly, the sequential aggregation, the Galerkin product, its block Jacobi and coarse
+ * mask — as the partitioned setup runs it ONCE (on rank 0, then broadcast); sizes out. Used to
+ * measure that setup on a host without GPUs (scripts/northstar_setup_host.py). */
+ts_status ts_level2_setup_host(const ts_mesh* mesh, int32_t n_materials, const double* lambda, const double* mu,
+                               const uint8_t* dof_mask, int32_t aggregate_target, int32_t* n2, int64_t* nnzb2);
+
 /* build_solver_levels (adaptive_cg.hpp:39-67) for this rank's partition of the
  * GLOBAL mesh (every rank passes the same mesh / part); dof_mask NULL =
- * dirichlet_mask(mesh). The comm must outlive the level set. */
+ * dirichlet_mask(mesh). Level 2 is built once, on rank 0, and broadcast over the comm.
+ * The comm must outlive the level set. */
 ts_status ts_dist_levels_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda,
                                 const double* mu, const uint8_t* dof_mask, const int32_t* part,
                                 const ts_solver_config* cfg, ts_comm* comm, ts_dist_levels** out);

@@ -157,6 +157,7 @@ _sig = {
     "ts_dist_plan_sizes": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "ts_dist_plan_export": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
     "ts_dist_levels_create": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "ts_level2_setup_host": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp]),
     "ts_dist_levels_destroy": (None, [vp]),
     "ts_dist_levels_sizes": (C.c_int, [vp, vp, vp, vp]),
     "ts_dist_local_nodes": (C.c_int, [vp, vp]),

@@ -9,6 +9,7 @@
 #include "dist_api.h"
 #include "ebe.h"
 #include "mesh_io.h"
+#include "setup.h"
 
 namespace tsg {
 const std::string& last_error();
@@ -30,6 +31,16 @@ const std::string& last_error();
     return TS_ERR_VALIDATION;                                       \
   }                                                                 \
   return TS_OK;
+
+// a partitioned call that fails on one rank aborts the communicator, so peers
+// blocked in (or entering) a collective fail instead of waiting forever
+#define TS_ABORT_ON_FAIL(comm, ...) \
+  try {                             \
+    __VA_ARGS__;                    \
+  } catch (...) {                   \
+    if (comm) (comm)->abort();      \
+    throw;                          \
+  }
 
 #define TS_REQUIRE(cond, msg) \
   do {                        \
@@ -529,13 +540,35 @@ ts_status ts_dist_plan_export(const ts_mesh* mesh, const uint8_t* dof_mask, cons
   TS_API_END
 }
 
+ts_status ts_level2_setup_host(const ts_mesh* mesh, int32_t n_materials, const double* lambda, const double* mu,
+                                const uint8_t* dof_mask, int32_t aggregate_target, int32_t* n2, int64_t* nnzb2) {
+  TS_API_BEGIN
+  TS_REQUIRE(mesh && lambda && mu && n_materials >= 1, "level2 setup: null argument");
+  const tsg::Mesh& m = mesh->m;
+  const std::vector<uint8_t> gm = dof_mask ? std::vector<uint8_t>(dof_mask, dof_mask + 3 * size_t(m.n_nodes()))
+                                           : m.dirichlet_mask();
+  const std::vector<uint8_t> mask1(gm.begin(), gm.begin() + 3 * size_t(m.vertex_count));
+  std::vector<double> le(m.n_elems()), me(m.n_elems());
+  for (int32_t e = 0; e < m.n_elems(); ++e) {
+    const int32_t k = m.material_id[e];
+    TS_REQUIRE(k >= 0 && k < n_materials, "level2 setup: element references an undefined material");
+    le[e] = lambda[k];
+    me[e] = mu[k];
+  }
+  const tsg::Level2Host l2 = tsg::build_level2_host(m, le, me, mask1, aggregate_target);
+  if (n2) *n2 = l2.n2;
+  if (nnzb2) *nnzb2 = l2.row_ptr[l2.n2];
+  TS_API_END
+}
+
 ts_status ts_dist_levels_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda, const double* mu,
                                 const uint8_t* dof_mask, const int32_t* part, const ts_solver_config* cfg,
                                 ts_comm* comm, ts_dist_levels** out) {
   TS_API_BEGIN
   TS_REQUIRE(mesh && lambda && mu && part && cfg && comm && out, "dist levels: null argument");
   TS_REQUIRE(n_materials >= 1, "dist levels: need at least one material");
-  *out = tsg::dist_levels_create(mesh->m, n_materials, lambda, mu, dof_mask, part, *cfg, comm->c.get());
+  TS_ABORT_ON_FAIL(comm->c, *out = tsg::dist_levels_create(mesh->m, n_materials, lambda, mu, dof_mask, part, *cfg,
+                                                          comm->c.get()));
   TS_API_END
 }
 
@@ -561,7 +594,7 @@ ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, d
   TS_API_BEGIN
   TS_REQUIRE(lv && f && u0 && u_out && cfg && rep, "solve: null argument");
   TS_REQUIRE(size_t(n_local) == tsg::dist_local_nodes(*lv).size(), "solve: dimension mismatch");
-  tsg::dist_solve_host(*lv, f, u0, u_out, batch, *cfg, *rep);
+  TS_ABORT_ON_FAIL(tsg::dist_levels_comm(*lv), tsg::dist_solve_host(*lv, f, u0, u_out, batch, *cfg, *rep));
   TS_API_END
 }
 
@@ -570,7 +603,8 @@ ts_status ts_dist_solve_device(ts_dist_levels* lv, const double* f, const double
   TS_API_BEGIN
   TS_REQUIRE(lv && f && u0 && u_out && cfg && rep, "solve: null argument");
   TS_REQUIRE(size_t(n_local) == tsg::dist_local_nodes(*lv).size(), "solve: dimension mismatch");
-  tsg::dist_solve_device(*lv, f, u0, u_out, batch, *cfg, *rep, static_cast<cudaStream_t>(stream));
+  TS_ABORT_ON_FAIL(tsg::dist_levels_comm(*lv),
+                   tsg::dist_solve_device(*lv, f, u0, u_out, batch, *cfg, *rep, static_cast<cudaStream_t>(stream)));
   TS_API_END
 }
 
@@ -578,7 +612,8 @@ ts_status ts_dist_ebe_apply(ts_dist_levels* lv, int32_t which, const void* u, vo
   TS_API_BEGIN
   TS_REQUIRE(lv && u && f, "dist apply: null argument");
   TS_REQUIRE(batch >= 1, "dist apply: batch must be >= 1");
-  tsg::dist_ebe_apply(*lv, which, u, f, batch, static_cast<cudaStream_t>(stream));
+  TS_ABORT_ON_FAIL(tsg::dist_levels_comm(*lv),
+                   tsg::dist_ebe_apply(*lv, which, u, f, batch, static_cast<cudaStream_t>(stream)));
   TS_API_END
 }
 
@@ -589,7 +624,8 @@ ts_status ts_dist_ebe_create(const ts_mesh* mesh, int32_t order, int32_t n_mater
   TS_REQUIRE(mesh && lambda && mu && part && comm && out, "dist ebe: null argument");
   TS_REQUIRE(order == 1 || order == 2, "dist ebe: order must be 1 or 2");
   TS_REQUIRE(prec == 32 || prec == 64, "dist ebe: precision must be 32 or 64");
-  *out = tsg::dist_ebe_create(mesh->m, order, n_materials, lambda, mu, dof_mask, part, prec, comm->c.get());
+  TS_ABORT_ON_FAIL(comm->c, *out = tsg::dist_ebe_create(mesh->m, order, n_materials, lambda, mu, dof_mask, part,
+                                                       prec, comm->c.get()));
   TS_API_END
 }
 
@@ -615,7 +651,7 @@ ts_status ts_dist_ebe_op_apply(ts_dist_ebe* op, const void* u, void* f, int32_t 
   TS_API_BEGIN
   TS_REQUIRE(op && u && f, "dist ebe: null argument");
   TS_REQUIRE(batch >= 1, "dist ebe: batch must be >= 1");
-  tsg::dist_ebe_apply_op(*op, u, f, batch, static_cast<cudaStream_t>(stream));
+  TS_ABORT_ON_FAIL(tsg::dist_ebe_comm(*op), tsg::dist_ebe_apply_op(*op, u, f, batch, static_cast<cudaStream_t>(stream)));
   TS_API_END
 }
 

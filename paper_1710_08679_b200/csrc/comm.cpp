@@ -27,6 +27,7 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -50,9 +51,10 @@ const NcclApi& nccl() {
     a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.Send && a.Recv && a.GroupStart &&
-           a.GroupEnd && a.GetErrorString;
+           a.GroupEnd && a.Broadcast && a.GetErrorString;
     if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
     return a;
   }();
@@ -108,6 +110,19 @@ class NcclComm final : public Comm {
     TS_CUDA(cudaDeviceSynchronize());
     cudaFree(d);
   }
+  void broadcast(void* host, size_t n, int root) override {
+    if (n_ == 1 || n == 0) return;
+    void* d = nullptr;
+    TS_CUDA(cudaMalloc(&d, n));
+    struct Free {
+      void* p;
+      ~Free() { cudaFree(p); }
+    } guard{d};
+    if (r_ == root) TS_CUDA(cudaMemcpy(d, host, n, cudaMemcpyHostToDevice));
+    TS_NCCL(nccl().Broadcast(d, d, n, ncclChar, root, comm_, nullptr));
+    TS_CUDA(cudaStreamSynchronize(nullptr));
+    if (r_ != root) TS_CUDA(cudaMemcpy(host, d, n, cudaMemcpyDeviceToHost));
+  }
   const char* kind() const override { return "nccl"; }
 
  private:
@@ -150,16 +165,28 @@ struct ThreadWorld {
   std::vector<size_t> sbytes;
   std::vector<std::vector<double>> hd;
   std::vector<std::vector<float>> hf;
+  const void* bcast = nullptr;
+  bool aborted = false;
   void wait() {
     std::unique_lock<std::mutex> lk(mu);
+    if (aborted) fail(TS_ERR_NCCL, "thread comm: a peer rank failed");
     const uint64_t g = gen;
     if (++arrived == n) {
       arrived = 0;
       ++gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return gen != g; });
+      cv.wait(lk, [&] { return gen != g || aborted; });
+      if (gen == g) {  // woken by an abort, not by the last arrival
+        --arrived;
+        fail(TS_ERR_NCCL, "thread comm: a peer rank failed");
+      }
     }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
   }
 };
 
@@ -200,7 +227,10 @@ class ThreadComm final : public Comm {
     w_->wait();
     for (int k = 0; k < nn; ++k) {
       const size_t idx = size_t(nbr[k]) * w_->n + r_;
-      if (w_->sbytes[idx] != rbytes[k]) fail(TS_ERR_VALIDATION, "thread comm: halo size mismatch");
+      if (w_->sbytes[idx] != rbytes[k]) {
+        w_->abort();
+        fail(TS_ERR_VALIDATION, "thread comm: halo size mismatch");
+      }
       if (rbytes[k])
         TS_CUDA(cudaMemcpyPeerAsync(rbuf[k], dev_, w_->sptr[idx], w_->dev[nbr[k]], rbytes[k], s));
     }
@@ -208,6 +238,14 @@ class ThreadComm final : public Comm {
     w_->wait();  // peers may now reuse their send buffers
   }
   void barrier() override { w_->wait(); }
+  void broadcast(void* host, size_t n, int root) override {
+    if (w_->n == 1 || n == 0) return;
+    if (r_ == root) w_->bcast = host;
+    w_->wait();
+    if (r_ != root) std::memcpy(host, w_->bcast, n);
+    w_->wait();  // the root's buffer stays valid until every copy is done
+  }
+  void abort() override { w_->abort(); }
   const char* kind() const override { return "thread"; }
 
  private:

@@ -39,6 +39,10 @@ struct Comm {
   virtual void exchange(int nn, const int* nbr, void* const* sbuf, const size_t* sbytes, void* const* rbuf,
                         const size_t* rbytes, cudaStream_t s) = 0;
   virtual void barrier() = 0;
+  // HOST bytes from `root` to every rank (setup data built once, e.g. level 2)
+  virtual void broadcast(void* host, size_t n, int root) = 0;
+  // a rank failed: peers blocked in (or entering) a collective fail too instead of waiting forever
+  virtual void abort() {}
   virtual const char* kind() const = 0;
 };
 

@@ -20,6 +20,8 @@
 // The control loops are the single-device ones (solver_core.h), so the
 // reference's recurrences, breakdown rules and termination tests apply
 // unchanged to the global quantities.
+#include <omp.h>
+
 #include <algorithm>
 #include <cstring>
 #include <memory>
@@ -336,26 +338,52 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
     L->p1t_ptr.upload(tptr);
     L->p1t_idx.upload(tidx);
   }
-  // level 2 from the global mesh (identical to the single-device hierarchy)
+  // level 2: the reference's sequential aggregation of the GLOBAL K1 (identical to the
+  // single-device hierarchy), built ONCE on rank 0 with all host cores and broadcast
   {
     const int32_t V = m.vertex_count;
-    const std::vector<uint8_t> gmask1(gmask.begin(), gmask.begin() + 3 * size_t(V));
-    const std::vector<double> lam_e = per_element(m, n_mat, lam), mu_e = per_element(m, n_mat, mu);
-    const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, gmask1);
-    const Aggregation agg = aggregate_p1(k1, cfg.aggregate_target);
-    const BcsrD a2 = build_level2(k1, agg, gmask1);
-    L->n2 = agg.n_aggregates;
-    std::vector<float> bl(a2.blocks.size());
-    for (size_t q = 0; q < bl.size(); ++q) bl[q] = static_cast<float>(a2.blocks[q]);
-    L->l2_row_ptr.upload(a2.row_ptr);
-    L->l2_col_idx.upload(a2.col_idx);
-    L->l2_blocks.upload(bl);
-    L->m2.upload(bcsr_block_jacobi_f32(a2));
-    L->mask2.upload(coarse_mask(agg, gmask1));
+    int64_t sizes[2] = {0, 0};  // n2, nnzb2
+    std::vector<int32_t> agg_g(V), rp2, ci2;
+    std::vector<float> bl2, m2h;
+    std::vector<uint8_t> mk2;
+    if (comm->rank() == 0) {
+      const int saved = omp_get_max_threads();
+      omp_set_num_threads(omp_get_num_procs());
+      const std::vector<uint8_t> gmask1(gmask.begin(), gmask.begin() + 3 * size_t(V));
+      Level2Host l2 = build_level2_host(m, per_element(m, n_mat, lam), per_element(m, n_mat, mu), gmask1,
+                                        cfg.aggregate_target);
+      omp_set_num_threads(saved);
+      sizes[0] = l2.n2;
+      sizes[1] = l2.row_ptr[l2.n2];
+      agg_g = std::move(l2.agg_of_node);
+      rp2 = std::move(l2.row_ptr);
+      ci2 = std::move(l2.col_idx);
+      bl2 = std::move(l2.blocks);
+      m2h = std::move(l2.m2);
+      mk2 = std::move(l2.mask2);
+    }
+    comm->broadcast(sizes, sizeof sizes, 0);
+    L->n2 = static_cast<int32_t>(sizes[0]);
+    rp2.resize(size_t(L->n2) + 1);
+    ci2.resize(sizes[1]);
+    bl2.resize(9 * size_t(sizes[1]));
+    m2h.resize(9 * size_t(L->n2));
+    mk2.resize(3 * size_t(L->n2));
+    comm->broadcast(agg_g.data(), agg_g.size() * sizeof(int32_t), 0);
+    comm->broadcast(rp2.data(), rp2.size() * sizeof(int32_t), 0);
+    comm->broadcast(ci2.data(), ci2.size() * sizeof(int32_t), 0);
+    comm->broadcast(bl2.data(), bl2.size() * sizeof(float), 0);
+    comm->broadcast(m2h.data(), m2h.size() * sizeof(float), 0);
+    comm->broadcast(mk2.data(), mk2.size(), 0);
+    L->l2_row_ptr.upload(rp2);
+    L->l2_col_idx.upload(ci2);
+    L->l2_blocks.upload(bl2);
+    L->m2.upload(m2h);
+    L->mask2.upload(mk2);
     const int32_t Vl = L->n1;
     std::vector<int32_t> agg_l(Vl), aptr(L->n2 + 1, 0);
     for (int32_t i = 0; i < Vl; ++i) {
-      agg_l[i] = agg.agg_of_node[P.l2g[i]];
+      agg_l[i] = agg_g[P.l2g[i]];
       if (P.owned[i]) ++aptr[agg_l[i] + 1];
     }
     for (int32_t a = 0; a < L->n2; ++a) aptr[a + 1] += aptr[a];
@@ -432,6 +460,7 @@ void dist_levels_sizes(const ts_dist_levels& L, int32_t* n0, int32_t* n1, int32_
 }
 
 const std::vector<int32_t>& dist_local_nodes(const ts_dist_levels& L) { return L.plan.l2g; }
+Comm* dist_levels_comm(const ts_dist_levels& L) { return L.comm; }
 
 // host-buffer solve: H2D of f / u0, solve on a private stream, D2H of u
 void dist_solve_host(ts_dist_levels& L, const double* f, const double* u0, double* u, int32_t B,
@@ -524,5 +553,6 @@ void dist_ebe_apply_op(ts_dist_ebe& D, const void* u, void* f, int32_t B, cudaSt
 }
 
 ts_ebe* dist_ebe_local(ts_dist_ebe& D) { return D.d.op.get(); }
+Comm* dist_ebe_comm(const ts_dist_ebe& D) { return D.d.comm; }
 
 }  // namespace tsg

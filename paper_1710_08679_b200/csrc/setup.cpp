@@ -337,4 +337,25 @@ std::vector<float> bcsr_block_jacobi_f32(const BcsrD& a) {
   return inv;
 }
 
+Level2Host build_level2_host(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
+                             const std::vector<uint8_t>& mask1, int32_t aggregate_target) {
+  const BcsrD k1 = assemble_tet4(m, lam_e, mu_e, mask1);
+  setup_mark("level2: K1 assembly");
+  Aggregation agg = aggregate_p1(k1, aggregate_target);
+  setup_mark("level2: aggregation");
+  const BcsrD a2 = build_level2(k1, agg, mask1);
+  setup_mark("level2: Galerkin");
+  Level2Host out;
+  out.n2 = agg.n_aggregates;
+  out.row_ptr = a2.row_ptr;
+  out.col_idx.assign(a2.col_idx.begin(), a2.col_idx.end());
+  out.blocks.resize(a2.blocks.size());
+  for (size_t q = 0; q < a2.blocks.size(); ++q) out.blocks[q] = static_cast<float>(a2.blocks[q]);
+  out.m2 = bcsr_block_jacobi_f32(a2);
+  out.mask2 = coarse_mask(agg, mask1);
+  out.agg_of_node = std::move(agg.agg_of_node);
+  out.seeds = std::move(agg.seeds);
+  return out;
+}
+
 }  // namespace tsg

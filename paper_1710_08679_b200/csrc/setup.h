@@ -29,4 +29,16 @@ BcsrD build_level2(const BcsrD& k1, const Aggregation& agg, const std::vector<ui
 std::vector<uint8_t> coarse_mask(const Aggregation& agg, const std::vector<uint8_t>& fine_mask);
 std::vector<float> bcsr_block_jacobi_f32(const BcsrD& a);
 
+// Level 2 of build_solver_levels (adaptive_cg.hpp:53-65) from the GLOBAL mesh: K1 assembly,
+// the sequential aggregation, the Galerkin product, its block Jacobi and coarse mask, as the
+// fp32 arrays the device level uses (host-only; the partitioned setup builds it on one rank)
+struct Level2Host {
+  int32_t n2 = 0;
+  std::vector<int32_t> agg_of_node, seeds, row_ptr, col_idx;
+  std::vector<float> blocks, m2;
+  std::vector<uint8_t> mask2;
+};
+Level2Host build_level2_host(const Mesh& m, const std::vector<double>& lam_e, const std::vector<double>& mu_e,
+                             const std::vector<uint8_t>& mask1, int32_t aggregate_target);
+
 }  // namespace tsg
