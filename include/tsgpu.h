@@ -193,6 +193,11 @@ ts_status ts_ebe_block_jacobi_host(const ts_ebe* op, void* inv_blocks);
 ts_status ts_ebe_set_timing(ts_ebe* op, int32_t enable);
 ts_status ts_ebe_last_kernel_ms(const ts_ebe* op, float* ms);
 ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t batch, int32_t* n);
+/* the element sweep's unit plan: kind 2 = edge fans, 1 = face pairs, 0 = element-parallel;
+ * units, node rows gathered (= scatter-added) per element, fraction of elements in closed
+ * fans (pairs: paired fraction), elements per unit */
+ts_status ts_ebe_unit_stats(const ts_ebe* op, int32_t* kind, int32_t* units, double* rows_per_element,
+                            double* closed_fraction, double* elements_per_unit);
 /* deterministic mode (on != 0): the colored sweep (greedy element coloring, build_coloring
  * ebe_operator.hpp:190-214, one launch per color, plain read-add-writes) — every node sums its
  * elements in a fixed order, so results are bitwise reproducible and independent of the batch

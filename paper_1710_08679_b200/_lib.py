@@ -103,6 +103,7 @@ _sig = {
     "ts_ebe_set_timing": (C.c_int, [vp, i32]),
     "ts_ebe_last_kernel_ms": (C.c_int, [vp, vp]),
     "ts_ebe_launches_per_apply": (C.c_int, [vp, i32, vp]),
+    "ts_ebe_unit_stats": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "ts_ebe_set_deterministic": (C.c_int, [vp, i32]),
     "ts_levels_create": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "ts_levels_destroy": (None, [vp]),

@@ -432,6 +432,34 @@ ts_status ts_ebe_launches_per_apply(const ts_ebe* op, int32_t batch, int32_t* n)
   TS_API_END
 }
 
+ts_status ts_ebe_unit_stats(const ts_ebe* op, int32_t* kind, int32_t* units, double* rows_per_element,
+                            double* closed_fraction, double* elements_per_unit) {
+  TS_API_BEGIN
+  TS_REQUIRE(op && kind && units && rows_per_element && closed_fraction && elements_per_unit, "ebe: null argument");
+  if (op->fan) {
+    *kind = 2;
+    *units = op->fan->n_units;
+    *rows_per_element = op->fan->rows_per_element;
+    *closed_fraction = op->fan->closed_fraction;
+    *elements_per_unit = op->fan->mean_k;
+  } else if (op->pair) {
+    *kind = 1;
+    *units = op->pair->n_units;
+    const double pf = op->pair->paired_fraction;
+    const int npe = op->npe, nr = npe == 10 ? 14 : 5;
+    *rows_per_element = pf * nr / 2.0 + (1.0 - pf) * npe;
+    *closed_fraction = pf;
+    *elements_per_unit = op->pair->n_units ? double(op->n_elems) / op->pair->n_units : 0.0;
+  } else {
+    *kind = 0;
+    *units = op->n_elems;
+    *rows_per_element = op->npe;
+    *closed_fraction = 0.0;
+    *elements_per_unit = 1.0;
+  }
+  TS_API_END
+}
+
 // ------------------------------------------------------------ partitioned solve
 ts_status ts_comm_nccl_available(char* why, int32_t why_len) {
   TS_API_BEGIN

@@ -546,7 +546,8 @@ void apply_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, 
   }
   // Default dispatch (6, measured: profiles/r01_ebe_tile.txt, r01_ebe_pair_ncu.txt): the face-pair sweep
   // (ebe_pair.cu) for every batch width it covers (1, 2, 4, 8, 16), else the element-parallel sweep.
-  if (!done && (op.kernel == 7 || op.kernel == 6)) done = ebe_pair_apply(op, u, f, batch, s, part);
+  if (!done && op.fan) done = ebe_fan_apply(op, u, f, batch, s, part);
+  if (!done && op.pair) done = ebe_pair_apply(op, u, f, batch, s, part);
   if (!done && op.kernel >= 3)
     done = (op.order == 2)
                ? (sizeof(T) == 4 && batch % 2 == 0 ? launch_fast<T, float2_or<T>, 10, 12>(op, u, f, batch, s, e0, e1)
@@ -603,7 +604,11 @@ int ebe_launches_per_apply(const ts_ebe& op, int32_t batch) {
     for (size_t k = 0; k + 1 < op.color->color_ptr.size(); ++k) n += op.color->color_ptr[k + 1] > op.color->color_ptr[k];
     return init + n;
   }
-  if (op.kernel == 7 || op.kernel == 6) {
+  if (op.fan) {
+    const int p = ebe_fan_launches(op, batch);
+    if (p >= 0) return init + p;
+  }
+  if (op.pair) {
     const int p = ebe_pair_launches(op, batch);
     if (p >= 0) return init + p;
   }
@@ -843,7 +848,8 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   setup_mark("ebe: element records");
   if (kernel_override >= 0) op->kernel = kernel_override;
   else if (const char* k = std::getenv("TSGPU_EBE_KERNEL"))
-    op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "pair" ? 7 : 6;
+    op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "pair" ? 7
+               : std::string(k) == "fan" ? 8 : 6;
   const char* kenv = std::getenv("TSGPU_EBE_KERNEL");
   const bool colored = kernel_override < 0 && kenv && std::string(kenv) == "color";
   {
@@ -865,7 +871,13 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
     op->conn3.upload(conn3);
   }
   setup_mark("ebe: conn3");
-  if (op->kernel == 7 || op->kernel == 6) build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32, pair_topology);
+  // face pairs by default; edge fans (tet10) on request (TSGPU_EBE_KERNEL=fan; measured in
+  // faster at r = 1, slower at r >= 4 on the FP-latency-bound sweep)
+  const bool fans = order == 2 && op->kernel == 8;
+  if (fans) build_fan_plan(*op, m, conn, cs, op->coef64, prec == 32);
+  setup_mark("ebe: fan plan");
+  if (!fans && (op->kernel == 7 || op->kernel == 6 || op->kernel == 8))  // (tet4 under "fan": pairs)
+    build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32, pair_topology);
   setup_mark("ebe: pair plan");
   op->conn.upload(conn);
   op->coef.upload(coef);

@@ -29,6 +29,19 @@ struct EbePairPlan {
   tsg::DevBuf<unsigned char> coef;  // [units][24] of T: A and B coefficient records
 };
 
+// Edge fans for the fan sweep (ebe_fan.cu): element j of a fan around edge (p, q) is
+// (p, q, r_j, r_{j+1}); elements are stored in fan order.
+struct EbeFanPlan {
+  int32_t n_units = 0;            // fans, in element-group order
+  int32_t group_split = 0;        // fans [0, split) cover element group 0
+  double closed_fraction = 0.0;   // elements in closed fans
+  double mean_k = 0.0;            // elements per fan
+  double rows_per_element = 0.0;  // node rows gathered (= reduced) per element
+  tsg::DevBuf<int32_t> words;     // [E][12]: flags, the rows the element adds (node | mask << 28)
+  tsg::DevBuf<unsigned char> coef;  // [E][12] of T, slot-order coefficient records
+  tsg::DevBuf<int32_t> ufirst;    // [U + 1] first element (fan order) of each fan
+};
+
 // Elements sweep in slabs of their lowest vertex id (then Morton order), ebe.cu;
 // TSGPU_EBE_SLABS overrides (1 = plain Morton)
 constexpr int kEbeSlabs = 16;
@@ -87,10 +100,11 @@ struct ts_ebe {
   std::unique_ptr<EbeColorPlan> color;  // greedy element coloring (deterministic sweep)
   bool deterministic = false;           // colored sweep: order-fixed sums, batch-independent bits
   int32_t group_split = 0;              // elements [0, split) = group 0 (partition boundary), rest group 1
-  std::unique_ptr<EbePairPlan> pair;    // face-sharing pairs (kernel 7)
-  int kernel = 6;  // 2 pipelined generic, 3 pipelined batch-specialised, 6 = 7 = face pairs (default);
-                   // each falls back to 3, then 2, for batch widths it does not cover; `deterministic`
-                   // overrides all of them with the colored sweep
+  std::unique_ptr<EbePairPlan> pair;    // face-sharing pairs (kernels 6 = default, 7)
+  std::unique_ptr<EbeFanPlan> fan;      // edge fans (kernel 8, tet10)
+  int kernel = 6;  // 2 pipelined generic, 3 pipelined batch-specialised, 6 = 7 face pairs (default),
+                   // 8 edge fans; each falls back to 3, then 2, for batch widths it does not cover;
+                   // `deterministic` overrides all of them with the colored sweep
   mutable std::mutex host_mu;            // guards the host-entry staging buffers (and `stream`)
   mutable std::unique_ptr<EbeStreamPlan> stream;  // built at the first pinned-host apply
   mutable tsg::DevBuf<unsigned char> stage_u, stage_f;
@@ -131,6 +145,20 @@ KernelFit kernel_fit(int threads, size_t smem) {
   return fit[dev];
 }
 
+// Units per launch of a persistent unit sweep (ebe_pair.cu): long sweeps split into
+// launches of a bounded number of grid strides (TSGPU_EBE_PAIR_STRIDES)
+int64_t pair_launch_units(int64_t units_per_stride, int64_t units);
+// fan sweep (ebe_fan.cu): units [q0, q1) / an element group; false if `batch` is not covered
+bool ebe_fan_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t q0,
+                         int32_t q1);
+bool ebe_fan_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
+int ebe_fan_launches(const ts_ebe& op, int32_t batch);
+void build_fan_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_words, int cs,
+                    const HostVec<double>& coef64, bool fp32);
+// the active unit sweep (fans, else pairs) over its units [q0, q1); unit count of the active plan
+bool ebe_unit_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t q0,
+                          int32_t q1);
+int32_t ebe_unit_count(const ts_ebe& op);
 // pair sweep over units [p0, p1) (no init); false if the pair kernel does not cover `batch`
 bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t p0,
                           int32_t p1);

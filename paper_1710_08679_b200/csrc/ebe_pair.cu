@@ -286,6 +286,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 // number of strides re-aligns the front (TSGPU_EBE_PAIR_STRIDES, 0 = one launch).
 // configs[3] on one device, fp32 r=8: 29.3 -> 24.6 ms (5300 strides); configs[1] stays one launch (`profiles/r01_pair_strides.txt`).
 constexpr int64_t kPairLaunchStrides = 1024;
+}  // namespace
 int64_t pair_launch_units(int64_t units_per_stride, int64_t units) {
   static const int64_t strides = [] {
     const char* e = std::getenv("TSGPU_EBE_PAIR_STRIDES");
@@ -296,6 +297,7 @@ int64_t pair_launch_units(int64_t units_per_stride, int64_t units) {
   const int64_t cap = strides * units_per_stride, n = (units + cap - 1) / cap;
   return std::max<int64_t>((units + n - 1) / n, 1);
 }
+namespace {
 
 template <typename T, typename V, int NPE, int B>
 bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p0, int32_t p1) {
@@ -406,6 +408,14 @@ int ebe_pair_launches(const ts_ebe& op, int32_t batch) {
   const int a = count(0, sp), b = count(sp, n);
   return a < 0 || b < 0 ? -1 : a + b;
 }
+
+bool ebe_unit_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t q0,
+                          int32_t q1) {
+  if (op.fan) return ebe_fan_apply_range(op, u, f, batch, s, q0, q1);
+  return ebe_pair_apply_range(op, u, f, batch, s, q0, q1);
+}
+
+int32_t ebe_unit_count(const ts_ebe& op) { return op.fan ? op.fan->n_units : op.pair ? op.pair->n_units : 0; }
 
 bool ebe_pair_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t p0,
                           int32_t p1) {

@@ -4,7 +4,7 @@
 //
 // Copy-apply-copy moves 3·N·r·s bytes up, sweeps, and moves the same back: at
 // 10M DOF × 16 fp32 cases that is 2 × 650 MB over PCIe around a ~1.2 ms sweep,
-// so the transfers are the whole cost. The pair units are swept in element
+// so the transfers are the whole cost. The sweep's units (fans or pairs) go in element
 // order (slab-major Morton, ebe.cu), so cutting them into chunks gives each node
 // a first chunk that reads it and a last chunk that writes it. The schedule then
 // runs three streams:
@@ -45,25 +45,78 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-std::unique_ptr<EbeStreamPlan> build_stream_plan(const ts_ebe& op) {
-  auto P = std::make_unique<EbeStreamPlan>();
-  if (!op.pair || op.pair->n_units < 2 * kMinUnitsPerChunk) return P;  // small: copy-apply-copy is as fast
+// The active unit sweep's node rows per unit, in unit order (fans: every element's
+// new rows; pairs: the 14 / 5 gathered rows), with each unit's slab key: the
+// lowest vertex id of its first element.
+struct UnitRows {
+  std::vector<int64_t> ptr;   // [U + 1] into rows
+  std::vector<int32_t> rows;  // node ids (rows with all three dofs constrained are left out)
+  std::vector<int32_t> lo;    // [U] lowest vertex id of the unit's first element
+};
+
+UnitRows unit_rows(const ts_ebe& op) {
+  UnitRows R;
+  if (op.fan) {
+    const int32_t U = op.fan->n_units, E = op.n_elems;
+    constexpr int kW = 12;  // ebe_fan.cu record width
+    std::vector<int32_t> uf(size_t(U) + 1), wv(size_t(E) * kW);
+    TS_CUDA(cudaMemcpy(uf.data(), op.fan->ufirst.get(), uf.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    TS_CUDA(cudaMemcpy(wv.data(), op.fan->words.get(), wv.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    R.ptr.assign(1, 0);
+    for (int32_t i = 0; i < U; ++i) {
+      int32_t lo = INT32_MAX;
+      for (int32_t x = uf[i]; x < uf[i + 1]; ++x) {
+        const int32_t* w = wv.data() + kW * size_t(x);
+        const bool start = (w[0] & 1) != 0;
+        const int n = start ? 10 : 4;
+        for (int q = 1; q <= n; ++q) {
+          const int32_t v = w[q];
+          if (v == -1) continue;
+          if ((static_cast<uint32_t>(v) >> 28) == 7u) continue;
+          R.rows.push_back(v & 0x0FFFFFFF);
+        }
+        if (x == uf[i])  // p, q, r0, r1 are the first element's vertices
+          for (int q : {1, 2, 4, 7}) lo = std::min(lo, w[q] & 0x0FFFFFFF);
+      }
+      R.lo.push_back(lo);
+      R.ptr.push_back(static_cast<int64_t>(R.rows.size()));
+    }
+    return R;
+  }
   const int npe = op.npe;
   const int W = npe == 10 ? 16 : 8, NR = npe == 10 ? 14 : 5;
-  const int32_t U = op.pair->n_units, N = op.n_nodes;
+  const int32_t U = op.pair->n_units;
   std::vector<int32_t> pc(size_t(U) * W);
   TS_CUDA(cudaMemcpy(pc.data(), op.pair->conn.get(), pc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  // chunks = the element slabs (ebe.cu): units are in element order, slab-major,
-  // and a unit's slab is that of its lowest vertex id (A's slots 0-3)
+  R.ptr.assign(1, 0);
+  for (int32_t i = 0; i < U; ++i) {
+    const int32_t* w = pc.data() + size_t(i) * W;
+    R.lo.push_back(std::min(std::min(w[0], w[1]), std::min(w[2], w[3])) / 3);
+    const uint32_t ma = static_cast<uint32_t>(w[NR]), mb = static_cast<uint32_t>(w[NR + 1]);
+    for (int r = 0; r < NR; ++r) {
+      const uint32_t bits = r < npe ? (ma >> (3 * r)) & 7u : (mb >> (3 * (r - npe))) & 7u;
+      if (bits == 7u) continue;  // row neither gathered nor reduced (e.g. a null B's own rows)
+      R.rows.push_back(w[r] / 3);
+    }
+    R.ptr.push_back(static_cast<int64_t>(R.rows.size()));
+  }
+  return R;
+}
+
+std::unique_ptr<EbeStreamPlan> build_stream_plan(const ts_ebe& op) {
+  auto P = std::make_unique<EbeStreamPlan>();
+  const int32_t U = ebe_unit_count(op), N = op.n_nodes;
+  const int32_t min_units = op.fan ? kMinUnitsPerChunk / 3 : kMinUnitsPerChunk;  // a fan is ~3 pairs of work
+  if (U < 2 * min_units) return P;  // small: copy-apply-copy is as fast
+  const UnitRows R = unit_rows(op);
+  // chunks = the element slabs (ebe.cu): units are in element order, slab-major
   const int64_t V = std::max<int32_t>(1, op.n_vertices);
   P->unit_ptr.assign(1, 0);
   int prev = -1;
   for (int32_t i = 0; i < U; ++i) {
-    const int32_t* w = pc.data() + size_t(i) * W;
-    const int32_t lo = std::min(std::min(w[0], w[1]), std::min(w[2], w[3])) / 3;
-    const int sl = ebe_slab_of(lo, V, op.n_slabs);
+    const int sl = ebe_slab_of(R.lo[i], V, op.n_slabs);
     if (sl < prev) return P;  // not slab-ordered (e.g. grouped partition operators)
-    if (sl != prev && i > 0 && i - P->unit_ptr.back() >= kMinUnitsPerChunk) P->unit_ptr.push_back(i);
+    if (sl != prev && i > 0 && i - P->unit_ptr.back() >= min_units) P->unit_ptr.push_back(i);
     prev = sl;
   }
   P->unit_ptr.push_back(U);
@@ -72,17 +125,12 @@ std::unique_ptr<EbeStreamPlan> build_stream_plan(const ts_ebe& op) {
   P->chunks = K;
   std::vector<int32_t> first(N, K), last(N, -1);
   for (int k = 0; k < K; ++k)
-    for (int32_t i = P->unit_ptr[k]; i < P->unit_ptr[k + 1]; ++i) {
-      const int32_t* w = pc.data() + size_t(i) * W;
-      const uint32_t ma = static_cast<uint32_t>(w[NR]), mb = static_cast<uint32_t>(w[NR + 1]);
-      for (int r = 0; r < NR; ++r) {
-        const uint32_t bits = r < npe ? (ma >> (3 * r)) & 7u : (mb >> (3 * (r - npe))) & 7u;
-        if (bits == 7u) continue;  // row neither gathered nor reduced (e.g. a null B's own rows)
-        const int32_t n = w[r] / 3;
+    for (int32_t i = P->unit_ptr[k]; i < P->unit_ptr[k + 1]; ++i)
+      for (int64_t q = R.ptr[i]; q < R.ptr[i + 1]; ++q) {
+        const int32_t n = R.rows[q];
         first[n] = std::min(first[n], k);
         last[n] = k;  // chunks are visited in order
       }
-    }
   for (int32_t n = 0; n < N; ++n)
     if (last[n] < 0) first[n] = last[n] = 0;  // untouched: identity / zero rows, out after chunk 0
   // Node rows move in kBlocks contiguous blocks: a block goes up before the
@@ -155,8 +203,8 @@ bool apply_streamed(const ts_ebe& op, const EbeStreamPlan& P, const T* uh, T* fh
   const size_t row = 3 * static_cast<size_t>(batch);  // scalars per node
   T* du = reinterpret_cast<T*>(op.stage_u.get());
   T* df = reinterpret_cast<T*>(op.stage_f.get());
-  // probe: does the pair sweep cover this batch width? (an empty range launches nothing)
-  if (!ebe_pair_apply_range(op, du, df, batch, P.s_comp, 0, 0)) return false;
+  // probe: does the unit sweep cover this batch width? (an empty range launches nothing)
+  if (!ebe_unit_apply_range(op, du, df, batch, P.s_comp, 0, 0)) return false;
   // the pipeline's non-blocking streams start after work already queued on the legacy default
   // stream (e.g. a producer of u or a pending reader of f), as the copy-apply-copy path would
   TS_CUDA(cudaEventRecord(P.ev_entry, nullptr));
@@ -178,7 +226,7 @@ bool apply_streamed(const ts_ebe& op, const EbeStreamPlan& P, const T* uh, T* fh
                                                                                         du, df);
       TS_CUDA_LAUNCH();
     }
-    ebe_pair_apply_range(op, du, df, batch, P.s_comp, P.unit_ptr[k], P.unit_ptr[k + 1]);
+    ebe_unit_apply_range(op, du, df, batch, P.s_comp, P.unit_ptr[k], P.unit_ptr[k + 1]);
     TS_CUDA(cudaEventRecord(P.ev_done[k], P.s_comp));
     TS_CUDA(cudaStreamWaitEvent(P.s_out, P.ev_done[k], 0));
     for (int32_t q = P.out_ptr[k]; q < P.out_ptr[k + 1]; ++q) {
@@ -199,7 +247,7 @@ void ebe_apply_host(const ts_ebe& op, const void* u, void* f, int32_t batch) {
   std::lock_guard<std::mutex> lock(op.host_mu);
   op.stage_u.ensure(bytes);
   op.stage_f.ensure(bytes);
-  if (op.kernel >= 6 && op.pair && !op.deterministic && is_pinned(u) && is_pinned(f)) {
+  if (op.kernel >= 6 && (op.pair || op.fan) && !op.deterministic && is_pinned(u) && is_pinned(f)) {
     if (!op.stream) op.stream = build_stream_plan(op);
     if (op.stream->usable) {
       const bool done =

@@ -216,6 +216,160 @@ __device__ __forceinline__ void tet10_product(const V (&u)[10][3], const V (&b)[
   }
 }
 
+// tet10 product writing through an accessor F(s, c) -> V& (compile-time slot s,
+// component c) that ACCUMULATES into the slots of the bit mask ACC (the rest are
+// overwritten). Same operations as tet10_product; an accumulated slot costs at
+// most one extra op per component (the first write of slots 0-3 becomes a
+// subtraction / addition; slots 4-9 fold into the FMA that first writes them).
+// Used by the fan sweep (ebe_fan.cu), where rows shared with the previous element
+// of the fan keep their partial sums in registers.
+template <unsigned ACC, class V, class F>
+__device__ __forceinline__ void tet10_product_acc(const V (&u)[10][3], const V (&b)[3][3], V lp, V mp, F&& fr) {
+  using O = LaneOps<V>;
+  constexpr bool A0 = ACC & 1u, A1 = ACC & 2u, A2 = ACC & 4u, A3 = ACC & 8u, A4 = ACC & 16u, A5 = ACC & 32u,
+                 A6 = ACC & 64u, A7 = ACC & 128u, A8 = ACC & 256u, A9 = ACC & 512u;
+  const V three = O::splat(3), four = O::splat(4), mfour = O::splat(-4), mthree = O::splat(-3);
+  const V mp2 = O::add(mp, mp);
+  V S[4][6];
+  {
+    V E[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V m = O::mul(mthree, u[0][c]);
+      E[c][0] = O::fma(four, u[4][c], O::sub(m, u[1][c]));
+      E[c][1] = O::fma(four, u[6][c], O::sub(m, u[2][c]));
+      E[c][2] = O::fma(four, u[7][c], O::sub(m, u[3][c]));
+    }
+    V G[3][3];
+    grad_from(E, b, G);
+    stress6(G, lp, mp2, mp, S[0]);
+  }
+  {
+    V E[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V s = O::fma(mfour, u[4][c], u[0][c]);
+      E[c][0] = O::fma(three, u[1][c], s);
+      E[c][1] = O::fma(four, u[5][c], O::sub(s, u[2][c]));
+      E[c][2] = O::fma(four, u[8][c], O::sub(s, u[3][c]));
+    }
+    V G[3][3];
+    grad_from(E, b, G);
+    stress6(G, lp, mp2, mp, S[1]);
+  }
+  {
+    V E[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V s = O::fma(mfour, u[6][c], u[0][c]);
+      E[c][0] = O::fma(four, u[5][c], O::sub(s, u[1][c]));
+      E[c][1] = O::fma(three, u[2][c], s);
+      E[c][2] = O::fma(four, u[9][c], O::sub(s, u[3][c]));
+    }
+    V G[3][3];
+    grad_from(E, b, G);
+    stress6(G, lp, mp2, mp, S[2]);
+  }
+  {
+    V E[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V s = O::fma(mfour, u[7][c], u[0][c]);
+      E[c][0] = O::fma(four, u[8][c], O::sub(s, u[1][c]));
+      E[c][1] = O::fma(four, u[9][c], O::sub(s, u[2][c]));
+      E[c][2] = O::fma(three, u[3][c], s);
+    }
+    V G[3][3];
+    grad_from(E, b, G);
+    stress6(G, lp, mp2, mp, S[3]);
+  }
+  V Ssum[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) Ssum[q] = O::add(O::add(S[0][q], S[1][q]), O::add(S[2][q], S[3][q]));
+  // first writes: accumulated slots 1-3 hold (H - acc), so the negations below give (acc - H)
+  V t0[3], s0[3];
+  {
+    V sh[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sh[q] = O::add(S[0][q], Ssum[q]);
+    V h1[3], h2[3], h3[3];
+    sym_mul(sh, b[0], h1);
+    sym_mul(sh, b[1], h2);
+    sym_mul(sh, b[2], h3);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      t0[c] = O::add(O::add(h1[c], h2[c]), h3[c]);
+      fr(4, c) = A4 ? O::fma(four, h1[c], fr(4, c)) : O::mul(four, h1[c]);
+      fr(6, c) = A6 ? O::fma(four, h2[c], fr(6, c)) : O::mul(four, h2[c]);
+      fr(7, c) = A7 ? O::fma(four, h3[c], fr(7, c)) : O::mul(four, h3[c]);
+      fr(1, c) = A1 ? O::sub(h1[c], fr(1, c)) : h1[c];
+      fr(2, c) = A2 ? O::sub(h2[c], fr(2, c)) : h2[c];
+      fr(3, c) = A3 ? O::sub(h3[c], fr(3, c)) : h3[c];
+    }
+  }
+  {
+    V sh[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sh[q] = O::add(S[1][q], Ssum[q]);
+    V h1[3], h2[3], h3[3];
+    sym_mul(sh, b[0], h1);
+    sym_mul(sh, b[1], h2);
+    sym_mul(sh, b[2], h3);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
+      s0[c] = t;
+      fr(4, c) = O::fma(mfour, t, fr(4, c));
+      fr(1, c) = O::fma(three, h1[c], O::neg(fr(1, c)));
+      fr(5, c) = A5 ? O::fma(four, h2[c], fr(5, c)) : O::mul(four, h2[c]);
+      fr(2, c) = O::add(fr(2, c), h2[c]);
+      fr(8, c) = A8 ? O::fma(four, h3[c], fr(8, c)) : O::mul(four, h3[c]);
+      fr(3, c) = O::add(fr(3, c), h3[c]);
+    }
+  }
+  {
+    V sh[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sh[q] = O::add(S[2][q], Ssum[q]);
+    V h1[3], h2[3], h3[3];
+    sym_mul(sh, b[0], h1);
+    sym_mul(sh, b[1], h2);
+    sym_mul(sh, b[2], h3);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
+      s0[c] = O::add(s0[c], t);
+      fr(6, c) = O::fma(mfour, t, fr(6, c));
+      fr(5, c) = O::fma(four, h1[c], fr(5, c));
+      fr(1, c) = O::sub(fr(1, c), h1[c]);
+      fr(2, c) = O::fma(three, h2[c], O::neg(fr(2, c)));
+      fr(9, c) = A9 ? O::fma(four, h3[c], fr(9, c)) : O::mul(four, h3[c]);
+      fr(3, c) = O::add(fr(3, c), h3[c]);
+    }
+  }
+  {
+    V sh[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sh[q] = O::add(S[3][q], Ssum[q]);
+    V h1[3], h2[3], h3[3];
+    sym_mul(sh, b[0], h1);
+    sym_mul(sh, b[1], h2);
+    sym_mul(sh, b[2], h3);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V t = O::add(O::add(h1[c], h2[c]), h3[c]);
+      fr(0, c) = A0 ? O::fma(mthree, t0[c], O::add(O::add(s0[c], t), fr(0, c)))
+                    : O::fma(mthree, t0[c], O::add(s0[c], t));
+      fr(7, c) = O::fma(mfour, t, fr(7, c));
+      fr(8, c) = O::fma(four, h1[c], fr(8, c));
+      fr(1, c) = O::sub(fr(1, c), h1[c]);
+      fr(9, c) = O::fma(four, h2[c], fr(9, c));
+      fr(2, c) = O::sub(fr(2, c), h2[c]);
+      fr(3, c) = O::fma(three, h3[c], O::neg(fr(3, c)));
+    }
+  }
+}
+
 // tet4 (constant strain): G = sum_k (u_k - u_0) b_k^T ; f_k = V sigma b_k ; f_0 = -sum f_k
 template <class V>
 __device__ __forceinline__ void tet4_product(const V (&u)[4][3], const V (&b)[3][3], V lp, V mp,

@@ -477,6 +477,14 @@ class EbeOperator:
         _ck(lib.ts_ebe_launches_per_apply(self._h, int(batch), C.byref(n)))
         return n.value
 
+    def unit_stats(self) -> dict:
+        """The element sweep's unit plan (edge fans / face pairs / elements)."""
+        k, u = C.c_int32(), C.c_int32()
+        rpe, cf, epu = C.c_double(), C.c_double(), C.c_double()
+        _ck(lib.ts_ebe_unit_stats(self._h, C.byref(k), C.byref(u), C.byref(rpe), C.byref(cf), C.byref(epu)))
+        return {"kind": {2: "fans", 1: "pairs", 0: "elements"}[k.value], "units": u.value,
+                "rows_per_element": rpe.value, "closed_fraction": cf.value, "elements_per_unit": epu.value}
+
     def host_stream_chunks(self) -> int:
         """Chunks of the pinned-host streaming schedule (0 = copy-apply-copy)."""
         n = C.c_int32()

@@ -41,8 +41,8 @@ CASES = [
 ]
 
 
-KERNELS = ["auto", "pipe", "fast", "color", "pair"]  # TSGPU_EBE_KERNEL: default dispatch, generic and batch-specialised
-# element-parallel RED sweeps, deterministic colored sweep, face-pair sweep
+KERNELS = ["auto", "pipe", "fast", "color", "pair", "fan"]  # TSGPU_EBE_KERNEL: default dispatch, generic and
+# batch-specialised element-parallel RED sweeps, deterministic colored sweep, face-pair sweep, edge-fan sweep
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -192,13 +192,15 @@ def test_ebe_many_chunks_per_block(checker, monkeypatch, kernel, prec, batch, or
     assert np.array_equal(got[mask == 1], u[mask == 1])
 
 
+@pytest.mark.parametrize("kernel", ["auto", "fan"])
 @pytest.mark.parametrize("order", [2, 1])
 @pytest.mark.parametrize("prec", [32, 64])
 @pytest.mark.parametrize("batch", [1, 4, 16, 3])
-def test_host_apply_streams_and_matches_device(order, prec, batch):
+def test_host_apply_streams_and_matches_device(monkeypatch, kernel, order, prec, batch):
     """ts_ebe_apply_host with pinned buffers overlaps H2D / sweep / D2H chunk by
     chunk (ebe_stream.cu): same f as the device apply, every row copied back;
-    batch 3 (no pair kernel) and pageable buffers take copy-apply-copy."""
+    batch 3 (no pair / fan kernel) and pageable buffers take copy-apply-copy."""
+    monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
     cells = (40, 40, 20) if order == 2 else (60, 60, 30)
     mesh = ts.generate_box_mesh((4000.0, 4000.0, 2000.0), cells, (1200.0,))
     nn = mesh.node_count() if order == 2 else mesh.vertex_count

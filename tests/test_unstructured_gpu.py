@@ -68,7 +68,7 @@ def meshes(checker):
     return scrambled_mesh(checker, (3000.0, 2000.0, 1500.0), (6, 5, 4), 5)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "pipe", "fast", "color"])
+@pytest.mark.parametrize("kernel", ["auto", "pipe", "fast", "color", "fan"])
 @pytest.mark.parametrize("order", [2, 1])
 @pytest.mark.parametrize("prec", [32, 64])
 @pytest.mark.parametrize("batch", [1, 4, 16, 3])
@@ -158,3 +158,32 @@ def test_partitioned_product_unstructured(meshes):
             raise e
     for dofs, fl in out:
         assert rel(fl, want[dofs]) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel", ["fan", "pair"])
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("batch", [1, 8, 16])
+def test_ebe_holey_mesh(checker, meshes, monkeypatch, kernel, prec, batch):
+    """A third of the elements removed at random: edge rings break into open fans of every
+    length (and closed fans of other valences), faces lose their partners, some nodes touch
+    no element. The fan cover / pair matching must still produce exactly K u."""
+    from oracle import MeshArrays
+    monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
+    m, _ = meshes
+    keep = np.random.default_rng(3).random(len(m.tets10)) > 0.33
+    h = MeshArrays(m.coords, np.ascontiguousarray(m.tets10[keep]), np.ascontiguousarray(m.material_id[keep]),
+                   m.vertex_count, m.bc_node, m.bc_axis)
+    pm = ts.Mesh.from_arrays(h.coords, h.tets10, h.material_id, h.vertex_count, h.bc_node, h.bc_axis)
+    mask = h.dirichlet_mask()
+    lam, mu = lame(TWO_LAYER)
+    op = ts.EbeOperator(pm, 2, mats(), mask, prec=prec)
+    st = op.unit_stats()
+    assert st["kind"] == ("fans" if kernel == "fan" else "pairs")
+    if kernel == "fan":
+        assert 0.0 < st["closed_fraction"] < 1.0 and 4.0 < st["rows_per_element"] < 10.0
+    dt = np.float32 if prec == 32 else np.float64
+    u = checker.rng_sym(17 + batch, 3 * h.n_nodes * batch).reshape(3 * h.n_nodes, batch).astype(dt)
+    want = checker.ebe_apply(h, 2, lam, mu, mask, prec, u)
+    got = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    assert rel(got, want) <= (1e-5 if prec == 32 else 1e-12)
+    assert np.array_equal(got[mask == 1], u[mask == 1])
