@@ -18,6 +18,13 @@ explicit flush is needed between steps.
   cpu_baseline: the UNMODIFIED reference (oracle/_ref/libtsref.so) timing the
            same apply on this host's cores (rank 0, N = 1).
   --impl reference: the reference's own CPU implementation as the arm.
+  northstar: BASELINE configs[3], the north-star run: the multigrid solve of r = 8
+           cases on ONE layered-crust mesh partitioned over the N GPUs (RCB; NCCL
+           halo exchange inside every product, all-reduced dots; level 2 built
+           once and broadcast): time per case = the slowest rank's solve / r, the
+           per-rank level-0 sweep roofline and interface bytes. N > 1: the 405M-DOF
+           configs[3] mesh; N = 1: the configs[2] mesh on in-process ranks
+           (--northstar-threads P; 1 by default) of the one GPU.
   greens : the Green's-function bank (configs[4] workflow at one-GPU scale):
            48 unit slips on a vertical fault in the configs[1] box, batch 16,
            through ts_greens_bank; total sweep time and time per case.
@@ -336,23 +343,14 @@ def main_partitioned(args, world, rank, local):
     import paper_1710_08679_b200 as ts
     from paper_1710_08679_b200.dist import Comm, DistEbeOperator, partition_rcb
 
-    # pre-flight of our own NCCL communicator (all ranks agree through torch.distributed before any
-    # partitioned work): on failure every rank falls back to independent replicas
-    err = ""
-    try:
-        with stdout_to_stderr():  # NCCL prints its version banner on stdout; the JSON line must be alone there
-            comm = Comm.nccl_from_torch(local)
-        probe = comm.allreduce_sum(torch.ones(4, dtype=torch.float64, device="cuda"))
-        torch.cuda.synchronize()
-        if not bool((probe == world).all()):
-            err = f"all-reduce self-test returned {probe.tolist()}"
-    except Exception as exc:  # noqa: BLE001
-        err = f"{type(exc).__name__}: {exc}"
-    bad = torch.tensor([1.0 if err else 0.0], device="cuda")
-    dist.all_reduce(bad)
-    if bad.item() > 0:
-        log(f"[rank {rank}] partitioned path unavailable ({err or 'another rank failed'}); running replicas")
-        return f"partitioned path unavailable: {err or 'another rank failed'}"
+    # our own NCCL communicator over the torch.distributed ranks; a failure is fatal (no silent
+    # fallback to replicas: the partitioned path is what N > 1 measures)
+    with stdout_to_stderr():  # NCCL prints its version banner on stdout; the JSON line must be alone there
+        comm = Comm.nccl_from_torch(local)
+    probe = comm.allreduce_sum(torch.ones(4, dtype=torch.float64, device="cuda"))
+    torch.cuda.synchronize()
+    if not bool((probe == world).all()):
+        raise RuntimeError(f"NCCL all-reduce self-test returned {probe.tolist()} on rank {rank}")
 
     cells = (args.cells[0], args.cells[1] * world, args.cells[2])
     ext, div, ifs = mesh_spec(cells)
@@ -410,10 +408,22 @@ def main_partitioned(args, world, rank, local):
     io_bytes = int(u.numel() * u.element_size())
     peak, peak_kind = hbm_peak()
     halo_bytes = int(op.halo_rows) * 3 * r * s
+    del u, f, ud, fd, uh, fh, op
+    torch.cuda.empty_cache()
+    northstar = None
+    if not args.no_northstar:  # BASELINE configs[3]: the partitioned 400M-DOF solve, r = 8, on these N GPUs
+        def sync():
+            torch.cuda.synchronize()
+            dist.barrier()
+        cells_ns = (tuple(args.northstar_cells) if args.northstar_cells
+                    else NORTHSTAR_CELLS if world > 1 else tuple(args.solve_cells))
+        mine = northstar_rank(ts, torch, cells_ns, args.northstar_cases, comm, rank, world, sync, args.steps)
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        northstar = northstar_summary(allr, cells_ns, args.northstar_cases, world, f"NCCL x{world}", hbm_peak()[0])
+        torch.cuda.empty_cache()
     solve = None
     if not args.no_solve:
-        del u, f, ud, fd, uh, fh, op
-        torch.cuda.empty_cache()
         solve = solve_leg(args, ts, torch, world, rank, local)
     if rank == 0:
         out = {
@@ -437,6 +447,7 @@ def main_partitioned(args, world, rank, local):
             "cpu_baseline": None,
             "clocks": clk.summary(),
             "gpu_launches": 5 * args.steps,
+            "northstar": northstar,
             "solve": solve,
         }
         print(json.dumps(out), flush=True)
@@ -498,6 +509,150 @@ def greens_leg(args, ts, torch, world, rank, local):
             "clocks": clk.summary()}
 
 
+# ------------------------------------------------- north star: partitioned solve
+FOUR_LAYER = THREE_LAYER + [(8000.0, 4500.0, 3300.0)]  # configs[3]: layered crust over mantle (synthetic)
+NORTHSTAR_CELLS = (281, 423, 141)  # configs[3]: 405M DOF (2.8 km cells over 792 x 1192 x 400 km)
+
+
+def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps):
+    """One rank of the configs[3] workload: build_solver_levels on this rank's RCB
+    partition of the global layered-crust mesh (DistLevels: level 2 built once on
+    rank 0 and broadcast), manufactured fields (acceptance_main.cpp:82-102) ->
+    f = K u* through the partitioned fp64 operator, then ONE timed solve of r cases
+    (fp64 outer, fp32 inner, halo exchange inside every product, all-reduced dots).
+    `sync()` is a barrier over the ranks. Returns this rank's numbers."""
+    import numpy as np
+    from paper_1710_08679_b200.dist import DistLevels, partition_rcb
+
+    ext = tuple(c * CELL_KM * 1e3 for c in cells)
+    ifs = (0.2 * ext[2], 0.45 * ext[2], 0.8 * ext[2])
+    t0 = time.perf_counter()
+    mesh = ts.generate_box_mesh(ext, cells, ifs)
+    t_mesh = time.perf_counter() - t0
+    part = partition_rcb(mesh, nranks)
+    cfg = ts.SolverConfig(batch_size=r)
+    mats = [ts.material_from_wavespeeds(*t) for t in FOUR_LAYER]
+    dl = DistLevels(mesh, mats, part, comm, cfg)
+    info = dl.info()
+    l2g = dl.local_nodes().astype(np.int64)
+    xyz = torch.from_numpy(np.asarray(mesh.coords).reshape(-1, 3)[l2g]).cuda()
+    mask = torch.from_numpy(mesh.dirichlet_mask().reshape(-1, 3)[l2g].reshape(-1).copy()).cuda().bool()
+    n_glob, e_glob = mesh.node_count(), mesh.element_count()
+    dl.mesh = None
+    del mesh, part
+    sync()
+    t_setup = time.perf_counter() - t0
+    n = dl.n_local
+    g = torch.Generator(device="cuda").manual_seed(31)  # same cases on every rank
+    amp = 0.05 * (1 + 0.2 * (torch.rand(r, device="cuda", dtype=torch.float64, generator=g) * 2 - 1))
+    ky = 1.0 + (torch.rand(r, device="cuda", dtype=torch.float64, generator=g) > 0.5).double()
+    X, Y, Z = [xyz[:, k:k + 1] / ext[k] for k in range(3)]
+    sz = torch.sin(0.5 * torch.pi * Z)
+    us = torch.stack([amp * torch.sin(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz,
+                      amp * torch.cos(torch.pi * X) * torch.sin(ky * torch.pi * Y) * sz,
+                      amp * torch.cos(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz], 1).reshape(3 * n, r)
+    us = us.contiguous()
+    us[mask] = 0
+    del X, Y, Z, sz, xyz
+    f = torch.empty_like(us)
+    dl.apply(0, us, f)
+    # the partitioned level-0 sweep (fp32, halo exchange overlapped with the interior elements)
+    u32 = us.float()
+    f32 = torch.empty_like(u32)
+    for _ in range(3):
+        dl.apply(1, u32, f32)
+    sync()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        dl.apply(1, u32, f32)
+    b.record()
+    sync()
+    l0_ms = a.elapsed_time(b) / steps
+    del u32, f32
+    # warm-up: one capped outer iteration allocates the solver workspaces
+    try:
+        dl.solve(f, torch.zeros_like(f), ts.SolverConfig(batch_size=r, outer_max_iter=1))
+    except ts.ConvergenceError:
+        pass
+    sync()
+    a.record()
+    u, rep = dl.solve(f, torch.zeros_like(f), cfg)
+    b.record()
+    sync()
+    solve_s = a.elapsed_time(b) / 1e3
+    err2 = torch.tensor([float(((u - us) ** 2)[~mask].sum()), float((us ** 2)[~mask].sum())], dtype=torch.float64)
+    free, total = torch.cuda.mem_get_info()
+    return {"rank": rank, "n_local": n, "elements": info["elements"], "halo_rows0": info["halo_rows0"],
+            "neighbours": info["neighbours"], "n2": dl.n2, "levels_setup_s": info["setup_s"], "mesh_s": t_mesh,
+            "setup_s": t_setup, "l0_ms": l0_ms, "solve_s": solve_s, "outer": rep.outer_iterations,
+            "inner": list(rep.inner_iterations), "time_inner_s": list(rep.time_inner_s),
+            "max_final_rel_residual": rep.max_final_residual(), "err2": err2.tolist(),
+            "device_used_gb": (total - free) / 1e9, "n_global": n_glob, "e_global": e_glob}
+
+
+def northstar_summary(per_rank, cells, r, nranks, backend, peak):
+    """BASELINE metric 'time per case (s)' of the partitioned solve: the slowest rank's
+    solve time / r; the per-rank level-0 sweep roofline (algorithmic bytes / time)."""
+    solve_s = max(x["solve_s"] for x in per_rank)
+    l0 = []
+    for x in per_rank:
+        B = alg_bytes(x["elements"], x["n_local"], r, 4)
+        l0.append({"rank": x["rank"], "ms": round(x["l0_ms"], 4), "GBps": round(B / x["l0_ms"] / 1e6, 1),
+                   "frac": round(B / x["l0_ms"] / 1e6 / peak, 4), "interface_rows": x["halo_rows0"],
+                   "interface_bytes": int(x["halo_rows0"]) * 3 * r * 4, "neighbours": x["neighbours"]})
+    e2 = sum(x["err2"][0] for x in per_rank)
+    n2 = sum(x["err2"][1] for x in per_rank)
+    x0 = per_rank[0]
+    return {"metric": "time per case (s)", "higher_is_better": False,
+            "workload": f"configs[3]-shaped partitioned solve: {list(cells)} cells, {3 * x0['n_global']} DOF, "
+                        f"{x0['e_global']} tet10, 4-layer crust, {r} cases, RCB over {nranks} ranks",
+            "value": round(solve_s / r, 5), "unit": "s", "ranks": nranks, "backend": backend, "cases": r,
+            "solve_s": round(solve_s, 4), "setup_s": round(max(x["setup_s"] for x in per_rank), 2),
+            "levels_setup_s": round(max(x["levels_setup_s"] for x in per_rank), 2),
+            "mesh_s": round(max(x["mesh_s"] for x in per_rank), 2),
+            "outer_iterations": x0["outer"], "inner_iterations": x0["inner"],
+            "time_inner_s_rank0": [round(t, 3) for t in x0["time_inner_s"]],
+            "max_final_rel_residual": max(x["max_final_rel_residual"] for x in per_rank),
+            "rel_err_vs_manufactured": (e2 / max(n2, 1e-300)) ** 0.5, "n2": x0["n2"],
+            "l0_sweep_per_rank": l0, "device_used_gb_max": round(max(x["device_used_gb"] for x in per_rank), 1),
+            "entry": "ts_dist_levels_create + ts_dist_solve_device (device-resident f / u per rank)"}
+
+
+def northstar_threads(args, ts, torch, cells, r, P):
+    """The north-star leg with P in-process ranks on ONE GPU (ThreadWorld: the same SPMD
+    device code as NCCL ranks, halo / all-reduce through device copies)."""
+    import threading
+    from paper_1710_08679_b200.dist import Comm, ThreadWorld
+    world = ThreadWorld(P)
+    comms = [Comm.thread(world, k, 0) for k in range(P)]
+    bar = threading.Barrier(P)
+    out, err = [None] * P, [None] * P
+
+    def body(k):
+        try:
+            torch.cuda.set_device(0)
+
+            def sync():
+                torch.cuda.synchronize()
+                bar.wait()
+            with torch.cuda.stream(torch.cuda.Stream()):  # each rank its own stream, as on its own GPU
+                out[k] = northstar_rank(ts, torch, cells, r, comms[k], k, P, sync, args.steps)
+        except BaseException as e:  # noqa: BLE001
+            err[k] = e
+            bar.abort()
+    th = [threading.Thread(target=body, args=(k,)) for k in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    real = [e for e in err if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if real:  # the first rank's own failure, not a peer's "a peer rank failed"
+        real.sort(key=lambda e: "peer rank failed" in str(e))
+        raise real[0]
+    return northstar_summary(out, cells, r, P, f"threads x{P} on one GPU", hbm_peak()[0])
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -518,6 +673,12 @@ def main():
     ap.add_argument("--solve-cells", type=int, nargs=3, default=[140, 210, 70], help="configs[2]: 50M DOF")
     ap.add_argument("--solve-cases", type=int, default=16)
     ap.add_argument("--cpu-solve-cells", type=int, nargs=3, default=[16, 16, 16])
+    ap.add_argument("--no-northstar", action="store_true", help="skip the partitioned-solve (configs[3]) leg")
+    ap.add_argument("--northstar-cells", type=int, nargs=3, default=None,
+                    help="mesh of the partitioned solve (default: configs[3] at N > 1, configs[2] at N = 1)")
+    ap.add_argument("--northstar-cases", type=int, default=8)
+    ap.add_argument("--northstar-threads", type=int, default=1,
+                    help="N = 1: in-process ranks of the partitioned solve on the one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -551,10 +712,7 @@ def main():
         with stdout_to_stderr():
             dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
         if not args.replicas:
-            fallback = main_partitioned(args, world, rank, local)
-            if fallback is None:
-                return None
-            args.partitioned_fallback = fallback
+            return main_partitioned(args, world, rank, local)
 
     cells = tuple(args.cells)
     ext, div, ifs = mesh_spec(cells)
@@ -689,6 +847,11 @@ def main():
     if not args.no_greens:
         torch.cuda.empty_cache()
         greens = greens_leg(args, ts, torch, world, rank, local)
+    northstar = None
+    if world == 1 and not args.no_northstar:  # the partitioned path on this one GPU (in-process ranks)
+        torch.cuda.empty_cache()
+        cells_ns = tuple(args.northstar_cells) if args.northstar_cells else tuple(args.solve_cells)
+        northstar = northstar_threads(args, ts, torch, cells_ns, args.northstar_cases, args.northstar_threads)
 
     if rank == 0:
         out = {
@@ -711,9 +874,8 @@ def main():
             "e2e_result_matches_device": ok,
             "solve": solve,
             "greens": greens,
+            "northstar": northstar,
         }
-        if getattr(args, "partitioned_fallback", None):
-            out["partitioned_fallback"] = args.partitioned_fallback
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

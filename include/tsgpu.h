@@ -401,6 +401,10 @@ void ts_dist_levels_destroy(ts_dist_levels* lv);
 ts_status ts_dist_levels_sizes(const ts_dist_levels* lv, int32_t* n_local, int32_t* n_local_vertices,
                                int32_t* n2);
 ts_status ts_dist_local_nodes(const ts_dist_levels* lv, int32_t* l2g);
+/* this rank's partition: elements, level-0 interface rows (summed over neighbours, i.e. the
+ * rows one level-0 product sends), neighbour ranks, and the wall time of ts_dist_levels_create */
+ts_status ts_dist_levels_info(const ts_dist_levels* lv, int32_t* n_elements, int64_t* halo_rows0,
+                              int32_t* n_neighbours, double* setup_s);
 /* solve (adaptive_cg.hpp:242-263) on local vectors; host or device buffers */
 ts_status ts_dist_solve(ts_dist_levels* lv, const double* f, const double* u0, double* u_out,
                         int32_t n_local, int32_t batch, const ts_solver_config* cfg, ts_solve_report* rep);

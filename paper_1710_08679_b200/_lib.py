@@ -161,6 +161,7 @@ _sig = {
     "ts_level2_setup_host": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp]),
     "ts_dist_levels_destroy": (None, [vp]),
     "ts_dist_levels_sizes": (C.c_int, [vp, vp, vp, vp]),
+    "ts_dist_levels_info": (C.c_int, [vp, vp, vp, vp, vp]),
     "ts_dist_local_nodes": (C.c_int, [vp, vp]),
     "ts_dist_solve": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp]),
     "ts_dist_solve_device": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp, vp]),

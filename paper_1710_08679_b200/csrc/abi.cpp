@@ -33,13 +33,21 @@ const std::string& last_error();
   return TS_OK;
 
 // a partitioned call that fails on one rank aborts the communicator, so peers
-// blocked in (or entering) a collective fail instead of waiting forever
-#define TS_ABORT_ON_FAIL(comm, ...) \
-  try {                             \
-    __VA_ARGS__;                    \
-  } catch (...) {                   \
-    if (comm) (comm)->abort();      \
-    throw;                          \
+// blocked in (or entering) a collective fail instead of waiting forever. The
+// solver's own outcomes (no convergence, breakdown, non-finite residual) are
+// decided on all-reduced numbers, so every rank reaches them at the same point:
+// they end the call on all ranks together and leave the communicator usable.
+#define TS_ABORT_ON_FAIL(comm, ...)                                              \
+  try {                                                                          \
+    __VA_ARGS__;                                                                 \
+  } catch (const tsg::Error& e_) {                                               \
+    if ((comm) && e_.code != TS_ERR_NO_CONVERGENCE && e_.code != TS_ERR_BREAKDOWN && \
+        e_.code != TS_ERR_NONFINITE)                                             \
+      (comm)->abort();                                                           \
+    throw;                                                                       \
+  } catch (...) {                                                                \
+    if (comm) (comm)->abort();                                                   \
+    throw;                                                                       \
   }
 
 #define TS_REQUIRE(cond, msg) \
@@ -606,6 +614,14 @@ ts_status ts_dist_levels_sizes(const ts_dist_levels* lv, int32_t* n_local, int32
   TS_API_BEGIN
   TS_REQUIRE(lv, "dist levels: null handle");
   tsg::dist_levels_sizes(*lv, n_local, n_local_vertices, n2);
+  TS_API_END
+}
+
+ts_status ts_dist_levels_info(const ts_dist_levels* lv, int32_t* n_elements, int64_t* halo_rows0,
+                              int32_t* n_neighbours, double* setup_s) {
+  TS_API_BEGIN
+  TS_REQUIRE(lv && n_elements && halo_rows0 && n_neighbours && setup_s, "dist levels: null argument");
+  tsg::dist_levels_info(*lv, n_elements, halo_rows0, n_neighbours, setup_s);
   TS_API_END
 }
 

@@ -10,6 +10,8 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
 void dist_levels_destroy(ts_dist_levels* L);
 void dist_levels_sizes(const ts_dist_levels& L, int32_t* n0, int32_t* n1, int32_t* n2);
 const std::vector<int32_t>& dist_local_nodes(const ts_dist_levels& L);
+void dist_levels_info(const ts_dist_levels& L, int32_t* n_elements, int64_t* halo_rows0, int32_t* n_nbr,
+                      double* setup_s);
 void dist_solve_device(ts_dist_levels& L, const double* f, const double* u0, double* u, int32_t B,
                        const ts_solver_config& cfg, ts_solve_report& rep, cudaStream_t s);
 void dist_solve_host(ts_dist_levels& L, const double* f, const double* u0, double* u, int32_t B,

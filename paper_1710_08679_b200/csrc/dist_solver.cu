@@ -460,6 +460,14 @@ void dist_levels_sizes(const ts_dist_levels& L, int32_t* n0, int32_t* n1, int32_
 }
 
 const std::vector<int32_t>& dist_local_nodes(const ts_dist_levels& L) { return L.plan.l2g; }
+
+void dist_levels_info(const ts_dist_levels& L, int32_t* n_elements, int64_t* halo_rows0, int32_t* n_nbr,
+                      double* setup_s) {
+  *n_elements = static_cast<int32_t>(L.plan.elems.size());
+  *halo_rows0 = L.plan.halo0.rows_total();
+  *n_nbr = static_cast<int32_t>(L.plan.halo0.nbr.size());
+  *setup_s = L.setup_s;
+}
 Comm* dist_levels_comm(const ts_dist_levels& L) { return L.comm; }
 
 // host-buffer solve: H2D of f / u0, solve on a private stream, D2H of u

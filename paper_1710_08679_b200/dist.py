@@ -152,6 +152,14 @@ class DistLevels:
         _ck(lib.ts_dist_local_nodes(self._h, _p(l2g)))
         return l2g
 
+    def info(self) -> dict:
+        """This rank's partition: elements, level-0 interface rows sent per product,
+        neighbour ranks, setup wall time."""
+        ne, nn = C.c_int32(), C.c_int32()
+        hr, st = C.c_int64(), C.c_double()
+        _ck(lib.ts_dist_levels_info(self._h, C.byref(ne), C.byref(hr), C.byref(nn), C.byref(st)))
+        return {"elements": ne.value, "halo_rows0": hr.value, "neighbours": nn.value, "setup_s": st.value}
+
     def local_dofs(self) -> np.ndarray:
         """global dof index of every local dof row (3 per node)."""
         l2g = self.local_nodes().astype(np.int64)
