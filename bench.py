@@ -25,6 +25,11 @@ explicit flush is needed between steps.
            per-rank level-0 sweep roofline and interface bytes. N > 1: the 405M-DOF
            configs[3] mesh; N = 1: the configs[2] mesh on in-process ranks
            (--northstar-threads P; 1 by default) of the one GPU.
+  greens_partitioned: BASELINE configs[4]: the Green's bank of unit slips batched
+           r = 16 on the configs[3] mesh partitioned over the N GPUs (N > 1; 32 of
+           the 368 cases by default, --greens-cases 368 for the whole sweep; the
+           full-sweep time is projected from the per-case time). N = 1:
+           --greens-partitioned P runs it on P in-process ranks.
   greens : the Green's-function bank (configs[4] workflow at one-GPU scale):
            48 unit slips on a vertical fault in the configs[1] box, batch 16,
            through ts_greens_bank; total sweep time and time per case.
@@ -422,6 +427,18 @@ def main_partitioned(args, world, rank, local):
         dist.all_gather_object(allr, mine)
         northstar = northstar_summary(allr, cells_ns, args.northstar_cases, world, f"NCCL x{world}", hbm_peak()[0])
         torch.cuda.empty_cache()
+    greens_part = None
+    if not args.no_greens_partitioned:  # BASELINE configs[4]: the sweep on the partitioned configs[3] mesh
+        def sync():
+            torch.cuda.synchronize()
+            dist.barrier()
+        cells_g = (tuple(args.greens_cells) if args.greens_cells
+                   else NORTHSTAR_CELLS if world > 1 else tuple(args.cells))
+        mine = greens_dist_rank(ts, torch, cells_g, comm, rank, world, sync, args.greens_cases, 16)
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        greens_part = greens_dist_summary(allr, cells_g, world, f"NCCL x{world}", 16, 368)
+        torch.cuda.empty_cache()
     solve = None
     if not args.no_solve:
         solve = solve_leg(args, ts, torch, world, rank, local)
@@ -448,6 +465,7 @@ def main_partitioned(args, world, rank, local):
             "clocks": clk.summary(),
             "gpu_launches": 5 * args.steps,
             "northstar": northstar,
+            "greens_partitioned": greens_part,
             "solve": solve,
         }
         print(json.dumps(out), flush=True)
@@ -653,6 +671,101 @@ def northstar_threads(args, ts, torch, cells, r, P):
     return northstar_summary(out, cells, r, P, f"threads x{P} on one GPU", hbm_peak()[0])
 
 
+# --------------------------------------- configs[4]: Green's sweep on the partitioned mesh
+def greens_dist_rank(ts, torch, cells, comm, rank, nranks, sync, n_cases, batch):
+    """One rank of the configs[4] workload: compute_greens_bank (greens.hpp:114-145) of
+    n_cases unit slips (dip + strike on a grid of centres on a vertical fault) on the
+    partitioned layered-crust mesh, batch r = `batch` per solve (ts_dist_greens_bank:
+    slip lifting on the fault band per rank, partitioned solve, owner-rank sampling,
+    one all-reduce of the bank). One warm-up batch first; returns this rank's numbers."""
+    import numpy as np
+    from paper_1710_08679_b200.dist import DistFaultedModel, partition_rcb
+    from paper_1710_08679_b200.greens import DIP, STRIKE, find_plane_fault_faces
+
+    ext = tuple(c * CELL_KM * 1e3 for c in cells)
+    ifs = (0.2 * ext[2], 0.45 * ext[2], 0.8 * ext[2])
+    h = CELL_KM * 1e3
+    xm = (cells[0] // 2) * h
+    t0 = time.perf_counter()
+    mesh = ts.generate_box_mesh(ext, cells, ifs)
+    lo = (xm, 4 * h, 4 * h)
+    hi = (xm, (cells[1] - 4) * h, (cells[2] - 8) * h)
+    faces = find_plane_fault_faces(mesh, 0, xm, lo, hi)
+    part = partition_rcb(mesh, nranks)
+    cfg = ts.SolverConfig(batch_size=batch)
+    dfm = DistFaultedModel(mesh, [ts.material_from_wavespeeds(*t) for t in FOUR_LAYER], faces, part, comm, cfg)
+    del mesh, part
+    sync()
+    t_setup = time.perf_counter() - t0
+    nc = n_cases // 2
+    ny = max(1, int(round((nc * (hi[1] - lo[1]) / (hi[2] - lo[2])) ** 0.5)))
+    nz = max(1, -(-nc // ny))
+    ys = np.linspace(lo[1] + 0.1 * (hi[1] - lo[1]), hi[1] - 0.1 * (hi[1] - lo[1]), ny)
+    zs = np.linspace(lo[2] + 0.1 * (hi[2] - lo[2]), hi[2] - 0.1 * (hi[2] - lo[2]), nz)
+    centers = np.array([[xm, y, z] for y in ys for z in zs for _ in (DIP, STRIKE)])[:n_cases]
+    dirs = np.array([d for _ in ys for _ in zs for d in (DIP, STRIKE)], np.int32)[:n_cases]
+    radii = np.full(len(dirs), 1.5 * (hi[1] - lo[1]) / ny)
+    gx, gy = np.meshgrid(np.linspace(0.1, 0.9, 10) * ext[0], np.linspace(0.1, 0.9, 10) * ext[1])
+    pts = np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, ext[2])], 1)
+    axes = (np.arange(len(pts)) % 3).astype(np.int32)
+    dfm.greens_bank(centers[:batch], dirs[:batch], radii[:batch], pts, axes, cfg)  # warm-up batch
+    sync()
+    t1 = time.perf_counter()
+    bank, calls, outer = dfm.greens_bank(centers, dirs, radii, pts, axes, cfg)
+    sync()
+    return {"rank": rank, "sweep_s": time.perf_counter() - t1, "setup_s": t_setup, "calls": calls, "outer": outer,
+            "faces": int(len(faces)), "cases": int(len(dirs)), "bank_finite": bool(np.isfinite(bank).all()),
+            "bank_absmax": float(np.abs(bank).max()), "bank_sum": float(bank.sum())}
+
+
+def greens_dist_summary(per_rank, cells, nranks, backend, batch, full_cases):
+    sweep = max(x["sweep_s"] for x in per_rank)
+    x0 = per_rank[0]
+    n = x0["cases"]
+    return {"metric": "Green's sweep time per case (s)", "higher_is_better": False,
+            "workload": f"configs[4]-shaped sweep: {n} unit slips (of the configuration's {full_cases}) on a "
+                        f"vertical fault ({x0['faces']} faces) in the {list(cells)}-cell 4-layer crust, batch {batch}, "
+                        f"mesh partitioned over {nranks} ranks (RCB), 100 surface observations",
+            "value": round(sweep / n, 5), "unit": "s", "ranks": nranks, "backend": backend, "cases": n,
+            "sweep_s": round(sweep, 3), "projected_full_sweep_s": round(sweep / n * full_cases, 1),
+            "setup_s": round(max(x["setup_s"] for x in per_rank), 2), "solver_calls": x0["calls"],
+            "outer_iterations": x0["outer"], "bank_finite": all(x["bank_finite"] for x in per_rank),
+            "bank_identical_on_ranks": len({(x["bank_absmax"], x["bank_sum"]) for x in per_rank}) == 1,
+            "entry": "ts_dist_faulted_model_create + ts_dist_greens_bank"}
+
+
+def greens_dist_threads(ts, torch, cells, P, n_cases, batch, full_cases):
+    import threading
+    from paper_1710_08679_b200.dist import Comm, ThreadWorld
+    world = ThreadWorld(P)
+    comms = [Comm.thread(world, k, 0) for k in range(P)]
+    bar = threading.Barrier(P)
+    out, err = [None] * P, [None] * P
+
+    def body(k):
+        try:
+            torch.cuda.set_device(0)
+
+            def sync():
+                torch.cuda.synchronize()
+                bar.wait()
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[k] = greens_dist_rank(ts, torch, cells, comms[k], k, P, sync, n_cases, batch)
+        except BaseException as e:  # noqa: BLE001
+            err[k] = e
+            bar.abort()
+    th = [threading.Thread(target=body, args=(k,)) for k in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    real = [e for e in err if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if real:
+        real.sort(key=lambda e: "peer rank failed" in str(e))
+        raise real[0]
+    return greens_dist_summary(out, cells, P, f"threads x{P} on one GPU", batch, full_cases)
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -677,6 +790,14 @@ def main():
     ap.add_argument("--northstar-cells", type=int, nargs=3, default=None,
                     help="mesh of the partitioned solve (default: configs[3] at N > 1, configs[2] at N = 1)")
     ap.add_argument("--northstar-cases", type=int, default=8)
+    ap.add_argument("--no-greens-partitioned", action="store_true",
+                    help="N > 1: skip the configs[4] Green's sweep on the partitioned mesh")
+    ap.add_argument("--greens-partitioned", type=int, default=0,
+                    help="N = 1: run the partitioned Green's sweep on this many in-process ranks")
+    ap.add_argument("--greens-cases", type=int, default=32,
+                    help="unit slips of the partitioned sweep (configs[4]: 368 = 23 batches of 16)")
+    ap.add_argument("--greens-cells", type=int, nargs=3, default=None,
+                    help="mesh of the partitioned sweep (default: configs[3] at N > 1, configs[1] at N = 1)")
     ap.add_argument("--northstar-threads", type=int, default=1,
                     help="N = 1: in-process ranks of the partitioned solve on the one GPU")
     args = ap.parse_args()
@@ -852,6 +973,11 @@ def main():
         torch.cuda.empty_cache()
         cells_ns = tuple(args.northstar_cells) if args.northstar_cells else tuple(args.solve_cells)
         northstar = northstar_threads(args, ts, torch, cells_ns, args.northstar_cases, args.northstar_threads)
+    greens_part = None
+    if world == 1 and args.greens_partitioned > 0:
+        torch.cuda.empty_cache()
+        cells_g = tuple(args.greens_cells) if args.greens_cells else tuple(args.cells)
+        greens_part = greens_dist_threads(ts, torch, cells_g, args.greens_partitioned, args.greens_cases, 16, 368)
 
     if rank == 0:
         out = {
@@ -875,6 +1001,7 @@ def main():
             "solve": solve,
             "greens": greens,
             "northstar": northstar,
+            "greens_partitioned": greens_part,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

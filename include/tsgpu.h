@@ -465,6 +465,28 @@ ts_status ts_greens_bank(ts_faulted* fm, int32_t n_slips, const double* centers,
                          const ts_solver_config* cfg, double* bank, int32_t* solver_calls,
                          int64_t* outer_iterations);
 
+/* The same bank on a PARTITIONED base mesh (BASELINE configs[4]: the sweep on the
+ * configs[3] mesh over the GPUs of one box; greens.hpp:114-145 with the solve of
+ * ts_dist_solve). Every rank passes the same global mesh, faces and element
+ * partition; each builds its partition's level set, the fault patch and the fault
+ * band of the split mesh (slip lifting replicated per rank, no communication),
+ * samples the observations whose containing element it owns, and one all-reduce
+ * gives every rank the full bank. The comm must outlive the model. */
+typedef struct ts_dist_faulted ts_dist_faulted;
+ts_status ts_dist_faulted_model_create(const ts_mesh* mesh, int32_t n_materials, const double* lambda,
+                                       const double* mu, const int32_t* faces, int32_t n_faces, const int32_t* part,
+                                       const ts_solver_config* cfg, ts_comm* comm, ts_dist_faulted** out);
+void ts_dist_faulted_model_destroy(ts_dist_faulted* fm);
+ts_status ts_dist_faulted_levels(const ts_dist_faulted* fm, ts_dist_levels** levels);
+/* this rank's rows [3 n_local][n_slips] of slip_to_rhs (local node order, ts_dist_local_nodes) */
+ts_status ts_dist_slip_to_rhs(ts_dist_faulted* fm, int32_t n_slips, const double* centers, const int32_t* directions,
+                              const double* radii, double* f_local_host);
+/* bank [n_obs][n_slips] row-major, identical on every rank */
+ts_status ts_dist_greens_bank(ts_dist_faulted* fm, int32_t n_slips, const double* centers, const int32_t* directions,
+                              const double* radii, int32_t n_obs, const double* points, const int32_t* axes,
+                              const ts_solver_config* cfg, double* bank, int32_t* solver_calls,
+                              int64_t* outer_iterations);
+
 #ifdef __cplusplus
 }
 #endif

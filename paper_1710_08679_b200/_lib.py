@@ -180,6 +180,11 @@ _sig = {
     "ts_reconstruct_split_solution": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "ts_slip_to_rhs": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     "ts_greens_bank": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]),
+    "ts_dist_faulted_model_create": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp]),
+    "ts_dist_faulted_model_destroy": (None, [vp]),
+    "ts_dist_faulted_levels": (C.c_int, [vp, vp]),
+    "ts_dist_slip_to_rhs": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+    "ts_dist_greens_bank": (C.c_int, [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _fn = getattr(lib, _name, None)

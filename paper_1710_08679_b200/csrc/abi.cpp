@@ -58,6 +58,7 @@ const std::string& last_error();
 struct ts_comm {
   std::unique_ptr<tsg::Comm> c;
 };
+tsg::Comm* tsg::comm_of(ts_comm* c) { return c ? c->c.get() : nullptr; }
 struct ts_thread_world {
   std::shared_ptr<tsg::ThreadWorld> w;
 };

@@ -58,3 +58,9 @@ std::shared_ptr<ThreadWorld> make_thread_world(int nranks);
 std::unique_ptr<Comm> make_thread_comm(const std::shared_ptr<ThreadWorld>& w, int rank, int device);
 
 }  // namespace tsg
+
+// the communicator behind an ABI handle (abi.cpp)
+struct ts_comm;
+namespace tsg {
+Comm* comm_of(ts_comm* c);
+}  // namespace tsg

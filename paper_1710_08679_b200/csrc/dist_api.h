@@ -25,5 +25,6 @@ const std::vector<int32_t>& dist_ebe_local_nodes(const ts_dist_ebe& D);
 void dist_ebe_apply_op(ts_dist_ebe& D, const void* u, void* f, int32_t B, cudaStream_t s);
 ts_ebe* dist_ebe_local(ts_dist_ebe& D);
 Comm* dist_levels_comm(const ts_dist_levels& L);
+const uint8_t* dist_levels_mask0(const ts_dist_levels& L);  // device [3 n_local] dof mask
 Comm* dist_ebe_comm(const ts_dist_ebe& D);
 }  // namespace tsg

@@ -469,6 +469,7 @@ void dist_levels_info(const ts_dist_levels& L, int32_t* n_elements, int64_t* hal
   *setup_s = L.setup_s;
 }
 Comm* dist_levels_comm(const ts_dist_levels& L) { return L.comm; }
+const uint8_t* dist_levels_mask0(const ts_dist_levels& L) { return L.mask0.get(); }
 
 // host-buffer solve: H2D of f / u0, solve on a private stream, D2H of u
 void dist_solve_host(ts_dist_levels& L, const double* f, const double* u0, double* u, int32_t B,

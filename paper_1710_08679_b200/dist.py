@@ -133,6 +133,16 @@ def dist_plan(mesh: Mesh, part, nranks: int, rank: int, dof_mask=None) -> dict:
 class DistLevels:
     """build_solver_levels (adaptive_cg.hpp:39-67) on one rank's partition."""
 
+    @classmethod
+    def _view(cls, handle, comm: Comm, owner) -> "DistLevels":
+        """A level set owned by another object (e.g. DistFaultedModel's base hierarchy)."""
+        self = cls.__new__(cls)
+        self._h, self.comm, self.mesh, self._owner = handle, comm, None, owner
+        n0, n1, n2 = C.c_int32(), C.c_int32(), C.c_int32()
+        _ck(lib.ts_dist_levels_sizes(self._h, C.byref(n0), C.byref(n1), C.byref(n2)))
+        self.n_local, self.n_local_vertices, self.n2 = n0.value, n1.value, n2.value
+        return self
+
     def __init__(self, mesh: Mesh, materials, part, comm: Comm, cfg: SolverConfig | None = None, dof_mask=None):
         cfg = cfg or SolverConfig()
         lam, mu = _lame(materials)
@@ -142,7 +152,7 @@ class DistLevels:
         h = C.c_void_p()
         _ck(lib.ts_dist_levels_create(mesh._h, len(lam), _p(lam), _p(mu), _p(mk), _p(part), C.byref(c), comm._h,
                                       C.byref(h)))
-        self._h, self.comm, self.mesh = h, comm, mesh
+        self._h, self.comm, self.mesh, self._owner = h, comm, mesh, None
         n0, n1, n2 = C.c_int32(), C.c_int32(), C.c_int32()
         _ck(lib.ts_dist_levels_sizes(self._h, C.byref(n0), C.byref(n1), C.byref(n2)))
         self.n_local, self.n_local_vertices, self.n2 = n0.value, n1.value, n2.value
@@ -200,7 +210,8 @@ class DistLevels:
 
     def __del__(self):
         try:
-            lib.ts_dist_levels_destroy(self._h)
+            if getattr(self, "_owner", None) is None:
+                lib.ts_dist_levels_destroy(self._h)
         except Exception:
             pass
 
@@ -236,5 +247,55 @@ class DistEbeOperator:
     def __del__(self):
         try:
             lib.ts_dist_ebe_destroy(self._h)
+        except Exception:
+            pass
+
+
+class DistFaultedModel:
+    """build_faulted_model (model.hpp:41-51) on one rank's partition of the base mesh, for the
+    partitioned Green's-function bank (ts_dist_faulted_*: BASELINE configs[4])."""
+
+    def __init__(self, mesh: Mesh, materials, faces, part, comm: Comm, cfg: SolverConfig | None = None):
+        cfg = cfg or SolverConfig()
+        lam, mu = _lame(materials)
+        faces = np.ascontiguousarray(faces, np.int32)
+        part = np.ascontiguousarray(part, np.int32)
+        c = cfg.to_c()
+        h = C.c_void_p()
+        _ck(lib.ts_dist_faulted_model_create(mesh._h, len(lam), _p(lam), _p(mu), _p(faces), len(faces), _p(part),
+                                             C.byref(c), comm._h, C.byref(h)))
+        self._h, self.comm = h, comm
+        lv = C.c_void_p()
+        _ck(lib.ts_dist_faulted_levels(self._h, C.byref(lv)))
+        self.levels = DistLevels._view(lv, comm, owner=self)
+
+    def slip_to_rhs(self, centers, directions, radii) -> np.ndarray:
+        """This rank's rows [3 n_local, n_slips] of slip_to_rhs (fault.hpp:363-388)."""
+        centers = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        directions = np.ascontiguousarray(directions, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        f = np.zeros((3 * self.levels.n_local, len(directions)), np.float64)
+        _ck(lib.ts_dist_slip_to_rhs(self._h, len(directions), _p(centers), _p(directions), _p(radii), _p(f)))
+        return f
+
+    def greens_bank(self, centers, directions, radii, points, axes, cfg: SolverConfig | None = None):
+        """compute_greens_bank (greens.hpp:114-145) over the partition: (bank [n_obs, n_slips] —
+        the same on every rank —, solver_calls, outer_iterations)."""
+        cfg = cfg or SolverConfig()
+        c = cfg.to_c()
+        centers = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        directions = np.ascontiguousarray(directions, np.int32)
+        radii = np.ascontiguousarray(radii, np.float64)
+        points = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        axes = np.ascontiguousarray(axes, np.int32)
+        bank = np.zeros((len(axes), len(directions)), np.float64)
+        calls, outer = C.c_int32(), C.c_int64()
+        _ck(lib.ts_dist_greens_bank(self._h, len(directions), _p(centers), _p(directions), _p(radii), len(axes),
+                                    _p(points), _p(axes), C.byref(c), _p(bank), C.byref(calls), C.byref(outer)))
+        return bank, calls.value, outer.value
+
+    def __del__(self):
+        try:
+            lib.ts_dist_faulted_model_destroy(self._h)
         except Exception:
             pass

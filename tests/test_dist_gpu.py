@@ -193,3 +193,43 @@ def test_comm_allreduce_sum(P):
         t = torch.full((7,), 2.5, dtype=torch.float64, device="cuda")
         comm.allreduce_sum(t)
         assert torch.equal(t.cpu(), torch.full((7,), 2.5, dtype=torch.float64))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_partitioned_greens_bank_matches_single_device(P):
+    """ts_dist_greens_bank (configs[4]'s sweep on a partitioned mesh) against the single-device
+    bank (itself pinned to the reference in test_greens_gpu.py): this rank's slip_to_rhs rows
+    equal the global right-hand side's (1e-12), the bank within 1e-6, the same solver calls and
+    outer iterations within +-2 %, and every rank holds the same bank."""
+    from paper_1710_08679_b200.dist import DistFaultedModel
+    from paper_1710_08679_b200.greens import DIP, STRIKE, FaultedModel, find_plane_fault_faces
+    ext, div, ifs = (8000.0, 8000.0, 6000.0), (8, 8, 6), (4500.0,)
+    m = ts.generate_box_mesh(ext, div, ifs)
+    faces = find_plane_fault_faces(m, 0, 4000.0, (4000.0, 2000.0, 1000.0), (4000.0, 6000.0, 5000.0))
+    centers = np.array([[4000.0, 4000.0, 3000.0], [4000.0, 3000.0, 2500.0], [4000.0, 5000.0, 4000.0],
+                        [4000.0, 4000.0, 3000.0], [4000.0, 3500.0, 2000.0]])
+    dirs = np.array([DIP, DIP, STRIKE, STRIKE, DIP], np.int32)
+    radii = np.array([1500.0, 1000.0, 1200.0, 1500.0, 900.0])
+    obs = np.array([[1000.0, 2000.0, 6000.0], [3000.0, 4000.0, 6000.0], [5000.0, 4000.0, 6000.0],
+                    [6500.0, 1500.0, 6000.0], [4000.0, 7000.0, 6000.0], [2500.0, 2500.0, 5500.0]])
+    axes = np.array([0, 1, 2, 0, 2, 1], np.int32)
+    cfg = ts.SolverConfig(batch_size=2)
+    fm = FaultedModel(m, mats(), faces, cfg)
+    want_f = fm.slip_to_rhs(centers, dirs, radii)
+    want, wcalls, wouter = fm.greens_bank(centers, dirs, radii, obs, axes, cfg)
+    part = partition_rcb(m, P)
+
+    def fn(r, comm):
+        dfm = DistFaultedModel(m, mats(), faces, part, comm, cfg)
+        f = dfm.slip_to_rhs(centers, dirs, radii)
+        bank, calls, outer = dfm.greens_bank(centers, dirs, radii, obs, axes, cfg)
+        return dfm.levels.local_dofs(), f, bank, calls, outer
+
+    out = run_ranks(P, fn)
+    for dofs, f, bank, calls, outer in out:
+        assert rel(f, want_f[dofs]) <= 1e-12
+        assert calls == wcalls
+        assert abs(outer - wouter) <= max(1, 0.02 * wouter)
+        assert rel(bank, want) <= 1e-6
+        assert np.array_equal(bank, out[0][2])
+    assert np.abs(want).max() > 0
