@@ -189,7 +189,7 @@ def run_reference(args, world, rank):
               f"1 warm-up + {steps} timed applies")
     print(json.dumps({**base, "value": round(val, 4), "ms_per_step": round(sec * 1e3, 2),
                       "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                                       "sample": sample},
+                                       "cpu_model": cpu_model(), "sample": sample},
                       "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                       "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
                       "config": config_dict(cells, r, prec, world, E, N)}))
@@ -198,10 +198,29 @@ def run_reference(args, world, rank):
 METRIC = "EBE matvec HBM GB/s (tet10 K u, r load cases, 10M-DOF layered crust)"
 
 
+def precision_tier(prec):
+    if prec == 32:
+        return ("fp32 (level-0 operator): element arithmetic in fp32 on fp32-rounded geometry and Lame values, "
+                "fp32 accumulation; the reference's EbeOperator<float> forms K_e and the local product in fp64 "
+                "and accumulates in fp32 (SURVEY A6); matvec parity 1e-5 relative")
+    return "fp64 (outer operator): fp64 element arithmetic and accumulation; matvec parity 1e-12 relative"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def config_dict(cells, r, prec, world, E, N):
     return {"workload": "configs[1]: EBE matvec microbench, 10M-DOF layered-crust tet10 box",
             "cells": list(cells), "elements": E, "nodes": N, "dof": 3 * N, "cases_r": r,
-            "precision_tier": f"fp{prec} (level-0 operator)", "parallelism": f"replicas x{world} (cases batched across GPUs)",
+            "precision_tier": precision_tier(prec), "parallelism": f"replicas x{world} (cases batched across GPUs)",
             "l2_policy": "inputs larger than L2 (u, f = 650 MB each vs 126 MB L2); no flush"}
 
 
@@ -317,7 +336,89 @@ def solve_leg(args, ts, torch, world, rank, local):
                     "gpu_inner_iterations": gs["inner_iterations"]}
         except Exception as exc:  # reported, never fatal
             out["cpu_reference_sample"] = {"failed": str(exc)}
+        try:
+            out["configs0"] = configs0_leg(ts, torch)
+        except Exception as exc:  # reported, never fatal
+            out["configs0"] = {"failed": str(exc)}
+    out["cpu_reference_extrapolation"] = config2_cpu_extrapolation(g)
     return out
+
+
+def configs0_leg(ts, torch):
+    """BASELINE configs[0] (the cube the CPU reference solves in full: 8^3 cells, extents 8,
+    one interface at 4, two layers, r = 4): the reference's own solve() and solve_pcge() on
+    this host's cores beside ours through the host entries, same manufactured right-hand sides
+    (BASELINE.md §3 config 1)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, SolverConfig as OCfg, have_reference
+    if not have_reference():
+        return {"failed": "oracle/_ref not built on this box"}
+    ref = Oracle("reference")
+    cores = ref.hw_threads()
+    ext, cells, ifs, r = (8.0, 8.0, 8.0), (8, 8, 8), (4.0,), 4
+    lam = [rho * (vp * vp - 2 * vs * vs) for vp, vs, rho in TWO_LAYER]
+    mu = [rho * vs * vs for vp, vs, rho in TWO_LAYER]
+    om = ref.box_mesh(ext, cells, ifs, 1)
+    t0 = time.perf_counter()
+    olv = ref.levels(om, lam, mu, OCfg.default(batch_size=r), workers=cores)
+    ref_setup = time.perf_counter() - t0
+    mesh = ts.generate_box_mesh(ext, cells, ifs)
+    us = manufactured(mesh, ext, mesh.dirichlet_mask(), r, 31, torch).cpu().numpy()
+    f = olv.outer_apply(us)
+    t0 = time.perf_counter()
+    uo, ro = olv.solve(f)
+    ref_solve = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    up, rp = olv.solve_pcge(f)
+    ref_pcge = time.perf_counter() - t0
+    cfg = ts.SolverConfig(batch_size=r)
+    t0 = time.perf_counter()
+    model = ts.build_crust_model(mesh, [ts.material_from_wavespeeds(*t) for t in TWO_LAYER], cfg)
+    torch.cuda.synchronize()
+    our_setup = time.perf_counter() - t0
+    ts.solve(model.levels, f, np.zeros_like(f), cfg)  # warm-up (workspaces)
+    t0 = time.perf_counter()
+    u, rep = ts.solve(model.levels, f, np.zeros_like(f), cfg)
+    our_solve = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    u2, rep2 = ts.solve_pcge(model.levels.outer, f, np.zeros_like(f), 1e-8, 100000)
+    our_pcge = time.perf_counter() - t0
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    return {"workload": f"configs[0]: {list(cells)} cells, {3 * mesh.node_count()} DOF, r={r}, two layers",
+            "cores": cores, "cpu_model": cpu_model(),
+            "reference": {"setup_s": round(ref_setup, 4), "solve_s": round(ref_solve, 4), "pcge_s": round(ref_pcge, 4),
+                          "outer": ro["outer_iterations"], "inner": list(ro["inner_iterations"]),
+                          "pcge_iterations": rp["outer_iterations"]},
+            "ours": {"setup_s": round(our_setup, 4), "solve_s": round(our_solve, 4), "pcge_s": round(our_pcge, 4),
+                     "outer": rep.outer_iterations, "inner": list(rep.inner_iterations),
+                     "pcge_iterations": rep2.outer_iterations, "entry": "ts_solve / ts_solve_pcge (host buffers)"},
+            "u_rel_diff_solve": rel(u, uo), "u_rel_diff_pcge": rel(u2, up)}
+
+
+def config2_cpu_extrapolation(g):
+    """a full CPU solve of configs[2] takes about a day, so the reference
+    was run capped at one outer iteration (tests/golden/make_config2_capped.py, the UNMODIFIED
+    reference, r = 4, in the build container); the LABELLED extrapolation scales its time per
+    outer iteration by the outer iterations this GPU solve needed and by r (per-case linearity)."""
+    path = os.path.join(ROOT, "tests", "golden", "config2_outer1_reference.json")
+    try:
+        with open(path) as fh:
+            cap = json.load(fh)
+    except OSError:
+        return None
+    per_outer = cap["seconds"]["report_total"] / max(1, cap["outer_iterations"])
+    scale_r = g["cases"] / cap["batch"]
+    est = cap["seconds"]["levels_setup"] + per_outer * g["outer_iterations"] * scale_r
+    return {"label": "EXTRAPOLATED, not measured: reference solve() at configs[2] capped at outer_max_iter=1 "
+                     f"(r={cap['batch']}, {cap['host']['workers']} threads, {cap['host']['cpu_model']}, build "
+                     f"container) x {g['outer_iterations']} outer iterations x {scale_r:g} (r={g['cases']} / "
+                     f"r={cap['batch']}, assumed linear in r) + its level setup",
+            "reference_capped_solve_s": cap["seconds"]["report_total"], "reference_setup_s":
+                cap["seconds"]["levels_setup"], "reference_first_outer_inner": cap["inner_iterations"],
+            "estimated_full_solve_s": round(est, 1), "estimated_s_per_case": round(est / g["cases"], 1),
+            "gpu_s_per_case": round(g["s_per_case"], 5),
+            "source": "tests/golden/config2_outer1_reference.json"}
 
 
 class stdout_to_stderr:
@@ -450,7 +551,7 @@ def main_partitioned(args, world, rank, local):
             "config": {"workload": f"configs[1] x {world}: one {list(cells)}-cell layered-crust tet10 mesh "
                                    f"partitioned over {world} GPUs (RCB), halo exchange every matvec",
                        "cells": list(cells), "elements_per_rank_rank0": E, "nodes_per_rank_rank0": N, "cases_r": r,
-                       "precision_tier": f"fp{args.prec} (level-0 operator)",
+                       "precision_tier": precision_tier(args.prec),
                        "parallelism": f"mesh partition x{world} (NCCL send/recv interface halo, overlapped)",
                        "l2_policy": "inputs larger than L2; no flush",
                        "interface_bytes_per_step_rank0": halo_bytes},
@@ -777,6 +878,7 @@ def main():
     ap.add_argument("--cases", type=int, default=16, help="load cases r per GPU")
     ap.add_argument("--prec", type=int, default=32, choices=[32, 64])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-single", action="store_true", help="skip the workers=1 reference timing")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--no-solve", action="store_true")
@@ -948,9 +1050,14 @@ def main():
                 mu = [m.mu for m in mats]
                 sec, _ = ref.time_ebe_apply_box(ext, div, ifs, 1, 2, lam, mu, args.prec, cores, r, args.cpu_reps)
                 cpu = {"value": round(B / sec / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                       "cpu_model": cpu_model(),
                        "sample": f"reference EbeOperator<{'float' if args.prec == 32 else 'double'}>::apply on the same "
                                  f"{cells} mesh, r={r}, workers={cores}, 1 warm-up + {args.cpu_reps} timed "
                                  f"({sec:.2f} s/apply)"}
+                if not args.no_cpu_single:  # also workers = 1 (the reference's serial path)
+                    sec1, _ = ref.time_ebe_apply_box(ext, div, ifs, 1, 2, lam, mu, args.prec, 1, r, 1)
+                    cpu["workers1"] = {"value": round(B / sec1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                                       "s_per_apply": round(sec1, 2), "sample": "1 warm-up + 1 timed apply, workers=1"}
             else:
                 cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                        "sample": "oracle/_ref not built on this box"}

@@ -204,6 +204,7 @@ void dist_ensure_vecs(ts_dist_levels& L, int32_t B) {
 // apply_multigrid_preconditioner (adaptive_cg.hpp:80-120) on a partition
 void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const double* r, double* z, int32_t B,
                      ts_solve_report& rep, cudaStream_t s) {
+  NvtxRange nv("dist mg preconditioner");
   DistVecs& v = L.v;
   Comm& comm = *L.comm;
   const int64_t len0 = 3 * int64_t(L.n0) * B;

@@ -590,6 +590,7 @@ void det_inv3(const double j[3][3], double inv[3][3], double* det) {
 }  // namespace
 
 void ebe_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s) {
+  NvtxRange nv("ebe apply");
   if (batch < 1) validation("ebe apply: batch must be >= 1");
   if (u == f) validation("ebe apply: input and output must not alias");
   if (op.prec == 32) apply_t<float>(op, static_cast<const float*>(u), static_cast<float*>(f), batch, s, -1, true);

@@ -512,7 +512,11 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_wor
       int64_t bd = 0;
       for (int k = 0; k < 4; ++k) {
         const int32_t j = nbr[e][k];
-        if (j < 0 || j == e || mate[j] >= 0 || group_of(j) != group_of(e)) continue;
+        // only later elements: the unit's leader (its lower element) then always carries the face
+        // index. On a manifold mesh an unmatched earlier neighbour cannot exist (it would have taken
+        // e); on a non-manifold one (a face shared by three elements) the face relation is not
+        // symmetric and an earlier j could not name its face towards e.
+        if (j < 0 || j <= e || mate[j] >= 0 || group_of(j) != group_of(e)) continue;
         const int64_t d = std::llabs(int64_t(j) - e);
         if (best < 0 || d < bd) {
           best = k;

@@ -79,6 +79,7 @@ void ensure_vecs(ts_levels& lv, int32_t B) {
 // apply_multigrid_preconditioner (adaptive_cg.hpp:80-120)
 void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, double* z, int32_t B,
                 ts_solve_report& rep, cudaStream_t s) {
+  NvtxRange nv("mg preconditioner");
   LevelVecs& v = lv.v;
   const int64_t len0 = 3 * int64_t(lv.n0) * B;
   cast_d2f(r, v.r0.get(), len0, s);
@@ -91,8 +92,12 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
   auto a2 = [&](const float* x, float* y, bool) {
     bcsr_apply_f32(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s);
   };
-  const InnerStats s2 = inner_pcg<float>(a2, lv.m2.get(), v.r2.get(), v.u2.get(), lv.n2, B, cfg.level_tol[2],
-                                         cfg.level_max_iter[2], v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s);
+  InnerStats s2;
+  {
+    NvtxRange nl("inner pcg level 2");
+    s2 = inner_pcg<float>(a2, lv.m2.get(), v.r2.get(), v.u2.get(), lv.n2, B, cfg.level_tol[2], cfg.level_max_iter[2],
+                          v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s);
+  }
   const auto t1 = clk::now();
   p2_apply(v.u2.get(), v.u1.get(), lv.agg.get(), lv.n1, lv.mask1.get(), B, s);
   auto a1 = [&](const float* x, float* y, bool init) {
@@ -101,15 +106,21 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
     else
       ebe_apply_part(*lv.l1, x, y, B, s, -1, init);
   };
-  const InnerStats s1 = inner_pcg<float>(a1, lv.m1.get(), v.r1.get(), v.u1.get(), lv.n1, B, cfg.level_tol[1],
-                                         cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s,
-                                         !lv.l1_assembled, lv.mask1.get());
+  InnerStats s1;
+  {
+    NvtxRange nl("inner pcg level 1");
+    s1 = inner_pcg<float>(a1, lv.m1.get(), v.r1.get(), v.u1.get(), lv.n1, B, cfg.level_tol[1], cfg.level_max_iter[1],
+                          v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s, !lv.l1_assembled, lv.mask1.get());
+  }
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), lv.p1_ends.get(), lv.n1, lv.n0, lv.mask0.get(), B, s);
   auto a0 = [&](const float* x, float* y, bool init) { ebe_apply_part(*lv.l0, x, y, B, s, -1, init); };
-  const InnerStats s0 = inner_pcg<float>(a0, lv.m0.get(), v.r0.get(), v.u0.get(), lv.n0, B, cfg.level_tol[0],
-                                         cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s,
-                                         true, lv.mask0.get());
+  InnerStats s0;
+  {
+    NvtxRange nl("inner pcg level 0");
+    s0 = inner_pcg<float>(a0, lv.m0.get(), v.r0.get(), v.u0.get(), lv.n0, B, cfg.level_tol[0], cfg.level_max_iter[0],
+                          v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s, true, lv.mask0.get());
+  }
   const auto t3 = clk::now();
   rep.inner_iterations[2] += s2.iterations;
   rep.inner_iterations[1] += s1.iterations;
@@ -128,6 +139,7 @@ void check_cfg(const ts_solver_config* c) {
 // solve (adaptive_cg.hpp:242-263) on device buffers
 void solve_device(ts_levels& lv, const double* f, const double* u0, double* u, int32_t B, const ts_solver_config& cfg,
                   ts_solve_report& rep, cudaStream_t s) {
+  NvtxRange nv("tetsolve solve");
   check_cfg(&cfg);
   if (B < 1 || B > kRedThreads) validation("solve: batch must be in [1, 256]");
   ensure_vecs(lv, B);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <memory>
@@ -107,6 +108,15 @@ class DevBuf {
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
+};
+
+// NVTX range for the whole scope (solve, outer iterations, multigrid levels, EBE
+// products, Green's batches): free without a profiler, named phases under nsys / ncu
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // setup phase timing to stderr when TSGPU_SETUP_PROFILE is set
