@@ -735,6 +735,9 @@ def northstar_summary(per_rank, cells, r, nranks, backend, peak):
             "max_final_rel_residual": max(x["max_final_rel_residual"] for x in per_rank),
             "rel_err_vs_manufactured": (e2 / max(n2, 1e-300)) ** 0.5, "n2": x0["n2"],
             "l0_sweep_per_rank": l0, "device_used_gb_max": round(max(x["device_used_gb"] for x in per_rank), 1),
+            "level2": (os.environ.get("TSGPU_DIST_L2", "auto") if os.environ.get("TSGPU_DIST_L2", "auto") != "auto"
+                       else ("distributed" if nranks >= 4 else "replicated")),
+            "level2_share_of_solve": round(max(x["time_inner_s"][2] for x in per_rank) / max(solve_s, 1e-9), 4),
             "entry": "ts_dist_levels_create + ts_dist_solve_device (device-resident f / u per rank)"}
 
 
@@ -892,6 +895,9 @@ def main():
     ap.add_argument("--northstar-cells", type=int, nargs=3, default=None,
                     help="mesh of the partitioned solve (default: configs[3] at N > 1, configs[2] at N = 1)")
     ap.add_argument("--northstar-cases", type=int, default=8)
+    ap.add_argument("--northstar-l2", default="auto", choices=["auto", "replicated", "distributed"],
+                    help="level 2 of the partitioned solve: replicated on every rank, split by coarse rows, "
+                         "or auto (split from 4 ranks on)")
     ap.add_argument("--no-greens-partitioned", action="store_true",
                     help="N > 1: skip the configs[4] Green's sweep on the partitioned mesh")
     ap.add_argument("--greens-partitioned", type=int, default=0,
@@ -904,6 +910,7 @@ def main():
                     help="N = 1: in-process ranks of the partitioned solve on the one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    os.environ["TSGPU_DIST_L2"] = args.northstar_l2  # read by ts_dist_levels_create
     world, rank, local = dist_setup()
 
     if args.impl == "reference":

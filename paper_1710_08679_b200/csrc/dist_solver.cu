@@ -71,6 +71,25 @@ __global__ void k_halo_sum(T* __restrict__ x, const int32_t* __restrict__ sh, in
   x[node * W + j] = acc;
 }
 
+// y[i] = x[rows[i]] over rows of width W (gather of this rank's coarse rows)
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ x, const int32_t* __restrict__ rows, int64_t n, int W,
+                              T* __restrict__ y) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * W) return;
+  const int64_t r = i / W;
+  y[i] = x[int64_t(rows[r]) * W + (i - r * W)];
+}
+// x[rows[i]] = y[i] (scatter back into a zeroed full-length vector)
+template <typename T>
+__global__ void k_scatter_rows(const T* __restrict__ y, const int32_t* __restrict__ rows, int64_t n, int W,
+                               T* __restrict__ x) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * W) return;
+  const int64_t r = i / W;
+  x[int64_t(rows[r]) * W + (i - r * W)] = y[i];
+}
+
 // Device image of a Halo plus its message buffers.
 struct HaloDev {
   std::vector<int> nbr;
@@ -163,6 +182,40 @@ struct DistVecs {
   int32_t batch = 0;
   DevBuf<double> r, q, z, p, scratch, f, u;
   DevBuf<float> r0, u0, e0, p0, q0, r1, u1, e1, p1, q1, r2, u2, e2, p2, q2;
+  DevBuf<float> r2d, u2d, e2d, p2d, q2d;  // distributed level 2: owned rows (+ halo rows for u, p)
+};
+
+// Distributed level 2: this rank's coarse rows of the Galerkin operator and the
+// gather halo its SpMV needs (owner values of the columns it references).
+struct Level2Dist {
+  int32_t n_own = 0, n_halo = 0;
+  DevBuf<int32_t> own;                 // [n_own] global coarse ids, ascending
+  DevBuf<int32_t> row_ptr, col_idx;    // owned rows; columns: owned [0, n_own), then halo
+  DevBuf<float> blocks, m2;
+  std::vector<int> nbr;                // neighbour ranks, ascending (symmetric: A2 is)
+  std::vector<int64_t> soff, roff;     // [nn + 1] send / receive row offsets per neighbour
+  DevBuf<int32_t> send;                // owned local ids sent, neighbour-major
+  DevBuf<float> sbuf;
+  // x (device, n_own + n_halo rows of width W): owner values into the halo rows
+  void exchange(float* x, int W, Comm& comm, cudaStream_t s) {
+    if (nbr.empty()) return;
+    const int64_t ns = soff.back();
+    sbuf.ensure(size_t(ns) * W);
+    if (ns > 0) {
+      k_halo_pack<float><<<grid_for(ns * W, 256), 256, 0, s>>>(x, send.get(), ns, W, sbuf.get());
+      TS_CUDA_LAUNCH();
+    }
+    const int nn = static_cast<int>(nbr.size());
+    std::vector<void*> sp(nn), rp(nn);
+    std::vector<size_t> sb(nn), rb(nn);
+    for (int k = 0; k < nn; ++k) {
+      sp[k] = sbuf.get() + size_t(soff[k]) * W;
+      sb[k] = size_t(soff[k + 1] - soff[k]) * W * sizeof(float);
+      rp[k] = x + (size_t(n_own) + size_t(roff[k])) * W;
+      rb[k] = size_t(roff[k + 1] - roff[k]) * W * sizeof(float);
+    }
+    comm.exchange(nn, nbr.data(), sp.data(), sb.data(), rp.data(), rb.data(), s);
+  }
 };
 
 }  // namespace
@@ -178,6 +231,8 @@ struct ts_dist_levels {
   tsg::DevBuf<float> l2_blocks, m0, m1, m2;
   tsg::DevBuf<uint8_t> mask0, mask1, mask2, owned0;
   tsg::DistVecs v;
+  bool l2_dist = false;  // TSGPU_DIST_L2=distributed: level 2 split by coarse rows (else replicated)
+  tsg::Level2Dist l2d;
   tsg::ColScalars cs;
   tsg::Workspace ws;
   double setup_s = 0.0;
@@ -194,6 +249,11 @@ void dist_ensure_vecs(ts_dist_levels& L, int32_t B) {
   for (auto* b : {&v.r0, &v.u0, &v.e0, &v.p0, &v.q0}) b->alloc(l0);
   for (auto* b : {&v.r1, &v.u1, &v.e1, &v.p1, &v.q1}) b->alloc(l1);
   for (auto* b : {&v.r2, &v.u2, &v.e2, &v.p2, &v.q2}) b->alloc(l2);
+  if (L.l2_dist) {
+    const size_t own = 3 * size_t(L.l2d.n_own) * B, ext = 3 * size_t(L.l2d.n_own + L.l2d.n_halo) * B;
+    for (auto* b : {&v.r2d, &v.e2d, &v.q2d}) b->alloc(std::max<size_t>(own, 1));
+    for (auto* b : {&v.u2d, &v.p2d}) b->alloc(std::max<size_t>(ext, 1));
+  }
   v.f.release();
   v.u.release();
   v.batch = B;
@@ -221,13 +281,42 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
   p2_restrict(v.u1.get(), v.u2.get(), L.p2t_ptr.get(), L.p2t_idx.get(), L.n2, L.mask2.get(), B, s);
   comm.allreduce_sum(v.u2.get(), 3 * size_t(L.n2) * B, s);
   const auto t0 = clk::now();
-  L.ws.comm = nullptr;  // level 2 is replicated: identical on every rank, no collectives
-  L.ws.owned = nullptr;
-  auto a2 = [&](const float* x, float* y, bool) {
-    bcsr_apply_f32(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s);
-  };
-  const InnerStats s2 = inner_pcg<float>(a2, L.m2.get(), v.r2.get(), v.u2.get(), L.n2, B, cfg.level_tol[2],
-                                         cfg.level_max_iter[2], v.e2.get(), v.p2.get(), v.q2.get(), L.cs, L.ws, s);
+  InnerStats s2;
+  if (L.l2_dist) {  // this rank's coarse rows; halo exchange in every product, all-reduced dots
+    Level2Dist& D = L.l2d;
+    const int W = 3 * B;
+    if (D.n_own > 0) {
+      k_gather_rows<float><<<grid_for(int64_t(D.n_own) * W, 256), 256, 0, s>>>(v.r2.get(), D.own.get(), D.n_own, W,
+                                                                               v.r2d.get());
+      TS_CUDA_LAUNCH();
+      k_gather_rows<float><<<grid_for(int64_t(D.n_own) * W, 256), 256, 0, s>>>(v.u2.get(), D.own.get(), D.n_own, W,
+                                                                               v.u2d.get());
+      TS_CUDA_LAUNCH();
+    }
+    L.ws.comm = L.comm;
+    L.ws.owned = nullptr;
+    auto a2 = [&](const float* x, float* y, bool) {
+      D.exchange(const_cast<float*>(x), W, comm, s);
+      bcsr_apply_f32(D.row_ptr.get(), D.col_idx.get(), D.blocks.get(), D.n_own, x, y, B, s);
+    };
+    s2 = inner_pcg<float>(a2, D.m2.get(), v.r2d.get(), v.u2d.get(), D.n_own, B, cfg.level_tol[2],
+                          cfg.level_max_iter[2], v.e2d.get(), v.p2d.get(), v.q2d.get(), L.cs, L.ws, s);
+    TS_CUDA(cudaMemsetAsync(v.u2.get(), 0, 3 * size_t(L.n2) * B * sizeof(float), s));
+    if (D.n_own > 0) {
+      k_scatter_rows<float><<<grid_for(int64_t(D.n_own) * W, 256), 256, 0, s>>>(v.u2d.get(), D.own.get(), D.n_own,
+                                                                                W, v.u2.get());
+      TS_CUDA_LAUNCH();
+    }
+    comm.allreduce_sum(v.u2.get(), 3 * size_t(L.n2) * B, s);  // every rank: the whole coarse correction
+  } else {
+    L.ws.comm = nullptr;  // level 2 is replicated: identical on every rank, no collectives
+    L.ws.owned = nullptr;
+    auto a2 = [&](const float* x, float* y, bool) {
+      bcsr_apply_f32(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s);
+    };
+    s2 = inner_pcg<float>(a2, L.m2.get(), v.r2.get(), v.u2.get(), L.n2, B, cfg.level_tol[2], cfg.level_max_iter[2],
+                          v.e2.get(), v.p2.get(), v.q2.get(), L.cs, L.ws, s);
+  }
   const auto t1 = clk::now();
   L.ws.comm = L.comm;
   L.ws.owned = L.owned0.get();  // the vertex prefix of the level-0 flags
@@ -262,6 +351,94 @@ std::vector<double> per_element(const Mesh& m, int32_t n_mat, const double* x) {
     out[e] = x[mid];
   }
   return out;
+}
+
+// The distributed level 2 of one rank, from the replicated global operator every rank
+// holds after the broadcast: coarse row a belongs to the owner of its lowest vertex
+// (a vertex's owner is the lowest rank touching it), so a rank's coarse rows sit on its
+// partition; its SpMV needs the owner values of the off-rank columns it references.
+void build_level2_dist(ts_dist_levels& L, const Mesh& m, const int32_t* part, const std::vector<int32_t>& agg_g,
+                       const std::vector<int32_t>& rp2, const std::vector<int32_t>& ci2, const std::vector<float>& bl2,
+                       const std::vector<float>& m2h) {
+  const int me = L.comm->rank(), P = L.comm->size();
+  const int32_t V = m.vertex_count, n2 = L.n2;
+  std::vector<int32_t> vown(V, INT32_MAX), owner(n2, -1);
+  for (int32_t e = 0; e < m.n_elems(); ++e)
+    for (int a = 0; a < 4; ++a) {
+      int32_t& o = vown[m.tets10[10 * size_t(e) + a]];
+      o = std::min(o, part[e]);
+    }
+  for (int32_t v = 0; v < V; ++v)  // ascending: the aggregate's lowest vertex decides
+    if (owner[agg_g[v]] < 0) owner[agg_g[v]] = vown[v] == INT32_MAX ? 0 : vown[v];
+  Level2Dist& D = L.l2d;
+  std::vector<int32_t> own, loc(n2, -1);
+  for (int32_t a = 0; a < n2; ++a)
+    if (owner[a] == me) {
+      loc[a] = static_cast<int32_t>(own.size());
+      own.push_back(a);
+    }
+  D.n_own = static_cast<int32_t>(own.size());
+  // halo: off-rank columns of my rows, by owner rank then global id
+  std::vector<std::vector<int32_t>> need(P);
+  {
+    std::vector<uint8_t> seen(n2, 0);
+    for (int32_t a : own)
+      for (int32_t q = rp2[a]; q < rp2[a + 1]; ++q) {
+        const int32_t c = ci2[q];
+        if (owner[c] != me && !seen[c]) {
+          seen[c] = 1;
+          need[owner[c]].push_back(c);
+        }
+      }
+  }
+  D.roff.assign(1, 0);
+  D.nbr.clear();
+  for (int k = 0; k < P; ++k) {
+    if (need[k].empty()) continue;
+    std::sort(need[k].begin(), need[k].end());
+    for (size_t i = 0; i < need[k].size(); ++i)
+      loc[need[k][i]] = D.n_own + static_cast<int32_t>(D.roff.back() + static_cast<int64_t>(i));
+    D.nbr.push_back(k);
+    D.roff.push_back(D.roff.back() + static_cast<int64_t>(need[k].size()));
+  }
+  D.n_halo = static_cast<int32_t>(D.roff.back());
+  // what each neighbour needs from me: my coarse rows referenced by its rows (same order it expects)
+  std::vector<int32_t> send;
+  D.soff.assign(1, 0);
+  for (int k : D.nbr) {
+    std::vector<int32_t> want;
+    std::vector<uint8_t> seen(n2, 0);
+    for (int32_t a = 0; a < n2; ++a) {
+      if (owner[a] != k) continue;
+      for (int32_t q = rp2[a]; q < rp2[a + 1]; ++q) {
+        const int32_t c = ci2[q];
+        if (owner[c] == me && !seen[c]) {
+          seen[c] = 1;
+          want.push_back(c);
+        }
+      }
+    }
+    std::sort(want.begin(), want.end());
+    for (int32_t c : want) send.push_back(loc[c]);
+    D.soff.push_back(static_cast<int64_t>(send.size()));
+  }
+  // my rows with local column ids, their block-Jacobi blocks
+  std::vector<int32_t> rp(1, 0), ci;
+  std::vector<float> bl, mb;
+  for (int32_t a : own) {
+    for (int32_t q = rp2[a]; q < rp2[a + 1]; ++q) {
+      ci.push_back(loc[ci2[q]]);
+      bl.insert(bl.end(), bl2.begin() + 9 * size_t(q), bl2.begin() + 9 * size_t(q + 1));
+    }
+    rp.push_back(static_cast<int32_t>(ci.size()));
+    mb.insert(mb.end(), m2h.begin() + 9 * size_t(a), m2h.begin() + 9 * size_t(a + 1));
+  }
+  D.own.upload(own);
+  D.row_ptr.upload(rp);
+  D.col_idx.upload(ci);
+  D.blocks.upload(bl);
+  D.m2.upload(mb);
+  D.send.upload(send);
 }
 
 }  // namespace
@@ -381,6 +558,16 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
     L->l2_blocks.upload(bl2);
     L->m2.upload(m2h);
     L->mask2.upload(mk2);
+    // level 2 replicated on every rank (no collectives inside its PCG, but every rank does all of
+    // it) or split by coarse rows (1/P of it, plus a gather halo per product and all-reduced dots);
+    // TSGPU_DIST_L2 = replicated | distributed | auto (default: split from 4 ranks on, where the
+    // replicated coarse solve becomes the Amdahl term — DESIGN.md §6)
+    {
+      const char* e = std::getenv("TSGPU_DIST_L2");
+      const std::string mode = e ? e : "auto";
+      L->l2_dist = mode == "distributed" || (mode == "auto" && comm->size() >= 4);
+    }
+    if (L->l2_dist) build_level2_dist(*L, m, part, agg_g, rp2, ci2, bl2, m2h);
     const int32_t Vl = L->n1;
     std::vector<int32_t> agg_l(Vl), aptr(L->n2 + 1, 0);
     for (int32_t i = 0; i < Vl; ++i) {

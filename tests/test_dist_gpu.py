@@ -121,8 +121,12 @@ def smooth(coords, ext, mask, B, seed):
     return u
 
 
+@pytest.mark.parametrize("l2", ["replicated", "distributed"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_partitioned_solve_matches_single_device(P):
+def test_partitioned_solve_matches_single_device(P, l2, monkeypatch):
+    """Level 2 either replicated on every rank or split by coarse rows with a gather halo in
+    every product (TSGPU_DIST_L2): the same solution and iteration counts either way."""
+    monkeypatch.setenv("TSGPU_DIST_L2", l2)
     m = ts.generate_box_mesh(*SPEC)
     mask = m.dirichlet_mask()
     B = 3
