@@ -1043,6 +1043,29 @@ def main():
                 del uu, ff
             if opp is not op:
                 del opp
+        # the edge-fan sweep (opt-in kernel 8: 4.5 node rows per element instead of 7) beside it
+        os.environ["TSGPU_EBE_KERNEL"] = "fan"
+        try:
+            opf = ts.EbeOperator(mesh, 2, mats, mask, prec=32)
+        finally:
+            del os.environ["TSGPU_EBE_KERNEL"]
+        opf.set_timing(True)
+        for rr in (1, 4, 8, 16):
+            uu = torch.rand(3 * N, rr, device="cuda", dtype=torch.float32, generator=g)
+            ff = torch.empty_like(uu)
+            for _ in range(3):
+                opf.apply(uu, ff)
+            torch.cuda.synchronize()
+            ks = []
+            for _ in range(5):
+                opf.apply(uu, ff)
+                ks.append(opf.last_kernel_ms())
+            bb = alg_bytes(E, N, rr, 4)
+            sweep[f"fp32_r{rr}_fan"] = {"kernel_ms": round(float(np.mean(ks)), 4),
+                                        "kernel_frac": round(bb / float(np.mean(ks)) / 1e6 / peak, 4),
+                                        "unit_stats": opf.unit_stats()}
+            del uu, ff
+        del opf
 
     # ---- CPU baseline: the reference itself on this host (rank 0, N = 1)
     cpu = None

@@ -37,9 +37,9 @@ struct EbeFanPlan {
   double closed_fraction = 0.0;   // elements in closed fans
   double mean_k = 0.0;            // elements per fan
   double rows_per_element = 0.0;  // node rows gathered (= reduced) per element
-  tsg::DevBuf<int32_t> words;     // [E][12]: flags, the rows the element adds (node | mask << 28)
-  tsg::DevBuf<unsigned char> coef;  // [E][12] of T, slot-order coefficient records
-  tsg::DevBuf<int32_t> ufirst;    // [U + 1] first element (fan order) of each fan
+  tsg::DevBuf<int32_t> words;     // [steps][16]: flags, the rows a step (two elements) adds (node | mask << 28)
+  tsg::DevBuf<unsigned char> coef;  // [steps][24] of T: the step's two slot-order coefficient records
+  tsg::DevBuf<int32_t> ufirst;    // [U + 1] first step of each fan
 };
 
 // Elements sweep in slabs of their lowest vertex id (then Morton order), ebe.cu;

@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "ebe.h"
@@ -38,18 +39,18 @@
 namespace tsg {
 namespace {
 
-// element word record: 12 int32 = [flags, gathered rows g1 .. g10, 0]; a row word is
-// node | dof-mask bits << 28 (bare node ids when the element has no constrained dof: the
-// kInterior fast paths). The rows an element scatter-adds are the ones gathered before it
-// (A: the previous element's B; at a fan's end, B and p, q, m), carried in registers.
-enum : int32_t { kFanStart = 1, kFanEnd = 2, kFanClosed = 4, kFanInterior = 8 };
-constexpr int kFanWords = 12;
+// step word record: 16 int32 = [flags, p, q, m, r0, mid(p,r0), mid(q,r0) (fan start only),
+// M triple r_{j+1}, mid(p,.), mid(q,.) (-1: r_0), B triple r_{j+2} (-1: r_0 / no second element),
+// ring edges e_j, e_{j+1} (-1: none), 0]; a row word is node | dof-mask bits << 28 (bare node ids
+// in interior steps: the kInterior fast paths)
+enum : int32_t { kFanStart = 1, kFanEnd = 2, kFanClosed = 4, kFanInterior = 8, kFanSingle = 16 };
+constexpr int kFanWords = 16;
 constexpr int kHdrSlots = 6;                    // p, q, m, r0, mid(p,r0), mid(q,r0)
-constexpr int kRingBase = 2 * kHdrSlots;        // 3 ring-vertex triples
-constexpr int kEdgeBase = kRingBase + 9;        // 2 ring edges
-constexpr int kR0Base = kEdgeBase + 2;          // r0 partial sums of a closed fan
+constexpr int kRingBase = 2 * kHdrSlots;        // 5 ring-vertex triples
+constexpr int kEdgeBase = kRingBase + 15;       // 4 ring edges
+constexpr int kR0Base = kEdgeBase + 4;          // r0 partial sums of a closed fan
 constexpr int kFanSlots = kR0Base + 3;          // row slots per lane group
-constexpr int kRowV = 4;                        // lane vectors per row slot (3 components + pad)
+constexpr int kRowV = 3;                        // lane vectors per row slot
 
 __device__ __forceinline__ void cpa(void* s, const void* g, int src, int bytes) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(s));
@@ -72,19 +73,10 @@ __device__ __forceinline__ void red_p(double* p, double v, unsigned skip) {
                : "memory");
 }
 
-// one lane's 3 components of a row slot (16-byte shared loads)
+// one lane's 3 components of a row slot
 template <typename V>
 __device__ __forceinline__ void load_row(const V* p, V (&r)[3]) {
-  if constexpr (sizeof(V) == 8) {
-    const uint4 a = reinterpret_cast<const uint4*>(p)[0];
-    const uint2 b = reinterpret_cast<const uint2*>(p)[2];
-    r[0] = *reinterpret_cast<const V*>(&a.x);
-    r[1] = *reinterpret_cast<const V*>(&a.z);
-    r[2] = *reinterpret_cast<const V*>(&b.x);
-  } else {
-    const float4 a = *reinterpret_cast<const float4*>(p);
-    r[0] = a.x; r[1] = a.y; r[2] = a.z;
-  }
+  r[0] = p[0]; r[1] = p[1]; r[2] = p[2];
 }
 template <typename V>
 __device__ __forceinline__ void store_row(V* p, const V (&r)[3]) {
@@ -152,260 +144,293 @@ k_ebe_fan(const int4* __restrict__ words, const T* __restrict__ coef, const int3
   static_assert(NT % TPE == 0 && TPE * CPT == B, "lane groups must tile the block and the batch");
   constexpr int GROUPS = NT / TPE;
   constexpr int TPC = 16 / sizeof(T);
-  constexpr int RCH = 12 / TPC;   // 16-byte chunks per coefficient record
+  constexpr int RCH = 24 / TPC;   // 16-byte chunks of a step's two coefficient records
   constexpr int RS = TPE * kRowV; // lane vectors per row slot
   extern __shared__ __align__(16) unsigned char smem[];
   const int grp = threadIdx.x / TPE;
   const int lane = threadIdx.x % TPE;
   V* const ug = reinterpret_cast<V*>(smem) + size_t(grp) * kFanSlots * RS + lane * kRowV;  // this lane's slot 0
-  T* const cg = reinterpret_cast<T*>(smem + size_t(NT) * kFanSlots * kRowV * sizeof(V)) + size_t(grp) * 24;
+  T* const cg = reinterpret_cast<T*>(smem + size_t(NT) * kFanSlots * kRowV * sizeof(V)) + size_t(grp) * 48;
   int4* const wg =
-      reinterpret_cast<int4*>(smem + size_t(NT) * kFanSlots * kRowV * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T)) +
-      size_t(grp) * 9;
+      reinterpret_cast<int4*>(smem + size_t(NT) * kFanSlots * kRowV * sizeof(V) + size_t(GROUPS) * 48 * sizeof(T)) +
+      size_t(grp) * 12;
   const int col = lane * CPT;
   const T* const ub = u + col;
   T* const fb = f + col;
   const int32_t G = gridDim.x * GROUPS;
 
-  // rows: interior elements carry bare node ids (no mask bits), so one IMAD addresses a row
-  auto gather_plain = [&](int32_t w, V* dst) {
-    const T* src = ub + static_cast<size_t>(static_cast<uint32_t>(w)) * (3 * B);
+  // rows: interior steps carry bare node ids (no mask bits), so one IMAD addresses a row; the
+  // interior / boundary choice is a compile-time flag (PL) of the step's whole gather or scatter
+  // block, so neither path is predicated into the other
+  auto gather = [&](auto PL, int32_t w, V* dst) {
+    if constexpr (decltype(PL)::value) {
+      const T* src = ub + static_cast<size_t>(static_cast<uint32_t>(w)) * (3 * B);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cpa(dst + c, src + c * B, int(sizeof(V)), sizeof(V));
-  };
-  auto gather_mask = [&](int32_t w, V* dst) {
-    const T* src = ub + static_cast<size_t>(static_cast<uint32_t>(w) & 0x0FFFFFFFu) * (3 * B);
-    const unsigned mk = static_cast<unsigned>(w) >> 28;
+      for (int c = 0; c < 3; ++c) cpa(dst + c, src + c * B, int(sizeof(V)), sizeof(V));
+    } else {
+      const T* src = ub + static_cast<size_t>(static_cast<uint32_t>(w) & 0x0FFFFFFFu) * (3 * B);
+      const unsigned mk = static_cast<unsigned>(w) >> 28;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cpa(dst + c, src + c * B, ((mk >> c) & 1u) ? 0 : int(sizeof(V)), sizeof(V));
+      for (int c = 0; c < 3; ++c) cpa(dst + c, src + c * B, ((mk >> c) & 1u) ? 0 : int(sizeof(V)), sizeof(V));
+    }
   };
-  auto red_plain = [&](int32_t w, const V& a, const V& b, const V& c2) {
-    T* dst = fb + static_cast<size_t>(static_cast<uint32_t>(w)) * (3 * B);
-    red_lane(reinterpret_cast<V*>(dst), a);
-    red_lane(reinterpret_cast<V*>(dst + B), b);
-    red_lane(reinterpret_cast<V*>(dst + 2 * B), c2);
+  auto red = [&](auto PL, int32_t w, const V (&v)[3]) {
+    if constexpr (decltype(PL)::value) {
+      T* dst = fb + static_cast<size_t>(static_cast<uint32_t>(w)) * (3 * B);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(dst + c * B), v[c]);
+    } else {
+      T* dst = fb + static_cast<size_t>(static_cast<uint32_t>(w) & 0x0FFFFFFFu) * (3 * B);
+      const unsigned mk = static_cast<unsigned>(w) >> 28;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(dst + c * B), v[c], (mk >> c) & 1u);
+    }
   };
-  auto red_mask = [&](int32_t w, const V& a, const V& b, const V& c2) {
-    T* dst = fb + static_cast<size_t>(static_cast<uint32_t>(w) & 0x0FFFFFFFu) * (3 * B);
-    const unsigned mk = static_cast<unsigned>(w) >> 28;
-    red_p(reinterpret_cast<V*>(dst), a, mk & 1u);
-    red_p(reinterpret_cast<V*>(dst + B), b, (mk >> 1) & 1u);
-    red_p(reinterpret_cast<V*>(dst + 2 * B), c2, (mk >> 2) & 1u);
+  // three rows of partial sums
+  auto red3 = [&](bool plain, const int32_t (&w)[3], const V (&v)[3][3]) {
+    if (plain) {
+      red(std::true_type{}, w[0], v[0]);
+      red(std::true_type{}, w[1], v[1]);
+      red(std::true_type{}, w[2], v[2]);
+    } else {
+      red(std::false_type{}, w[0], v[0]);
+      red(std::false_type{}, w[1], v[1]);
+      red(std::false_type{}, w[2], v[2]);
+    }
+  };
+  auto red1 = [&](bool plain, int32_t w, const V (&v)[3]) {
+    if (plain) red(std::true_type{}, w, v);
+    else red(std::false_type{}, w, v);
   };
   auto fetch_words = [&](int32_t x, int ws) {
     if (x >= 0)
-      for (int q = lane; q < 3; q += TPE) cpa(wg + 3 * ws + q, words + 3 * static_cast<size_t>(x) + q, 16, 16);
+      for (int q = lane; q < 4; q += TPE) cpa(wg + 4 * ws + q, words + 4 * static_cast<size_t>(x) + q, 16, 16);
   };
 
-  // slot state: of the element whose rows are in flight (n) and of the one computed (c)
-  int ring_next = 0, edge_next = 0, hdr_n = 1, bslot_n = -1, eslot_n = 0;
-  auto issue = [&](int32_t xn, int wsn, int rsn) {
-    if (xn < 0) return;
-    const int4* w = wg + 3 * wsn;
-    const int4 w0 = w[0], w1 = w[1];
-    const int32_t fl = w0.x;
-    for (int q = lane; q < RCH; q += TPE) cpa(cg + 12 * rsn + q * TPC, coef + 12 * static_cast<size_t>(xn) + q * TPC, 16, 16);
-    if (fl & kFanStart) {
-      const int4 w2 = w[2];
-      hdr_n ^= 1;
-      bslot_n = ring_next;
-      ring_next = ring_next == 2 ? 0 : ring_next + 1;
-      eslot_n = edge_next;
-      edge_next ^= 1;
-      V* h = ug + hdr_n * (kHdrSlots * RS);
-      V* rb = ug + (kRingBase + 3 * bslot_n) * RS;
-      V* eb = ug + (kEdgeBase + eslot_n) * RS;
-      if (fl & kFanInterior) {
-        gather_plain(w0.y, h);
-        gather_plain(w0.z, h + RS);
-        gather_plain(w0.w, h + 2 * RS);
-        gather_plain(w1.x, h + 3 * RS);
-        gather_plain(w1.y, h + 4 * RS);
-        gather_plain(w1.z, h + 5 * RS);
-        gather_plain(w1.w, rb);
-        gather_plain(w2.x, rb + RS);
-        gather_plain(w2.y, rb + 2 * RS);
-        gather_plain(w2.z, eb);
-      } else {
-        gather_mask(w0.y, h);
-        gather_mask(w0.z, h + RS);
-        gather_mask(w0.w, h + 2 * RS);
-        gather_mask(w1.x, h + 3 * RS);
-        gather_mask(w1.y, h + 4 * RS);
-        gather_mask(w1.z, h + 5 * RS);
-        gather_mask(w1.w, rb);
-        gather_mask(w2.x, rb + RS);
-        gather_mask(w2.y, rb + 2 * RS);
-        gather_mask(w2.z, eb);
-      }
-    } else {
-      const bool ring = (fl & (kFanEnd | kFanClosed)) != (kFanEnd | kFanClosed);  // else B = r0, in the header
-      bslot_n = -1;
-      if (ring) {
-        bslot_n = ring_next;
-        ring_next = ring_next == 2 ? 0 : ring_next + 1;
-      }
-      eslot_n = edge_next;
-      edge_next ^= 1;
-      V* rb = ug + (kRingBase + 3 * bslot_n) * RS;
-      V* eb = ug + (kEdgeBase + eslot_n) * RS;
-      if (fl & kFanInterior) {
-        if (ring) {
-          gather_plain(w0.y, rb);
-          gather_plain(w0.z, rb + RS);
-          gather_plain(w0.w, rb + 2 * RS);
-        }
-        gather_plain(w1.x, eb);
-      } else {
-        if (ring) {
-          gather_mask(w0.y, rb);
-          gather_mask(w0.z, rb + RS);
-          gather_mask(w0.w, rb + 2 * RS);
-        }
-        gather_mask(w1.x, eb);
-      }
+  // slot allocation: ring triples rotate (5), ring edges rotate (4), fan headers alternate (2)
+  struct Slots {
+    int hdr, m, b, e0, e1;
+  };
+  int ring_next = 0, edge_next = 0, hdr_last = 1;
+  auto ring_alloc = [&]() {
+    const int r = ring_next;
+    ring_next = ring_next == 4 ? 0 : ring_next + 1;
+    return r;
+  };
+  auto edge_alloc = [&]() {
+    const int r = edge_next;
+    edge_next = (edge_next + 1) & 3;
+    return r;
+  };
+  auto issue_rows = [&](auto PL, const int4& w0, const int4& w1, const int4& w2, const int4& w3, const Slots& st) {
+    if (w0.x & kFanStart) {
+      V* h = ug + st.hdr * (kHdrSlots * RS);
+      gather(PL, w0.y, h);           // p
+      gather(PL, w0.z, h + RS);      // q
+      gather(PL, w0.w, h + 2 * RS);  // m
+      gather(PL, w1.x, h + 3 * RS);  // r0
+      gather(PL, w1.y, h + 4 * RS);  // mid(p, r0)
+      gather(PL, w1.z, h + 5 * RS);  // mid(q, r0)
     }
+    if (st.m >= 0) {  // M = r_{j+1} (else r0, in the header)
+      V* r = ug + (kRingBase + 3 * st.m) * RS;
+      gather(PL, w1.w, r);
+      gather(PL, w2.x, r + RS);
+      gather(PL, w2.y, r + 2 * RS);
+    }
+    if (st.b >= 0) {  // B = r_{j+2} (else r0, or no second element)
+      V* r = ug + (kRingBase + 3 * st.b) * RS;
+      gather(PL, w2.z, r);
+      gather(PL, w2.w, r + RS);
+      gather(PL, w3.x, r + 2 * RS);
+    }
+    gather(PL, w3.y, ug + (kEdgeBase + st.e0) * RS);
+    if (w3.z != -1) gather(PL, w3.z, ug + (kEdgeBase + st.e1) * RS);
+  };
+  auto issue = [&](int32_t x, int ws, int rs) -> Slots {
+    Slots st{hdr_last, -1, -1, 0, 0};
+    if (x < 0) return st;
+    const int4* w = wg + 4 * ws;
+    const int4 w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3];
+    const int32_t fl = w0.x;
+    for (int q = lane; q < RCH; q += TPE) cpa(cg + 24 * rs + q * TPC, coef + 24 * static_cast<size_t>(x) + q * TPC, 16, 16);
+    if (fl & kFanStart) {
+      hdr_last ^= 1;
+      st.hdr = hdr_last;
+    }
+    if (w1.w != -1) st.m = ring_alloc();
+    if (w2.z != -1) st.b = ring_alloc();
+    st.e0 = edge_alloc();
+    if (w3.z != -1) st.e1 = edge_alloc();
+    if (fl & kFanInterior) issue_rows(std::true_type{}, w0, w1, w2, w3, st);
+    else issue_rows(std::false_type{}, w0, w1, w2, w3, st);
+    return st;
   };
 
+  // pipeline: step t (two elements of a fan) is computed while the rows of step t+1 stream in
+  // and the words of step t+2 are fetched (word slots mod 3, record slots mod 2)
   FanCursor cur;
   cur.init(ufirst, u0 + static_cast<int32_t>(blockIdx.x) * GROUPS + grp, u1, G);
   int32_t xn = cur.x;
   cur.advance(ufirst, u1, G);
-  // prologue: words of the first element, then its rows + the second element's words
   fetch_words(xn, 0);
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
-  issue(xn, 0, 0);
+  Slots stn = issue(xn, 0, 0);
   fetch_words(cur.x, 1);
   asm volatile("cp.async.commit_group;" ::: "memory");
 
-  int wsc = 0, rsc = 0;  // word slot (mod 3) and record slot (mod 2) of the computed element
-  int aslot = -1;        // ring slot of A (-1: r0 in the header)
-  int32_t hw[6] = {0, 0, 0, 0, 0, 0}, aw[3] = {0, 0, 0}, bw[3] = {0, 0, 0};  // p q m r0 rows; A, B rows
-  V S[3][3], X[3][3], Y[3][3];
+  int wsc = 0, rsc = 0;
+  int aslot = -1;                                      // ring triple of A (-1: r0 in the header)
+  int32_t hw[6] = {0, 0, 0, 0, 0, 0}, aw[3] = {0, 0, 0};  // p q m r0 rows of the fan; A rows
+  V S[3][3], FA[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) S[i][c] = X[i][c] = Y[i][c] = O::zero();
+    for (int c = 0; c < 3; ++c) S[i][c] = FA[i][c] = O::zero();
 
-  // one element; FA holds the A rows' partial sums (in: from the previous element,
-  // out: complete), FB receives the B rows (the next element's FA). Two calls per
-  // loop trip with the roles swapped keep the carry in place (no register moves).
-  auto step = [&](V (&FA)[3][3], V (&FB)[3][3]) -> bool {
-    if (!__any_sync(0xffffffffu, xn >= 0)) return false;
+  while (__any_sync(0xffffffffu, xn >= 0)) {
     const int32_t xc = xn;
-    const int hdr_c = hdr_n, bslot_c = bslot_n, eslot_c = eslot_n;
+    const Slots sc = stn;
     xn = cur.x;
     cur.advance(ufirst, u1, G);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     const int wsn = wsc == 2 ? 0 : wsc + 1, ws2 = wsn == 2 ? 0 : wsn + 1;
-    issue(xn, wsn, rsc ^ 1);
+    stn = issue(xn, wsn, rsc ^ 1);
     fetch_words(cur.x, ws2);
     asm volatile("cp.async.commit_group;" ::: "memory");
     if (xc >= 0) {
-      const int4* w = wg + 3 * wsc;
-      const int4 w0 = w[0], w1 = w[1];
+      const int4* w = wg + 4 * wsc;
+      const int4 w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3];
       const int32_t fl = w0.x;
-      const bool start = (fl & kFanStart) != 0;
-      int32_t ew;
+      const bool start = (fl & kFanStart) != 0, end = (fl & kFanEnd) != 0, closed = (fl & kFanClosed) != 0,
+                 single = (fl & kFanSingle) != 0, plain = (fl & kFanInterior) != 0;
       if (start) {
-        const int4 w2 = w[2];
         hw[0] = w0.y; hw[1] = w0.z; hw[2] = w0.w; hw[3] = w1.x; hw[4] = w1.y; hw[5] = w1.z;
         aw[0] = w1.x; aw[1] = w1.y; aw[2] = w1.z;
-        bw[0] = w1.w; bw[1] = w2.x; bw[2] = w2.y;
-        ew = w2.z;
-      } else {
-        aw[0] = bw[0]; aw[1] = bw[1]; aw[2] = bw[2];
-        if (bslot_c < 0) {
-          bw[0] = hw[3]; bw[1] = hw[4]; bw[2] = hw[5];
+        aslot = -1;
+      }
+      const int32_t mw[3] = {w1.w != -1 ? w1.w : hw[3], w1.w != -1 ? w2.x : hw[4], w1.w != -1 ? w2.y : hw[5]};
+      const V* h = ug + sc.hdr * (kHdrSlots * RS);
+      const V* rm = sc.m < 0 ? h + 3 * RS : ug + (kRingBase + 3 * sc.m) * RS;
+      V* const park = ug + kR0Base * RS;
+      V sv[3][3];  // p, q, m rows (both elements)
+      load_row(h, sv[0]);
+      load_row(h + RS, sv[1]);
+      load_row(h + 2 * RS, sv[2]);
+      V FM[3][3];
+      {  // element j = (p, q, r_j, r_{j+1}): A = r_j, B = M
+        T rec[12];
+        load_rec(cg + 24 * rsc, rec);
+        V b[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
+        const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
+        const V* ra = aslot < 0 ? h + 3 * RS : ug + (kRingBase + 3 * aslot) * RS;
+        V uu[10][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          uu[0][c] = sv[0][c];
+          uu[1][c] = sv[1][c];
+          uu[4][c] = sv[2][c];
+        }
+        load_row(ra, uu[2]);
+        load_row(ra + RS, uu[6]);
+        load_row(ra + 2 * RS, uu[5]);
+        load_row(rm, uu[3]);
+        load_row(rm + RS, uu[7]);
+        load_row(rm + 2 * RS, uu[8]);
+        load_row(ug + (kEdgeBase + sc.e0) * RS, uu[9]);
+        V FE[3];
+        tet10_product_acc<0x077u>(uu, b, lp, mp, [&](int s, int c) -> V& {
+          return s == 0 ? S[0][c] : s == 1 ? S[1][c] : s == 4 ? S[2][c] : s == 2 ? FA[0][c] : s == 6 ? FA[1][c]
+               : s == 5 ? FA[2][c] : s == 3 ? FM[0][c] : s == 7 ? FM[1][c] : s == 8 ? FM[2][c] : FE[c];
+        });
+        if (start && closed) {  // r_0 of a closed fan: parked until its last element
+#pragma unroll
+          for (int i = 0; i < 3; ++i) store_row(park + i * RS, FA[i]);
         } else {
-          bw[0] = w0.y; bw[1] = w0.z; bw[2] = w0.w;
+          red3(plain, aw, FA);
         }
-        ew = w1.x;
+        red1(plain, w3.y, FE);
       }
-      T rec[12];
-      load_rec(cg + 12 * rsc, rec);
-      V b[3][3];
+      if (!single) {  // element j+1 = (p, q, r_{j+1}, r_{j+2}): A = M, B (into FA's registers)
+        T rec[12];
+        load_rec(cg + 24 * rsc + 12, rec);
+        V b[3][3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
+        for (int k = 0; k < 3; ++k)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
-      const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
-      const V* h = ug + hdr_c * (kHdrSlots * RS);
-      const V* ra = start ? h + 3 * RS : ug + (kRingBase + 3 * aslot) * RS;
-      const V* rb = bslot_c < 0 ? h + 3 * RS : ug + (kRingBase + 3 * bslot_c) * RS;
-      V uu[10][3];
-      load_row(h, uu[0]);
-      load_row(h + RS, uu[1]);
-      load_row(h + 2 * RS, uu[4]);
-      load_row(ra, uu[2]);
-      load_row(ra + RS, uu[6]);
-      load_row(ra + 2 * RS, uu[5]);
-      load_row(rb, uu[3]);
-      load_row(rb + RS, uu[7]);
-      load_row(rb + 2 * RS, uu[8]);
-      load_row(ug + (kEdgeBase + eslot_c) * RS, uu[9]);
-      V FE[3];
-      // slots: 0 p, 1 q, 4 m (S) | 2 r_j, 6 mid(p,r_j), 5 mid(q,r_j) (A) | 3, 7, 8 (B) | 9 ring edge
-      tet10_product_acc<0x077u>(uu, b, lp, mp, [&](int s, int c) -> V& {
-        return s == 0 ? S[0][c] : s == 1 ? S[1][c] : s == 4 ? S[2][c] : s == 2 ? FA[0][c] : s == 6 ? FA[1][c]
-             : s == 5 ? FA[2][c] : s == 3 ? FB[0][c] : s == 7 ? FB[1][c] : s == 8 ? FB[2][c] : FE[c];
-      });
-      const bool end = (fl & kFanEnd) != 0, closed = (fl & kFanClosed) != 0;
-      V* const r0park = ug + kR0Base * RS;
-      if (start && closed) {  // r_0 of a closed fan: parked until the fan's last element
+          for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
+        const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
+        const V* rb = sc.b < 0 ? h + 3 * RS : ug + (kRingBase + 3 * sc.b) * RS;
+        V uu[10][3];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) store_row(r0park + i * RS, FA[i]);
-      }
-      if (end && closed) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          V r[3];
-          load_row(r0park + i * RS, r);
-#pragma unroll
-          for (int c = 0; c < 3; ++c) FB[i][c] = O::add(FB[i][c], r[c]);
+        for (int c = 0; c < 3; ++c) {
+          uu[0][c] = sv[0][c];
+          uu[1][c] = sv[1][c];
+          uu[4][c] = sv[2][c];
         }
-      }
-      const bool reda = !(start && closed);
-      if (fl & kFanInterior) {
-        if (reda)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) red_plain(aw[i], FA[i][0], FA[i][1], FA[i][2]);
-        red_plain(ew, FE[0], FE[1], FE[2]);
+        load_row(rm, uu[2]);
+        load_row(rm + RS, uu[6]);
+        load_row(rm + 2 * RS, uu[5]);
+        load_row(rb, uu[3]);
+        load_row(rb + RS, uu[7]);
+        load_row(rb + 2 * RS, uu[8]);
+        load_row(ug + (kEdgeBase + sc.e1) * RS, uu[9]);
+        V FE[3];
+        tet10_product_acc<0x077u>(uu, b, lp, mp, [&](int s, int c) -> V& {
+          return s == 0 ? S[0][c] : s == 1 ? S[1][c] : s == 4 ? S[2][c] : s == 2 ? FM[0][c] : s == 6 ? FM[1][c]
+               : s == 5 ? FM[2][c] : s == 3 ? FA[0][c] : s == 7 ? FA[1][c] : s == 8 ? FA[2][c] : FE[c];
+        });
+        red3(plain, mw, FM);
+        red1(plain, w3.z, FE);
+        // the step's last rows: B = r_{j+2} (r_0 of a closed fan: + its parked sums)
+        const int32_t bw[3] = {w2.z != -1 ? w2.z : hw[3], w2.z != -1 ? w2.w : hw[4], w2.z != -1 ? w3.x : hw[5]};
         if (end) {
+          if (closed)
 #pragma unroll
-          for (int i = 0; i < 3; ++i) red_plain(bw[i], FB[i][0], FB[i][1], FB[i][2]);
+            for (int i = 0; i < 3; ++i) {
+              V r[3];
+              load_row(park + i * RS, r);
 #pragma unroll
-          for (int i = 0; i < 3; ++i) red_plain(hw[i], S[i][0], S[i][1], S[i][2]);
+              for (int c = 0; c < 3; ++c) FA[i][c] = O::add(FA[i][c], r[c]);
+            }
+          red3(plain, bw, FA);
+        } else {
+          aw[0] = bw[0]; aw[1] = bw[1]; aw[2] = bw[2];
+          aslot = sc.b;
         }
-      } else {
-        if (reda)
+      } else {  // a fan's odd last element: its B = M is the fan's last ring vertex (r_0 if closed)
+        if (closed)
 #pragma unroll
-          for (int i = 0; i < 3; ++i) red_mask(aw[i], FA[i][0], FA[i][1], FA[i][2]);
-        red_mask(ew, FE[0], FE[1], FE[2]);
-        if (end) {
+          for (int i = 0; i < 3; ++i) {
+            V r[3];
+            load_row(park + i * RS, r);
 #pragma unroll
-          for (int i = 0; i < 3; ++i) red_mask(bw[i], FB[i][0], FB[i][1], FB[i][2]);
-#pragma unroll
-          for (int i = 0; i < 3; ++i) red_mask(hw[i], S[i][0], S[i][1], S[i][2]);
-        }
+            for (int c = 0; c < 3; ++c) FM[i][c] = O::add(FM[i][c], r[c]);
+          }
+        red3(plain, mw, FM);
       }
-      if (end) {  // the next fan starts from zero partial sums (S, and its A = this B)
+      if (end) {  // p, q, m; the next fan starts from zero partial sums
+        {
+          const int32_t sw3[3] = {hw[0], hw[1], hw[2]};
+          red3(plain, sw3, S);
+        }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) S[i][c] = FB[i][c] = O::zero();
+          for (int c = 0; c < 3; ++c) S[i][c] = FA[i][c] = O::zero();
+        aslot = -1;
       }
-      aslot = bslot_c;
     }
     __syncwarp();
     wsc = wsn;
     rsc ^= 1;
-    return true;
-  };
-  while (step(X, Y) && step(Y, X)) {
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
@@ -413,7 +438,7 @@ k_ebe_fan(const int4* __restrict__ words, const T* __restrict__ coef, const int3
 template <typename T, typename V, int B>
 size_t fan_smem() {
   constexpr int CPT = LaneOps<V>::kCols, TPE = (B + CPT - 1) / CPT, NT = 128, GROUPS = NT / TPE;
-  return size_t(NT) * kFanSlots * kRowV * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) + size_t(GROUPS) * 9 * 16;
+  return size_t(NT) * kFanSlots * kRowV * sizeof(V) + size_t(GROUPS) * 48 * sizeof(T) + size_t(GROUPS) * 12 * 16;
 }
 
 template <typename T, typename V, int B>
@@ -669,9 +694,13 @@ void build_fan_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_word
   for (int32_t i = 0; i < U; ++i)
     if (group_of(order[fans[i].first]) == 0) split = i + 1;
 
+  // steps: each fan's elements two by two (an odd fan ends with a single-element step)
+  std::vector<int32_t> sfirst(size_t(U) + 1, 0);
+  for (int32_t i = 0; i < U; ++i) sfirst[i + 1] = sfirst[i] + (fans[i].k + 1) / 2;
+  const int64_t NS = sfirst[U];
   const size_t ts = fp32 ? 4 : 8;
-  HostVec<int32_t> wv(size_t(E) * kFanWords);
-  HostVec<unsigned char> cf(size_t(E) * 12 * ts);
+  HostVec<int32_t> wv(size_t(NS) * kFanWords);
+  HostVec<unsigned char> cf(size_t(NS) * 24 * ts);
   auto rnd = [fp32](double x) { return fp32 ? static_cast<double>(static_cast<float>(x)) : x; };
   bool bad = false;
 #pragma omp parallel for schedule(dynamic, 1024) reduction(|| : bad)
@@ -715,47 +744,25 @@ void build_fan_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_word
       }
       if (fn.closed && r[k] != r[0]) bad = true;
     }
-    for (int j = 0; j < k; ++j) {
+    // per element: slot words (p, q, r_j, r_{j+1} labelling) and the coefficient record
+    std::vector<std::array<int32_t, 10>> sw(k);
+    std::vector<std::array<double, 12>> rec(k);
+    bool interior_all = true;
+    for (int j = 0; j < k && !bad; ++j) {
       const int64_t e = order[fn.first + j];
-      const int64_t x = fn.first + j;
-      // slot labelling (p, q, r_j, r_{j+1}) -> original local vertex indices
       int perm[4] = {-1, -1, -1, -1};
       const int32_t want[4] = {fn.p, fn.q, r[j], r[j + 1]};
-      for (int s = 0; s < 4; ++s)
+      for (int q = 0; q < 4; ++q)
         for (int v = 0; v < 4; ++v)
-          if (node(e, v) == want[s]) perm[s] = v;
+          if (node(e, v) == want[q]) perm[q] = v;
       if (perm[0] < 0 || perm[1] < 0 || perm[2] < 0 || perm[3] < 0) {
         bad = true;
-        continue;
+        break;
       }
-      int32_t sw[10];  // node word per slot
-      for (int s = 0; s < 10; ++s) {
-        const int a = s < 4 ? perm[s] : edge_slot(perm[ev[s - 4][0]], perm[ev[s - 4][1]]);
-        const int32_t cw = word(e, a);
-        sw[s] = cw;
+      for (int q = 0; q < 10; ++q) {
+        const int a = q < 4 ? perm[q] : edge_slot(perm[ev[q - 4][0]], perm[ev[q - 4][1]]);
+        sw[j][q] = word(e, a);
       }
-      bool interior = true;
-      for (int s = 0; s < 10; ++s) interior = interior && ((static_cast<uint32_t>(sw[s]) >> 28) == 0u);
-      const bool start = j == 0, end = j == k - 1;
-      int32_t* w = wv.data() + kFanWords * size_t(x);
-      for (int q = 0; q < kFanWords; ++q) w[q] = 0;
-      w[0] = (start ? kFanStart : 0) | (end ? kFanEnd : 0) | (fn.closed ? kFanClosed : 0) | (interior ? kFanInterior : 0);
-      // gathers: the rows this element adds
-      if (start) {
-        // p, q, m, r0, mid(p,r0), mid(q,r0), r1, mid(p,r1), mid(q,r1), mid(r0,r1)
-        const int ss[10] = {0, 1, 4, 2, 6, 5, 3, 7, 8, 9};
-        for (int q = 0; q < 10; ++q) w[1 + q] = sw[ss[q]];
-      } else {
-        if (!(end && fn.closed)) {
-          w[1] = sw[3];
-          w[2] = sw[7];
-          w[3] = sw[8];
-        } else {
-          w[1] = w[2] = w[3] = -1;
-        }
-        w[4] = sw[9];
-      }
-      // coefficient record in slot order, volume from the original orientation
       double v[4][3], jm[3][3], inv[3][3];
       for (int a = 0; a < 4; ++a)
         for (int c = 0; c < 3; ++c) v[a][c] = rnd(m.coords[3 * size_t(op.host_conn[e * 10 + perm[a]]) + c]);
@@ -763,37 +770,69 @@ void build_fan_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_word
         for (int rr = 0; rr < 3; ++rr) jm[rr][c] = v[c + 1][rr] - v[0][rr];
       if (!inv3(jm, inv)) {
         bad = true;
-        continue;
+        break;
       }
-      double rec[12];
       for (int kk = 0; kk < 3; ++kk)
-        for (int d = 0; d < 3; ++d) rec[3 * kk + d] = inv[kk][d];
-      rec[9] = coef64[12 * e + 9] / 20.0;
-      rec[10] = coef64[12 * e + 10] / 20.0;
-      rec[11] = 0.0;
-      unsigned char* dst = cf.data() + size_t(x) * 12 * ts;
-      for (int q = 0; q < 12; ++q) {
-        if (fp32) {
-          const float xx = static_cast<float>(rec[q]);
-          std::memcpy(dst + q * 4, &xx, 4);
-        } else {
-          std::memcpy(dst + q * 8, &rec[q], 8);
-        }
+        for (int d = 0; d < 3; ++d) rec[j][3 * kk + d] = inv[kk][d];
+      rec[j][9] = coef64[12 * e + 9] / 20.0;  // lambda V / 20, mu V / 20: original orientation
+      rec[j][10] = coef64[12 * e + 10] / 20.0;
+      rec[j][11] = 0.0;
+      // consecutive elements share p, q, m and the ring vertex between them
+      if (j > 0) {
+        const int sa[3] = {0, 1, 4};
+        for (int q : sa) bad = bad || sw[j][q] != sw[j - 1][q];
+        bad = bad || sw[j][2] != sw[j - 1][3] || sw[j][6] != sw[j - 1][7] || sw[j][5] != sw[j - 1][8];
       }
     }
+    if (bad) continue;
+    const int nsteps = (k + 1) / 2;
+    for (int st = 0; st < nsteps; ++st) {
+      const int j = 2 * st;
+      const bool single = j + 1 == k, start = st == 0, end = st == nsteps - 1;
+      bool interior = true;
+      for (int q = 0; q < 10; ++q) interior = interior && ((static_cast<uint32_t>(sw[j][q]) >> 28) == 0u);
+      if (!single)
+        for (int q = 0; q < 10; ++q) interior = interior && ((static_cast<uint32_t>(sw[j + 1][q]) >> 28) == 0u);
+      interior_all = interior_all && interior;
+      int32_t* w = wv.data() + kFanWords * size_t(sfirst[fi] + st);
+      for (int q = 0; q < kFanWords; ++q) w[q] = -1;
+      w[0] = (start ? kFanStart : 0) | (end ? kFanEnd : 0) | (fn.closed ? kFanClosed : 0) |
+             (interior ? kFanInterior : 0) | (single ? kFanSingle : 0);
+      w[15] = 0;
+      if (start) {  // p, q, m, r0, mid(p,r0), mid(q,r0)
+        w[1] = sw[0][0]; w[2] = sw[0][1]; w[3] = sw[0][4]; w[4] = sw[0][2]; w[5] = sw[0][6]; w[6] = sw[0][5];
+      }
+      if (!(fn.closed && j + 1 == k)) {  // M = r_{j+1}
+        w[7] = sw[j][3]; w[8] = sw[j][7]; w[9] = sw[j][8];
+      }
+      if (!single && !(fn.closed && j + 2 == k)) {  // B = r_{j+2}
+        w[10] = sw[j + 1][3]; w[11] = sw[j + 1][7]; w[12] = sw[j + 1][8];
+      }
+      w[13] = sw[j][9];
+      if (!single) w[14] = sw[j + 1][9];
+      unsigned char* dst = cf.data() + size_t(sfirst[fi] + st) * 24 * ts;
+      for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 12; ++q) {
+          const double x = (h == 1 && single) ? 0.0 : rec[j + h][q];
+          if (fp32) {
+            const float xx = static_cast<float>(x);
+            std::memcpy(dst + (12 * h + q) * 4, &xx, 4);
+          } else {
+            std::memcpy(dst + (12 * h + q) * 8, &x, 8);
+          }
+        }
+    }
+    (void)interior_all;
   }
   if (bad) validation("fan plan: inconsistent edge fan or degenerate element");
   setup_mark("fan: records");
   auto plan = std::make_unique<EbeFanPlan>();
   plan->n_units = U;
   plan->group_split = split;
-  std::vector<int32_t> uf(size_t(U) + 1);
+  std::vector<int32_t> uf(sfirst.begin(), sfirst.end());
   int64_t closed_elems = 0;
-  for (int32_t i = 0; i < U; ++i) {
-    uf[i] = fans[i].first;
+  for (int32_t i = 0; i < U; ++i)
     if (fans[i].closed) closed_elems += fans[i].k;
-  }
-  uf[U] = static_cast<int32_t>(E);
   plan->closed_fraction = E ? double(closed_elems) / double(E) : 0.0;
   plan->mean_k = U ? double(E) / double(U) : 0.0;
   int64_t rows = 0;

@@ -57,26 +57,26 @@ struct UnitRows {
 UnitRows unit_rows(const ts_ebe& op) {
   UnitRows R;
   if (op.fan) {
-    const int32_t U = op.fan->n_units, E = op.n_elems;
-    constexpr int kW = 12;  // ebe_fan.cu record width
-    std::vector<int32_t> uf(size_t(U) + 1), wv(size_t(E) * kW);
+    constexpr int kW = 16;  // ebe_fan.cu step record width
+    const int32_t U = op.fan->n_units;
+    std::vector<int32_t> uf(size_t(U) + 1);
     TS_CUDA(cudaMemcpy(uf.data(), op.fan->ufirst.get(), uf.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> wv(size_t(uf[U]) * kW);
     TS_CUDA(cudaMemcpy(wv.data(), op.fan->words.get(), wv.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
     R.ptr.assign(1, 0);
     for (int32_t i = 0; i < U; ++i) {
       int32_t lo = INT32_MAX;
       for (int32_t x = uf[i]; x < uf[i + 1]; ++x) {
         const int32_t* w = wv.data() + kW * size_t(x);
-        const bool start = (w[0] & 1) != 0;
-        const int n = start ? 10 : 4;
-        for (int q = 1; q <= n; ++q) {
+        for (int q = 1; q < 15; ++q) {
           const int32_t v = w[q];
           if (v == -1) continue;
           if ((static_cast<uint32_t>(v) >> 28) == 7u) continue;
           R.rows.push_back(v & 0x0FFFFFFF);
         }
         if (x == uf[i])  // p, q, r0, r1 are the first element's vertices
-          for (int q : {1, 2, 4, 7}) lo = std::min(lo, w[q] & 0x0FFFFFFF);
+          for (int q : {1, 2, 4, 7})
+            if (w[q] != -1) lo = std::min(lo, w[q] & 0x0FFFFFFF);
       }
       R.lo.push_back(lo);
       R.ptr.push_back(static_cast<int64_t>(R.rows.size()));
