@@ -662,21 +662,26 @@ def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps):
     sync()
     t_setup = time.perf_counter() - t0
     n = dl.n_local
-    g = torch.Generator(device="cuda").manual_seed(31)  # same cases on every rank
-    amp = 0.05 * (1 + 0.2 * (torch.rand(r, device="cuda", dtype=torch.float64, generator=g) * 2 - 1))
-    ky = 1.0 + (torch.rand(r, device="cuda", dtype=torch.float64, generator=g) > 0.5).double()
-    X, Y, Z = [xyz[:, k:k + 1] / ext[k] for k in range(3)]
-    sz = torch.sin(0.5 * torch.pi * Z)
-    us = torch.stack([amp * torch.sin(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz,
-                      amp * torch.cos(torch.pi * X) * torch.sin(ky * torch.pi * Y) * sz,
-                      amp * torch.cos(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz], 1).reshape(3 * n, r)
-    us = us.contiguous()
-    us[mask] = 0
-    del X, Y, Z, sz, xyz
+
+    def manufactured_local():  # acceptance_main.cpp:82-102 fields at this rank's nodes (same cases everywhere)
+        g = torch.Generator(device="cuda").manual_seed(31)
+        amp = 0.05 * (1 + 0.2 * (torch.rand(r, device="cuda", dtype=torch.float64, generator=g) * 2 - 1))
+        ky = 1.0 + (torch.rand(r, device="cuda", dtype=torch.float64, generator=g) > 0.5).double()
+        X, Y, Z = [xyz[:, k:k + 1] / ext[k] for k in range(3)]
+        sz = torch.sin(0.5 * torch.pi * Z)
+        v = torch.stack([amp * torch.sin(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz,
+                         amp * torch.cos(torch.pi * X) * torch.sin(ky * torch.pi * Y) * sz,
+                         amp * torch.cos(torch.pi * X) * torch.cos(ky * torch.pi * Y) * sz], 1).reshape(3 * n, r)
+        v = v.contiguous()
+        v[mask] = 0
+        return v
+
+    us = manufactured_local()
     f = torch.empty_like(us)
     dl.apply(0, us, f)
     # the partitioned level-0 sweep (fp32, halo exchange overlapped with the interior elements)
     u32 = us.float()
+    del us  # regenerated after the solve (device memory: at configs[3] / 2 ranks every fp64 batch is 13 GB)
     f32 = torch.empty_like(u32)
     for _ in range(3):
         dl.apply(1, u32, f32)
@@ -700,8 +705,10 @@ def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps):
     b.record()
     sync()
     solve_s = a.elapsed_time(b) / 1e3
-    err2 = torch.tensor([float(((u - us) ** 2)[~mask].sum()), float((us ** 2)[~mask].sum())], dtype=torch.float64)
     free, total = torch.cuda.mem_get_info()
+    del f
+    us = manufactured_local()
+    err2 = torch.tensor([float(((u - us) ** 2)[~mask].sum()), float((us ** 2)[~mask].sum())], dtype=torch.float64)
     return {"rank": rank, "n_local": n, "elements": info["elements"], "halo_rows0": info["halo_rows0"],
             "neighbours": info["neighbours"], "n2": dl.n2, "levels_setup_s": info["setup_s"], "mesh_s": t_mesh,
             "setup_s": t_setup, "l0_ms": l0_ms, "solve_s": solve_s, "outer": rep.outer_iterations,
