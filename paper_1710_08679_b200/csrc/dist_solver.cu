@@ -232,6 +232,12 @@ struct ts_dist_levels {
   tsg::DevBuf<uint8_t> mask0, mask1, mask2, owned0;
   tsg::DistVecs v;
   bool l2_dist = false;  // TSGPU_DIST_L2=distributed: level 2 split by coarse rows (else replicated)
+  // level 1 as this partition's assembled K1 (fp32 blocks from its own elements; interface rows then
+  // summed by the level-1 halo exchange), like the single-device hierarchy; TSGPU_L1=ebe keeps the
+  // element-by-element tet4 operator
+  bool l1_assembled = true;
+  tsg::DevBuf<int32_t> l1a_row_ptr, l1a_col_idx;
+  tsg::DevBuf<float> l1a_blocks;
   tsg::Level2Dist l2d;
   tsg::ColScalars cs;
   tsg::Workspace ws;
@@ -259,6 +265,16 @@ void dist_ensure_vecs(ts_dist_levels& L, int32_t B) {
   v.batch = B;
   L.cs.ensure(B);
   L.ws.ensure(B);
+}
+
+// level-1 product of a partition: assembled rows + interface sums, or the element sweep
+void dist_l1_apply(ts_dist_levels& L, const float* x, float* y, int32_t B, cudaStream_t s, bool init) {
+  if (L.l1_assembled) {
+    bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s);
+    L.l1.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, s);
+  } else {
+    L.l1.apply<float>(x, y, B, s, init);
+  }
 }
 
 // apply_multigrid_preconditioner (adaptive_cg.hpp:80-120) on a partition
@@ -321,10 +337,10 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
   L.ws.comm = L.comm;
   L.ws.owned = L.owned0.get();  // the vertex prefix of the level-0 flags
   p2_apply(v.u2.get(), v.u1.get(), L.agg.get(), L.n1, L.mask1.get(), B, s);
-  auto a1 = [&](const float* x, float* y, bool init) { L.l1.apply<float>(x, y, B, s, init); };
+  auto a1 = [&](const float* x, float* y, bool init) { dist_l1_apply(L, x, y, B, s, init); };
   const InnerStats s1 = inner_pcg<float>(a1, L.m1.get(), v.r1.get(), v.u1.get(), L.n1, B, cfg.level_tol[1],
                                          cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), L.cs, L.ws, s,
-                                         true, L.mask1.get());
+                                         !L.l1_assembled, L.mask1.get());
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), L.p1_ends.get(), L.n1, L.n0, L.mask0.get(), B, s);
   auto a0 = [&](const float* x, float* y, bool init) { L.l0.apply<float>(x, y, B, s, init); };
@@ -596,6 +612,17 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
     bj_invert(d1.get(), L->mask1.get(), L->n1, 32, L->m1.get(), s);
     for (ts_ebe* op : {L->l0.op.get(), L->l1.op.get(), L->outer.op.get()}) HostVec<double>().swap(op->coef64);
   }
+  if (const char* e = std::getenv("TSGPU_L1")) L->l1_assembled = std::string(e) != "ebe";
+  if (L->l1_assembled) {  // this partition's K1 (float-rounded inputs, ebe_operator.hpp:54-62)
+    HostVec<float> k1f;
+    const BcsrD k1 = assemble_tet4(P.local, per_element(P.local, n_mat, lam), per_element(P.local, n_mat, mu), mask1,
+                                   &k1f);
+    L->l1a_row_ptr.upload(k1.row_ptr);
+    L->l1a_col_idx.upload(k1.col_idx);
+    L->l1a_blocks.upload(k1f);
+    TS_CUDA(cudaDeviceSynchronize());
+    L->l1.op.reset();  // the element operator only served the block-Jacobi diagonal
+  }
   TS_CUDA(cudaDeviceSynchronize());
   comm->barrier();
   L->setup_s = secs(t0, clk::now());
@@ -635,7 +662,7 @@ void dist_ebe_apply(ts_dist_levels& L, int which, const void* u, void* f, int32_
   TS_CUDA(cudaSetDevice(L.comm->device()));
   if (which == 0) L.outer.apply<double>(static_cast<const double*>(u), static_cast<double*>(f), B, s);
   else if (which == 1) L.l0.apply<float>(static_cast<const float*>(u), static_cast<float*>(f), B, s);
-  else if (which == 2) L.l1.apply<float>(static_cast<const float*>(u), static_cast<float*>(f), B, s);
+  else if (which == 2) dist_l1_apply(L, static_cast<const float*>(u), static_cast<float*>(f), B, s, true);
   else validation("dist apply: operator must be 0 (outer), 1 (level 0) or 2 (level 1)");
 }
 

@@ -175,9 +175,10 @@ class DistLevels:
         l2g = self.local_nodes().astype(np.int64)
         return (3 * l2g[:, None] + np.arange(3)[None, :]).reshape(-1)
 
-    def solve(self, f, u0, cfg: SolverConfig | None = None):
+    def solve(self, f, u0, cfg: SolverConfig | None = None, out=None):
         """solve (adaptive_cg.hpp:242-263) on local (3 n_local, batch) vectors; numpy
-        (host entry) or CUDA float64 tensors (device entry). Returns (u, report)."""
+        (host entry) or CUDA float64 tensors (device entry). Returns (u, report). `out`
+        (device entry): the solution buffer; it may be u0 itself (solved in place)."""
         cfg = cfg or SolverConfig()
         c = cfg.to_c()
         batch = int(f.shape[1])
@@ -187,7 +188,13 @@ class DistLevels:
             import torch
             f = _device_vec(f, rows, torch.float64, "solve")
             u0 = _device_vec(u0, rows, torch.float64, "solve: initial guess", batch)
-            u = torch.empty_like(f)
+            if out is not None:
+                if not (_is_torch(out) and out.shape == f.shape and out.dtype == torch.float64 and out.is_cuda
+                        and out.is_contiguous() and out.device == f.device):
+                    raise ValueError("solve: out must be a contiguous CUDA float64 tensor shaped like f")
+                u = out
+            else:
+                u = torch.empty_like(f)
             rc = lib.ts_dist_solve_device(self._h, C.c_void_p(f.data_ptr()), C.c_void_p(u0.data_ptr()),
                                           C.c_void_p(u.data_ptr()), self.n_local, batch, C.byref(c), C.byref(rb.c),
                                           _stream())
