@@ -33,6 +33,8 @@ explicit flush is needed between steps.
   greens : the Green's-function bank (configs[4] workflow at one-GPU scale):
            48 unit slips on a vertical fault in the configs[1] box, batch 16,
            through ts_greens_bank; total sweep time and time per case.
+  (N > 1: the configs[3] mesh and partition are built once for both partitioned legs;
+           the configs[2] replica solves below run there only with --solve-replicas)
   solve  : BASELINE's other metric, time per case: the full multigrid solve
            (build_crust_model + solve, adaptive_cg.hpp:242-263) of configs[2]
            (50M-DOF 3-layer crust, 16 cases, mixed-precision PCG) through the
@@ -516,32 +518,35 @@ def main_partitioned(args, world, rank, local):
     halo_bytes = int(op.halo_rows) * 3 * r * s
     del u, f, ud, fd, uh, fh, op
     torch.cuda.empty_cache()
+    def sync():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    cells_ns = (tuple(args.northstar_cells) if args.northstar_cells
+                else NORTHSTAR_CELLS if world > 1 else tuple(args.solve_cells))
+    cells_g = (tuple(args.greens_cells) if args.greens_cells
+               else NORTHSTAR_CELLS if world > 1 else tuple(args.cells))
+    # the configs[3] mesh and its partition are built once for both legs when they share it
+    shared = (crust_mesh(ts, cells_ns, world)
+              if not args.no_northstar and not args.no_greens_partitioned and cells_ns == cells_g else None)
     northstar = None
     if not args.no_northstar:  # BASELINE configs[3]: the partitioned 400M-DOF solve, r = 8, on these N GPUs
-        def sync():
-            torch.cuda.synchronize()
-            dist.barrier()
-        cells_ns = (tuple(args.northstar_cells) if args.northstar_cells
-                    else NORTHSTAR_CELLS if world > 1 else tuple(args.solve_cells))
-        mine = northstar_rank(ts, torch, cells_ns, args.northstar_cases, comm, rank, world, sync, args.steps)
+        mine = northstar_rank(ts, torch, cells_ns, args.northstar_cases, comm, rank, world, sync, args.steps,
+                              prebuilt=shared)
         allr = [None] * world
         dist.all_gather_object(allr, mine)
         northstar = northstar_summary(allr, cells_ns, args.northstar_cases, world, f"NCCL x{world}", hbm_peak()[0])
         torch.cuda.empty_cache()
     greens_part = None
     if not args.no_greens_partitioned:  # BASELINE configs[4]: the sweep on the partitioned configs[3] mesh
-        def sync():
-            torch.cuda.synchronize()
-            dist.barrier()
-        cells_g = (tuple(args.greens_cells) if args.greens_cells
-                   else NORTHSTAR_CELLS if world > 1 else tuple(args.cells))
-        mine = greens_dist_rank(ts, torch, cells_g, comm, rank, world, sync, args.greens_cases, 16)
+        mine = greens_dist_rank(ts, torch, cells_g, comm, rank, world, sync, args.greens_cases, 16, prebuilt=shared)
         allr = [None] * world
         dist.all_gather_object(allr, mine)
         greens_part = greens_dist_summary(allr, cells_g, world, f"NCCL x{world}", 16, 368)
         torch.cuda.empty_cache()
+    del shared
     solve = None
-    if not args.no_solve:
+    if not args.no_solve and args.solve_replicas:  # configs[2] replicas (cases batched across the GPUs)
         solve = solve_leg(args, ts, torch, world, rank, local)
     if rank == 0:
         out = {
@@ -633,7 +638,16 @@ FOUR_LAYER = THREE_LAYER + [(8000.0, 4500.0, 3300.0)]  # configs[3]: layered cru
 NORTHSTAR_CELLS = (281, 423, 141)  # configs[3]: 405M DOF (2.8 km cells over 792 x 1192 x 400 km)
 
 
-def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps):
+def crust_mesh(ts, cells, nranks):
+    """The configs[3]-style 4-layer crust box and its RCB partition (every rank builds the same)."""
+    from paper_1710_08679_b200.dist import partition_rcb
+    ext = tuple(c * CELL_KM * 1e3 for c in cells)
+    t0 = time.perf_counter()
+    mesh = ts.generate_box_mesh(ext, cells, (0.2 * ext[2], 0.45 * ext[2], 0.8 * ext[2]))
+    return mesh, partition_rcb(mesh, nranks), time.perf_counter() - t0
+
+
+def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps, prebuilt=None):
     """One rank of the configs[3] workload: build_solver_levels on this rank's RCB
     partition of the global layered-crust mesh (DistLevels: level 2 built once on
     rank 0 and broadcast), manufactured fields (acceptance_main.cpp:82-102) ->
@@ -641,14 +655,12 @@ def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps):
     (fp64 outer, fp32 inner, halo exchange inside every product, all-reduced dots).
     `sync()` is a barrier over the ranks. Returns this rank's numbers."""
     import numpy as np
-    from paper_1710_08679_b200.dist import DistLevels, partition_rcb
+    from paper_1710_08679_b200.dist import DistLevels
 
     ext = tuple(c * CELL_KM * 1e3 for c in cells)
-    ifs = (0.2 * ext[2], 0.45 * ext[2], 0.8 * ext[2])
     t0 = time.perf_counter()
-    mesh = ts.generate_box_mesh(ext, cells, ifs)
-    t_mesh = time.perf_counter() - t0
-    part = partition_rcb(mesh, nranks)
+    prebuilt_given = prebuilt is not None
+    mesh, part, t_mesh = prebuilt if prebuilt_given else crust_mesh(ts, cells, nranks)
     cfg = ts.SolverConfig(batch_size=r)
     mats = [ts.material_from_wavespeeds(*t) for t in FOUR_LAYER]
     dl = DistLevels(mesh, mats, part, comm, cfg)
@@ -658,9 +670,9 @@ def northstar_rank(ts, torch, cells, r, comm, rank, nranks, sync, steps):
     mask = torch.from_numpy(mesh.dirichlet_mask().reshape(-1, 3)[l2g].reshape(-1).copy()).cuda().bool()
     n_glob, e_glob = mesh.node_count(), mesh.element_count()
     dl.mesh = None
-    del mesh, part
+    del mesh, part, prebuilt
     sync()
-    t_setup = time.perf_counter() - t0
+    t_setup = time.perf_counter() - t0 + (t_mesh if prebuilt_given else 0.0)
     n = dl.n_local
 
     g = torch.Generator(device="cuda").manual_seed(31)  # the same cases on every rank
@@ -801,31 +813,30 @@ def northstar_threads(args, ts, torch, cells, r, P):
 
 
 # --------------------------------------- configs[4]: Green's sweep on the partitioned mesh
-def greens_dist_rank(ts, torch, cells, comm, rank, nranks, sync, n_cases, batch):
+def greens_dist_rank(ts, torch, cells, comm, rank, nranks, sync, n_cases, batch, prebuilt=None):
     """One rank of the configs[4] workload: compute_greens_bank (greens.hpp:114-145) of
     n_cases unit slips (dip + strike on a grid of centres on a vertical fault) on the
     partitioned layered-crust mesh, batch r = `batch` per solve (ts_dist_greens_bank:
     slip lifting on the fault band per rank, partitioned solve, owner-rank sampling,
     one all-reduce of the bank). One warm-up batch first; returns this rank's numbers."""
     import numpy as np
-    from paper_1710_08679_b200.dist import DistFaultedModel, partition_rcb
+    from paper_1710_08679_b200.dist import DistFaultedModel
     from paper_1710_08679_b200.greens import DIP, STRIKE, find_plane_fault_faces
 
     ext = tuple(c * CELL_KM * 1e3 for c in cells)
-    ifs = (0.2 * ext[2], 0.45 * ext[2], 0.8 * ext[2])
     h = CELL_KM * 1e3
     xm = (cells[0] // 2) * h
     t0 = time.perf_counter()
-    mesh = ts.generate_box_mesh(ext, cells, ifs)
+    prebuilt_given = prebuilt is not None
+    mesh, part, t_mesh = prebuilt if prebuilt_given else crust_mesh(ts, cells, nranks)
     lo = (xm, 4 * h, 4 * h)
     hi = (xm, (cells[1] - 4) * h, (cells[2] - 8) * h)
     faces = find_plane_fault_faces(mesh, 0, xm, lo, hi)
-    part = partition_rcb(mesh, nranks)
     cfg = ts.SolverConfig(batch_size=batch)
     dfm = DistFaultedModel(mesh, [ts.material_from_wavespeeds(*t) for t in FOUR_LAYER], faces, part, comm, cfg)
-    del mesh, part
+    del mesh, part, prebuilt
     sync()
-    t_setup = time.perf_counter() - t0
+    t_setup = time.perf_counter() - t0 + (t_mesh if prebuilt_given else 0.0)
     nc = n_cases // 2
     ny = max(1, int(round((nc * (hi[1] - lo[1]) / (hi[2] - lo[2])) ** 0.5)))
     nz = max(1, -(-nc // ny))
@@ -923,6 +934,8 @@ def main():
     ap.add_argument("--northstar-l2", default="auto", choices=["auto", "replicated", "distributed"],
                     help="level 2 of the partitioned solve: replicated on every rank, split by coarse rows, "
                          "or auto (split from 4 ranks on)")
+    ap.add_argument("--solve-replicas", action="store_true",
+                    help="N > 1: also run configs[2] solves as independent replicas (one per GPU)")
     ap.add_argument("--no-greens-partitioned", action="store_true",
                     help="N > 1: skip the configs[4] Green's sweep on the partitioned mesh")
     ap.add_argument("--greens-partitioned", type=int, default=0,
