@@ -60,10 +60,14 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+@pytest.mark.parametrize("kernel", ["auto", "fan"])
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("overlap", ["1", "0"])
-def test_partitioned_products_match_single_device(P, overlap, monkeypatch):
+def test_partitioned_products_match_single_device(P, overlap, kernel, monkeypatch):
+    """(kernel: the partitions' element sweeps as face pairs or edge fans; fans never cross the
+    boundary / interior element groups the overlapped exchange relies on)"""
     monkeypatch.setenv("TSGPU_DIST_OVERLAP", overlap)
+    monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
     m = ts.generate_box_mesh(*SPEC)
     mask = m.dirichlet_mask()
     V = m.vertex_count
@@ -121,12 +125,15 @@ def smooth(coords, ext, mask, B, seed):
     return u
 
 
+@pytest.mark.parametrize("kernel", ["auto", "fan"])
 @pytest.mark.parametrize("l2", ["replicated", "distributed"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_partitioned_solve_matches_single_device(P, l2, monkeypatch):
+def test_partitioned_solve_matches_single_device(P, l2, kernel, monkeypatch):
     """Level 2 either replicated on every rank or split by coarse rows with a gather halo in
-    every product (TSGPU_DIST_L2): the same solution and iteration counts either way."""
+    every product (TSGPU_DIST_L2), element sweeps as face pairs or edge fans: the same solution
+    and iteration counts either way."""
     monkeypatch.setenv("TSGPU_DIST_L2", l2)
+    monkeypatch.setenv("TSGPU_EBE_KERNEL", kernel)
     m = ts.generate_box_mesh(*SPEC)
     mask = m.dirichlet_mask()
     B = 3
