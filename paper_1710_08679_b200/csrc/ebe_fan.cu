@@ -320,6 +320,10 @@ k_ebe_fan(const int4* __restrict__ words, const T* __restrict__ coef, const int3
       load_row(h, sv[0]);
       load_row(h + RS, sv[1]);
       load_row(h + 2 * RS, sv[2]);
+      V mv[3][3];  // M rows: element j's B, element j+1's A (loaded once)
+      load_row(rm, mv[0]);
+      load_row(rm + RS, mv[1]);
+      load_row(rm + 2 * RS, mv[2]);
       V FM[3][3];
       {  // element j = (p, q, r_j, r_{j+1}): A = r_j, B = M
         T rec[12];
@@ -341,9 +345,12 @@ k_ebe_fan(const int4* __restrict__ words, const T* __restrict__ coef, const int3
         load_row(ra, uu[2]);
         load_row(ra + RS, uu[6]);
         load_row(ra + 2 * RS, uu[5]);
-        load_row(rm, uu[3]);
-        load_row(rm + RS, uu[7]);
-        load_row(rm + 2 * RS, uu[8]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          uu[3][c] = mv[0][c];
+          uu[7][c] = mv[1][c];
+          uu[8][c] = mv[2][c];
+        }
         load_row(ug + (kEdgeBase + sc.e0) * RS, uu[9]);
         V FE[3];
         tet10_product_acc<0x077u>(uu, b, lp, mp, [&](int s, int c) -> V& {
@@ -375,9 +382,12 @@ k_ebe_fan(const int4* __restrict__ words, const T* __restrict__ coef, const int3
           uu[1][c] = sv[1][c];
           uu[4][c] = sv[2][c];
         }
-        load_row(rm, uu[2]);
-        load_row(rm + RS, uu[6]);
-        load_row(rm + 2 * RS, uu[5]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          uu[2][c] = mv[0][c];
+          uu[6][c] = mv[1][c];
+          uu[5][c] = mv[2][c];
+        }
         load_row(rb, uu[3]);
         load_row(rb + RS, uu[7]);
         load_row(rb + 2 * RS, uu[8]);
