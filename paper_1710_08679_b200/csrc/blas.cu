@@ -545,12 +545,13 @@ __global__ void k_bcsr(const int32_t* __restrict__ row_ptr, const int32_t* __res
 template <int W, typename ACC>
 __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                             const float* __restrict__ blocks, int32_t n, const float* __restrict__ u,
-                            float* __restrict__ f, int32_t B) {
+                            float* __restrict__ f, int32_t B, const int32_t* __restrict__ rows) {
   const int qpr = B / W;
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t r = t / qpr;
-  if (r >= n) return;
-  const int b0 = static_cast<int>(t - r * qpr) * W;
+  const int64_t k = t / qpr;
+  if (k >= n) return;
+  const int b0 = static_cast<int>(t - k * qpr) * W;
+  const int64_t r = rows ? int64_t(__ldg(rows + k)) : k;  // rows (nullable): a subset of the rows, in this order
   ACC acc[3][W];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -883,13 +884,14 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
                     float* f, int32_t B, cudaStream_t s) {
   // fp64 row sums as the reference; W cases of a block row per thread, 16-byte u packs
   TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W, double><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
-                                   row_ptr, col_idx, blocks, n, u, f, B)));
+                                   row_ptr, col_idx, blocks, n, u, f, B, nullptr)));
   TS_CUDA_LAUNCH();
 }
 void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
-                   float* f, int32_t B, cudaStream_t s) {
+                   float* f, int32_t B, cudaStream_t s, const int32_t* rows) {
+  if (n <= 0) return;
   TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W, float><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
-                                   row_ptr, col_idx, blocks, n, u, f, B)));
+                                   row_ptr, col_idx, blocks, n, u, f, B, rows)));
   TS_CUDA_LAUNCH();
 }
 void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s) {

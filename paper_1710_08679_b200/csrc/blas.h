@@ -110,8 +110,9 @@ void bj_apply(const T* inv, const T* r, T* z, int32_t n_nodes, int32_t batch, cu
 void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
                     const float* u, float* f, int32_t batch, cudaStream_t s);
 // the assembled level-1 operator (fp32 blocks, fp32 accumulation): y = K1 x
+// rows (nullable): apply only these n rows (row ids) instead of rows [0, n)
 void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
-                   float* f, int32_t batch, cudaStream_t s);
+                   float* f, int32_t batch, cudaStream_t s, const int32_t* rows = nullptr);
 // casts (cast_batch, vector_batch.hpp:43-49)
 void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s);
 void cast_f2d(const float* x, double* y, int64_t n, cudaStream_t s);

@@ -238,6 +238,8 @@ struct ts_dist_levels {
   bool l1_assembled = true;
   tsg::DevBuf<int32_t> l1a_row_ptr, l1a_col_idx;
   tsg::DevBuf<float> l1a_blocks;
+  tsg::DevBuf<int32_t> l1a_iface, l1a_inner;  // rows of interface vertices / the rest (overlap split)
+  int32_t n_l1_iface = 0, n_l1_inner = 0;
   tsg::Level2Dist l2d;
   tsg::ColScalars cs;
   tsg::Workspace ws;
@@ -270,8 +272,27 @@ void dist_ensure_vecs(ts_dist_levels& L, int32_t B) {
 // level-1 product of a partition: assembled rows + interface sums, or the element sweep
 void dist_l1_apply(ts_dist_levels& L, const float* x, float* y, int32_t B, cudaStream_t s, bool init) {
   if (L.l1_assembled) {
-    bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s);
-    L.l1.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, s);
+    DistEbe& D = L.l1;  // its halo, side stream and events
+    if (!D.overlap || D.halo.nbr.empty()) {
+      bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s);
+      D.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, s);
+      return;
+    }
+    // interface rows first; their partial sums travel while the interior rows are computed
+    bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n_l1_iface, x, y, B, s,
+                  L.l1a_iface.get());
+    if (!D.side) {
+      TS_CUDA(cudaStreamCreateWithFlags(&D.side, cudaStreamNonBlocking));
+      TS_CUDA(cudaEventCreateWithFlags(&D.ev_b, cudaEventDisableTiming));
+      TS_CUDA(cudaEventCreateWithFlags(&D.ev_h, cudaEventDisableTiming));
+    }
+    TS_CUDA(cudaEventRecord(D.ev_b, s));
+    TS_CUDA(cudaStreamWaitEvent(D.side, D.ev_b, 0));
+    D.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, D.side);
+    TS_CUDA(cudaEventRecord(D.ev_h, D.side));
+    bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n_l1_inner, x, y, B, s,
+                  L.l1a_inner.get());
+    TS_CUDA(cudaStreamWaitEvent(s, D.ev_h, 0));
   } else {
     L.l1.apply<float>(x, y, B, s, init);
   }
@@ -620,6 +641,16 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
     L->l1a_row_ptr.upload(k1.row_ptr);
     L->l1a_col_idx.upload(k1.col_idx);
     L->l1a_blocks.upload(k1f);
+    {  // rows of the level-1 interface vertices (exchanged) and the rest (computed under the exchange)
+      std::vector<uint8_t> iface(L->n1, 0);
+      for (int32_t v : P.halo1.sh_nodes) iface[v] = 1;
+      std::vector<int32_t> ri, rn;
+      for (int32_t v = 0; v < L->n1; ++v) (iface[v] ? ri : rn).push_back(v);
+      L->n_l1_iface = static_cast<int32_t>(ri.size());
+      L->n_l1_inner = static_cast<int32_t>(rn.size());
+      L->l1a_iface.upload(ri);
+      L->l1a_inner.upload(rn);
+    }
     TS_CUDA(cudaDeviceSynchronize());
     L->l1.op.reset();  // the element operator only served the block-Jacobi diagonal
   }
