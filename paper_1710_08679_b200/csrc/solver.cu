@@ -55,6 +55,7 @@ struct ts_levels {
   ColScalars cs;
   tsg::Workspace ws;
   std::mutex mu;
+  DevBuf<double> host_f, host_u;  // staging of the host-buffer entry, kept across calls (no per-call cudaMalloc)
 };
 
 namespace tsg {
@@ -447,7 +448,10 @@ ts_status ts_solve(ts_levels* lv, const double* f, const double* u0, double* u_o
   ts_solve_report& r = rep ? *rep : local;
   std::lock_guard<std::mutex> lock(lv->mu);
   const size_t bytes = 3 * size_t(lv->n0) * batch * sizeof(double);
-  DevBuf<double> df(bytes / 8), du(bytes / 8);
+  DevBuf<double>& df = lv->host_f;
+  DevBuf<double>& du = lv->host_u;
+  df.ensure(bytes / 8);
+  du.ensure(bytes / 8);
   cudaStream_t s = nullptr;
   TS_CUDA(cudaMemcpyAsync(df.get(), f, bytes, cudaMemcpyHostToDevice, s));
   TS_CUDA(cudaMemcpyAsync(du.get(), u0, bytes, cudaMemcpyHostToDevice, s));
