@@ -850,7 +850,7 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   if (kernel_override >= 0) op->kernel = kernel_override;
   else if (const char* k = std::getenv("TSGPU_EBE_KERNEL"))
     op->kernel = std::string(k) == "pipe" ? 2 : std::string(k) == "fast" ? 3 : std::string(k) == "pair" ? 7
-               : std::string(k) == "fan" ? 8 : std::string(k) == "fantile" ? 9 : 6;
+               : std::string(k) == "fan" ? 8 : 6;
   const char* kenv = std::getenv("TSGPU_EBE_KERNEL");
   const bool colored = kernel_override < 0 && kenv && std::string(kenv) == "color";
   {
@@ -874,10 +874,10 @@ ts_ebe* ebe_create(const Mesh& m, int order, int32_t n_mat, const double* lambda
   setup_mark("ebe: conn3");
   // face pairs by default; edge fans (tet10) on request (TSGPU_EBE_KERNEL=fan; measured in
   // faster at r = 1, slower at r >= 4 on the FP-latency-bound sweep)
-  const bool fans = order == 2 && (op->kernel == 8 || op->kernel == 9);
+  const bool fans = order == 2 && op->kernel == 8;
   if (fans) build_fan_plan(*op, m, conn, cs, op->coef64, prec == 32);
   setup_mark("ebe: fan plan");
-  if (!fans && (op->kernel == 7 || op->kernel == 6 || op->kernel == 8 || op->kernel == 9))  // (tet4 under "fan": pairs)
+  if (!fans && (op->kernel == 7 || op->kernel == 6 || op->kernel == 8))  // (tet4 under "fan": pairs)
     build_pair_plan(*op, m, conn, cs, op->coef64, prec == 32, pair_topology);
   setup_mark("ebe: pair plan");
   op->conn.upload(conn);

@@ -40,13 +40,6 @@ struct EbeFanPlan {
   tsg::DevBuf<int32_t> words;     // [steps][16]: flags, the rows a step (two elements) adds (node | mask << 28)
   tsg::DevBuf<unsigned char> coef;  // [steps][24] of T: the step's two slot-order coefficient records
   tsg::DevBuf<int32_t> ufirst;    // [U + 1] first step of each fan
-  // tiled fans (kernel 9): consecutive fans whose node rows, step words and records a block stages at once
-  int32_t n_tiles = 0, tile_split = 0;  // tiles [0, split) cover element group 0
-  double tile_rows_per_element = 0.0;   // staged node rows per element
-  tsg::DevBuf<int32_t> tile_meta;      // [tiles][8]: row begin, rows, step begin, steps, fan begin, fans, 0, 0
-  tsg::DevBuf<int32_t> tile_rows;       // node words (node | mask << 28) of each tile's rows, tile-local order
-  tsg::DevBuf<double> tile_zero;        // 256 zero bytes: the source of constrained row components
-  tsg::DevBuf<int32_t> tile_words;      // [steps][16]: the step words with tile-local row indices
 };
 
 // Elements sweep in slabs of their lowest vertex id (then Morton order), ebe.cu;

@@ -31,7 +31,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
-#include <unordered_map>
 #include <vector>
 
 #include "ebe.h"
@@ -446,379 +445,6 @@ k_ebe_fan(const int4* __restrict__ words, const T* __restrict__ coef, const int3
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// ---------------------------------------------------------------------------------------------
-// Tiled fans (kernel 9): a thread block stages a TILE — up to kTileFans consecutive fans of the
-// fan order (spatially compact: the fan order follows the Morton sweep order) — into shared
-// memory in one go: the union of their node rows (≈ 2.1 rows per element on the box meshes
-// instead of the fan sweep's 4.5), their step words (row references as tile-local indices) and
-// coefficient records. Each lane group then runs its fans' element products from shared memory
-// alone (no per-step gather pipeline); the scatter stays the fan sweep's (each row reduced once
-// per fan). Two resident blocks per SM overlap one's staging with the other's products.
-template <typename T>
-struct TileCaps;
-template <> struct TileCaps<float> {
-  static constexpr int kRows = 416, kFans = 32, kSteps = 128;
-};
-template <> struct TileCaps<double> {
-  static constexpr int kRows = 208, kFans = 16, kSteps = 64;
-};
-
-template <typename T, int B>
-constexpr size_t fantile_buf_bytes() {  // one tile's rows, step words, records and fan step offsets
-  using Cap = TileCaps<T>;
-  return size_t(Cap::kRows) * 3 * B * sizeof(T) + size_t(Cap::kSteps) * 64 + size_t(Cap::kSteps) * 24 * sizeof(T) +
-         size_t(Cap::kFans + 4) * 4;
-}
-template <typename T>
-constexpr size_t fantile_word_bytes() {  // one tile's node words
-  return size_t(TileCaps<T>::kRows) * 4;
-}
-
-// Pipeline per block (tiles t, t + G, t + 2G, ... of its stride): while tile t is computed from
-// row buffer t&1, tile t+G's rows stream into the other row buffer (addressed through its node
-// words, already in shared memory) and tile t+2G's node words into the third word buffer; one
-// barrier per tile. Tile metadata: int4 pair {row begin, rows, step begin, steps}, {fan begin,
-// fans, 0, 0}.
-template <typename T, typename V, int B>
-__global__ void __launch_bounds__(256, 1)
-k_ebe_fantile(const int4* __restrict__ tile_meta, const int32_t* __restrict__ tile_rows,
-              const int32_t* __restrict__ ufirst, const int4* __restrict__ twords, const T* __restrict__ coef,
-              const T* __restrict__ zero, int32_t t0, int32_t t1, const T* __restrict__ u, T* __restrict__ f) {
-  using O = LaneOps<V>;
-  using Cap = TileCaps<T>;
-  constexpr int CPT = O::kCols;
-  constexpr int TPE = (B + CPT - 1) / CPT;
-  constexpr int NT = 256;
-  static_assert(NT % TPE == 0 && TPE * CPT == B, "lane groups must tile the block and the batch");
-  constexpr int GROUPS = NT / TPE;
-  constexpr int RW = 3 * B;                              // scalars per node row
-  constexpr int CH = RW * int(sizeof(T)) / 16;           // 16-byte chunks per row
-  static_assert(RW * sizeof(T) % 16 == 0, "rows must be whole 16-byte chunks");
-  constexpr int CCH = 24 * int(sizeof(T)) / 16;          // 16-byte chunks per step record pair
-  constexpr size_t kBuf = fantile_buf_bytes<T, B>();
-  constexpr size_t kWBuf = fantile_word_bytes<T>();
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int grp = threadIdx.x / TPE;
-  const int lane = threadIdx.x % TPE;
-  const int col = lane * CPT;
-  T* const fb = f + col;
-  auto rows_of = [&](int b) { return reinterpret_cast<T*>(smem + b * kBuf); };
-  auto sw_of = [&](int b) { return reinterpret_cast<int4*>(rows_of(b) + size_t(Cap::kRows) * RW); };
-  auto sc_of = [&](int b) { return reinterpret_cast<T*>(sw_of(b) + 4 * Cap::kSteps); };
-  auto fo_of = [&](int b) { return reinterpret_cast<int32_t*>(sc_of(b) + 24 * Cap::kSteps); };
-  auto wrow_of = [&](int k) { return reinterpret_cast<int32_t*>(smem + 2 * kBuf + k * kWBuf); };
-
-  auto meta = [&](int32_t t, int4& m0, int4& m1) {
-    if (t < t1) {
-      m0 = __ldg(tile_meta + 2 * size_t(t));
-      m1 = __ldg(tile_meta + 2 * size_t(t) + 1);
-    } else {
-      m0 = m1 = make_int4(0, 0, 0, 0);
-    }
-  };
-  auto stage_words = [&](const int4& m0, int k) {
-    int32_t* const wr = wrow_of(k);
-    for (int32_t i = threadIdx.x; i < m0.y; i += NT) cpa(wr + i, tile_rows + m0.x + i, 4, 4);
-  };
-  uint64_t* const mbar = reinterpret_cast<uint64_t*>(smem + 2 * kBuf + 3 * kWBuf);  // row buffers' barriers
-  auto sa = [](const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); };
-  // rows: one bulk copy per row (per component for rows with constrained components, whose
-  // masked components come from the zero page), completing on the buffer's mbarrier
-  auto stage_tile = [&](const int4& m0, const int4& m1, int b, int k) {
-    const int32_t* const wr = wrow_of(k);
-    T* const ut = rows_of(b);
-    const int32_t nr = m0.y, sb = m0.z, ns = m0.w;
-    const unsigned mb = sa(mbar + b);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (threadIdx.x == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
-                   "r"(static_cast<unsigned>(nr * RW * sizeof(T)))
-                   : "memory");
-    for (int32_t r = threadIdx.x; r < nr; r += NT) {
-      const int32_t w = wr[r];
-      const unsigned mk = static_cast<unsigned>(w) >> 28;
-      const T* src = u + static_cast<size_t>(static_cast<uint32_t>(w) & 0x0FFFFFFFu) * RW;
-      T* dst = ut + size_t(r) * RW;
-      if (mk == 0u) {
-        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         sa(dst)),
-                     "l"(src), "r"(static_cast<unsigned>(RW * sizeof(T))), "r"(mb)
-                     : "memory");
-      } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           sa(dst + c * B)),
-                       "l"(((mk >> c) & 1u) ? zero : src + c * B), "r"(static_cast<unsigned>(B * sizeof(T))), "r"(mb)
-                       : "memory");
-      }
-    }
-    int4* const sw = sw_of(b);
-    for (int32_t i = threadIdx.x; i < ns * 4; i += NT) cpa(sw + i, twords + 4 * size_t(sb) + i, 16, 16);
-    unsigned char* const sc = reinterpret_cast<unsigned char*>(sc_of(b));
-    for (int32_t i = threadIdx.x; i < ns * CCH; i += NT)
-      cpa(sc + 16 * size_t(i), reinterpret_cast<const unsigned char*>(coef + 24 * size_t(sb)) + 16 * size_t(i), 16,
-          16);
-    int32_t* const fo = fo_of(b);
-    for (int32_t i = threadIdx.x; i <= m1.y; i += NT) cpa(fo + i, ufirst + m1.x + i, 4, 4);
-  };
-
-  const int32_t G = static_cast<int32_t>(gridDim.x);
-  const int32_t tf = t0 + static_cast<int32_t>(blockIdx.x);
-  int4 mc0, mc1, mn0, mn1, mm0, mm1;  // metadata of tiles t, t + G, t + 2G
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(mbar)));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(mbar + 1)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  unsigned ph[2] = {0u, 0u};
-  meta(tf, mc0, mc1);
-  meta(tf + G, mn0, mn1);
-  stage_words(mc0, 0);
-  stage_words(mn0, 1);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  if (tf < t1) stage_tile(mc0, mc1, 0, 0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  int buf = 0, wk = 0;
-  for (int32_t tile = tf; tile < t1; tile += G) {
-    meta(tile + 2 * G, mm0, mm1);
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    {
-      unsigned done = 0;
-      while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
-                     : "=r"(done)
-                     : "r"(sa(mbar + buf)), "r"(ph[buf])
-                     : "memory");
-      ph[buf] ^= 1u;
-    }
-    __syncthreads();  // tile's rows and tile + G's node words have landed; tile - G is done everywhere
-    const int wn = wk == 2 ? 0 : wk + 1, wn2 = wn == 2 ? 0 : wn + 1;
-    if (tile + G < t1) stage_tile(mn0, mn1, buf ^ 1, wn);
-    stage_words(mm0, wn2);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    const T* const ut = rows_of(buf);
-    const int32_t* const wrow = wrow_of(wk);
-    const int4* const sw = sw_of(buf);
-    const T* const sc = sc_of(buf);
-    const int32_t* const fo = fo_of(buf);
-    const int32_t sb = mc0.z, nf = mc1.y;
-
-    auto load3 = [&](int32_t li, V (&r)[3]) {
-      const T* p = ut + size_t(li) * RW + col;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) r[c] = *reinterpret_cast<const V*>(p + c * B);
-    };
-    auto red = [&](auto PL, int32_t li, const V (&v)[3]) {
-      const int32_t w = wrow[li];
-      if constexpr (decltype(PL)::value) {
-        T* dst = fb + static_cast<size_t>(static_cast<uint32_t>(w)) * RW;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) red_lane(reinterpret_cast<V*>(dst + c * B), v[c]);
-      } else {
-        T* dst = fb + static_cast<size_t>(static_cast<uint32_t>(w) & 0x0FFFFFFFu) * RW;
-        const unsigned mk = static_cast<unsigned>(w) >> 28;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) red_p(reinterpret_cast<V*>(dst + c * B), v[c], (mk >> c) & 1u);
-      }
-    };
-    auto red3 = [&](bool plain, const int32_t (&li)[3], const V (&v)[3][3]) {
-      if (plain) {
-        red(std::true_type{}, li[0], v[0]);
-        red(std::true_type{}, li[1], v[1]);
-        red(std::true_type{}, li[2], v[2]);
-      } else {
-        red(std::false_type{}, li[0], v[0]);
-        red(std::false_type{}, li[1], v[1]);
-        red(std::false_type{}, li[2], v[2]);
-      }
-    };
-    auto red1 = [&](bool plain, int32_t li, const V (&v)[3]) {
-      if (plain) red(std::true_type{}, li, v);
-      else red(std::false_type{}, li, v);
-    };
-
-    for (int32_t fan = grp; fan < nf; fan += GROUPS) {
-      const int32_t s0 = fo[fan] - sb, s1 = fo[fan + 1] - sb;
-      int32_t hw[6] = {0, 0, 0, 0, 0, 0}, aw[3] = {0, 0, 0};
-      V S[3][3], FA[3][3], R0[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) S[i][c] = FA[i][c] = R0[i][c] = O::zero();
-      for (int32_t ls = s0; ls < s1; ++ls) {
-        const int4* w = sw + 4 * ls;
-        const int4 w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3];
-        const int32_t fl = w0.x;
-        const bool start = (fl & kFanStart) != 0, end = (fl & kFanEnd) != 0, closed = (fl & kFanClosed) != 0,
-                   single = (fl & kFanSingle) != 0, plain = (fl & kFanInterior) != 0;
-        if (start) {
-          hw[0] = w0.y; hw[1] = w0.z; hw[2] = w0.w; hw[3] = w1.x; hw[4] = w1.y; hw[5] = w1.z;
-          aw[0] = w1.x; aw[1] = w1.y; aw[2] = w1.z;
-        }
-        const int32_t mw[3] = {w1.w != -1 ? w1.w : hw[3], w1.w != -1 ? w2.x : hw[4], w1.w != -1 ? w2.y : hw[5]};
-        V sv[3][3], mv[3][3];
-        load3(hw[0], sv[0]);
-        load3(hw[1], sv[1]);
-        load3(hw[2], sv[2]);
-        load3(mw[0], mv[0]);
-        load3(mw[1], mv[1]);
-        load3(mw[2], mv[2]);
-        V FM[3][3];
-        {  // element j = (p, q, r_j, r_{j+1}): A = r_j, B = M
-          T rec[12];
-          load_rec(sc + 24 * ls, rec);
-          V b[3][3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
-          const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
-          V uu[10][3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            uu[0][c] = sv[0][c];
-            uu[1][c] = sv[1][c];
-            uu[4][c] = sv[2][c];
-            uu[3][c] = mv[0][c];
-            uu[7][c] = mv[1][c];
-            uu[8][c] = mv[2][c];
-          }
-          load3(aw[0], uu[2]);
-          load3(aw[1], uu[6]);
-          load3(aw[2], uu[5]);
-          load3(w3.y, uu[9]);
-          V FE[3];
-          tet10_product_acc<0x077u>(uu, b, lp, mp, [&](int s, int c) -> V& {
-            return s == 0 ? S[0][c] : s == 1 ? S[1][c] : s == 4 ? S[2][c] : s == 2 ? FA[0][c] : s == 6 ? FA[1][c]
-                 : s == 5 ? FA[2][c] : s == 3 ? FM[0][c] : s == 7 ? FM[1][c] : s == 8 ? FM[2][c] : FE[c];
-          });
-          if (start && closed) {  // r_0 of a closed fan: kept until its last element
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-              for (int c = 0; c < 3; ++c) R0[i][c] = FA[i][c];
-          } else {
-            red3(plain, aw, FA);
-          }
-          red1(plain, w3.y, FE);
-        }
-        if (!single) {  // element j+1 = (p, q, r_{j+1}, r_{j+2}): A = M, B (into FA's registers)
-          T rec[12];
-          load_rec(sc + 24 * ls + 12, rec);
-          V b[3][3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) b[k][d] = O::splat(rec[3 * k + d]);
-          const V lp = O::splat(rec[9]), mp = O::splat(rec[10]);
-          const int32_t bw[3] = {w2.z != -1 ? w2.z : hw[3], w2.z != -1 ? w2.w : hw[4], w2.z != -1 ? w3.x : hw[5]};
-          V uu[10][3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            uu[0][c] = sv[0][c];
-            uu[1][c] = sv[1][c];
-            uu[4][c] = sv[2][c];
-            uu[2][c] = mv[0][c];
-            uu[6][c] = mv[1][c];
-            uu[5][c] = mv[2][c];
-          }
-          load3(bw[0], uu[3]);
-          load3(bw[1], uu[7]);
-          load3(bw[2], uu[8]);
-          load3(w3.z, uu[9]);
-          V FE[3];
-          tet10_product_acc<0x077u>(uu, b, lp, mp, [&](int s, int c) -> V& {
-            return s == 0 ? S[0][c] : s == 1 ? S[1][c] : s == 4 ? S[2][c] : s == 2 ? FM[0][c] : s == 6 ? FM[1][c]
-                 : s == 5 ? FM[2][c] : s == 3 ? FA[0][c] : s == 7 ? FA[1][c] : s == 8 ? FA[2][c] : FE[c];
-          });
-          red3(plain, mw, FM);
-          red1(plain, w3.z, FE);
-          if (end) {
-            if (closed)
-#pragma unroll
-              for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) FA[i][c] = O::add(FA[i][c], R0[i][c]);
-            red3(plain, bw, FA);
-          } else {
-            aw[0] = bw[0]; aw[1] = bw[1]; aw[2] = bw[2];
-          }
-        } else {  // a fan's odd last element: its B = M is the fan's last ring vertex (r_0 if closed)
-          if (closed)
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-              for (int c = 0; c < 3; ++c) FM[i][c] = O::add(FM[i][c], R0[i][c]);
-          red3(plain, mw, FM);
-        }
-        if (end) {
-          const int32_t s3[3] = {hw[0], hw[1], hw[2]};
-          red3(plain, s3, S);
-        }
-      }
-    }
-    mc0 = mn0; mc1 = mn1; mn0 = mm0; mn1 = mm1;
-    buf ^= 1;
-    wk = wn;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
-template <typename T, typename V, int B>
-size_t fantile_smem() {
-  return 2 * fantile_buf_bytes<T, B>() + 3 * fantile_word_bytes<T>() + 16;
-}
-
-template <typename T, typename V, int B>
-bool launch_fantile_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t t0, int32_t t1, int* launches) {
-  constexpr int CPT = LaneOps<V>::kCols;
-  constexpr int TPE = (B + CPT - 1) / CPT;
-  if constexpr (256 % TPE != 0 || TPE * CPT != B || (3 * B * sizeof(T)) % 16 != 0) {
-    return false;
-  } else {
-    const size_t smem = fantile_smem<T, V, B>();
-    const KernelFit fit = kernel_fit<k_ebe_fantile<T, V, B>>(256, smem);
-    if (t1 <= t0) return true;
-    const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(int64_t(t1) - t0, int64_t(fit.sms) * std::max(fit.per_sm, 1))));
-    if (launches) {
-      ++*launches;
-      return true;
-    }
-    const EbeFanPlan& P = *op.fan;
-    k_ebe_fantile<T, V, B><<<grid, 256, smem, s>>>(reinterpret_cast<const int4*>(P.tile_meta.get()), P.tile_rows.get(),
-                                                   P.ufirst.get(), reinterpret_cast<const int4*>(P.tile_words.get()),
-                                                   reinterpret_cast<const T*>(P.coef.get()),
-                                                   reinterpret_cast<const T*>(P.tile_zero.get()), t0, t1, u, f);
-    TS_CUDA_LAUNCH();
-    return true;
-  }
-}
-
-// tiled fans cover the two widths the sweeps are sized for (the tile caps assume them): r = 8, 16
-template <typename T, typename V>
-bool launch_fantile_t(const ts_ebe& op, const T* u, T* f, int32_t batch, cudaStream_t s, int32_t t0, int32_t t1,
-                      int* launches) {
-  switch (batch) {
-    case 8: return launch_fantile_b<T, V, 8>(op, u, f, s, t0, t1, launches);
-    case 16: return launch_fantile_b<T, V, 16>(op, u, f, s, t0, t1, launches);
-    default: return false;
-  }
-}
-
-bool fantile_dispatch(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t t0,
-                      int32_t t1, int* launches) {
-  if (!op.fan || op.fan->n_tiles == 0) return false;
-  if (op.prec == 32)
-    return launch_fantile_t<float, float2>(op, static_cast<const float*>(u), static_cast<float*>(f), batch, s, t0, t1,
-                                           launches);
-  return launch_fantile_t<double, double>(op, static_cast<const double*>(u), static_cast<double*>(f), batch, s, t0,
-                                          t1, launches);
-}
-
 template <typename T, typename V, int B>
 size_t fan_smem() {
   constexpr int CPT = LaneOps<V>::kCols, TPE = (B + CPT - 1) / CPT, NT = 128, GROUPS = NT / TPE;
@@ -894,90 +520,6 @@ bool inv3(const double j[3][3], double inv[3][3]) {
   return true;
 }
 
-// Tiles of consecutive fans (kernel 9): greedy in fan order, closed when the next fan would
-// overflow the row, fan or step capacity, and at the group split (a tile stays in one element
-// group). Row references of a tile's step words become tile-local indices into its staged rows.
-void build_fan_tiles(EbeFanPlan& P, bool fp32, const std::vector<int32_t>& uf, const HostVec<int32_t>& wv,
-                     int32_t split) {
-  const int max_rows = fp32 ? TileCaps<float>::kRows : TileCaps<double>::kRows;
-  const int max_fans = fp32 ? TileCaps<float>::kFans : TileCaps<double>::kFans;
-  const int max_steps = fp32 ? TileCaps<float>::kSteps : TileCaps<double>::kSteps;
-  const int32_t U = static_cast<int32_t>(uf.size()) - 1;
-  std::vector<int32_t> row_ptr{0}, rows, fan_ptr{0};
-  HostVec<int32_t> tw(wv.size());
-  std::unordered_map<int32_t, int32_t> local;  // node -> tile-local row
-  local.reserve(2 * max_rows);
-  std::vector<int32_t> fresh;
-  auto fan_rows = [&](int32_t fi) {  // nodes of fan fi not yet in the tile
-    fresh.clear();
-    for (int32_t st = uf[fi]; st < uf[fi + 1]; ++st)
-      for (int q = 1; q < 15; ++q) {
-        const int32_t w = wv[kFanWords * size_t(st) + q];
-        if (w == -1) continue;
-        const int32_t n = w & 0x0FFFFFFF;
-        if (!local.count(n) && std::find(fresh.begin(), fresh.end(), w) == fresh.end()) fresh.push_back(w);
-      }
-  };
-  int32_t tile_fans = 0, tile_steps = 0, tile_split = -1;
-  auto close_tile = [&]() {
-    if (tile_fans == 0) return;
-    row_ptr.push_back(static_cast<int32_t>(rows.size()));
-    fan_ptr.push_back(fan_ptr.back() + tile_fans);
-    local.clear();
-    tile_fans = tile_steps = 0;
-  };
-  for (int32_t fi = 0; fi < U; ++fi) {
-    if (fi == split) {
-      close_tile();
-      tile_split = static_cast<int32_t>(fan_ptr.size()) - 1;
-    }
-    const int ns = uf[fi + 1] - uf[fi];
-    fan_rows(fi);
-    const int nr = static_cast<int>(rows.size()) - row_ptr.back();
-    if (tile_fans > 0 && (tile_fans == max_fans || tile_steps + ns > max_steps ||
-                          nr + static_cast<int>(fresh.size()) > max_rows)) {
-      close_tile();
-      fan_rows(fi);
-    }
-    if (static_cast<int>(fresh.size()) > max_rows || ns > max_steps) {  // cannot tile (a huge fan)
-      P.n_tiles = 0;
-      return;
-    }
-    for (int32_t w : fresh) {
-      local.emplace(w & 0x0FFFFFFF, static_cast<int32_t>(rows.size()) - row_ptr.back());
-      rows.push_back(w);
-    }
-    for (int32_t st = uf[fi]; st < uf[fi + 1]; ++st) {
-      const int32_t* w = wv.data() + kFanWords * size_t(st);
-      int32_t* o = tw.data() + kFanWords * size_t(st);
-      o[0] = w[0];
-      o[15] = 0;
-      for (int q = 1; q < 15; ++q) o[q] = w[q] == -1 ? -1 : local.at(w[q] & 0x0FFFFFFF);
-    }
-    ++tile_fans;
-    tile_steps += ns;
-  }
-  close_tile();
-  P.n_tiles = static_cast<int32_t>(fan_ptr.size()) - 1;
-  P.tile_split = tile_split < 0 ? P.n_tiles : tile_split;
-  const double E = std::max(1.0, double(P.n_units) * P.mean_k);
-  P.tile_rows_per_element = double(rows.size()) / E;
-  std::vector<int32_t> meta(size_t(P.n_tiles) * 8, 0);
-  for (int32_t t = 0; t < P.n_tiles; ++t) {
-    int32_t* mt = meta.data() + 8 * size_t(t);
-    mt[0] = row_ptr[t];
-    mt[1] = row_ptr[t + 1] - row_ptr[t];
-    mt[2] = uf[fan_ptr[t]];
-    mt[3] = uf[fan_ptr[t + 1]] - uf[fan_ptr[t]];
-    mt[4] = fan_ptr[t];
-    mt[5] = fan_ptr[t + 1] - fan_ptr[t];
-  }
-  P.tile_meta.upload(meta);
-  P.tile_zero.upload(std::vector<double>(32, 0.0));
-  P.tile_rows.upload(rows);
-  P.tile_words.upload(tw);
-}
-
 }  // namespace
 
 bool ebe_fan_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t q0,
@@ -987,11 +529,6 @@ bool ebe_fan_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch
 
 bool ebe_fan_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part) {
   if (!op.fan) return false;
-  if (op.fan->n_tiles > 0) {  // tiled fans for the widths they cover
-    const int32_t t0 = part == 1 ? op.fan->tile_split : 0;
-    const int32_t t1 = part == 0 ? op.fan->tile_split : op.fan->n_tiles;
-    if (fantile_dispatch(op, u, f, batch, s, t0, t1, nullptr)) return true;
-  }
   const int32_t q0 = part == 1 ? op.fan->group_split : 0;
   const int32_t q1 = part == 0 ? op.fan->group_split : op.fan->n_units;
   return fan_dispatch(op, u, f, batch, s, q0, q1, nullptr);
@@ -1000,13 +537,6 @@ bool ebe_fan_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cuda
 int ebe_fan_launches(const ts_ebe& op, int32_t batch) {
   if (!op.fan) return -1;
   int n = 0;
-  if (op.fan->n_tiles > 0) {
-    const int32_t ts = op.fan->tile_split, T = op.fan->n_tiles;
-    if (fantile_dispatch(op, nullptr, nullptr, batch, nullptr, 0, ts, &n)) {
-      fantile_dispatch(op, nullptr, nullptr, batch, nullptr, ts, T, &n);
-      return n;
-    }
-  }
   const int32_t sp = op.fan->group_split, U = op.fan->n_units;
   if (!fan_dispatch(op, nullptr, nullptr, batch, nullptr, 0, sp, &n)) return -1;
   fan_dispatch(op, nullptr, nullptr, batch, nullptr, sp, U, &n);
@@ -1318,7 +848,6 @@ void build_fan_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_word
   int64_t rows = 0;
   for (int32_t i = 0; i < U; ++i) rows += 4 * int64_t(fans[i].k) + (fans[i].closed ? 3 : 6);
   plan->rows_per_element = E ? double(rows) / double(E) : 0.0;
-  if (op.kernel == 9) build_fan_tiles(*plan, fp32, uf, wv, split);
   plan->ufirst.upload(uf);
   plan->words.upload(wv);
   plan->coef.upload(cf);

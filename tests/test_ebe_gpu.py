@@ -41,7 +41,7 @@ CASES = [
 ]
 
 
-KERNELS = ["auto", "pipe", "fast", "color", "pair", "fan", "fantile"]  # TSGPU_EBE_KERNEL: default dispatch, generic and
+KERNELS = ["auto", "pipe", "fast", "color", "pair", "fan"]  # TSGPU_EBE_KERNEL: default dispatch, generic and
 # batch-specialised element-parallel RED sweeps, deterministic colored sweep, face-pair sweep, edge-fan sweep
 
 

@@ -68,7 +68,7 @@ def meshes(checker):
     return scrambled_mesh(checker, (3000.0, 2000.0, 1500.0), (6, 5, 4), 5)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "pipe", "fast", "color", "fan", "fantile"])
+@pytest.mark.parametrize("kernel", ["auto", "pipe", "fast", "color", "fan"])
 @pytest.mark.parametrize("order", [2, 1])
 @pytest.mark.parametrize("prec", [32, 64])
 @pytest.mark.parametrize("batch", [1, 4, 16, 3])
