@@ -3,6 +3,7 @@
 #pragma once
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -27,6 +28,8 @@ struct EbePairPlan {
   double paired_fraction = 0.0;  // elements that are in a pair
   tsg::DevBuf<int32_t> conn;     // [units][16 | 8]: A's slots, B's own slots (3*node), mask words
   tsg::DevBuf<unsigned char> coef;  // [units][24] of T: A and B coefficient records
+  tsg::DevBuf<int32_t> sched;       // unit-chunk counters of the dynamic schedule, one per launch slot
+  mutable std::atomic<uint32_t> next_slot{0};  // launches take counter slots round-robin
 };
 
 // Edge fans for the fan sweep (ebe_fan.cu): element j of a fan around edge (p, q) is
@@ -145,8 +148,10 @@ KernelFit kernel_fit(int threads, size_t smem) {
   return fit[dev];
 }
 
-// Units per launch of a persistent unit sweep (ebe_pair.cu): long sweeps split into
-// launches of a bounded number of grid strides (TSGPU_EBE_PAIR_STRIDES)
+// Units per launch of a persistent unit sweep (ebe_pair.cu): statically strided sweeps split
+// long sweeps into launches of a bounded number of grid strides (TSGPU_EBE_PAIR_STRIDES);
+// the pair sweep's dynamic schedule (pair_dynamic) runs one launch
+int64_t strided_launch_units(int64_t units_per_stride, int64_t units);
 int64_t pair_launch_units(int64_t units_per_stride, int64_t units);
 // fan sweep (ebe_fan.cu): units [q0, q1) / an element group; false if `batch` is not covered
 bool ebe_fan_apply_range(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int32_t q0,
@@ -184,6 +189,7 @@ void ebe_apply_part(const ts_ebe& op, const void* u, void* f, int32_t batch, cud
 int ebe_launches_per_apply(const ts_ebe& op, int32_t batch);
 int ebe_pair_launches(const ts_ebe& op, int32_t batch);
 // pair sweep (ebe_pair.cu); false when no instance covers this batch width
+bool pair_dynamic();  // TSGPU_EBE_DYN: pair units taken in warp chunks from a counter
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
 // face-pair topology of an element order (greedy matching result), shareable between the
 // level set's tet10 operators, which use the same mesh and element order

@@ -464,7 +464,7 @@ bool launch_fan_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t q0
     if (q1 <= q0) return true;
     const int64_t need = (int64_t(q1 - q0) + GROUPS - 1) / GROUPS;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(fit.sms) * std::max(fit.per_sm, 1))));
-    const int64_t step = pair_launch_units(int64_t(grid) * GROUPS, int64_t(q1) - q0);
+    const int64_t step = strided_launch_units(int64_t(grid) * GROUPS, int64_t(q1) - q0);
     for (int64_t a = q0; a < q1; a += step) {
       const int32_t b = static_cast<int32_t>(std::min<int64_t>(q1, a + step));
       if (launches) {

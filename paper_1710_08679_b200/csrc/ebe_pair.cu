@@ -109,7 +109,7 @@ __device__ __forceinline__ void red_p(double* p, double v, unsigned skip) {
 template <typename T, typename V, int NPE, int B>
 __global__ void __launch_bounds__(128, 2)
 k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32_t p_begin, int32_t p_end,
-           const T* __restrict__ u, T* __restrict__ f) {
+           const T* __restrict__ u, T* __restrict__ f, int32_t* __restrict__ sched) {
   using O = LaneOps<V>;
   using Geo = PairGeo<NPE>;
   constexpr int CPT = O::kCols;
@@ -138,7 +138,8 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
     return (q & 1) ? pr.b : pr.a;
   };
   const int col = lane * CPT;
-  int e = p_begin + blockIdx.x * GROUPS + grp;
+  int stat = p_begin + blockIdx.x * GROUPS + grp;  // static order: this group's next unit
+  int e = 0;
 
   int32_t nd[kPairWords];
   auto load_conn = [&](int ee) {
@@ -189,14 +190,47 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  load_conn(e);
-  issue(e, 0);
-  load_conn(e + G);
+  // unit order: static strides (sched == nullptr) or warp chunks taken from a counter in sweep
+  // order (sched), which keeps the front of concurrently swept units tight (no drift between lane
+  // groups, so the rows they share stay in L2); a chunk's successor is claimed one chunk ahead
+  constexpr int GPW = 32 / TPE < 1 ? 1 : 32 / TPE;  // lane groups per warp
+  constexpr int J = 4;                               // units per group per chunk
+  const int gi = (threadIdx.x & 31) / TPE;
+  int cbase = 0, k = 0, claim = 0;
+  auto take = [&]() {  // lane 0 claims a chunk; the value is read (shfl) one chunk later
+    if ((threadIdx.x & 31) == 0) claim = atomicAdd(sched, GPW * J);
+  };
+  auto next_unit = [&]() -> int {
+    if (!sched) {
+      const int r = stat;
+      stat += G;
+      return r;
+    }
+    const int r = p_begin + cbase + gi + k * GPW;
+    if (++k == J) {
+      k = 0;
+      cbase = __shfl_sync(0xffffffffu, claim, 0);
+      take();
+    }
+    return r;
+  };
+  if (sched) {
+    take();
+    cbase = __shfl_sync(0xffffffffu, claim, 0);
+    take();
+  }
+  int e_cur = next_unit(), e_nxt = next_unit(), e_far = next_unit();
+  load_conn(e_cur);
+  issue(e_cur, 0);
+  load_conn(e_nxt);
+  e = e_cur;
   int s = 0;
   while (__any_sync(0xffffffffu, e < p_end)) {
-    const int en = e + G;
+    const int en = e_nxt;
     issue(en, s ^ 1);
-    load_conn(en + G);
+    load_conn(e_far);
+    e_nxt = e_far;
+    e_far = next_unit();
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
     if (e < p_end) {
@@ -312,7 +346,14 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 // configs[3] on one device, fp32 r=8: 29.3 -> 24.6 ms (5300 strides); configs[1] stays one launch (`profiles/r01_pair_strides.txt`).
 constexpr int64_t kPairLaunchStrides = 1024;
 }  // namespace
-int64_t pair_launch_units(int64_t units_per_stride, int64_t units) {
+bool pair_dynamic() {
+  static const bool on = [] {
+    const char* e = std::getenv("TSGPU_EBE_DYN");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+int64_t strided_launch_units(int64_t units_per_stride, int64_t units) {
   static const int64_t strides = [] {
     const char* e = std::getenv("TSGPU_EBE_PAIR_STRIDES");
     return e ? std::max<int64_t>(0, std::atoll(e)) : kPairLaunchStrides;
@@ -321,6 +362,11 @@ int64_t pair_launch_units(int64_t units_per_stride, int64_t units) {
   // equal launches of at most `strides` strides each
   const int64_t cap = strides * units_per_stride, n = (units + cap - 1) / cap;
   return std::max<int64_t>((units + n - 1) / n, 1);
+}
+int64_t pair_launch_units(int64_t units_per_stride, int64_t units) {
+  // the dynamic schedule keeps the front tight by itself: one launch (unless strides are forced)
+  if (pair_dynamic() && !std::getenv("TSGPU_EBE_PAIR_STRIDES")) return std::max<int64_t>(units, 1);
+  return strided_launch_units(units_per_stride, units);
 }
 namespace {
 
@@ -344,8 +390,13 @@ bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p
     const int64_t step = pair_launch_units(int64_t(grid) * GROUPS, int64_t(p1) - p0);
     for (int64_t a = p0; a < p1; a += step) {
       const int32_t b = static_cast<int32_t>(std::min<int64_t>(p1, a + step));
+      int32_t* sched = nullptr;
+      if (pair_dynamic()) {
+        sched = op.pair->sched.get() + (op.pair->next_slot.fetch_add(1, std::memory_order_relaxed) & 63u);
+        TS_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), s));
+      }
       kern<<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()),
-                                  static_cast<int32_t>(a), b, u, f);
+                                  static_cast<int32_t>(a), b, u, f, sched);
       TS_CUDA_LAUNCH();
     }
     return true;
@@ -684,6 +735,7 @@ void build_pair_plan(ts_ebe& op, const Mesh& m, const HostVec<int32_t>& conn_wor
   plan->paired_fraction = E ? double(paired) / double(E) : 0.0;
   plan->conn.upload(pc);
   plan->coef.upload(pcf);
+  plan->sched.alloc(64);
   op.pair = std::move(plan);
 }
 

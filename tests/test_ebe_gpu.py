@@ -251,16 +251,21 @@ print(worst)
 """
 
 
-@pytest.mark.parametrize("strides", ["1", "3"])
-def test_pair_sweep_split_into_many_launches(strides):
-    """TSGPU_EBE_PAIR_STRIDES (read once per process, so in a child process): a sweep
-    split into launches of 1 or 3 grid strides each (up to ~30 launches here) gives
-    the reference's product, as the single-launch sweep does."""
+@pytest.mark.parametrize("dyn", ["1", "0"])
+@pytest.mark.parametrize("strides", ["1", "3", None])
+def test_pair_sweep_split_into_many_launches(strides, dyn):
+    """TSGPU_EBE_PAIR_STRIDES / TSGPU_EBE_DYN (read once per process, so in a child
+    process): a sweep split into launches of 1 or 3 grid strides each (up to ~30
+    launches here), with the dynamic unit schedule (a counter per launch) or the static
+    strides, gives the reference's product, as the single-launch sweep does."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TSGPU_EBE_PAIR_STRIDES=strides, TSGPU_EBE_KERNEL="pair")
+    env = dict(os.environ, TSGPU_EBE_DYN=dyn, TSGPU_EBE_KERNEL="pair")
+    env.pop("TSGPU_EBE_PAIR_STRIDES", None)
+    if strides is not None:
+        env["TSGPU_EBE_PAIR_STRIDES"] = strides
     out = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT, root], capture_output=True, text=True, env=env,
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
