@@ -194,7 +194,10 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
   // order (sched), which keeps the front of concurrently swept units tight (no drift between lane
   // groups, so the rows they share stay in L2); a chunk's successor is claimed one chunk ahead
   constexpr int GPW = 32 / TPE < 1 ? 1 : 32 / TPE;  // lane groups per warp
-  constexpr int J = 4;                               // units per group per chunk
+#ifndef PAIR_J
+#define PAIR_J 4
+#endif
+  constexpr int J = PAIR_J;                          // units per group per chunk
   const int gi = (threadIdx.x & 31) / TPE;
   int cbase = 0, k = 0, claim = 0;
   auto take = [&]() {  // lane 0 claims a chunk; the value is read (shfl) one chunk later
