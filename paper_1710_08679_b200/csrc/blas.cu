@@ -8,6 +8,7 @@
 // order, so results are bit-reproducible run to run and column-independent
 // (identical columns stay identical, test_solver.cpp:183-201).
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "blas.h"
@@ -588,6 +589,138 @@ __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* 
   }
 }
 
+// The level-1 product with each warp's block rows staged in shared memory: a warp owns RPW
+// consecutive rows (qpr = B / W threads each); their blocks and column indices are one
+// contiguous range of the BCSR arrays, brought in by two bulk copies (TMA, completing on a
+// per-warp mbarrier) instead of nine scalar loads per block and thread (which held k_bcsr_rows
+// at the L1 request limit). Same sums in the same order as k_bcsr_rows. A warp whose range
+// exceeds the staging capacity (or would read past the arrays' ends) loads from global memory.
+constexpr int kStageWarps = 8;
+template <int RPW>
+struct StageCap {
+  static constexpr int kBlocks = RPW * 20 + 8;                              // blocks per warp
+  static constexpr int kBlkBytes = (kBlocks * 36 + 16 + 15) & ~15;         // + alignment slack
+  static constexpr int kColBytes = (kBlocks * 4 + 16 + 15) & ~15;
+  static constexpr int kWarpBytes = kBlkBytes + kColBytes + 16;             // + mbarrier
+  static_assert(kBlkBytes % 16 == 0 && kColBytes % 16 == 0, "16-byte aligned staging regions");
+};
+
+template <int W, int RPW, typename ACC>
+__global__ void __launch_bounds__(32 * kStageWarps)
+k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                   const float* __restrict__ blocks, int32_t n, int64_t nnz, const float* __restrict__ u,
+                   float* __restrict__ f, int32_t B) {
+  using Cap = StageCap<RPW>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int qpr = 32 / RPW;
+  const int64_t r0 = (int64_t(blockIdx.x) * kStageWarps + wid) * RPW;
+  if (r0 >= n) return;  // whole warp
+  unsigned char* const wb = smem + size_t(wid) * Cap::kWarpBytes;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(wb + Cap::kBlkBytes + Cap::kColBytes);
+  const int64_t r1 = r0 + RPW < n ? r0 + RPW : n;
+  const int64_t eb = __ldg(row_ptr + r0), ee = __ldg(row_ptr + r1);
+  const int64_t bb0 = (eb * 36) & ~int64_t(15), bb1 = (ee * 36 + 15) & ~int64_t(15);
+  const int64_t cb0 = (eb * 4) & ~int64_t(15), cb1 = (ee * 4 + 15) & ~int64_t(15);
+  const bool staged = bb1 - bb0 <= Cap::kBlkBytes && cb1 - cb0 <= Cap::kColBytes && bb1 <= nnz * 36 &&
+                      cb1 <= nnz * 4 && ee > eb;
+  const unsigned sbar = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  if (staged) {
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar),
+                   "r"(static_cast<unsigned>(bb1 - bb0 + cb1 - cb0))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(wb))),
+                   "l"(reinterpret_cast<const unsigned char*>(blocks) + bb0), "r"(static_cast<unsigned>(bb1 - bb0)),
+                   "r"(sbar)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(wb + Cap::kBlkBytes))),
+                   "l"(reinterpret_cast<const unsigned char*>(col_idx) + cb0), "r"(static_cast<unsigned>(cb1 - cb0)),
+                   "r"(sbar)
+                   : "memory");
+    }
+  }
+  const int64_t r = r0 + lane / qpr;
+  const int b0 = (lane % qpr) * W;
+  ACC acc[3][W];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int c = 0; c < W; ++c) acc[i][c] = ACC(0);
+  const bool live = r < r1;
+  const int32_t e0 = live ? __ldg(row_ptr + r) : 0, e1 = live ? __ldg(row_ptr + r + 1) : 0;
+  const float* ub = u + b0;
+  auto block_step = [&](const float (&m)[9], int32_t col) {
+    const float* uc = ub + 3 * int64_t(col) * B;
+    const Pack<float, W> x0 = ld<float, W>(uc), x1 = ld<float, W>(uc + B), x2 = ld<float, W>(uc + 2 * B);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        if constexpr (sizeof(ACC) == 4)
+          acc[i][c] = fmaf(m[3 * i + 2], x2.v[c], fmaf(m[3 * i + 1], x1.v[c], fmaf(m[3 * i], x0.v[c], acc[i][c])));
+        else
+          acc[i][c] += double(m[3 * i]) * double(x0.v[c]) + double(m[3 * i + 1]) * double(x1.v[c]) +
+                       double(m[3 * i + 2]) * double(x2.v[c]);
+      }
+  };
+  if (staged) {
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0,1,0,p; }"
+                   : "=r"(done)
+                   : "r"(sbar)
+                   : "memory");
+    const unsigned char* const sb = wb - bb0;                 // byte address of block entry e: sb + 36 e
+    const int32_t* const sc = reinterpret_cast<const int32_t*>(wb + Cap::kBlkBytes - cb0);  // sc[e]
+#pragma unroll 4
+    for (int32_t e = e0; e < e1; ++e) {
+      const float* blk = reinterpret_cast<const float*>(sb + 36 * int64_t(e));
+      float m[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) m[q] = blk[q];
+      block_step(m, sc[e]);
+    }
+  } else {
+#pragma unroll 4
+    for (int32_t e = e0; e < e1; ++e) {
+      const float* blk = blocks + 9 * int64_t(e);
+      float m[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) m[q] = __ldg(blk + q);
+      block_step(m, __ldg(col_idx + e));
+    }
+  }
+  if (!live) return;
+  float* fr = f + 3 * r * B + b0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    Pack<float, W> o;
+#pragma unroll
+    for (int c = 0; c < W; ++c) o.v[c] = static_cast<float>(acc[i][c]);
+    st<float, W>(fr + i * B, o);
+  }
+}
+
+template <int W, int RPW, typename ACC>
+void launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, int64_t nnz,
+                        const float* u, float* f, int32_t B, cudaStream_t s) {
+  const size_t smem = size_t(kStageWarps) * StageCap<RPW>::kWarpBytes;
+  static bool configured = false;  // (per template instance; the attribute is per device function)
+  if (!configured) {
+    TS_CUDA(cudaFuncSetAttribute(k_bcsr_rows_staged<W, RPW, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    configured = true;
+  }
+  const int64_t rows_per_block = int64_t(kStageWarps) * RPW;
+  k_bcsr_rows_staged<W, RPW, ACC><<<static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block),
+                                     32 * kStageWarps, smem, s>>>(row_ptr, col_idx, blocks, n, nnz, u, f, B);
+}
+
 __global__ void k_cast_d2f(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) y[i] = static_cast<float>(x[i]);
@@ -888,8 +1021,18 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
   TS_CUDA_LAUNCH();
 }
 void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
-                   float* f, int32_t B, cudaStream_t s, const int32_t* rows) {
+                   float* f, int32_t B, cudaStream_t s, const int32_t* rows, int64_t nnz) {
   if (n <= 0) return;
+  static const bool staged = [] {  // TSGPU_L1_STAGED=0: the unstaged kernel for every product
+    const char* e = std::getenv("TSGPU_L1_STAGED");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (staged && !rows && nnz > 0 && pack_width<float>(B) == 4 && (B == 16 || B == 8)) {
+    if (B == 16) launch_rows_staged<4, 8, float>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
+    else launch_rows_staged<4, 16, float>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
+    TS_CUDA_LAUNCH();
+    return;
+  }
   TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W, float><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
                                    row_ptr, col_idx, blocks, n, u, f, B, rows)));
   TS_CUDA_LAUNCH();

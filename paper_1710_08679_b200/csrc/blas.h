@@ -111,8 +111,10 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
                     const float* u, float* f, int32_t batch, cudaStream_t s);
 // the assembled level-1 operator (fp32 blocks, fp32 accumulation): y = K1 x
 // rows (nullable): apply only these n rows (row ids) instead of rows [0, n)
+// nnz (the blocks / column entries stored; -1 = unknown) enables the warp-staged kernel for
+// whole-range products (rows == nullptr)
 void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
-                   float* f, int32_t batch, cudaStream_t s, const int32_t* rows = nullptr);
+                   float* f, int32_t batch, cudaStream_t s, const int32_t* rows = nullptr, int64_t nnz = -1);
 // casts (cast_batch, vector_batch.hpp:43-49)
 void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s);
 void cast_f2d(const float* x, double* y, int64_t n, cudaStream_t s);

@@ -274,7 +274,8 @@ void dist_l1_apply(ts_dist_levels& L, const float* x, float* y, int32_t B, cudaS
   if (L.l1_assembled) {
     DistEbe& D = L.l1;  // its halo, side stream and events
     if (!D.overlap || D.halo.nbr.empty()) {
-      bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s);
+      bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s, nullptr,
+                    static_cast<int64_t>(L.l1a_col_idx.size()));
       D.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, s);
       return;
     }

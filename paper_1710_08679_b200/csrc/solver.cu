@@ -103,7 +103,8 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
   p2_apply(v.u2.get(), v.u1.get(), lv.agg.get(), lv.n1, lv.mask1.get(), B, s);
   auto a1 = [&](const float* x, float* y, bool init) {
     if (lv.l1_assembled)
-      bcsr_rows_f32(lv.l1_row_ptr.get(), lv.l1_col_idx.get(), lv.l1_blocks.get(), lv.n1, x, y, B, s);
+      bcsr_rows_f32(lv.l1_row_ptr.get(), lv.l1_col_idx.get(), lv.l1_blocks.get(), lv.n1, x, y, B, s, nullptr,
+                    static_cast<int64_t>(lv.l1_col_idx.size()));
     else
       ebe_apply_part(*lv.l1, x, y, B, s, -1, init);
   };
@@ -398,7 +399,8 @@ ts_status ts_levels_apply(ts_levels* lv, int32_t which, const void* u, void* f, 
   else if (which == 1) tsg::ebe_apply(*lv->l0, u, f, batch, s);
   else if (which == 2 && lv->l1_assembled)
     tsg::bcsr_rows_f32(lv->l1_row_ptr.get(), lv->l1_col_idx.get(), lv->l1_blocks.get(), lv->n1,
-                       static_cast<const float*>(u), static_cast<float*>(f), batch, s);
+                       static_cast<const float*>(u), static_cast<float*>(f), batch, s, nullptr,
+                       static_cast<int64_t>(lv->l1_col_idx.size()));
   else if (which == 2) tsg::ebe_apply(*lv->l1, u, f, batch, s);
   else if (which == 3)
     tsg::bcsr_apply_f32(lv->l2_row_ptr.get(), lv->l2_col_idx.get(), lv->l2_blocks.get(), lv->n2,
