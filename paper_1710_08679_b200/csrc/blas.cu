@@ -596,21 +596,21 @@ __global__ void k_bcsr_rows(const int32_t* __restrict__ row_ptr, const int32_t* 
 // at the L1 request limit). Same sums in the same order as k_bcsr_rows. A warp whose range
 // exceeds the staging capacity (or would read past the arrays' ends) loads from global memory.
 constexpr int kStageWarps = 8;
-template <int RPW>
+template <int RPW, int PER_ROW = 20>
 struct StageCap {
-  static constexpr int kBlocks = RPW * 20 + 8;                              // blocks per warp
+  static constexpr int kBlocks = RPW * PER_ROW + 8;                         // blocks per warp
   static constexpr int kBlkBytes = (kBlocks * 36 + 16 + 15) & ~15;         // + alignment slack
   static constexpr int kColBytes = (kBlocks * 4 + 16 + 15) & ~15;
   static constexpr int kWarpBytes = kBlkBytes + kColBytes + 16;             // + mbarrier
   static_assert(kBlkBytes % 16 == 0 && kColBytes % 16 == 0, "16-byte aligned staging regions");
 };
 
-template <int W, int RPW, typename ACC>
+template <int W, int RPW, typename ACC, int PER_ROW = 20>
 __global__ void __launch_bounds__(32 * kStageWarps)
 k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                    const float* __restrict__ blocks, int32_t n, int64_t nnz, const float* __restrict__ u,
                    float* __restrict__ f, int32_t B) {
-  using Cap = StageCap<RPW>;
+  using Cap = StageCap<RPW, PER_ROW>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int qpr = 32 / RPW;
@@ -706,18 +706,18 @@ k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restric
   }
 }
 
-template <int W, int RPW, typename ACC>
+template <int W, int RPW, typename ACC, int PER_ROW = 20>
 void launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, int64_t nnz,
                         const float* u, float* f, int32_t B, cudaStream_t s) {
-  const size_t smem = size_t(kStageWarps) * StageCap<RPW>::kWarpBytes;
+  const size_t smem = size_t(kStageWarps) * StageCap<RPW, PER_ROW>::kWarpBytes;
   static bool configured = false;  // (per template instance; the attribute is per device function)
   if (!configured) {
-    TS_CUDA(cudaFuncSetAttribute(k_bcsr_rows_staged<W, RPW, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+    TS_CUDA(cudaFuncSetAttribute(k_bcsr_rows_staged<W, RPW, ACC, PER_ROW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     configured = true;
   }
   const int64_t rows_per_block = int64_t(kStageWarps) * RPW;
-  k_bcsr_rows_staged<W, RPW, ACC><<<static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block),
+  k_bcsr_rows_staged<W, RPW, ACC, PER_ROW><<<static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block),
                                      32 * kStageWarps, smem, s>>>(row_ptr, col_idx, blocks, n, nnz, u, f, B);
 }
 
@@ -1014,8 +1014,18 @@ void cg_update(double* r, double* u, const double* p, const double* q, int32_t n
 }
 
 void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
-                    float* f, int32_t B, cudaStream_t s) {
+                    float* f, int32_t B, cudaStream_t s, int64_t nnz) {
   // fp64 row sums as the reference; W cases of a block row per thread, 16-byte u packs
+  static const bool staged = [] {  // TSGPU_L2_STAGED=0: the unstaged kernel
+    const char* e = std::getenv("TSGPU_L2_STAGED");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (n > 0 && staged && nnz > 0 && pack_width<float>(B) == 4 && (B == 16 || B == 8)) {
+    if (B == 16) launch_rows_staged<4, 8, double, 32>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
+    else launch_rows_staged<4, 16, double, 32>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
+    TS_CUDA_LAUNCH();
+    return;
+  }
   TS_WIDTH_DISPATCH(float, B, (k_bcsr_rows<W, double><<<grid_for(int64_t(n) * (B / W), 256), 256, 0, s>>>(
                                    row_ptr, col_idx, blocks, n, u, f, B, nullptr)));
   TS_CUDA_LAUNCH();

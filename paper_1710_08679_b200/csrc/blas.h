@@ -108,7 +108,7 @@ template <typename T>
 void bj_apply(const T* inv, const T* r, T* z, int32_t n_nodes, int32_t batch, cudaStream_t s);
 // f = A u, 3x3 float blocks, fp64 row accumulation (block_csr.hpp:33-69)
 void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
-                    const float* u, float* f, int32_t batch, cudaStream_t s);
+                    const float* u, float* f, int32_t batch, cudaStream_t s, int64_t nnz = -1);
 // the assembled level-1 operator (fp32 blocks, fp32 accumulation): y = K1 x
 // rows (nullable): apply only these n rows (row ids) instead of rows [0, n)
 // nnz (the blocks / column entries stored; -1 = unknown) enables the warp-staged kernel for

@@ -335,7 +335,8 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
     L.ws.owned = nullptr;
     auto a2 = [&](const float* x, float* y, bool) {
       D.exchange(const_cast<float*>(x), W, comm, s);
-      bcsr_apply_f32(D.row_ptr.get(), D.col_idx.get(), D.blocks.get(), D.n_own, x, y, B, s);
+      bcsr_apply_f32(D.row_ptr.get(), D.col_idx.get(), D.blocks.get(), D.n_own, x, y, B, s,
+                     static_cast<int64_t>(D.col_idx.size()));
     };
     s2 = inner_pcg<float>(a2, D.m2.get(), v.r2d.get(), v.u2d.get(), D.n_own, B, cfg.level_tol[2],
                           cfg.level_max_iter[2], v.e2d.get(), v.p2d.get(), v.q2d.get(), L.cs, L.ws, s);
@@ -350,7 +351,8 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
     L.ws.comm = nullptr;  // level 2 is replicated: identical on every rank, no collectives
     L.ws.owned = nullptr;
     auto a2 = [&](const float* x, float* y, bool) {
-      bcsr_apply_f32(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s);
+      bcsr_apply_f32(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s,
+                     static_cast<int64_t>(L.l2_col_idx.size()));
     };
     s2 = inner_pcg<float>(a2, L.m2.get(), v.r2.get(), v.u2.get(), L.n2, B, cfg.level_tol[2], cfg.level_max_iter[2],
                           v.e2.get(), v.p2.get(), v.q2.get(), L.cs, L.ws, s);

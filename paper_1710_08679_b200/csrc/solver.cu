@@ -91,7 +91,8 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
   p2_restrict(v.u1.get(), v.u2.get(), lv.p2t_ptr.get(), lv.p2t_idx.get(), lv.n2, lv.mask2.get(), B, s);
   const auto t0 = clk::now();
   auto a2 = [&](const float* x, float* y, bool) {
-    bcsr_apply_f32(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s);
+    bcsr_apply_f32(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s,
+                   static_cast<int64_t>(lv.l2_col_idx.size()));
   };
   InnerStats s2;
   {
