@@ -1030,14 +1030,17 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
                                    row_ptr, col_idx, blocks, n, u, f, B, nullptr)));
   TS_CUDA_LAUNCH();
 }
-void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
-                   float* f, int32_t B, cudaStream_t s, const int32_t* rows, int64_t nnz) {
-  if (n <= 0) return;
+bool bcsr_rows_staged_ok(int32_t B) {
   static const bool staged = [] {  // TSGPU_L1_STAGED=0: the unstaged kernel for every product
     const char* e = std::getenv("TSGPU_L1_STAGED");
     return !e || std::atoi(e) != 0;
   }();
-  if (staged && !rows && nnz > 0 && pack_width<float>(B) == 4 && (B == 16 || B == 8)) {
+  return staged && pack_width<float>(B) == 4 && (B == 16 || B == 8);
+}
+void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,
+                   float* f, int32_t B, cudaStream_t s, const int32_t* rows, int64_t nnz) {
+  if (n <= 0) return;
+  if (!rows && nnz > 0 && bcsr_rows_staged_ok(B)) {
     if (B == 16) launch_rows_staged<4, 8, float>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
     else launch_rows_staged<4, 16, float>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
     TS_CUDA_LAUNCH();

@@ -111,6 +111,8 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
                     const float* u, float* f, int32_t batch, cudaStream_t s, int64_t nnz = -1);
 // the assembled level-1 operator (fp32 blocks, fp32 accumulation): y = K1 x
 // rows (nullable): apply only these n rows (row ids) instead of rows [0, n)
+// whether whole-range products of `batch` cases take the warp-staged kernel
+bool bcsr_rows_staged_ok(int32_t batch);
 // nnz (the blocks / column entries stored; -1 = unknown) enables the warp-staged kernel for
 // whole-range products (rows == nullptr)
 void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, const float* u,

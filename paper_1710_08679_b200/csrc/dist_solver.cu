@@ -273,7 +273,13 @@ void dist_ensure_vecs(ts_dist_levels& L, int32_t B) {
 void dist_l1_apply(ts_dist_levels& L, const float* x, float* y, int32_t B, cudaStream_t s, bool init) {
   if (L.l1_assembled) {
     DistEbe& D = L.l1;  // its halo, side stream and events
-    if (!D.overlap || D.halo.nbr.empty()) {
+    // the staged whole-range product beats the interface-first split (two unstaged row-list
+    // launches) by more than the exchange it no longer hides (TSGPU_DIST_L1_SPLIT=1 keeps the split)
+    static const bool split = [] {
+      const char* e = std::getenv("TSGPU_DIST_L1_SPLIT");
+      return e && e[0] == '1';
+    }();
+    if (!D.overlap || D.halo.nbr.empty() || (!split && bcsr_rows_staged_ok(B))) {
       bcsr_rows_f32(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s, nullptr,
                     static_cast<int64_t>(L.l1a_col_idx.size()));
       D.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, s);

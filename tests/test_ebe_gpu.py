@@ -270,3 +270,27 @@ def test_pair_sweep_split_into_many_launches(strides, dyn):
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 1.0
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_concurrent_applies_on_streams(prec):
+    """One operator applied concurrently on four CUDA streams (the pair sweep's dynamic
+    schedule gives each launch its own unit counter, ebe_pair.cu): every product equals the
+    one computed alone."""
+    mesh = ts.generate_box_mesh((3000.0, 3000.0, 2000.0), (24, 24, 16), (900.0,))
+    op = ts.EbeOperator(mesh, 2, mats(TWO_LAYER), mesh.dirichlet_mask(), prec=prec)
+    dt = torch.float32 if prec == 32 else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    us = [torch.rand(3 * op.n_nodes(), 16, device="cuda", dtype=dt, generator=g) * 2 - 1 for _ in range(4)]
+    alone = [op.apply(u) for u in us]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in us]
+    outs = [torch.empty_like(u) for u in us]
+    for _ in range(3):
+        for st, u, f in zip(streams, us, outs):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                op.apply(u, f)
+        torch.cuda.synchronize()
+        for f, a in zip(outs, alone):
+            assert rel_l2(f.double().cpu().numpy(), a.double().cpu().numpy()) <= TOL[prec]
