@@ -7,7 +7,9 @@
 // partial per column and a one-block finalize sums the partials in block
 // order, so results are bit-reproducible run to run and column-independent
 // (identical columns stay identical, test_solver.cpp:183-201).
+#include <atomic>
 #include <cfloat>
+#include <stdexcept>
 #include <cstdlib>
 #include <cmath>
 
@@ -710,11 +712,16 @@ template <int W, int RPW, typename ACC, int PER_ROW = 20>
 void launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, int64_t nnz,
                         const float* u, float* f, int32_t B, cudaStream_t s) {
   const size_t smem = size_t(kStageWarps) * StageCap<RPW, PER_ROW>::kWarpBytes;
-  static bool configured = false;  // (per template instance; the attribute is per device function)
-  if (!configured) {
+  // the shared-memory opt-in is a per-device attribute of the function: set once per device
+  constexpr int kMaxDevices = 64;
+  static std::atomic<bool> configured[kMaxDevices] = {};
+  int dev = 0;
+  TS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("bcsr rows: device ordinal out of range");
+  if (!configured[dev].load(std::memory_order_acquire)) {
     TS_CUDA(cudaFuncSetAttribute(k_bcsr_rows_staged<W, RPW, ACC, PER_ROW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = true;
+    configured[dev].store(true, std::memory_order_release);
   }
   const int64_t rows_per_block = int64_t(kStageWarps) * RPW;
   k_bcsr_rows_staged<W, RPW, ACC, PER_ROW><<<static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block),
