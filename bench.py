@@ -526,11 +526,19 @@ def main_partitioned(args, world, rank, local):
                 else NORTHSTAR_CELLS if world > 1 else tuple(args.solve_cells))
     cells_g = (tuple(args.greens_cells) if args.greens_cells
                else NORTHSTAR_CELLS if world > 1 else tuple(args.cells))
+    # a leg whose per-rank footprint exceeds the device is reported as skipped on every rank
+    # (e.g. the configs[4] sweep at r = 16 on 2 GPUs: SURVEY §8e) instead of failing the run
+    need_ns = rank_bytes_needed(cells_ns, world, args.northstar_cases)
+    need_g = rank_bytes_needed(cells_g, world, 16, greens=True)
+    run_ns, free_ns = fits_on_ranks(torch, need_ns) if not args.no_northstar else (False, 0)
+    run_g, free_g = fits_on_ranks(torch, need_g) if not args.no_greens_partitioned else (False, 0)
     # the configs[3] mesh and its partition are built once for both legs when they share it
-    shared = (crust_mesh(ts, cells_ns, world)
-              if not args.no_northstar and not args.no_greens_partitioned and cells_ns == cells_g else None)
+    shared = (crust_mesh(ts, cells_ns, world) if run_ns and run_g and cells_ns == cells_g else None)
     northstar = None
-    if not args.no_northstar:  # BASELINE configs[3]: the partitioned 400M-DOF solve, r = 8, on these N GPUs
+    if not args.no_northstar and not run_ns:
+        northstar = {"skipped": f"needs ~{need_ns / 1e9:.0f} GB per rank at r = {args.northstar_cases}, "
+                                f"{free_ns / 1e9:.0f} GB free", "cells": list(cells_ns), "ranks": world}
+    if run_ns:  # BASELINE configs[3]: the partitioned 400M-DOF solve, r = 8, on these N GPUs
         mine = northstar_rank(ts, torch, cells_ns, args.northstar_cases, comm, rank, world, sync, args.steps,
                               prebuilt=shared)
         allr = [None] * world
@@ -538,7 +546,10 @@ def main_partitioned(args, world, rank, local):
         northstar = northstar_summary(allr, cells_ns, args.northstar_cases, world, f"NCCL x{world}", hbm_peak()[0])
         torch.cuda.empty_cache()
     greens_part = None
-    if not args.no_greens_partitioned:  # BASELINE configs[4]: the sweep on the partitioned configs[3] mesh
+    if not args.no_greens_partitioned and not run_g:
+        greens_part = {"skipped": f"needs ~{need_g / 1e9:.0f} GB per rank at r = 16, {free_g / 1e9:.0f} GB free",
+                       "cells": list(cells_g), "ranks": world}
+    if run_g:  # BASELINE configs[4]: the sweep on the partitioned configs[3] mesh
         mine = greens_dist_rank(ts, torch, cells_g, comm, rank, world, sync, args.greens_cases, 16, prebuilt=shared)
         allr = [None] * world
         dist.all_gather_object(allr, mine)
@@ -636,6 +647,28 @@ def greens_leg(args, ts, torch, world, rank, local):
 # ------------------------------------------------- north star: partitioned solve
 FOUR_LAYER = THREE_LAYER + [(8000.0, 4500.0, 3300.0)]  # configs[3]: layered crust over mantle (synthetic)
 NORTHSTAR_CELLS = (281, 423, 141)  # configs[3]: 405M DOF (2.8 km cells over 792 x 1192 x 400 km)
+
+
+# Device bytes per DOF of one rank's partitioned solve at r cases (fp64 outer batches, fp32 level
+# vectors, operators, halo and level-2 workspaces): 852 B/DOF measured at r = 8
+# (profiles/r02_northstar_half_configs3_one_gpu.json: 173.1 GB for 203.1M DOF); the Green's sweep
+# at r = 16 measured 1,697 B/DOF (84.9 GB for 50.0M DOF, one rank: split-mesh fault band, RHS
+# batches), 1.03x the model.
+def rank_bytes_needed(cells, nranks, r, greens=False):
+    nodes = (2 * cells[0] + 1) * (2 * cells[1] + 1) * (2 * cells[2] + 1)
+    dof_rank = 3.0 * nodes / nranks * 1.03  # RCB parts are balanced; halo copies a few percent
+    return dof_rank * (55.0 + 100.0 * r) * (1.03 if greens else 1.0)
+
+
+def fits_on_ranks(torch, need, margin=3e9):
+    """Whether `need` bytes fit every rank's free device memory (decided together, so that no
+    rank starts a leg whose collectives another rank skips)."""
+    import torch.distributed as dist
+    free, _ = torch.cuda.mem_get_info()
+    ok = torch.tensor([1.0 if need + margin <= free else 0.0], device="cuda", dtype=torch.float64)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(ok.item() > 0.5), free
 
 
 def crust_mesh(ts, cells, nranks):
@@ -853,7 +886,9 @@ def greens_dist_rank(ts, torch, cells, comm, rank, nranks, sync, n_cases, batch,
     t1 = time.perf_counter()
     bank, calls, outer = dfm.greens_bank(centers, dirs, radii, pts, axes, cfg)
     sync()
+    free, total = torch.cuda.mem_get_info()
     return {"rank": rank, "sweep_s": time.perf_counter() - t1, "setup_s": t_setup, "calls": calls, "outer": outer,
+            "device_used_gb": (total - free) / 1e9,
             "faces": int(len(faces)), "cases": int(len(dirs)), "bank_finite": bool(np.isfinite(bank).all()),
             "bank_absmax": float(np.abs(bank).max()), "bank_sum": float(bank.sum())}
 
@@ -869,6 +904,7 @@ def greens_dist_summary(per_rank, cells, nranks, backend, batch, full_cases):
             "value": round(sweep / n, 5), "unit": "s", "ranks": nranks, "backend": backend, "cases": n,
             "sweep_s": round(sweep, 3), "projected_full_sweep_s": round(sweep / n * full_cases, 1),
             "setup_s": round(max(x["setup_s"] for x in per_rank), 2), "solver_calls": x0["calls"],
+            "device_used_gb_max": round(max(x.get("device_used_gb", 0.0) for x in per_rank), 1),
             "outer_iterations": x0["outer"], "bank_finite": all(x["bank_finite"] for x in per_rank),
             "bank_identical_on_ranks": len({(x["bank_absmax"], x["bank_sum"]) for x in per_rank}) == 1,
             "entry": "ts_dist_faulted_model_create + ts_dist_greens_bank"}
