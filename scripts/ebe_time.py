@@ -1,11 +1,11 @@
 """Time EBE sweep kernels (TSGPU_EBE_KERNEL variants) on the config-2 box; also checks variant agreement.
-args: [variants=fast,tile] [cells=82,123,41]"""
+args: [variants=pair,fan] [cells=82,123,41]"""
 import os, sys, json
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 import paper_1710_08679_b200 as ts
-variants = (sys.argv[1] if len(sys.argv) > 1 else "fast,tile").split(",")
+variants = (sys.argv[1] if len(sys.argv) > 1 else "pair,fan").split(",")
 cells = tuple(int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "82,123,41").split(","))
 ext = tuple(c * 2800.0 for c in cells)
 m = ts.generate_box_mesh(ext, cells, (0.75 * ext[2],), 1)
