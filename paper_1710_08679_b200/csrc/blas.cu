@@ -723,6 +723,11 @@ void launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const fl
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     configured[dev].store(true, std::memory_order_release);
   }
+  static const bool force_global = [] {  // test hook: every warp takes the unstaged (global-load) path
+    const char* e = std::getenv("TSGPU_STAGE_FORCE_GLOBAL");
+    return e && e[0] == '1';
+  }();
+  if (force_global) nnz = 0;
   const int64_t rows_per_block = int64_t(kStageWarps) * RPW;
   k_bcsr_rows_staged<W, RPW, ACC, PER_ROW><<<static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block),
                                      32 * kStageWarps, smem, s>>>(row_ptr, col_idx, blocks, n, nnz, u, f, B);

@@ -167,7 +167,7 @@ def test_convergence_error_carries_report():
 
 
 @pytest.mark.parametrize("which", [0, 1, 2])
-@pytest.mark.parametrize("batch", [1, 3, 16])
+@pytest.mark.parametrize("batch", [1, 3, 8, 16])
 def test_level_operators_match_reference(checker, which, batch):
     """The operators the solve applies (ts_levels_apply) against the reference's
     EbeOperator<double> order 2 (outer), <float> order 2 (level 0) and <float>
@@ -187,3 +187,44 @@ def test_level_operators_match_reference(checker, which, batch):
     got = lv.apply(which, torch.from_numpy(u).cuda()).cpu().numpy()
     assert rel(got.astype(np.float64), want.astype(np.float64)) <= (1e-12 if prec == 64 else 1e-5)
     assert np.array_equal(got[mask == 1], u[mask == 1])
+
+
+_STAGE_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/oracle"); sys.path.insert(0, sys.argv[1] + "/tests")
+import numpy as np, torch
+import paper_1710_08679_b200 as ts
+from oracle import Oracle
+from conftest import TWO_LAYER, lame
+chk = Oracle("port")
+ext, div, ifs = (16000.0, 20000.0, 10000.0), (6, 7, 4), (7000.0,)
+mesh = ts.generate_box_mesh(ext, div, ifs)
+om = chk.box_mesh(ext, div, ifs, 1)
+lam, mu = lame(TWO_LAYER)
+worst = 0.0
+for batch in (8, 16):
+    lv = ts.build_crust_model(mesh, [ts.material_from_wavespeeds(*t) for t in TWO_LAYER],
+                              ts.SolverConfig(batch_size=batch)).levels
+    nn = mesh.vertex_count
+    mask = mesh.dirichlet_mask()[: 3 * nn]
+    u = chk.rng_sym(60 + batch, 3 * nn * batch).reshape(3 * nn, batch).astype(np.float32)
+    want = chk.ebe_apply(om, 1, lam, mu, mask, 32, u)
+    got = lv.apply(2, torch.from_numpy(u).cuda()).cpu().numpy().astype(np.float64)
+    worst = max(worst, float(np.linalg.norm(got - want) / np.linalg.norm(want)) / 1e-5)
+print(worst)
+"""
+
+
+def test_staged_level1_global_path_matches_reference():
+    """TSGPU_STAGE_FORCE_GLOBAL (read once per process, so in a child process): every warp of
+    the staged level-1 product takes its unstaged path (the one a warp whose block range
+    exceeds the staging capacity takes) and still gives the reference's tet4 product."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSGPU_STAGE_FORCE_GLOBAL="1")
+    out = subprocess.run([sys.executable, "-c", _STAGE_SCRIPT, root], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1.0
