@@ -1034,8 +1034,10 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
     return !e || std::atoi(e) != 0;
   }();
   if (n > 0 && staged && nnz > 0 && pack_width<float>(B) == 4 && (B == 16 || B == 8)) {
-    if (B == 16) launch_rows_staged<4, 8, double, 32>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
-    else launch_rows_staged<4, 16, double, 32>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
+    // capacity 24 blocks per row; r = 8 as two cases per thread over four threads per row
+    // (measured at configs[2] size: level-2 solve time r = 8 0.218 -> 0.175 s, r = 16 unchanged)
+    if (B == 16) launch_rows_staged<4, 8, double, 24>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
+    else launch_rows_staged<2, 8, double, 24>(row_ptr, col_idx, blocks, n, nnz, u, f, B, s);
     TS_CUDA_LAUNCH();
     return;
   }
