@@ -607,30 +607,47 @@ struct StageCap {
   static_assert(kBlkBytes % 16 == 0 && kColBytes % 16 == 0, "16-byte aligned staging regions");
 };
 
-template <int W, int RPW, typename ACC, int PER_ROW = 20>
+// DOTS: a persistent grid (each warp strides over row sets) that also accumulates, per column, the
+// fp64 dots (p, q), (p, p), (q, q) of the product's input p and output q over its rows — the inner
+// PCG's gamma pass (k_gamma, pcg.hpp:82-88) without re-reading p and q — into per-block partials in
+// the reduce_pass layout, in a fixed order (static row-set assignment; shuffles, then warps in order).
+template <int W, int RPW, typename ACC, int PER_ROW = 20, bool DOTS = false>
 __global__ void __launch_bounds__(32 * kStageWarps)
 k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                    const float* __restrict__ blocks, int32_t n, int64_t nnz, const float* __restrict__ u,
-                   float* __restrict__ f, int32_t B) {
+                   float* __restrict__ f, int32_t B, double* __restrict__ partial) {
   using Cap = StageCap<RPW, PER_ROW>;
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double red[DOTS ? kStageWarps * 3 * 32 : 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int qpr = 32 / RPW;
-  const int64_t r0 = (int64_t(blockIdx.x) * kStageWarps + wid) * RPW;
-  if (r0 >= n) return;  // whole warp
   unsigned char* const wb = smem + size_t(wid) * Cap::kWarpBytes;
   uint64_t* const bar = reinterpret_cast<uint64_t*>(wb + Cap::kBlkBytes + Cap::kColBytes);
-  const int64_t r1 = r0 + RPW < n ? r0 + RPW : n;
-  const int64_t eb = __ldg(row_ptr + r0), ee = __ldg(row_ptr + r1);
-  const int64_t bb0 = (eb * 36) & ~int64_t(15), bb1 = (ee * 36 + 15) & ~int64_t(15);
-  const int64_t cb0 = (eb * 4) & ~int64_t(15), cb1 = (ee * 4 + 15) & ~int64_t(15);
-  const bool staged = bb1 - bb0 <= Cap::kBlkBytes && cb1 - cb0 <= Cap::kColBytes && bb1 <= nnz * 36 &&
-                      cb1 <= nnz * 4 && ee > eb;
   const unsigned sbar = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  if (staged) {
-    if (lane == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int b0 = (lane % qpr) * W;
+  const float* ub = u + b0;
+  unsigned phase = 0;
+  double dacc[3][W];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int c = 0; c < W; ++c) dacc[k][c] = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * kStageWarps * RPW;
+  for (int64_t r0 = (int64_t(blockIdx.x) * kStageWarps + wid) * RPW; r0 < n; r0 += stride) {
+    const int64_t r1 = r0 + RPW < n ? r0 + RPW : n;
+    const int64_t eb = __ldg(row_ptr + r0), ee = __ldg(row_ptr + r1);
+    const int64_t bb0 = (eb * 36) & ~int64_t(15), bb1 = (ee * 36 + 15) & ~int64_t(15);
+    const int64_t cb0 = (eb * 4) & ~int64_t(15), cb1 = (ee * 4 + 15) & ~int64_t(15);
+    const bool staged = bb1 - bb0 <= Cap::kBlkBytes && cb1 - cb0 <= Cap::kColBytes && bb1 <= nnz * 36 &&
+                        cb1 <= nnz * 4 && ee > eb;
+    if (staged && lane == 0) {
+      // the previous row set's shared reads (generic proxy) come before these async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar),
                    "r"(static_cast<unsigned>(bb1 - bb0 + cb1 - cb0))
                    : "memory");
@@ -645,84 +662,119 @@ k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restric
                    "r"(sbar)
                    : "memory");
     }
-  }
-  const int64_t r = r0 + lane / qpr;
-  const int b0 = (lane % qpr) * W;
-  ACC acc[3][W];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int c = 0; c < W; ++c) acc[i][c] = ACC(0);
-  const bool live = r < r1;
-  const int32_t e0 = live ? __ldg(row_ptr + r) : 0, e1 = live ? __ldg(row_ptr + r + 1) : 0;
-  const float* ub = u + b0;
-  auto block_step = [&](const float (&m)[9], int32_t col) {
-    const float* uc = ub + 3 * int64_t(col) * B;
-    const Pack<float, W> x0 = ld<float, W>(uc), x1 = ld<float, W>(uc + B), x2 = ld<float, W>(uc + 2 * B);
+    const int64_t r = r0 + lane / qpr;
+    ACC acc[3][W];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int c = 0; c < W; ++c) {
-        if constexpr (sizeof(ACC) == 4)
-          acc[i][c] = fmaf(m[3 * i + 2], x2.v[c], fmaf(m[3 * i + 1], x1.v[c], fmaf(m[3 * i], x0.v[c], acc[i][c])));
-        else
-          acc[i][c] += double(m[3 * i]) * double(x0.v[c]) + double(m[3 * i + 1]) * double(x1.v[c]) +
-                       double(m[3 * i + 2]) * double(x2.v[c]);
+      for (int c = 0; c < W; ++c) acc[i][c] = ACC(0);
+    const bool live = r < r1;
+    const int32_t e0 = live ? __ldg(row_ptr + r) : 0, e1 = live ? __ldg(row_ptr + r + 1) : 0;
+    auto block_step = [&](const float (&m)[9], int32_t col) {
+      const float* uc = ub + 3 * int64_t(col) * B;
+      const Pack<float, W> x0 = ld<float, W>(uc), x1 = ld<float, W>(uc + B), x2 = ld<float, W>(uc + 2 * B);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+          if constexpr (sizeof(ACC) == 4)
+            acc[i][c] = fmaf(m[3 * i + 2], x2.v[c], fmaf(m[3 * i + 1], x1.v[c], fmaf(m[3 * i], x0.v[c], acc[i][c])));
+          else
+            acc[i][c] += double(m[3 * i]) * double(x0.v[c]) + double(m[3 * i + 1]) * double(x1.v[c]) +
+                         double(m[3 * i + 2]) * double(x2.v[c]);
+        }
+    };
+    if (staged) {
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                     : "=r"(done)
+                     : "r"(sbar), "r"(phase)
+                     : "memory");
+      phase ^= 1u;
+      const unsigned char* const sb = wb - bb0;                 // byte address of block entry e: sb + 36 e
+      const int32_t* const sc = reinterpret_cast<const int32_t*>(wb + Cap::kBlkBytes - cb0);  // sc[e]
+#pragma unroll 4
+      for (int32_t e = e0; e < e1; ++e) {
+        const float* blk = reinterpret_cast<const float*>(sb + 36 * int64_t(e));
+        float m[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) m[q] = blk[q];
+        block_step(m, sc[e]);
       }
-  };
-  if (staged) {
-    unsigned done = 0;
-    while (!done)
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0,1,0,p; }"
-                   : "=r"(done)
-                   : "r"(sbar)
-                   : "memory");
-    const unsigned char* const sb = wb - bb0;                 // byte address of block entry e: sb + 36 e
-    const int32_t* const sc = reinterpret_cast<const int32_t*>(wb + Cap::kBlkBytes - cb0);  // sc[e]
+    } else {
 #pragma unroll 4
-    for (int32_t e = e0; e < e1; ++e) {
-      const float* blk = reinterpret_cast<const float*>(sb + 36 * int64_t(e));
-      float m[9];
+      for (int32_t e = e0; e < e1; ++e) {
+        const float* blk = blocks + 9 * int64_t(e);
+        float m[9];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) m[q] = blk[q];
-      block_step(m, sc[e]);
+        for (int q = 0; q < 9; ++q) m[q] = __ldg(blk + q);
+        block_step(m, __ldg(col_idx + e));
+      }
     }
-  } else {
-#pragma unroll 4
-    for (int32_t e = e0; e < e1; ++e) {
-      const float* blk = blocks + 9 * int64_t(e);
-      float m[9];
+    if (live) {
+      float* fr = f + 3 * r * B + b0;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) m[q] = __ldg(blk + q);
-      block_step(m, __ldg(col_idx + e));
+      for (int i = 0; i < 3; ++i) {
+        Pack<float, W> o;
+#pragma unroll
+        for (int c = 0; c < W; ++c) o.v[c] = static_cast<float>(acc[i][c]);
+        st<float, W>(fr + i * B, o);
+        if constexpr (DOTS) {
+          const Pack<float, W> pv = ld<float, W>(u + 3 * r * B + b0 + i * B);
+#pragma unroll
+          for (int c = 0; c < W; ++c) {
+            const double x = double(pv.v[c]), y = double(o.v[c]);
+            dacc[0][c] += x * y;
+            dacc[1][c] += x * x;
+            dacc[2][c] += y * y;
+          }
+        }
+      }
     }
+    __syncwarp();  // every lane is done with this row set's staging before it is refilled
+    if constexpr (!DOTS) break;
   }
-  if (!live) return;
-  float* fr = f + 3 * r * B + b0;
+  if constexpr (DOTS) {
+    // lanes l, l + qpr, ... hold the same columns: fold them (fixed shuffle order), then the warps in order
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    Pack<float, W> o;
+    for (int k = 0; k < 3; ++k)
 #pragma unroll
-    for (int c = 0; c < W; ++c) o.v[c] = static_cast<float>(acc[i][c]);
-    st<float, W>(fr + i * B, o);
+      for (int c = 0; c < W; ++c) {
+        double v = dacc[k][c];
+        for (int off = qpr; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane < qpr) red[(wid * 3 + k) * 32 + b0 + c] = v;
+      }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < 3 * B) {
+      const int k = t / B, b = t - k * B;
+      double sum = 0.0;
+      for (int w = 0; w < kStageWarps; ++w) sum += red[(w * 3 + k) * 32 + b];
+      partial[(int64_t(blockIdx.x) * 3 + k) * B + b] = sum;
+    }
   }
 }
 
-template <int W, int RPW, typename ACC, int PER_ROW = 20>
-void launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, int64_t nnz,
-                        const float* u, float* f, int32_t B, cudaStream_t s) {
+template <int W, int RPW, typename ACC, int PER_ROW = 20, bool DOTS = false>
+int launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, int64_t nnz,
+                       const float* u, float* f, int32_t B, cudaStream_t s, double* partial = nullptr) {
   const size_t smem = size_t(kStageWarps) * StageCap<RPW, PER_ROW>::kWarpBytes;
+  auto kern = k_bcsr_rows_staged<W, RPW, ACC, PER_ROW, DOTS>;
   // the shared-memory opt-in is a per-device attribute of the function: set once per device
   constexpr int kMaxDevices = 64;
-  static std::atomic<bool> configured[kMaxDevices] = {};
+  static std::atomic<int> per_sm[kMaxDevices] = {};  // 0: not configured yet
+  static std::atomic<int> sms[kMaxDevices] = {};
   int dev = 0;
   TS_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("bcsr rows: device ordinal out of range");
-  if (!configured[dev].load(std::memory_order_acquire)) {
-    TS_CUDA(cudaFuncSetAttribute(k_bcsr_rows_staged<W, RPW, ACC, PER_ROW>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-
-    configured[dev].store(true, std::memory_order_release);
+  if (per_sm[dev].load(std::memory_order_acquire) == 0) {
+    TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int ps = 0, ns = 0;
+    TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 32 * kStageWarps, smem));
+    TS_CUDA(cudaDeviceGetAttribute(&ns, cudaDevAttrMultiProcessorCount, dev));
+    sms[dev].store(ns, std::memory_order_relaxed);
+    per_sm[dev].store(std::max(ps, 1), std::memory_order_release);
   }
   static const bool force_global = [] {  // test hook: every warp takes the unstaged (global-load) path
     const char* e = std::getenv("TSGPU_STAGE_FORCE_GLOBAL");
@@ -730,8 +782,12 @@ void launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const fl
   }();
   if (force_global) nnz = 0;
   const int64_t rows_per_block = int64_t(kStageWarps) * RPW;
-  k_bcsr_rows_staged<W, RPW, ACC, PER_ROW><<<static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block),
-                                     32 * kStageWarps, smem, s>>>(row_ptr, col_idx, blocks, n, nnz, u, f, B);
+  int64_t grid = (n + rows_per_block - 1) / rows_per_block;
+  if (DOTS)  // persistent: one resident wave (the partial count the finalize sums), at most kRedBlocks
+    grid = std::min<int64_t>(grid, std::min<int64_t>(kRedBlocks, int64_t(sms[dev].load()) * per_sm[dev].load()));
+  kern<<<static_cast<unsigned>(grid), 32 * kStageWarps, smem, s>>>(row_ptr, col_idx, blocks, n, nnz, u, f, B,
+                                                                   partial);
+  return static_cast<int>(grid);
 }
 
 __global__ void k_cast_d2f(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
@@ -1069,6 +1125,33 @@ void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* 
                                    row_ptr, col_idx, blocks, n, u, f, B, rows)));
   TS_CUDA_LAUNCH();
 }
+bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
+                         const float* p, float* q, int32_t B, cudaStream_t s, int64_t nnz, Workspace& ws) {
+  static const bool on = [] {  // TSGPU_L1_FUSED_DOTS=0: the product, then the separate gamma pass
+    const char* e = std::getenv("TSGPU_L1_FUSED_DOTS");
+    return !e || e[0] != '0';
+  }();
+  if (!on || n <= 0 || nnz <= 0 || ws.comm || ws.owned || !bcsr_rows_staged_ok(B)) return false;
+  ws.ensure(B);
+  const int grid = B == 16 ? launch_rows_staged<4, 8, float, 16, true>(row_ptr, col_idx, blocks, n, nnz, p, q, B, s,
+                                                                        ws.partial.get())
+                           : launch_rows_staged<2, 8, float, 16, true>(row_ptr, col_idx, blocks, n, nnz, p, q, B, s,
+                                                                        ws.partial.get());
+  TS_CUDA_LAUNCH();
+  ws.nblk = grid;
+  return true;
+}
+
+template <typename T>
+void pcg_gamma_final(int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
+  const Partials pp = finish_partials(ws, 3, B, s);
+  k_gamma_final<T><<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
+                                     cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get());
+  TS_CUDA_LAUNCH();
+}
+template void pcg_gamma_final<float>(int32_t, const ColScalars&, Workspace&, cudaStream_t);
+template void pcg_gamma_final<double>(int32_t, const ColScalars&, Workspace&, cudaStream_t);
+
 void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s) {
   k_cast_d2f<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
   TS_CUDA_LAUNCH();

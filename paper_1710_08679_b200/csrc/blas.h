@@ -111,6 +111,14 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
                     const float* u, float* f, int32_t batch, cudaStream_t s, int64_t nnz = -1);
 // the assembled level-1 operator (fp32 blocks, fp32 accumulation): y = K1 x
 // rows (nullable): apply only these n rows (row ids) instead of rows [0, n)
+// level-1 product q = K1 p that also leaves the gamma pass's partials ((p,q), (p,p), (q,q) per
+// column, reduce_pass layout) in ws.partial / ws.nblk; false (nothing launched) when it does not
+// apply (unstaged width, distributed workspace)
+bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
+                         const float* p, float* q, int32_t batch, cudaStream_t s, int64_t nnz, Workspace& ws);
+// the gamma finalize (alpha, breakdown / stagnation) from partials already in ws
+template <typename T>
+void pcg_gamma_final(int32_t batch, const ColScalars& cs, Workspace& ws, cudaStream_t s);
 // whether whole-range products of `batch` cases take the warp-staged kernel
 bool bcsr_rows_staged_ok(int32_t batch);
 // nnz (the blocks / column entries stored; -1 = unknown) enables the warp-staged kernel for

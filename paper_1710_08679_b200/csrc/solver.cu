@@ -109,11 +109,17 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
     else
       ebe_apply_part(*lv.l1, x, y, B, s, -1, init);
   };
+  const std::function<bool(const float*, float*)> a1_dots = [&](const float* x, float* y) {
+    return lv.l1_assembled && bcsr_rows_f32_gamma(lv.l1_row_ptr.get(), lv.l1_col_idx.get(), lv.l1_blocks.get(),
+                                                   lv.n1, x, y, B, s, static_cast<int64_t>(lv.l1_col_idx.size()),
+                                                   lv.ws);
+  };
   InnerStats s1;
   {
     NvtxRange nl("inner pcg level 1");
     s1 = inner_pcg<float>(a1, lv.m1.get(), v.r1.get(), v.u1.get(), lv.n1, B, cfg.level_tol[1], cfg.level_max_iter[1],
-                          v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s, !lv.l1_assembled, lv.mask1.get());
+                          v.e1.get(), v.p1.get(), v.q1.get(), lv.cs, lv.ws, s, !lv.l1_assembled, lv.mask1.get(),
+                          &a1_dots);
   }
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), lv.p1_ends.get(), lv.n1, lv.n0, lv.mask0.get(), B, s);

@@ -4,6 +4,7 @@
 // Operators and preconditioners are callables; distributed runs set
 // Workspace::comm / ::owned so the same loops reduce across ranks.
 #pragma once
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -37,7 +38,8 @@ struct InnerStats {
 template <typename T, typename Op>
 InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t B, double tol, int max_iter, T* e,
                      T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s, bool fuse_init = false,
-                     const uint8_t* op_mask = nullptr) {
+                     const uint8_t* op_mask = nullptr,
+                     const std::function<bool(const T*, T*)>* product_with_dots = nullptr) {
   if (max_iter < 1) validation("inner_pcg: max_iter must be >= 1");
   A(u, e, true);
   pcg_init<T>(inv, r, e, n, B, cs, ws, s);
@@ -53,8 +55,13 @@ InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t 
     pcg_rho(B, first, cs, ws, s);
     pcg_direction<T>(inv, e, p, n, B, first, cs, s, fuse_init ? q : nullptr, op_mask, pending ? u : nullptr);
     pending = false;
-    A(p, q, !fuse_init);
-    pcg_gamma<T>(p, q, n, B, cs, ws, s);
+    // q = A p; gamma's partials from the product itself when it can (assembled levels), else a pass
+    if (product_with_dots && (*product_with_dots)(p, q)) {
+      pcg_gamma_final<T>(B, cs, ws, s);
+    } else {
+      A(p, q, !fuse_init);
+      pcg_gamma<T>(p, q, n, B, cs, ws, s);
+    }
     pcg_update<T>(inv, e, q, n, B, cs, ws, s);
     const PcgStatus& ps = read_status(ws, s);
     if (ps.breakdown_col >= 0)
