@@ -271,12 +271,13 @@ __global__ void __launch_bounds__(kRedThreads) k_gamma(const T* __restrict__ p, 
 template <typename T>
 __global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* partial, int nblk, int32_t B,
                                                              const double* rho_a, double* rho_b, double* gamma,
-                                                             double* alpha, PcgStatus* st) {
+                                                             double* alpha, PcgStatus* st, int pq_only = 0) {
   __shared__ double tot[kFinThreads], scr[kFinThreads];
-  __shared__ int stag, brk;
+  __shared__ int stag, brk, full;
   if (threadIdx.x == 0) {
     stag = 0;
     brk = INT32_MAX;
+    full = 0;
   }
   block_totals(partial, 3, B, nblk, tot, scr);
   const int b = threadIdx.x;
@@ -287,6 +288,9 @@ __global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* parti
     if (g > 0.0) {
       a = rho_a[b] / g;
     } else if (g == 0.0 && rho_a[b] == 0.0) {
+      a = 0.0;
+    } else if (pq_only) {
+      atomicExch(&full, 1);  // ||p||, ||q|| unknown here: the full pass decides
       a = 0.0;
     } else {
       const double pn = tot[B + b], qn = tot[2 * B + b];
@@ -299,10 +303,11 @@ __global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* parti
     alpha[b] = a;
   }
   __syncthreads();
-  if (b < B && !stag && brk == INT32_MAX) rho_b[b] = rho_a[b];
+  if (b < B && !stag && brk == INT32_MAX && !full) rho_b[b] = rho_a[b];
   if (threadIdx.x == 0) {
     st->stagnated = stag;
     st->breakdown_col = brk == INT32_MAX ? -1 : brk;
+    st->need_full = full;
   }
 }
 
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kRedThreads) k_update(const T* __restrict__ in
                                                         const double* __restrict__ alpha,
                                                         const PcgStatus* __restrict__ st_, double* partial,
                                                         const uint8_t* __restrict__ owned) {
-  const bool skip = st_->stagnated || st_->breakdown_col >= 0;
+  const bool skip = st_->stagnated || st_->breakdown_col >= 0 || st_->need_full;
   reduce_pass<2, W>(int64_t(n) * B, B, partial, owned, int64_t(B), [&](int64_t it, int b0, double(&acc)[2][W], bool own) {
     const int64_t node = it / B;
     const int64_t base = 3 * node * B + b0;
@@ -413,6 +418,7 @@ __global__ void __launch_bounds__(kFinThreads) k_init_final(const double* partia
   if (threadIdx.x == 0) {
     st->stagnated = 0;
     st->breakdown_col = -1;
+    st->need_full = 0;
   }
   write_ratio(en2, rn2, B, st);
 }
@@ -473,6 +479,7 @@ __global__ void __launch_bounds__(kFinThreads) k_cg_alpha(const double* partial,
   if (threadIdx.x == 0) {
     st->stagnated = 0;
     st->breakdown_col = brk == INT32_MAX ? -1 : brk;
+    st->need_full = 0;
   }
 }
 
@@ -916,6 +923,7 @@ void Workspace::ensure(int32_t batch) {
   summed.ensure(static_cast<size_t>(4) * batch);
   if (!status.get()) {
     status.alloc(1);
+    TS_CUDA(cudaMemset(status.get(), 0, sizeof(PcgStatus)));
     TS_CUDA(cudaMallocHost(&host_status, sizeof(PcgStatus)));
   }
 }
@@ -1143,14 +1151,15 @@ bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const f
 }
 
 template <typename T>
-void pcg_gamma_final(int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s) {
+void pcg_gamma_final(int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s, bool partial_pq_only) {
   const Partials pp = finish_partials(ws, 3, B, s);
   k_gamma_final<T><<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
-                                     cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get());
+                                     cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get(),
+                                     partial_pq_only ? 1 : 0);
   TS_CUDA_LAUNCH();
 }
-template void pcg_gamma_final<float>(int32_t, const ColScalars&, Workspace&, cudaStream_t);
-template void pcg_gamma_final<double>(int32_t, const ColScalars&, Workspace&, cudaStream_t);
+template void pcg_gamma_final<float>(int32_t, const ColScalars&, Workspace&, cudaStream_t, bool);
+template void pcg_gamma_final<double>(int32_t, const ColScalars&, Workspace&, cudaStream_t, bool);
 
 void cast_d2f(const double* x, float* y, int64_t n, cudaStream_t s) {
   k_cast_d2f<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);

@@ -31,7 +31,7 @@ struct PcgStatus {
   int stagnated;      // pcg.hpp:99-104
   int breakdown_col;  // first column with (p,Ap) <= 0 and no stagnation, else -1
   int nonfinite;
-  int pad;
+  int need_full;      // fused gamma partials hit the (p,Ap) <= 0 branch: rerun it with the full dot pass
 };
 
 // Collective hooks of a distributed solve (comm.h); null on one device.
@@ -116,9 +116,11 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
 // apply (unstaged width, distributed workspace)
 bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
                          const float* p, float* q, int32_t batch, cudaStream_t s, int64_t nnz, Workspace& ws);
-// the gamma finalize (alpha, breakdown / stagnation) from partials already in ws
+// the gamma finalize (alpha, breakdown / stagnation) from partials already in ws; partial_pq_only:
+// the partials hold (p,q) alone (element-wise products), so a column with (p,q) <= 0 sets
+// need_full instead of deciding stagnation / breakdown (pcg_update then leaves e alone)
 template <typename T>
-void pcg_gamma_final(int32_t batch, const ColScalars& cs, Workspace& ws, cudaStream_t s);
+void pcg_gamma_final(int32_t batch, const ColScalars& cs, Workspace& ws, cudaStream_t s, bool partial_pq_only = false);
 // whether whole-range products of `batch` cases take the warp-staged kernel
 bool bcsr_rows_staged_ok(int32_t batch);
 // nnz (the blocks / column entries stored; -1 = unknown) enables the warp-staged kernel for

@@ -106,10 +106,18 @@ __device__ __forceinline__ void red_p(double* p, double v, unsigned skip) {
 #define EXP_RED(p, v) red_lane(p, v)
 #endif
 
-template <typename T, typename V, int NPE, int B>
+__device__ __forceinline__ float lane_col(float2 v, int c) { return c ? v.y : v.x; }
+__device__ __forceinline__ float lane_col(float v, int) { return v; }
+__device__ __forceinline__ double lane_col(double v, int) { return v; }
+
+// DOTS (the inner PCG's gamma, fused): every element adds p_e . (K_e p_e) over its unconstrained
+// dofs — summed over elements that is (p, K p) restricted to the unconstrained dofs — per column
+// in fp64 per lane; the block folds its lane groups in order into dpart[block][3][B] ((p,Ap) in
+// slot 0; slots 1-2 zero: the constrained dofs' p.p and the norms come from elsewhere).
+template <typename T, typename V, int NPE, int B, bool DOTS = false>
 __global__ void __launch_bounds__(128, 2)
 k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32_t p_begin, int32_t p_end,
-           const T* __restrict__ u, T* __restrict__ f, int32_t* __restrict__ sched) {
+           const T* __restrict__ u, T* __restrict__ f, int32_t* __restrict__ sched, double* __restrict__ dpart) {
   using O = LaneOps<V>;
   using Geo = PairGeo<NPE>;
   constexpr int CPT = O::kCols;
@@ -142,6 +150,32 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
   int e = 0;
 
   int32_t nd[kPairWords];
+  double dacc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) dacc[c] = 0.0;
+  // p_e . ff over the element's unconstrained dofs (p_e as gathered; mask bits per dof)
+  auto edot = [&](const V (&uu)[NPE][3], const V (&ffe)[NPE][3], auto row_of, unsigned ma_, unsigned mb_,
+                    bool interior) {
+    V e = O::zero();
+    if (interior) {
+#pragma unroll
+      for (int a = 0; a < NPE; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) e = O::fma(uu[a][c], ffe[a][c], e);
+    } else {
+#pragma unroll
+      for (int a = 0; a < NPE; ++a) {
+        const int r = row_of(a);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const unsigned m = r < NPE ? (ma_ >> (3 * r + c)) & 1u : (mb_ >> (3 * (r - NPE) + c)) & 1u;
+          if (!m) e = O::fma(uu[a][c], ffe[a][c], e);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) dacc[c] += double(lane_col(e, c));
+  };
   auto load_conn = [&](int ee) {
     if (ee < p_end) {
       const int4* c4 = reinterpret_cast<const int4*>(pconn + static_cast<size_t>(ee) * kPairWords);
@@ -263,6 +297,7 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
         else tet4_product<V>(uu, b, lp, mp, ff);
 #endif
+        if constexpr (DOTS) edot(uu, ff, [](int a) { return a; }, ma, mb, ma == 0u);
         if (ma == 0u) {  // (branch hoisted out of the row loop: one divergence region, not one per row)
 #pragma unroll
           for (int k = 0; k < Geo::NA_OWN; ++k) {
@@ -306,6 +341,8 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
         if constexpr (NPE == 10) tet10_product<V>(uu, b, lp, mp, ff);
         else tet4_product<V>(uu, b, lp, mp, ff);
 #endif
+        if constexpr (DOTS)
+          edot(uu, ff, [](int a) { return Geo::b_row(a); }, ma, mb, ma == 0u && mb == unsigned(kHasB));
 #pragma unroll
         for (int k = 0; k < Geo::NFACE; ++k)
 #pragma unroll
@@ -339,6 +376,56 @@ k_ebe_pair(const int32_t* __restrict__ pconn, const T* __restrict__ pcoef, int32
 #if defined(EXP_NORED)
   if (reinterpret_cast<const float*>(&sink)[0] == 1.2345f) f[0] = T(1);
 #endif
+  if constexpr (DOTS) {  // lane groups folded in order: dpart[block][0][column]
+    __shared__ double dred[GROUPS * B];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) dred[grp * B + col + c] = dacc[c];
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < B) {
+      double sum = 0.0;
+      for (int g = 0; g < GROUPS; ++g) sum += dred[g * B + t];
+      dpart[(int64_t(blockIdx.x) * 3 + 0) * B + t] = sum;
+      dpart[(int64_t(blockIdx.x) * 3 + 1) * B + t] = 0.0;
+      dpart[(int64_t(blockIdx.x) * 3 + 2) * B + t] = 0.0;
+    }
+  }
+}
+
+// sum over the constrained dofs of p^2 per column (their product rows are the identity, so they
+// add p.p to (p, A p)); fixed block ranges and in-block order: reproducible. dpart[block][3][B].
+__global__ void __launch_bounds__(256) k_masked_pp(const float* __restrict__ p, const int32_t* __restrict__ dofs,
+                                                   int32_t n, int32_t B, double* __restrict__ dpart) {
+  __shared__ double sm[256];
+  const int t = threadIdx.x, per = 256 / B, col = t % B, slot = t / B;
+  double s = 0.0;
+  if (slot < per) {
+    const int64_t step = int64_t(gridDim.x) * per;
+    int64_t i = int64_t(blockIdx.x) * per + slot;
+    for (; i + 3 * step < n; i += 4 * step) {  // four independent loads in flight
+      int32_t d[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = __ldg(dofs + i + j * step);
+      float x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[j] = p[int64_t(d[j]) * B + col];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s += double(x[j]) * double(x[j]);
+    }
+    for (; i < n; i += step) {
+      const double x = double(p[int64_t(__ldg(dofs + i)) * B + col]);
+      s += x * x;
+    }
+  }
+  sm[t] = slot < per ? s : 0.0;
+  __syncthreads();
+  if (t < B) {
+    double sum = 0.0;
+    for (int j = 0; j < per; ++j) sum += sm[j * B + t];
+    dpart[(int64_t(blockIdx.x) * 3 + 0) * B + t] = sum;
+    dpart[(int64_t(blockIdx.x) * 3 + 1) * B + t] = 0.0;
+    dpart[(int64_t(blockIdx.x) * 3 + 2) * B + t] = 0.0;
+  }
 }
 
 // Units per launch. The persistent grid's lane groups stride through the units
@@ -384,8 +471,8 @@ bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p
     constexpr int NT = 128, GROUPS = NT / TPE;
     const size_t smem = 2 * (size_t((Geo::NR * 3 + 1) & ~1) * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
                              size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
-    auto kern = k_ebe_pair<T, V, NPE, B>;
-    const KernelFit fit = kernel_fit<k_ebe_pair<T, V, NPE, B>>(NT, smem);
+    auto kern = k_ebe_pair<T, V, NPE, B, false>;
+    const KernelFit fit = kernel_fit<k_ebe_pair<T, V, NPE, B, false>>(NT, smem);
     const int sms = fit.sms, per_sm = std::max(fit.per_sm, 1);
     if (p1 <= p0) return true;
     const int64_t need = (int64_t(p1 - p0) + GROUPS - 1) / GROUPS;
@@ -399,7 +486,7 @@ bool launch_pair_b(const ts_ebe& op, const T* u, T* f, cudaStream_t s, int32_t p
         TS_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), s));
       }
       kern<<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()),
-                                  static_cast<int32_t>(a), b, u, f, sched);
+                                  static_cast<int32_t>(a), b, u, f, sched, nullptr);
       TS_CUDA_LAUNCH();
     }
     return true;
@@ -418,7 +505,7 @@ int pair_launches_b(int32_t p0, int32_t p1) {
     constexpr int NT = 128, GROUPS = NT / TPE;
     const size_t smem = 2 * (size_t((Geo::NR * 3 + 1) & ~1) * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
                              size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
-    const KernelFit fit = kernel_fit<k_ebe_pair<T, V, NPE, B>>(NT, smem);
+    const KernelFit fit = kernel_fit<k_ebe_pair<T, V, NPE, B, false>>(NT, smem);
     if (p1 <= p0) return 0;
     const int64_t need = (int64_t(p1 - p0) + GROUPS - 1) / GROUPS;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(fit.sms) * std::max(fit.per_sm, 1))));
@@ -468,6 +555,49 @@ bool inv3(const double j[3][3], double inv[3][3]) {
 }
 
 }  // namespace
+
+constexpr int kPartialRows = 1184;  // blas.h kRedBlocks: rows of the gamma partials workspace
+template <int B>
+int launch_pair_dots(const ts_ebe& op, const float* u, float* f, cudaStream_t s, double* dpart) {
+  using T = float;
+  using V = float2;
+  using Geo = PairGeo<10>;
+  constexpr int CPT = LaneOps<V>::kCols, TPE = (B + CPT - 1) / CPT, NT = 128, GROUPS = NT / TPE;
+  const size_t smem = 2 * (size_t((Geo::NR * 3 + 1) & ~1) * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
+                           size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
+  const KernelFit fit = kernel_fit<k_ebe_pair<T, V, 10, B, true>>(NT, smem);
+  const int32_t U = op.pair->n_units;
+  const int64_t need = (int64_t(U) + GROUPS - 1) / GROUPS;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(fit.sms) * std::max(fit.per_sm, 1))));
+  int32_t* sched = op.pair->sched.get() + (op.pair->next_slot.fetch_add(1, std::memory_order_relaxed) & 63u);
+  TS_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), s));
+  k_ebe_pair<T, V, 10, B, true><<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()),
+                                                       0, U, u, f, sched, dpart);
+  TS_CUDA_LAUNCH();
+  int mb = 0;
+  if (op.has_mask && op.n_masked_dofs > 0) {
+    const int per = 256 / B;  // dofs per block pass; about 8 passes per thread, within the partial rows left
+    mb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kPartialRows - grid,
+                                                              (int64_t(op.n_masked_dofs) + 8 * per - 1) / (8 * per))));
+    k_masked_pp<<<mb, 256, 0, s>>>(u, op.masked_dofs.get(), op.n_masked_dofs, B, dpart + int64_t(grid) * 3 * B);
+    TS_CUDA_LAUNCH();
+  }
+  return grid + mb;
+}
+
+int ebe_pair_apply_dots(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, double* dpart) {
+  static const bool on = [] {  // TSGPU_EBE_FUSED_DOTS=0: the product, then the separate gamma pass
+    const char* e = std::getenv("TSGPU_EBE_FUSED_DOTS");
+    return !e || e[0] != '0';
+  }();
+  if (!on || !op.pair || !pair_dynamic() || op.prec != 32 || op.order != 2 || op.deterministic || op.fan) return -1;
+  if (op.pair->group_split != 0 && op.pair->group_split != op.pair->n_units) return -1;  // one element group
+  const float* uu = static_cast<const float*>(u);
+  float* ff = static_cast<float*>(f);
+  if (batch == 16) return launch_pair_dots<16>(op, uu, ff, s, dpart);
+  if (batch == 8) return launch_pair_dots<8>(op, uu, ff, s, dpart);
+  return -1;
+}
 
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part) {
   if (!op.pair) return false;

@@ -109,10 +109,11 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
     else
       ebe_apply_part(*lv.l1, x, y, B, s, -1, init);
   };
-  const std::function<bool(const float*, float*)> a1_dots = [&](const float* x, float* y) {
+  const std::function<int(const float*, float*)> a1_dots = [&](const float* x, float* y) {
     return lv.l1_assembled && bcsr_rows_f32_gamma(lv.l1_row_ptr.get(), lv.l1_col_idx.get(), lv.l1_blocks.get(),
                                                    lv.n1, x, y, B, s, static_cast<int64_t>(lv.l1_col_idx.size()),
-                                                   lv.ws);
+                                                   lv.ws)
+               ? 1 : 0;
   };
   InnerStats s1;
   {
@@ -124,11 +125,20 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), lv.p1_ends.get(), lv.n1, lv.n0, lv.mask0.get(), B, s);
   auto a0 = [&](const float* x, float* y, bool init) { ebe_apply_part(*lv.l0, x, y, B, s, -1, init); };
+  // q's start is written by the direction pass (fuse_init), so the dots product adds onto it
+  const std::function<int(const float*, float*)> a0_dots = [&](const float* x, float* y) {
+    if (lv.ws.comm || lv.ws.owned) return 0;
+    lv.ws.ensure(B);
+    const int nb = ebe_pair_apply_dots(*lv.l0, x, y, B, s, lv.ws.partial.get());
+    if (nb < 0) return 0;
+    lv.ws.nblk = nb;
+    return 2;
+  };
   InnerStats s0;
   {
     NvtxRange nl("inner pcg level 0");
     s0 = inner_pcg<float>(a0, lv.m0.get(), v.r0.get(), v.u0.get(), lv.n0, B, cfg.level_tol[0], cfg.level_max_iter[0],
-                          v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s, true, lv.mask0.get());
+                          v.e0.get(), v.p0.get(), v.q0.get(), lv.cs, lv.ws, s, true, lv.mask0.get(), &a0_dots);
   }
   const auto t3 = clk::now();
   rep.inner_iterations[2] += s2.iterations;

@@ -39,7 +39,7 @@ template <typename T, typename Op>
 InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t B, double tol, int max_iter, T* e,
                      T* p, T* q, ColScalars& cs, Workspace& ws, cudaStream_t s, bool fuse_init = false,
                      const uint8_t* op_mask = nullptr,
-                     const std::function<bool(const T*, T*)>* product_with_dots = nullptr) {
+                     const std::function<int(const T*, T*)>* product_with_dots = nullptr) {
   if (max_iter < 1) validation("inner_pcg: max_iter must be >= 1");
   A(u, e, true);
   pcg_init<T>(inv, r, e, n, B, cs, ws, s);
@@ -55,15 +55,23 @@ InnerStats inner_pcg(Op&& A, const T* inv, const T* r, T* u, int32_t n, int32_t 
     pcg_rho(B, first, cs, ws, s);
     pcg_direction<T>(inv, e, p, n, B, first, cs, s, fuse_init ? q : nullptr, op_mask, pending ? u : nullptr);
     pending = false;
-    // q = A p; gamma's partials from the product itself when it can (assembled levels), else a pass
-    if (product_with_dots && (*product_with_dots)(p, q)) {
-      pcg_gamma_final<T>(B, cs, ws, s);
+    // q = A p; gamma's partials from the product itself when it can (1: all three dots, assembled
+    // levels; 2: (p,Ap) alone, element-wise on the EBE level), else a separate pass
+    const int fused = product_with_dots ? (*product_with_dots)(p, q) : 0;
+    if (fused) {
+      pcg_gamma_final<T>(B, cs, ws, s, fused == 2);
     } else {
       A(p, q, !fuse_init);
       pcg_gamma<T>(p, q, n, B, cs, ws, s);
     }
     pcg_update<T>(inv, e, q, n, B, cs, ws, s);
-    const PcgStatus& ps = read_status(ws, s);
+    const PcgStatus* psp = &read_status(ws, s);
+    if (psp->need_full) {  // (p,Ap) <= 0 in some column: decide it with the full dots (pcg.hpp:83-110)
+      pcg_gamma<T>(p, q, n, B, cs, ws, s);
+      pcg_update<T>(inv, e, q, n, B, cs, ws, s);
+      psp = &read_status(ws, s);
+    }
+    const PcgStatus& ps = *psp;
     if (ps.breakdown_col >= 0)
       fail(TS_ERR_BREAKDOWN, "inner_pcg: breakdown (p,Ap) <= 0 at iteration " + std::to_string(st.iterations + 1) +
                                  ", column " + std::to_string(ps.breakdown_col));
