@@ -178,6 +178,36 @@ struct DistEbe {
   }
 };
 
+// The level-0 product with the inner PCG's (p, Ap) partials (ebe_pair_apply_dots): elements are
+// partitioned, so each rank's element sums are its share; the constrained dofs' p.p counts owned
+// nodes only. Same launch / exchange order as DistEbe::apply (init written by the caller).
+int dist_l0_apply_dots(DistEbe& D, const float* u, float* f, int32_t B, cudaStream_t s, double* dpart,
+                       const int32_t* masked_owned, int32_t n_masked_owned) {
+  const bool split = D.overlap && !D.halo.nbr.empty() && D.op->group_split < D.op->n_elems;
+  const int nb0 = ebe_pair_apply_dots(*D.op, u, f, B, s, dpart, 0);
+  if (nb0 < 0) return -1;
+  int nb1 = 0;
+  if (!split) {
+    nb1 = ebe_pair_apply_dots(*D.op, u, f, B, s, dpart + int64_t(nb0) * 3 * B, 1);
+    D.halo.run<float>(f, 3 * B, B, D.mask, *D.comm, s);
+  } else {
+    if (!D.side) {
+      TS_CUDA(cudaStreamCreateWithFlags(&D.side, cudaStreamNonBlocking));
+      TS_CUDA(cudaEventCreateWithFlags(&D.ev_b, cudaEventDisableTiming));
+      TS_CUDA(cudaEventCreateWithFlags(&D.ev_h, cudaEventDisableTiming));
+    }
+    TS_CUDA(cudaEventRecord(D.ev_b, s));
+    TS_CUDA(cudaStreamWaitEvent(D.side, D.ev_b, 0));
+    D.halo.run<float>(f, 3 * B, B, D.mask, *D.comm, D.side);
+    TS_CUDA(cudaEventRecord(D.ev_h, D.side));
+    nb1 = ebe_pair_apply_dots(*D.op, u, f, B, s, dpart + int64_t(nb0) * 3 * B, 1);
+    TS_CUDA(cudaStreamWaitEvent(s, D.ev_h, 0));
+  }
+  const int used = nb0 + nb1;
+  return used + ebe_masked_pp(masked_owned, n_masked_owned, u, B, s, dpart + int64_t(used) * 3 * B,
+                              kRedBlocks - used);
+}
+
 struct DistVecs {
   int32_t batch = 0;
   DevBuf<double> r, q, z, p, scratch, f, u;
@@ -230,6 +260,8 @@ struct ts_dist_levels {
   tsg::DevBuf<int32_t> l2_row_ptr, l2_col_idx;
   tsg::DevBuf<float> l2_blocks, m0, m1, m2;
   tsg::DevBuf<uint8_t> mask0, mask1, mask2, owned0;
+  tsg::DevBuf<int32_t> masked0_owned;  // constrained level-0 dofs of owned nodes (the fused gamma's p.p term)
+  int32_t n_masked0_owned = 0;
   tsg::DistVecs v;
   bool l2_dist = false;  // TSGPU_DIST_L2=distributed: level 2 split by coarse rows (else replicated)
   // level 1 as this partition's assembled K1 (fp32 blocks from its own elements; interface rows then
@@ -374,9 +406,17 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), L.p1_ends.get(), L.n1, L.n0, L.mask0.get(), B, s);
   auto a0 = [&](const float* x, float* y, bool init) { L.l0.apply<float>(x, y, B, s, init); };
+  const std::function<int(const float*, float*)> a0_dots = [&](const float* x, float* y) {
+    L.ws.ensure(B);
+    const int nb = dist_l0_apply_dots(L.l0, x, y, B, s, L.ws.partial.get(), L.masked0_owned.get(),
+                                      L.n_masked0_owned);
+    if (nb < 0) return 0;
+    L.ws.nblk = nb;
+    return 2;
+  };
   const InnerStats s0 = inner_pcg<float>(a0, L.m0.get(), v.r0.get(), v.u0.get(), L.n0, B, cfg.level_tol[0],
                                          cfg.level_max_iter[0], v.e0.get(), v.p0.get(), v.q0.get(), L.cs, L.ws, s,
-                                         true, L.mask0.get());
+                                         true, L.mask0.get(), &a0_dots);
   const auto t3 = clk::now();
   rep.inner_iterations[2] += s2.iterations;
   rep.inner_iterations[1] += s1.iterations;
@@ -515,6 +555,13 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
   L->mask0.upload(P.mask);
   L->mask1.upload(mask1);
   L->owned0.upload(P.owned);
+  {
+    std::vector<int32_t> mo;
+    for (size_t d = 0; d < P.mask.size(); ++d)
+      if (P.mask[d] && P.owned[d / 3]) mo.push_back(static_cast<int32_t>(d));
+    L->n_masked0_owned = static_cast<int32_t>(mo.size());
+    L->masked0_owned.upload(mo);
+  }
   for (DistEbe* d : {&L->outer, &L->l0}) {
     d->halo.build(P.halo0);
     d->mask = L->mask0.get();

@@ -190,10 +190,15 @@ int ebe_launches_per_apply(const ts_ebe& op, int32_t batch);
 int ebe_pair_launches(const ts_ebe& op, int32_t batch);
 // pair sweep (ebe_pair.cu); false when no instance covers this batch width
 bool pair_dynamic();  // TSGPU_EBE_DYN: pair units taken in warp chunks from a counter
-// f (its masked-identity start already written) += K u over the whole pair sweep, plus the
-// inner PCG's gamma partials of (u, f) in dpart[block][3][batch] (fp32 tet10, r = 8 / 16, one
-// element group, dynamic schedule); returns the partial block count, or -1 (nothing launched)
-int ebe_pair_apply_dots(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, double* dpart);
+// f (its masked-identity start already written) += K u over the pair sweep (part -1: whole, one
+// element group, + the constrained dofs' p.p; 0 / 1: that element group only), plus the inner
+// PCG's gamma partials (p, Ap) in dpart[block][3][batch] (fp32 tet10, r = 8 / 16, dynamic schedule);
+// returns the partial rows written, or -1 (nothing launched)
+int ebe_pair_apply_dots(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, double* dpart,
+                        int part = -1);
+// sum over the constrained dofs `dofs` of p^2 per column into dpart rows (at most rows_left); rows written
+int ebe_masked_pp(const int32_t* dofs, int32_t n, const float* p, int32_t batch, cudaStream_t s, double* dpart,
+                  int rows_left);
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part);
 // face-pair topology of an element order (greedy matching result), shareable between the
 // level set's tet10 operators, which use the same mesh and element order

@@ -558,7 +558,8 @@ bool inv3(const double j[3][3], double inv[3][3]) {
 
 constexpr int kPartialRows = 1184;  // blas.h kRedBlocks: rows of the gamma partials workspace
 template <int B>
-int launch_pair_dots(const ts_ebe& op, const float* u, float* f, cudaStream_t s, double* dpart) {
+int launch_pair_dots(const ts_ebe& op, const float* u, float* f, cudaStream_t s, double* dpart, int32_t p0,
+                     int32_t p1) {
   using T = float;
   using V = float2;
   using Geo = PairGeo<10>;
@@ -566,37 +567,45 @@ int launch_pair_dots(const ts_ebe& op, const float* u, float* f, cudaStream_t s,
   const size_t smem = 2 * (size_t((Geo::NR * 3 + 1) & ~1) * NT * sizeof(V) + size_t(GROUPS) * 24 * sizeof(T) +
                            size_t(GROUPS) * Geo::WORDS * sizeof(int32_t));
   const KernelFit fit = kernel_fit<k_ebe_pair<T, V, 10, B, true>>(NT, smem);
-  const int32_t U = op.pair->n_units;
-  const int64_t need = (int64_t(U) + GROUPS - 1) / GROUPS;
+  if (p1 <= p0) return 0;
+  const int64_t need = (int64_t(p1) - p0 + GROUPS - 1) / GROUPS;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(fit.sms) * std::max(fit.per_sm, 1))));
   int32_t* sched = op.pair->sched.get() + (op.pair->next_slot.fetch_add(1, std::memory_order_relaxed) & 63u);
   TS_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), s));
   k_ebe_pair<T, V, 10, B, true><<<grid, NT, smem, s>>>(op.pair->conn.get(), reinterpret_cast<const T*>(op.pair->coef.get()),
-                                                       0, U, u, f, sched, dpart);
+                                                       p0, p1, u, f, sched, dpart);
   TS_CUDA_LAUNCH();
-  int mb = 0;
-  if (op.has_mask && op.n_masked_dofs > 0) {
-    const int per = 256 / B;  // dofs per block pass; about 8 passes per thread, within the partial rows left
-    mb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kPartialRows - grid,
-                                                              (int64_t(op.n_masked_dofs) + 8 * per - 1) / (8 * per))));
-    k_masked_pp<<<mb, 256, 0, s>>>(u, op.masked_dofs.get(), op.n_masked_dofs, B, dpart + int64_t(grid) * 3 * B);
-    TS_CUDA_LAUNCH();
-  }
-  return grid + mb;
+  return grid;
 }
 
-int ebe_pair_apply_dots(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, double* dpart) {
+int ebe_masked_pp(const int32_t* dofs, int32_t n, const float* p, int32_t batch, cudaStream_t s, double* dpart,
+                  int rows_left) {
+  if (n <= 0 || rows_left <= 0) return 0;
+  const int per = 256 / batch;  // dofs per block pass; about 8 passes per thread, within the partial rows left
+  const int mb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(rows_left, (int64_t(n) + 8 * per - 1) / (8 * per))));
+  k_masked_pp<<<mb, 256, 0, s>>>(p, dofs, n, batch, dpart);
+  TS_CUDA_LAUNCH();
+  return mb;
+}
+
+int ebe_pair_apply_dots(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, double* dpart,
+                        int part) {
   static const bool on = [] {  // TSGPU_EBE_FUSED_DOTS=0: the product, then the separate gamma pass
     const char* e = std::getenv("TSGPU_EBE_FUSED_DOTS");
     return !e || e[0] != '0';
   }();
   if (!on || !op.pair || !pair_dynamic() || op.prec != 32 || op.order != 2 || op.deterministic || op.fan) return -1;
-  if (op.pair->group_split != 0 && op.pair->group_split != op.pair->n_units) return -1;  // one element group
+  if (batch != 16 && batch != 8) return -1;
+  const int32_t U = op.pair->n_units, sp = op.pair->group_split;
+  if (part < 0 && sp != 0 && sp != U) return -1;  // the whole sweep in one launch needs one element group
+  const int32_t p0 = part == 1 ? sp : 0, p1 = part == 0 ? sp : U;
   const float* uu = static_cast<const float*>(u);
   float* ff = static_cast<float*>(f);
-  if (batch == 16) return launch_pair_dots<16>(op, uu, ff, s, dpart);
-  if (batch == 8) return launch_pair_dots<8>(op, uu, ff, s, dpart);
-  return -1;
+  int nb = batch == 16 ? launch_pair_dots<16>(op, uu, ff, s, dpart, p0, p1) : launch_pair_dots<8>(op, uu, ff, s, dpart, p0, p1);
+  if (part < 0 && op.has_mask && op.n_masked_dofs > 0)  // one device: every constrained dof is this rank's
+    nb += ebe_masked_pp(op.masked_dofs.get(), op.n_masked_dofs, uu, batch, s, dpart + int64_t(nb) * 3 * batch,
+                        kPartialRows - nb);
+  return nb;
 }
 
 bool ebe_pair_apply(const ts_ebe& op, const void* u, void* f, int32_t batch, cudaStream_t s, int part) {
