@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(kFinThreads) k_gamma_final(const double* parti
     const double g = tot[b];
     gamma[b] = g;
     double a = 0.0;
-    if (g > 0.0) {
+    if (pq_only > 1) {  // test hook (TSGPU_TEST_FUSED_FALLBACK): every iteration takes the full-pass fallback
+      atomicExch(&full, 1);
+    } else if (g > 0.0) {
       a = rho_a[b] / g;
     } else if (g == 0.0 && rho_a[b] == 0.0) {
       a = 0.0;
@@ -1153,9 +1155,13 @@ bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const f
 template <typename T>
 void pcg_gamma_final(int32_t B, const ColScalars& cs, Workspace& ws, cudaStream_t s, bool partial_pq_only) {
   const Partials pp = finish_partials(ws, 3, B, s);
+  static const bool force_fallback = [] {
+    const char* e = std::getenv("TSGPU_TEST_FUSED_FALLBACK");
+    return e && e[0] == '1';
+  }();
   k_gamma_final<T><<<1, kFinThreads, 0, s>>>(pp.p, pp.nblk, B, cs[ColScalars::RHO_A], cs[ColScalars::RHO_B],
                                      cs[ColScalars::GAMMA], cs[ColScalars::ALPHA], ws.status.get(),
-                                     partial_pq_only ? 1 : 0);
+                                     partial_pq_only ? (force_fallback ? 2 : 1) : 0);
   TS_CUDA_LAUNCH();
 }
 template void pcg_gamma_final<float>(int32_t, const ColScalars&, Workspace&, cudaStream_t, bool);

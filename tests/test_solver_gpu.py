@@ -228,3 +228,47 @@ def test_staged_level1_global_path_matches_reference():
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 1.0
+
+
+_FALLBACK_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import numpy as np
+import paper_1710_08679_b200 as ts
+from conftest import TWO_LAYER
+mesh = ts.generate_box_mesh((24000.0, 28000.0, 12000.0), (8, 9, 5), (7000.0,))
+cfg = ts.SolverConfig(batch_size=8)
+model = ts.build_crust_model(mesh, [ts.material_from_wavespeeds(*t) for t in TWO_LAYER], cfg)
+rng = np.random.default_rng(9)
+us = rng.uniform(-0.05, 0.05, (3 * mesh.node_count(), 8))
+us[model.mask == 1] = 0
+f = model.levels.outer.apply(us)
+u, rep = ts.solve(model.levels, f, np.zeros_like(f), cfg)
+print(json.dumps({"inner": list(rep.inner_iterations), "outer": rep.outer_iterations,
+                  "err": float(np.linalg.norm(u - us) / np.linalg.norm(us))}))
+"""
+
+
+def test_fused_gamma_fallback_matches_separate_pass():
+    """The level-0 fused (p, Ap) path's fallback (need_full: skip the update, rerun gamma with the full dot
+    pass), forced on every iteration by TSGPU_TEST_FUSED_FALLBACK in a child process, gives the same solve as
+    the separate gamma pass (TSGPU_EBE_FUSED_DOTS=0): same iteration counts, same solution."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for name, extra in (("separate", {"TSGPU_EBE_FUSED_DOTS": "0"}), ("fallback", {"TSGPU_TEST_FUSED_FALLBACK": "1"}),
+                        ("fused", {})):
+        env = dict(os.environ, **extra)
+        out = subprocess.run([sys.executable, "-c", _FALLBACK_SCRIPT, root], capture_output=True, text=True, env=env,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        runs[name] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert runs["fallback"]["inner"] == runs["separate"]["inner"]
+    assert runs["fallback"]["outer"] == runs["separate"]["outer"]
+    for r in runs.values():
+        assert r["err"] < 1e-6
+    a, b = runs["fused"]["inner"], runs["separate"]["inner"]
+    assert all(abs(x - y) <= max(2, 0.02 * y) for x, y in zip(a, b))
