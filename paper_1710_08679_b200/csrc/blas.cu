@@ -624,7 +624,8 @@ template <int W, int RPW, typename ACC, int PER_ROW = 20, bool DOTS = false>
 __global__ void __launch_bounds__(32 * kStageWarps)
 k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                    const float* __restrict__ blocks, int32_t n, int64_t nnz, const float* __restrict__ u,
-                   float* __restrict__ f, int32_t B, double* __restrict__ partial) {
+                   float* __restrict__ f, int32_t B, double* __restrict__ partial,
+                   const uint8_t* __restrict__ rowsel) {
   using Cap = StageCap<RPW, PER_ROW>;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double red[DOTS ? kStageWarps * 3 * 32 : 1];
@@ -730,6 +731,7 @@ k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restric
         for (int c = 0; c < W; ++c) o.v[c] = static_cast<float>(acc[i][c]);
         st<float, W>(fr + i * B, o);
         if constexpr (DOTS) {
+          if (rowsel && !rowsel[r]) continue;  // (partitioned: other ranks' rows / rows completed later)
           const Pack<float, W> pv = ld<float, W>(u + 3 * r * B + b0 + i * B);
 #pragma unroll
           for (int c = 0; c < W; ++c) {
@@ -767,7 +769,8 @@ k_bcsr_rows_staged(const int32_t* __restrict__ row_ptr, const int32_t* __restric
 
 template <int W, int RPW, typename ACC, int PER_ROW = 20, bool DOTS = false>
 int launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n, int64_t nnz,
-                       const float* u, float* f, int32_t B, cudaStream_t s, double* partial = nullptr) {
+                       const float* u, float* f, int32_t B, cudaStream_t s, double* partial = nullptr,
+                       const uint8_t* rowsel = nullptr) {
   const size_t smem = size_t(kStageWarps) * StageCap<RPW, PER_ROW>::kWarpBytes;
   auto kern = k_bcsr_rows_staged<W, RPW, ACC, PER_ROW, DOTS>;
   // the shared-memory opt-in is a per-device attribute of the function: set once per device
@@ -795,7 +798,7 @@ int launch_rows_staged(const int32_t* row_ptr, const int32_t* col_idx, const flo
   if (DOTS)  // persistent: one resident wave (the partial count the finalize sums), at most kRedBlocks
     grid = std::min<int64_t>(grid, std::min<int64_t>(kRedBlocks, int64_t(sms[dev].load()) * per_sm[dev].load()));
   kern<<<static_cast<unsigned>(grid), 32 * kStageWarps, smem, s>>>(row_ptr, col_idx, blocks, n, nnz, u, f, B,
-                                                                   partial);
+                                                                   partial, rowsel);
   return static_cast<int>(grid);
 }
 
@@ -1136,20 +1139,64 @@ void bcsr_rows_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* 
   TS_CUDA_LAUNCH();
 }
 bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
-                         const float* p, float* q, int32_t B, cudaStream_t s, int64_t nnz, Workspace& ws) {
+                         const float* p, float* q, int32_t B, cudaStream_t s, int64_t nnz, Workspace& ws,
+                         const uint8_t* rowsel) {
   static const bool on = [] {  // TSGPU_L1_FUSED_DOTS=0: the product, then the separate gamma pass
     const char* e = std::getenv("TSGPU_L1_FUSED_DOTS");
     return !e || e[0] != '0';
   }();
-  if (!on || n <= 0 || nnz <= 0 || ws.comm || ws.owned || !bcsr_rows_staged_ok(B)) return false;
+  if (!on || n <= 0 || nnz <= 0 || !bcsr_rows_staged_ok(B)) return false;
+  if (!rowsel && (ws.comm || ws.owned)) return false;  // partitioned callers select their rows
   ws.ensure(B);
   const int grid = B == 16 ? launch_rows_staged<4, 8, float, 16, true>(row_ptr, col_idx, blocks, n, nnz, p, q, B, s,
-                                                                        ws.partial.get())
+                                                                        ws.partial.get(), rowsel)
                            : launch_rows_staged<2, 8, float, 16, true>(row_ptr, col_idx, blocks, n, nnz, p, q, B, s,
-                                                                        ws.partial.get());
+                                                                        ws.partial.get(), rowsel);
   TS_CUDA_LAUNCH();
   ws.nblk = grid;
   return true;
+}
+
+// (p,q), (p,p), (q,q) per column over the listed node rows, into partial rows [ws.nblk, ...): the
+// rows the fused product left out (a partition's interface rows, complete only after the exchange)
+__global__ void __launch_bounds__(256) k_rows_dots(const float* __restrict__ p, const float* __restrict__ q,
+                                                   const int32_t* __restrict__ rows, int32_t n, int32_t B,
+                                                   double* __restrict__ partial) {
+  __shared__ double sm[3][256];
+  const int t = threadIdx.x, per = 256 / B, col = t % B, slot = t / B;
+  double a = 0.0, b = 0.0, c = 0.0;
+  if (slot < per)
+    for (int64_t i = int64_t(blockIdx.x) * per + slot; i < n; i += int64_t(gridDim.x) * per) {
+      const int64_t base = 3 * int64_t(__ldg(rows + i)) * B + col;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double x = double(p[base + d * B]), y = double(q[base + d * B]);
+        a += x * y;
+        b += x * x;
+        c += y * y;
+      }
+    }
+  sm[0][t] = slot < per ? a : 0.0;
+  sm[1][t] = slot < per ? b : 0.0;
+  sm[2][t] = slot < per ? c : 0.0;
+  __syncthreads();
+  if (t < B)
+    for (int k = 0; k < 3; ++k) {
+      double sum = 0.0;
+      for (int j = 0; j < per; ++j) sum += sm[k][j * B + t];
+      partial[(int64_t(blockIdx.x) * 3 + k) * B + t] = sum;
+    }
+}
+
+void rows_dots_append(const float* p, const float* q, const int32_t* rows, int32_t n, int32_t B, cudaStream_t s,
+                      Workspace& ws) {
+  if (n <= 0) return;
+  const int per = 256 / B;
+  const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kRedBlocks - ws.nblk,
+                                                                        (int64_t(n) + 8 * per - 1) / (8 * per))));
+  k_rows_dots<<<nb, 256, 0, s>>>(p, q, rows, n, B, ws.partial.get() + int64_t(ws.nblk) * 3 * B);
+  TS_CUDA_LAUNCH();
+  ws.nblk += nb;
 }
 
 template <typename T>

@@ -115,7 +115,12 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
 // column, reduce_pass layout) in ws.partial / ws.nblk; false (nothing launched) when it does not
 // apply (unstaged width, distributed workspace)
 bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
-                         const float* p, float* q, int32_t batch, cudaStream_t s, int64_t nnz, Workspace& ws);
+                         const float* p, float* q, int32_t batch, cudaStream_t s, int64_t nnz, Workspace& ws,
+                         const uint8_t* rowsel = nullptr);
+// partitioned: rowsel[r] = 1 for the rows the fused product counts; the rest of this rank's rows (its
+// owned interface rows, complete after the exchange) are added by rows_dots_append
+void rows_dots_append(const float* p, const float* q, const int32_t* rows, int32_t n, int32_t batch, cudaStream_t s,
+                      Workspace& ws);
 // the gamma finalize (alpha, breakdown / stagnation) from partials already in ws; partial_pq_only:
 // the partials hold (p,q) alone (element-wise products), so a column with (p,q) <= 0 sets
 // need_full instead of deciding stagnation / breakdown (pcg_update then leaves e alone)

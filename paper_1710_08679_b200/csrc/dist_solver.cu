@@ -262,6 +262,9 @@ struct ts_dist_levels {
   tsg::DevBuf<uint8_t> mask0, mask1, mask2, owned0;
   tsg::DevBuf<int32_t> masked0_owned;  // constrained level-0 dofs of owned nodes (the fused gamma's p.p term)
   int32_t n_masked0_owned = 0;
+  tsg::DevBuf<uint8_t> l1_dot_rows;    // level-1 rows the fused product's dots count: owned, not interface
+  tsg::DevBuf<int32_t> l1_iface_owned; // owned interface rows: their dots after the exchange
+  int32_t n_l1_iface_owned = 0;
   tsg::DistVecs v;
   bool l2_dist = false;  // TSGPU_DIST_L2=distributed: level 2 split by coarse rows (else replicated)
   // level 1 as this partition's assembled K1 (fp32 blocks from its own elements; interface rows then
@@ -400,9 +403,24 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
   L.ws.owned = L.owned0.get();  // the vertex prefix of the level-0 flags
   p2_apply(v.u2.get(), v.u1.get(), L.agg.get(), L.n1, L.mask1.get(), B, s);
   auto a1 = [&](const float* x, float* y, bool init) { dist_l1_apply(L, x, y, B, s, init); };
+  // the staged whole-range product (dist_l1_apply's unsplit form) with gamma's dots of this rank's
+  // owned rows: interior ones in the product, interface ones after the exchange completes them
+  const std::function<int(const float*, float*)> a1_dots = [&](const float* x, float* y) {
+    static const bool split = [] {
+      const char* e = std::getenv("TSGPU_DIST_L1_SPLIT");
+      return e && e[0] == '1';
+    }();
+    if (!L.l1_assembled || split) return 0;
+    if (!bcsr_rows_f32_gamma(L.l1a_row_ptr.get(), L.l1a_col_idx.get(), L.l1a_blocks.get(), L.n1, x, y, B, s,
+                             static_cast<int64_t>(L.l1a_col_idx.size()), L.ws, L.l1_dot_rows.get()))
+      return 0;
+    L.l1.halo.run<float>(y, 3 * B, B, L.mask1.get(), *L.comm, s);
+    rows_dots_append(x, y, L.l1_iface_owned.get(), L.n_l1_iface_owned, B, s, L.ws);
+    return 1;
+  };
   const InnerStats s1 = inner_pcg<float>(a1, L.m1.get(), v.r1.get(), v.u1.get(), L.n1, B, cfg.level_tol[1],
                                          cfg.level_max_iter[1], v.e1.get(), v.p1.get(), v.q1.get(), L.cs, L.ws, s,
-                                         !L.l1_assembled, L.mask1.get());
+                                         !L.l1_assembled, L.mask1.get(), &a1_dots);
   const auto t2 = clk::now();
   p1_apply(v.u1.get(), v.u0.get(), L.p1_ends.get(), L.n1, L.n0, L.mask0.get(), B, s);
   auto a0 = [&](const float* x, float* y, bool init) { L.l0.apply<float>(x, y, B, s, init); };
@@ -704,6 +722,16 @@ ts_dist_levels* dist_levels_create(const Mesh& m, int32_t n_mat, const double* l
       for (int32_t v = 0; v < L->n1; ++v) (iface[v] ? ri : rn).push_back(v);
       L->n_l1_iface = static_cast<int32_t>(ri.size());
       L->n_l1_inner = static_cast<int32_t>(rn.size());
+      std::vector<uint8_t> sel(L->n1, 0);
+      std::vector<int32_t> io;
+      for (int32_t v = 0; v < L->n1; ++v) {
+        if (!P.owned[v]) continue;
+        if (iface[v]) io.push_back(v);
+        else sel[v] = 1;
+      }
+      L->l1_dot_rows.upload(sel);
+      L->l1_iface_owned.upload(io);
+      L->n_l1_iface_owned = static_cast<int32_t>(io.size());
       L->l1a_iface.upload(ri);
       L->l1a_inner.upload(rn);
     }
