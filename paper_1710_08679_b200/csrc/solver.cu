@@ -421,7 +421,8 @@ ts_status ts_levels_apply(ts_levels* lv, int32_t which, const void* u, void* f, 
   else if (which == 2) tsg::ebe_apply(*lv->l1, u, f, batch, s);
   else if (which == 3)
     tsg::bcsr_apply_f32(lv->l2_row_ptr.get(), lv->l2_col_idx.get(), lv->l2_blocks.get(), lv->n2,
-                        static_cast<const float*>(u), static_cast<float*>(f), batch, s);
+                        static_cast<const float*>(u), static_cast<float*>(f), batch, s,
+                        static_cast<int64_t>(lv->l2_col_idx.size()));
   else tsg::validation("levels apply: operator index must be 0 (outer), 1 (level0), 2 (level1) or 3 (level2)");
   TS_API_END
 }
