@@ -1157,6 +1157,29 @@ bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const f
   return true;
 }
 
+bool bcsr_apply_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
+                          const float* p, float* q, int32_t B, cudaStream_t s, int64_t nnz, Workspace& ws) {
+  static const bool on = [] {  // TSGPU_L2_FUSED_DOTS=0: the product, then the separate gamma pass
+    const char* e = std::getenv("TSGPU_L2_FUSED_DOTS");
+    return !e || e[0] != '0';
+  }();
+  static const bool staged = [] {
+    const char* e = std::getenv("TSGPU_L2_STAGED");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || !staged || n <= 0 || nnz <= 0 || ws.comm || ws.owned || pack_width<float>(B) != 4 ||
+      (B != 16 && B != 8))
+    return false;
+  ws.ensure(B);
+  const int grid = B == 16 ? launch_rows_staged<4, 8, double, 24, true>(row_ptr, col_idx, blocks, n, nnz, p, q, B, s,
+                                                                         ws.partial.get())
+                           : launch_rows_staged<2, 8, double, 24, true>(row_ptr, col_idx, blocks, n, nnz, p, q, B, s,
+                                                                         ws.partial.get());
+  TS_CUDA_LAUNCH();
+  ws.nblk = grid;
+  return true;
+}
+
 // (p,q), (p,p), (q,q) per column over the listed node rows, into partial rows [ws.nblk, ...): the
 // rows the fused product left out (a partition's interface rows, complete only after the exchange)
 __global__ void __launch_bounds__(256) k_rows_dots(const float* __restrict__ p, const float* __restrict__ q,

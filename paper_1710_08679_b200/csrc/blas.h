@@ -117,6 +117,9 @@ void bcsr_apply_f32(const int32_t* row_ptr, const int32_t* col_idx, const float*
 bool bcsr_rows_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
                          const float* p, float* q, int32_t batch, cudaStream_t s, int64_t nnz, Workspace& ws,
                          const uint8_t* rowsel = nullptr);
+// the level-2 product (fp64 row sums) with gamma's partials, as bcsr_rows_f32_gamma; one device / replicated only
+bool bcsr_apply_f32_gamma(const int32_t* row_ptr, const int32_t* col_idx, const float* blocks, int32_t n,
+                          const float* p, float* q, int32_t batch, cudaStream_t s, int64_t nnz, Workspace& ws);
 // partitioned: rowsel[r] = 1 for the rows the fused product counts; the rest of this rank's rows (its
 // owned interface rows, complete after the exchange) are added by rows_dots_append
 void rows_dots_append(const float* p, const float* q, const int32_t* rows, int32_t n, int32_t batch, cudaStream_t s,

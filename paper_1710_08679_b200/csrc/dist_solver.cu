@@ -395,8 +395,13 @@ void dist_mg_precond(ts_dist_levels& L, const ts_solver_config& cfg, const doubl
       bcsr_apply_f32(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s,
                      static_cast<int64_t>(L.l2_col_idx.size()));
     };
+    const std::function<int(const float*, float*)> a2_dots = [&](const float* x, float* y) {
+      return bcsr_apply_f32_gamma(L.l2_row_ptr.get(), L.l2_col_idx.get(), L.l2_blocks.get(), L.n2, x, y, B, s,
+                                  static_cast<int64_t>(L.l2_col_idx.size()), L.ws)
+                 ? 1 : 0;
+    };
     s2 = inner_pcg<float>(a2, L.m2.get(), v.r2.get(), v.u2.get(), L.n2, B, cfg.level_tol[2], cfg.level_max_iter[2],
-                          v.e2.get(), v.p2.get(), v.q2.get(), L.cs, L.ws, s);
+                          v.e2.get(), v.p2.get(), v.q2.get(), L.cs, L.ws, s, false, nullptr, &a2_dots);
   }
   const auto t1 = clk::now();
   L.ws.comm = L.comm;

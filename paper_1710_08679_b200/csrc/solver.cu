@@ -94,11 +94,16 @@ void mg_precond(ts_levels& lv, const ts_solver_config& cfg, const double* r, dou
     bcsr_apply_f32(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s,
                    static_cast<int64_t>(lv.l2_col_idx.size()));
   };
+  const std::function<int(const float*, float*)> a2_dots = [&](const float* x, float* y) {
+    return bcsr_apply_f32_gamma(lv.l2_row_ptr.get(), lv.l2_col_idx.get(), lv.l2_blocks.get(), lv.n2, x, y, B, s,
+                                static_cast<int64_t>(lv.l2_col_idx.size()), lv.ws)
+               ? 1 : 0;
+  };
   InnerStats s2;
   {
     NvtxRange nl("inner pcg level 2");
     s2 = inner_pcg<float>(a2, lv.m2.get(), v.r2.get(), v.u2.get(), lv.n2, B, cfg.level_tol[2], cfg.level_max_iter[2],
-                          v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s);
+                          v.e2.get(), v.p2.get(), v.q2.get(), lv.cs, lv.ws, s, false, nullptr, &a2_dots);
   }
   const auto t1 = clk::now();
   p2_apply(v.u2.get(), v.u1.get(), lv.agg.get(), lv.n1, lv.mask1.get(), B, s);
